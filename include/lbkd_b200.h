@@ -1,0 +1,100 @@
+/*
+ * lbkd_b200.h -- C ABI of the B200-native left-balanced k-d tree builder
+ * (arXiv 2211.00120).  Plain pointers and sizes only; every pointer named
+ * d_* is a device pointer on the context's device; `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).
+ *
+ * Each entry point replaces one interface of the reference package `lbkd`
+ * (/root/reference/pkg/src/lbkd):
+ *
+ *   lbkd_build_rr        builder.build_round_robin       builder.py:200-236
+ *   lbkd_build_widest    widest.build_widest             widest.py:134-191
+ *   lbkd_update_tags_rr  kernels_*.update_tags_round_robin
+ *                        (accel plugin seam)             kernels_numba.py:21-46,
+ *                                                        accel.py:48-58
+ *   lbkd_update_tags_widest  kernels_*.update_tags_widest kernels_numba.py:49-110
+ *   lbkd_num_levels      treemath.num_levels             treemath.py:57-61
+ *   lbkd_strerror        the ValueError texts of ingest  builder.py:117-141,
+ *                        and the widest capacity check   widest.py:147-156
+ *
+ * Output contract of the build calls (KdTree, builder.py:26-60):
+ *   d_points_out[s*k + c]  coordinate c of the point stored at node s
+ *                          (level order, children of s at 2s+1, 2s+2)
+ *   d_perm[s]              input row of that point (KdTree.payload for the
+ *                          default arange payload); may be NULL
+ *   d_split_dims[s]        widest only: split dimension of node s
+ * The permutation is bit-identical to the reference's on the same float32
+ * input, ties included (stable w.r.t. current order, -0.0 == +0.0).
+ * d_points_out may alias d_points (in-place reordering, as in the paper).
+ *
+ * Threading: a context is used by one host thread at a time; work is
+ * enqueued on `stream`.  The build calls end with one stream
+ * synchronisation to read back the non-finite flag (disable with
+ * lbkd_set_check(ctx, 0) to keep a build fully asynchronous).
+ */
+#ifndef LBKD_B200_H
+#define LBKD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum lbkd_status {
+    LBKD_OK = 0,
+    LBKD_EINVAL_SHAPE = 1,   /* k < 1, k > LBKD_MAX_K, n < 0, bad pointers */
+    LBKD_ENONFINITE = 2,     /* a coordinate is NaN or +-inf (builder.py:134-135) */
+    LBKD_ECAPACITY = 3,      /* n > 2^31-1, or n << dim_bits > 2^31-1 (widest) */
+    LBKD_ECUDA = 4,          /* CUDA runtime error (see lbkd_last_cuda_error) */
+    LBKD_ENOPEER = 5,        /* multi-device: no peer access */
+    LBKD_ENOMEM = 6,         /* device allocation failed */
+    LBKD_EUNSUPPORTED = 7    /* e.g. trace requested for a multi-CTA build */
+};
+
+#define LBKD_MAX_K 16
+
+typedef struct lbkd_ctx lbkd_ctx;
+
+int lbkd_create(lbkd_ctx **out, int device);
+void lbkd_destroy(lbkd_ctx *ctx);
+void lbkd_set_check(lbkd_ctx *ctx, int check_nonfinite);
+
+/* builder.build_round_robin(points, k) -- builder.py:200-236 */
+int lbkd_build_rr(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int64_t n, int k,
+                  uint32_t *d_perm, void *stream);
+
+/* widest.build_widest(points, k) -- widest.py:134-191 */
+int lbkd_build_widest(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int64_t n, int k,
+                      uint32_t *d_perm, uint8_t *d_split_dims, void *stream);
+
+/* Round-robin build that also records, for every sort level l, the order of
+ * the not-yet-final points after the sort: d_trace[l*n + p] = index (into
+ * d_points) of the point at working position p (the reference's array with
+ * the finalized prefix cut off).  This is what BuildRecorder(capture=True)
+ * needs (builder.py:63-105).  Only for n <= lbkd_single_cta_capacity(k). */
+int lbkd_build_rr_trace(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int64_t n, int k,
+                        uint32_t *d_perm, uint32_t *d_trace, void *stream);
+int lbkd_build_widest_trace(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int64_t n, int k,
+                            uint32_t *d_perm, uint8_t *d_split_dims, uint32_t *d_trace, void *stream);
+
+/* The accel plugin seam (accel.py:48-58): in-place tag refinement. */
+int lbkd_update_tags_rr(uint32_t *d_tags, int64_t n, int levels, int l, void *stream);
+int lbkd_update_tags_widest(uint32_t *d_tags, const double *d_coords, int k, uint8_t *d_split_dims,
+                            const double *d_world_lo, const double *d_world_hi, int64_t n, int levels,
+                            int l, int dim_bits, void *stream);
+
+int lbkd_num_levels(int64_t n);
+int64_t lbkd_single_cta_capacity(int k, int widest);
+/* Geometry chosen for (n, k, mode): subtree bits b (M = 2^b - 1 points per
+ * CTA), first in-CTA level lam0, number of global levels. */
+int lbkd_plan_info(int64_t n, int k, int widest, int *b, int *lam0);
+/* Kernel launches enqueued by the last build on this context. */
+int64_t lbkd_last_launch_count(const lbkd_ctx *ctx);
+const char *lbkd_strerror(int code);
+const char *lbkd_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

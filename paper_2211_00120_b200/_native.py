@@ -1,0 +1,122 @@
+"""ctypes binding of the in-tree C-ABI library (include/lbkd_b200.h).
+
+There is exactly one backend: the sm_100a CUDA library.  If it is missing or
+no CUDA device is present the build entry points raise -- there is no CPU
+fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "liblbkd_b200.so")
+
+LBKD_OK = 0
+LBKD_EINVAL_SHAPE = 1
+LBKD_ENONFINITE = 2
+LBKD_ECAPACITY = 3
+LBKD_ECUDA = 4
+LBKD_ENOPEER = 5
+LBKD_ENOMEM = 6
+LBKD_EUNSUPPORTED = 7
+
+EXPORTED = (
+    "lbkd_create", "lbkd_destroy", "lbkd_set_check",
+    "lbkd_build_rr", "lbkd_build_widest",
+    "lbkd_build_rr_trace", "lbkd_build_widest_trace",
+    "lbkd_update_tags_rr", "lbkd_update_tags_widest",
+    "lbkd_num_levels", "lbkd_single_cta_capacity", "lbkd_plan_info",
+    "lbkd_last_launch_count", "lbkd_strerror", "lbkd_last_cuda_error",
+)
+
+_lib = None
+_lock = threading.Lock()
+_ctxs: dict = {}
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        lib = load()
+        msg = lib.lbkd_strerror(code).decode()
+        if code == LBKD_ECUDA:
+            msg += ": " + lib.lbkd_last_cuda_error().decode()
+        super().__init__(f"{where}: {msg} (code {code})")
+        self.code = code
+
+
+def load():
+    """Load the library (building it first if this checkout has none)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            from . import build_native
+            build_native.build()
+        lib = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        lib.lbkd_create.argtypes = [ctypes.POINTER(vp), i32]
+        lib.lbkd_create.restype = i32
+        lib.lbkd_destroy.argtypes = [vp]
+        lib.lbkd_destroy.restype = None
+        lib.lbkd_set_check.argtypes = [vp, i32]
+        lib.lbkd_set_check.restype = None
+        lib.lbkd_build_rr.argtypes = [vp, vp, vp, i64, i32, vp, vp]
+        lib.lbkd_build_rr.restype = i32
+        lib.lbkd_build_widest.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp]
+        lib.lbkd_build_widest.restype = i32
+        lib.lbkd_build_rr_trace.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp]
+        lib.lbkd_build_rr_trace.restype = i32
+        lib.lbkd_build_widest_trace.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp, vp]
+        lib.lbkd_build_widest_trace.restype = i32
+        lib.lbkd_update_tags_rr.argtypes = [vp, i64, i32, i32, vp]
+        lib.lbkd_update_tags_rr.restype = i32
+        lib.lbkd_update_tags_widest.argtypes = [vp, vp, i32, vp, vp, vp, i64, i32, i32, i32, vp]
+        lib.lbkd_update_tags_widest.restype = i32
+        lib.lbkd_num_levels.argtypes = [i64]
+        lib.lbkd_num_levels.restype = i32
+        lib.lbkd_single_cta_capacity.argtypes = [i32, i32]
+        lib.lbkd_single_cta_capacity.restype = i64
+        lib.lbkd_plan_info.argtypes = [i64, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+        lib.lbkd_plan_info.restype = i32
+        lib.lbkd_last_launch_count.argtypes = [vp]
+        lib.lbkd_last_launch_count.restype = i64
+        lib.lbkd_strerror.argtypes = [i32]
+        lib.lbkd_strerror.restype = ctypes.c_char_p
+        lib.lbkd_last_cuda_error.argtypes = []
+        lib.lbkd_last_cuda_error.restype = ctypes.c_char_p
+        _lib = lib
+        return lib
+
+
+def context(device: int):
+    """One lbkd_ctx per (thread, device); contexts own the scratch buffers."""
+    key = (threading.get_ident(), int(device))
+    ctx = _ctxs.get(key)
+    if ctx is None:
+        lib = load()
+        p = ctypes.c_void_p()
+        rc = lib.lbkd_create(ctypes.byref(p), int(device))
+        if rc != LBKD_OK:
+            raise NativeError(rc, "lbkd_create")
+        ctx = p
+        _ctxs[key] = ctx
+    return ctx
+
+
+def check(rc: int, where: str) -> None:
+    if rc != LBKD_OK:
+        raise NativeError(rc, where)
+
+
+def plan_info(n: int, k: int, widest: bool):
+    lib = load()
+    b = ctypes.c_int()
+    lam0 = ctypes.c_int()
+    check(lib.lbkd_plan_info(int(n), int(k), int(widest), ctypes.byref(b), ctypes.byref(lam0)), "lbkd_plan_info")
+    return b.value, lam0.value

@@ -1,0 +1,326 @@
+// capi.cu -- C ABI and host orchestration (see include/lbkd_b200.h).
+//
+// One build = the reference's loop (builder.py:224-232) re-cut for B200:
+//   global levels l = 0 .. lam0-1  (segments larger than a CTA can hold)
+//       rekey+histogram -> plan -> up to 4 onesweep digit passes, the last
+//       one fused with updateTags (pivot -> node, others -> child segment)
+//   in-CTA levels lam0 .. L-2      (one CTA per level-lam0 subtree)
+//       subtree_kernel: all remaining levels in shared memory
+// Everything is enqueued on the caller's stream with device-side plans, so
+// the only host synchronisation is the final non-finite check.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include "../../include/lbkd_b200.h"
+#include "kernels.cuh"
+
+using namespace lbkd;
+
+namespace {
+thread_local char g_cuda_err[256] = "";
+
+void note_cuda(cudaError_t e) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+}  // namespace
+
+namespace lbkd {
+void launch_update_tags_rr(u32* tags, long long n, int levels, int l, cudaStream_t st);
+void launch_update_tags_widest(u32* tags, const double* coords, int k, uint8_t* split_dims, const double* wlo,
+                               const double* whi, long long n, int levels, int l, int dim_bits, cudaStream_t st);
+}
+
+struct lbkd_ctx {
+    int device = 0;
+    int check = 1;
+    u32 epoch = 1;
+    int64_t launches = 0;
+    // grow-only device allocations
+    size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_ptsb = 0, cap_k = 0;
+    Buffers bf{};
+    float* pts_copy = nullptr;
+    u32* perm_scratch = nullptr;
+    uint8_t* dims_scratch = nullptr;
+    u32* minmax = nullptr;
+    u32* h_err = nullptr;  // pinned
+};
+
+static int choose_bits(int k, int mode) {
+    const size_t limit = 227 * 1024;
+    for (int b = 13; b >= 10; --b)
+        if (subtree_smem_bytes(b, k, mode) <= limit) return b;
+    return -1;
+}
+
+#define CK(x)                                  \
+    do {                                       \
+        cudaError_t e_ = (x);                  \
+        if (e_ != cudaSuccess) {               \
+            note_cuda(e_);                     \
+            return LBKD_ECUDA;                 \
+        }                                      \
+    } while (0)
+
+template <typename T>
+static int grow(T*& p, size_t& cap_unused, size_t count) {
+    (void)cap_unused;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 256);
+    if (e != cudaSuccess) {
+        note_cuda(e);
+        p = nullptr;
+        return LBKD_ENOMEM;
+    }
+    return LBKD_OK;
+}
+
+static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0, bool need_pts_copy) {
+    size_t dummy = 0;
+    int rc;
+    if (n > c->cap_n) {
+        for (int i = 0; i < 2; ++i) {
+            if ((rc = grow(c->bf.keys[i], dummy, n))) return rc;
+            if ((rc = grow(c->bf.vals[i], dummy, n))) return rc;
+        }
+        if ((rc = grow(c->perm_scratch, dummy, n))) return rc;
+        if ((rc = grow(c->dims_scratch, dummy, n))) return rc;
+        c->cap_n = n;
+    }
+    size_t nseg = (size_t)1 << (lam0 > 0 ? lam0 : 0);
+    if (nseg > c->cap_seg || (size_t)k > c->cap_k) {
+        if ((rc = grow(c->bf.hist, dummy, nseg * 1024))) return rc;
+        if ((rc = grow(c->bf.seg_and, dummy, nseg))) return rc;
+        if ((rc = grow(c->bf.seg_or, dummy, nseg))) return rc;
+        for (int i = 0; i < 2; ++i)
+            if ((rc = grow(c->bf.boxes[i], dummy, nseg * 2 * (size_t)LBKD_MAX_K))) return rc;
+        c->cap_seg = nseg;
+        c->cap_k = LBKD_MAX_K;
+    }
+    size_t T = (size_t)1 << (b - 1);
+    size_t tiles = (n + T - 1) / T + 1;
+    if (tiles > c->cap_tiles) {
+        if ((rc = grow(c->bf.status, dummy, tiles * 256))) return rc;
+        // status words are epoch-tagged; zero once so no stale word can match
+        CK(cudaMemset(c->bf.status, 0, tiles * 256 * sizeof(u64)));
+        c->cap_tiles = tiles;
+    }
+    if (!c->bf.tile_ctr) {
+        if ((rc = grow(c->bf.tile_ctr, dummy, 4 * 64))) return rc;
+        if ((rc = grow(c->bf.plan, dummy, 1))) return rc;
+        if ((rc = grow(c->bf.err, dummy, 4))) return rc;
+        if ((rc = grow(c->minmax, dummy, 2 * LBKD_MAX_K))) return rc;
+        CK(cudaMallocHost(&c->h_err, sizeof(u32) * 4));
+    }
+    if (need_pts_copy && n * (u64)k > c->cap_ptsb) {
+        if ((rc = grow(c->pts_copy, dummy, n * (u64)k))) return rc;
+        c->cap_ptsb = n * (u64)k;
+    }
+    return LBKD_OK;
+}
+
+static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in, int k, u32* d_perm,
+                 uint8_t* d_dims, u32* d_trace, int mode, cudaStream_t st) {
+    if (!c || n_in < 0 || k < 1 || k > LBKD_MAX_K) return LBKD_EINVAL_SHAPE;
+    if (n_in > 0x7fffffffll) return LBKD_ECAPACITY;
+    if (mode == kWidest) {
+        int db = bit_length((u64)(k - 1));
+        if ((n_in << db) > 0x7fffffffll) return LBKD_ECAPACITY;
+    }
+    c->launches = 0;
+    if (n_in == 0) return LBKD_OK;
+    if (!d_points || !d_out) return LBKD_EINVAL_SHAPE;
+    CK(cudaSetDevice(c->device));
+    const u64 n = (u64)n_in;
+    const int b = choose_bits(k, mode);
+    if (b < 0) return LBKD_EINVAL_SHAPE;
+    const int L = bit_length(n);
+    const int lam0 = L - b > 0 ? L - b : 0;
+    if (d_trace && lam0 > 0) return LBKD_EUNSUPPORTED;
+    const bool inplace = (const void*)d_points == (const void*)d_out;
+    int rc = ensure(c, n, k, b, lam0, inplace);
+    if (rc) return rc;
+
+    BuildParams bp;
+    bp.n = n;
+    bp.k = k;
+    bp.mode = mode;
+    bp.b = b;
+    bp.pts = d_points;
+    if (inplace) {
+        CK(cudaMemcpyAsync(c->pts_copy, d_points, n * (u64)k * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        bp.pts = c->pts_copy;
+    }
+    bp.out_pts = d_out;
+    bp.perm = d_perm ? d_perm : c->perm_scratch;
+    bp.split_dims = d_dims ? d_dims : c->dims_scratch;
+    bp.dbg = d_trace;
+    Buffers& bf = c->bf;
+
+    CK(cudaMemsetAsync(bf.tile_ctr, 0, sizeof(u32) * 4 * 64, st));
+    CK(cudaMemsetAsync(bf.plan, 0, sizeof(LevelPlan), st));
+    CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
+    if (mode == kWidest) {
+        CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
+        CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
+        launch_world_bounds(bp, c->minmax, st);
+        launch_widest_root(bp, c->minmax, bf.boxes[0], st);
+        c->launches += 2;
+    }
+    int ctr = 0;
+    for (int l = 0; l < lam0; ++l) {
+        const u64 nseg = 1ull << l;
+        CK(cudaMemsetAsync(bf.hist, 0, nseg * 1024 * sizeof(u32), st));
+        CK(cudaMemsetAsync(bf.seg_and, 0xff, nseg * sizeof(u32), st));
+        CK(cudaMemsetAsync(bf.seg_or, 0, nseg * sizeof(u32), st));
+        launch_rekey_hist(bp, bf, l, st);
+        launch_plan(bp, bf, l, st);
+        c->launches += 2;
+        for (int p = 0; p < 4; ++p) {
+            launch_pass(bp, bf, l, p, c->epoch, bf.tile_ctr + (ctr++ % 256), st);
+            c->epoch = (c->epoch + 1) & 0x3fffffffu;
+            if (c->epoch == 0) c->epoch = 1;
+            c->launches += 1;
+        }
+        if (mode == kWidest) {
+            launch_widest_nodes(bp, l, bf.boxes[l & 1], bf.boxes[(l + 1) & 1], st);
+            c->launches += 1;
+        }
+    }
+    launch_subtree(bp, bf, lam0, st);
+    c->launches += 1;
+    CK(cudaGetLastError());
+    if (c->check) {
+        CK(cudaMemcpyAsync(c->h_err, bf.err, sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (c->h_err[0]) return LBKD_ENONFINITE;
+    }
+    return LBKD_OK;
+}
+
+extern "C" {
+
+int lbkd_create(lbkd_ctx** out, int device) {
+    if (!out) return LBKD_EINVAL_SHAPE;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        note_cuda(e);
+        return LBKD_ECUDA;
+    }
+    lbkd_ctx* c = new lbkd_ctx();
+    c->device = device;
+    *out = c;
+    return LBKD_OK;
+}
+
+void lbkd_destroy(lbkd_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(c->bf.keys[i]);
+        cudaFree(c->bf.vals[i]);
+        cudaFree(c->bf.boxes[i]);
+    }
+    cudaFree(c->bf.hist);
+    cudaFree(c->bf.seg_and);
+    cudaFree(c->bf.seg_or);
+    cudaFree(c->bf.status);
+    cudaFree(c->bf.tile_ctr);
+    cudaFree(c->bf.plan);
+    cudaFree(c->bf.err);
+    cudaFree(c->pts_copy);
+    cudaFree(c->perm_scratch);
+    cudaFree(c->dims_scratch);
+    cudaFree(c->minmax);
+    if (c->h_err) cudaFreeHost(c->h_err);
+    delete c;
+}
+
+void lbkd_set_check(lbkd_ctx* c, int check) {
+    if (c) c->check = check ? 1 : 0;
+}
+
+int lbkd_build_rr(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n, int k, uint32_t* d_perm,
+                  void* stream) {
+    return build(c, d_points, d_out, n, k, d_perm, nullptr, nullptr, kRoundRobin, (cudaStream_t)stream);
+}
+
+int lbkd_build_widest(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n, int k, uint32_t* d_perm,
+                      uint8_t* d_dims, void* stream) {
+    return build(c, d_points, d_out, n, k, d_perm, d_dims, nullptr, kWidest, (cudaStream_t)stream);
+}
+
+int lbkd_build_rr_trace(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n, int k, uint32_t* d_perm,
+                        uint32_t* d_trace, void* stream) {
+    if (!d_trace) return LBKD_EINVAL_SHAPE;
+    return build(c, d_points, d_out, n, k, d_perm, nullptr, d_trace, kRoundRobin, (cudaStream_t)stream);
+}
+
+int lbkd_build_widest_trace(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n, int k,
+                            uint32_t* d_perm, uint8_t* d_dims, uint32_t* d_trace, void* stream) {
+    if (!d_trace) return LBKD_EINVAL_SHAPE;
+    return build(c, d_points, d_out, n, k, d_perm, d_dims, d_trace, kWidest, (cudaStream_t)stream);
+}
+
+int lbkd_update_tags_rr(uint32_t* d_tags, int64_t n, int levels, int l, void* stream) {
+    if (!d_tags || n < 1 || l < 0 || l > levels - 2) return LBKD_EINVAL_SHAPE;
+    launch_update_tags_rr(d_tags, n, levels, l, (cudaStream_t)stream);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        note_cuda(e);
+        return LBKD_ECUDA;
+    }
+    return LBKD_OK;
+}
+
+int lbkd_update_tags_widest(uint32_t* d_tags, const double* d_coords, int k, uint8_t* d_split_dims,
+                            const double* d_world_lo, const double* d_world_hi, int64_t n, int levels, int l,
+                            int dim_bits, void* stream) {
+    if (!d_tags || !d_coords || !d_split_dims || n < 1 || k < 1 || k > LBKD_MAX_K || l < 0 || l > levels - 2)
+        return LBKD_EINVAL_SHAPE;
+    launch_update_tags_widest(d_tags, d_coords, k, d_split_dims, d_world_lo, d_world_hi, n, levels, l, dim_bits,
+                              (cudaStream_t)stream);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        note_cuda(e);
+        return LBKD_ECUDA;
+    }
+    return LBKD_OK;
+}
+
+int lbkd_num_levels(int64_t n) { return n > 0 ? bit_length((u64)n) : 0; }
+
+int64_t lbkd_single_cta_capacity(int k, int widest) {
+    int b = choose_bits(k, widest ? kWidest : kRoundRobin);
+    return b < 0 ? 0 : ((int64_t)1 << b) - 1;
+}
+
+int lbkd_plan_info(int64_t n, int k, int widest, int* b_out, int* lam0_out) {
+    if (k < 1 || k > LBKD_MAX_K || n < 0) return LBKD_EINVAL_SHAPE;
+    int b = choose_bits(k, widest ? kWidest : kRoundRobin);
+    int L = n > 0 ? bit_length((u64)n) : 0;
+    if (b_out) *b_out = b;
+    if (lam0_out) *lam0_out = L - b > 0 ? L - b : 0;
+    return LBKD_OK;
+}
+
+int64_t lbkd_last_launch_count(const lbkd_ctx* c) { return c ? c->launches : 0; }
+
+const char* lbkd_strerror(int code) {
+    switch (code) {
+        case LBKD_OK: return "ok";
+        case LBKD_EINVAL_SHAPE: return "invalid shape or argument";
+        case LBKD_ENONFINITE: return "coordinates must be finite (no NaN or infinity)";
+        case LBKD_ECAPACITY: return "points exceed the 32-bit tag capacity";
+        case LBKD_ECUDA: return "CUDA error";
+        case LBKD_ENOPEER: return "peer access unavailable";
+        case LBKD_ENOMEM: return "device allocation failed";
+        case LBKD_EUNSUPPORTED: return "unsupported request";
+        default: return "unknown error";
+    }
+}
+
+const char* lbkd_last_cuda_error(void) { return g_cuda_err; }
+
+}  // extern "C"

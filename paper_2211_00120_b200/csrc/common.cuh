@@ -1,0 +1,189 @@
+// common.cuh -- shared device helpers for the B200 k-d tree builder.
+//
+// Implicit-tree arithmetic restated from the reference
+//   /root/reference/pkg/src/lbkd/treemath.py:46-140 (level, num_levels,
+//   subtree_size, segment_begin, pivot_pos) and the fused pivot formula of
+//   kernels_numpy._pivot_positions (kernels_numpy.py:21-38).
+//
+// Working-array convention: at level l
+// the working array W_l holds only the N - F(l) points that are not yet
+// final (F(l) = 2^l - 1), grouped by level-l node.  Segment j (node
+// F(l) + j) starts at bw(j) = segment_begin(F(l)+j) - F(l); finalized nodes
+// are written straight to the output, so W_l is the reference's array with
+// the finalized prefix cut off.
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+namespace lbkd {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr u32 kFullMask = 0xffffffffu;
+
+// Order-preserving map float32 -> uint32 with -0.0 canonicalised to +0.0.
+// numpy compares the float64-promoted values, for which -0.0 == +0.0 and the
+// stable sort keeps such pairs in current order.
+__host__ __device__ __forceinline__ u32 float_bits(float f) {
+#ifdef __CUDA_ARCH__
+    return __float_as_uint(f);
+#else
+    u32 u;
+    memcpy(&u, &f, 4);
+    return u;
+#endif
+}
+
+__host__ __device__ __forceinline__ float bits_float(u32 u) {
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(u);
+#else
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+#endif
+}
+
+__host__ __device__ __forceinline__ u32 flip_key(float f) {
+    u32 u = float_bits(f);
+    if (u == 0x80000000u) u = 0u;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__host__ __device__ __forceinline__ float unflip_key(u32 k) {
+    u32 u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    return bits_float(u);
+}
+
+// Geometry of one level of the implicit left-balanced tree.
+struct LevelGeom {
+    int l;        // level being split
+    int L;        // num_levels(N) = bit_length(N)
+    int sh;       // L - l - 1 (log2 of bottom-level slots per level-l subtree)
+    u64 n;        // N
+    u64 B;        // bottom_have = N - F(L-1)
+    u64 Fl;       // F(l) = 2^l - 1 (finalized nodes before level l)
+    u64 nl;       // N - F(l): elements in W_l
+    u64 nseg;     // 2^l segments
+};
+
+__host__ __device__ inline int bit_length(u64 v) {
+    int b = 0;
+    while (v) { ++b; v >>= 1; }
+    return b;
+}
+
+__host__ __device__ inline LevelGeom make_geom(u64 n, int l) {
+    LevelGeom g;
+    g.n = n;
+    g.L = bit_length(n);
+    g.l = l;
+    g.sh = g.L - l - 1;
+    g.B = n - ((1ull << (g.L - 1)) - 1ull);
+    g.Fl = (1ull << l) - 1ull;
+    g.nl = n - g.Fl;
+    g.nseg = 1ull << l;
+    return g;
+}
+
+// size of segment j (treemath.subtree_size, treemath.py:85-98)
+__host__ __device__ __forceinline__ u64 seg_size(const LevelGeom& g, u64 j) {
+    u64 w = 1ull << g.sh;
+    u64 lo = j << g.sh;
+    u64 on = g.B > lo ? g.B - lo : 0ull;
+    if (on > w) on = w;
+    return w - 1ull + on;
+}
+
+// begin of segment j inside W_l (treemath.segment_begin, treemath.py:108-126,
+// minus the F(l) finalized prefix)
+__host__ __device__ __forceinline__ u64 seg_begin(const LevelGeom& g, u64 j) {
+    u64 lo = j << g.sh;
+    return j * ((1ull << g.sh) - 1ull) + (lo < g.B ? lo : g.B);
+}
+
+// offset of the pivot inside segment j = size of the left child's subtree
+// (treemath.pivot_pos, treemath.py:129-140; kernels_numpy.py:33-38)
+__host__ __device__ __forceinline__ u64 pivot_off(const LevelGeom& g, u64 j) {
+    if (g.sh <= 0) return 0ull;
+    u64 cw = 1ull << (g.sh - 1);
+    u64 lo = (2ull * j) * cw;
+    u64 on = g.B > lo ? g.B - lo : 0ull;
+    if (on > cw) on = cw;
+    return cw - 1ull + on;
+}
+
+// segment containing W_l position p (inverse of seg_begin); O(1) with two
+// integer divisions -- evaluated once per tile, not per element.
+__host__ __device__ inline u64 seg_of(const LevelGeom& g, u64 p) {
+    u64 full = (2ull << g.sh) - 1ull;
+    u64 nf = g.B >> g.sh;
+    if (nf > g.nseg) nf = g.nseg;
+    u64 p1 = nf * full;
+    if (p < p1) return p / full;
+    u64 rem = g.B - (nf << g.sh);
+    u64 small = (1ull << g.sh) - 1ull;
+    u64 ps = small + rem;
+    u64 q = p - p1;
+    if (q < ps || small == 0) return nf;
+    return nf + 1ull + (q - ps) / small;
+}
+
+// ---- PTX helpers -----------------------------------------------------------
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
+    u64 v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled-lookback status word: [63:34] epoch, [33:32] flag, [31:0] count
+constexpr u64 kFlagAgg = 1ull;
+constexpr u64 kFlagInc = 2ull;
+__device__ __forceinline__ u64 pack_status(u32 epoch, u64 flag, u32 count) {
+    return ((u64)epoch << 34) | (flag << 32) | (u64)count;
+}
+
+// Exclusive block scan over blockDim.x values (blockDim.x multiple of 32,
+// at most 1024).  `warp_tot` must hold 32 entries.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        T t = lane < nw ? warp_tot[lane] : T(0);
+        T s = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(kFullMask, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) warp_tot[lane] = s - t;
+        if (lane == 31 && total) *total = s;
+    }
+    __syncthreads();
+    T r = x - v + warp_tot[warp];
+    __syncthreads();
+    return r;
+}
+
+}  // namespace lbkd

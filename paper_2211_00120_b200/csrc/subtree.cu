@@ -1,0 +1,328 @@
+// subtree.cu -- finish every level-lam0 subtree inside one CTA's shared
+// memory.  Once a subtree holds at most M = 2^b - 1 points (b = 13 for k <= 4)
+// all of its remaining levels (lam0 .. L-2) run without touching HBM: the
+// points are gathered once into shared memory, every level runs the same
+// stable (segment, coordinate) sort + updateTags split as the global levels
+// (builder.py:224-232 / widest.py:172-183), and each finished node is written
+// to its level-order slot exactly once.
+//
+// Per level, per CTA:
+//   keys: order-flipped coordinate in the split dimension of the element's
+//         node (RR: l mod k; widest: that node's dims, computed below)
+//   sort: LSD 8-bit digit passes over the key (digits constant across the
+//         whole subtree are skipped), then over the local segment id, each a
+//         stable block-wide pass ranked with warp match/ballot counters
+//   split: the element at each segment's pivot offset (kernels_numba.py:
+//         21-46 arithmetic) is the node; the rest move, compacted, into the
+//         child segments
+//   widest: child split dims = first argmax of the float64 widths of the
+//         clipped domain box (kernels_numba.py:80-110), by walking the
+//         in-CTA ancestors' (dim, plane) pairs up to the subtree root box
+#include "kernels.cuh"
+
+namespace lbkd {
+
+constexpr int kSubThreads = 1024;
+constexpr int kSubWarps = kSubThreads / 32;
+constexpr int kMaxRounds = 8;  // M <= 8191 -> at most 8 rounds of 1024
+constexpr int kMaxK = 16;
+
+struct SubtreeArgs {
+    u64 n;
+    int L, lam0, k, mode, M;
+    const u32* vals[2];
+    const LevelPlan* plan;
+    int identity_vals;
+    const float* pts;
+    float* out_pts;
+    u32* perm;
+    uint8_t* split_dims;
+    const float* boxes0;  // widest: boxes of level-lam0 nodes [nseg][2k]
+    u32* dbg;
+};
+
+size_t subtree_smem_bytes(int b, int k, int mode) {
+    size_t M = ((size_t)1 << b) - 1;
+    size_t bytes = 0;
+    bytes += sizeof(float) * (size_t)k * M;           // P (SoA)
+    bytes += 2 * sizeof(u32) * M;                       // E0, E1
+    bytes += sizeof(unsigned short) * kSubWarps * 256;  // per-warp counters
+    bytes += sizeof(u32) * 4 * 256;                     // group sums
+    bytes += sizeof(u32) * 64;                          // scratch
+    if (mode == kWidest) bytes += M * (sizeof(float) + 1) + 2 * kMaxK * sizeof(float);
+    return (bytes + 15) & ~(size_t)15;
+}
+
+// One stable block-wide counting pass: Eout[rank(e)] = e for the m elements
+// of Ein, ranked by digit(e) in 0..255 with ties kept in Ein order.
+template <typename DigitFn>
+__device__ __forceinline__ void block_pass(const u32* __restrict__ Ein, u32* __restrict__ Eout, int m,
+                                           DigitFn digit, unsigned short (*cnt)[256], u32 (*gsum)[256],
+                                           u32* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const int C = ((m + kSubThreads - 1) / kSubThreads) * 32;  // per-warp chunk
+    const int R = C / 32;
+    for (int i = tid; i < kSubWarps * 256 / 2; i += kSubThreads) reinterpret_cast<u32*>(&cnt[0][0])[i] = 0u;
+    __syncthreads();
+    const u32 lt = lanemask_lt();
+    u32 ev[kMaxRounds];
+    u32 dr[kMaxRounds];  // digit << 16 | warp-local rank
+#pragma unroll
+    for (int r = 0; r < kMaxRounds; ++r) {
+        if (r < R) {
+            int p = warp * C + r * 32 + lane;
+            bool valid = p < m;
+            u32 e = valid ? Ein[p] : 0u;
+            u32 d = valid ? digit(e) : (0x1000u | lane);
+            u32 peers = __match_any_sync(kFullMask, d);
+            int leader = __ffs(peers) - 1;
+            u32 c = 0;
+            if (lane == leader && valid) {
+                c = cnt[warp][d];
+                cnt[warp][d] = (unsigned short)(c + __popc(peers));
+            }
+            c = __shfl_sync(kFullMask, c, leader);
+            ev[r] = e;
+            dr[r] = ((d & 255u) << 16) | (c + __popc(peers & lt));
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // warp prefixes per digit: 4 groups of 8 warps walk the counter columns
+    {
+        const int d = tid & 255, grp = tid >> 8;
+        u32 s = 0;
+#pragma unroll
+        for (int w = grp * 8; w < grp * 8 + 8; ++w) {
+            u32 c = cnt[w][d];
+            cnt[w][d] = (unsigned short)s;
+            s += c;
+        }
+        gsum[grp][d] = s;
+    }
+    __syncthreads();
+    if (tid < 256) {
+        u32 g0 = gsum[0][tid], g1 = gsum[1][tid], g2 = gsum[2][tid], g3 = gsum[3][tid];
+        u32 tot = g0 + g1 + g2 + g3;
+        // exclusive scan over 256 digit totals within the first 8 warps
+        u32 x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 y = __shfl_up_sync(kFullMask, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) scratch[warp] = x;
+        asm volatile("bar.sync 1, 256;");
+        u32 wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += scratch[w];
+        u32 base = wpre + x - tot;
+        gsum[0][tid] = base;
+        gsum[1][tid] = base + g0;
+        gsum[2][tid] = base + g0 + g1;
+        gsum[3][tid] = base + g0 + g1 + g2;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kMaxRounds; ++r) {
+        if (r < R) {
+            int p = warp * C + r * 32 + lane;
+            if (p < m) {
+                u32 d = dr[r] >> 16;
+                u32 slot = gsum[warp >> 3][d] + cnt[warp][d] + (dr[r] & 0xffffu);
+                Eout[slot] = ev[r];
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M = a.M, k = a.k, tid = threadIdx.x;
+    unsigned char* sp = smem_raw;
+    float* P = reinterpret_cast<float*>(sp);
+    sp += sizeof(float) * (size_t)k * M;
+    u32* E[2];
+    E[0] = reinterpret_cast<u32*>(sp);
+    sp += sizeof(u32) * M;
+    E[1] = reinterpret_cast<u32*>(sp);
+    sp += sizeof(u32) * M;
+    unsigned short(*cnt)[256] = reinterpret_cast<unsigned short(*)[256]>(sp);
+    sp += sizeof(unsigned short) * kSubWarps * 256;
+    u32(*gsum)[256] = reinterpret_cast<u32(*)[256]>(sp);
+    sp += sizeof(u32) * 4 * 256;
+    u32* scratch = reinterpret_cast<u32*>(sp);
+    sp += sizeof(u32) * 64;
+    float* nplane = nullptr;
+    float* rootbox = nullptr;
+    unsigned char* ndim = nullptr;
+    if (a.mode == kWidest) {
+        nplane = reinterpret_cast<float*>(sp);
+        sp += sizeof(float) * M;
+        rootbox = reinterpret_cast<float*>(sp);
+        sp += sizeof(float) * 2 * kMaxK;
+        ndim = sp;
+    }
+
+    const u64 j = blockIdx.x;
+    const LevelGeom g0 = make_geom(a.n, a.lam0);
+    const u64 base = a.lam0 == 0 ? 0ull : seg_begin(g0, j);
+    const int m = (int)(a.lam0 == 0 ? a.n : seg_size(g0, j));
+    const u32* vin = a.identity_vals ? nullptr : a.vals[a.plan->next_sel] + base;
+
+    // gather the subtree's points (one HBM read per point for all levels)
+    for (int lid = tid; lid < m; lid += kSubThreads) {
+        u32 idx = vin ? vin[lid] : (u32)lid;
+        const float* q = a.pts + (u64)idx * k;
+        for (int c = 0; c < k; ++c) P[c * M + lid] = __ldg(q + c);
+        E[0][lid] = (u32)lid;
+    }
+    if (a.mode == kWidest) {
+        if (tid < 2 * k) rootbox[tid] = a.boxes0[j * 2ull * k + tid];
+        if (tid == 0) ndim[0] = a.split_dims[g0.Fl + j];
+    }
+    __syncthreads();
+
+    auto write_node = [&](u64 node, u32 lid) {
+        a.perm[node] = vin ? vin[lid] : lid;
+        float* dst = a.out_pts + node * (u64)k;
+        for (int c = 0; c < k; ++c) dst[c] = P[c * M + lid];
+    };
+
+    int cur = 0;
+    for (int lam = a.lam0; lam <= a.L - 2; ++lam) {
+        const LevelGeom g = make_geom(a.n, lam);
+        const int dl = lam - a.lam0;
+        const u64 nloc = 1ull << dl;
+        const u64 J0 = j << dl;
+        const u64 lb0 = seg_begin(g, J0);
+        const int mc = m - (int)(nloc - 1);
+        const int dim_rr = lam % k;
+        const u32 nb = (u32)(nloc - 1);  // local node index of segment 0
+
+        auto key_of = [&](u32 e) -> u32 {
+            u32 lid = e & 0xffffu;
+            int d = (a.mode == kWidest) ? (int)ndim[nb + (e >> 16)] : dim_rr;
+            return flip_key(P[d * M + lid]);
+        };
+
+        // digits constant over the whole subtree are skipped
+        u32 x_and = 0xffffffffu, x_or = 0u;
+        for (int p = tid; p < mc; p += kSubThreads) {
+            u32 kk = key_of(E[cur][p]);
+            x_and &= kk;
+            x_or |= kk;
+        }
+        x_and = __reduce_and_sync(kFullMask, x_and);
+        x_or = __reduce_or_sync(kFullMask, x_or);
+        if ((tid & 31) == 0) { scratch[32 + (tid >> 5)] = x_and ^ x_or; }
+        __syncthreads();
+        u32 vary = 0;
+        for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
+        __syncthreads();
+
+        bool moved = false;
+        for (int q = 0; q < 4; ++q) {
+            if (((vary >> (8 * q)) & 255u) == 0) continue;
+            const int sh = 8 * q;
+            block_pass(E[cur], E[cur ^ 1], mc, [&](u32 e) { return (key_of(e) >> sh) & 255u; }, cnt, gsum,
+                       scratch);
+            cur ^= 1;
+            moved = true;
+        }
+        if (moved && dl > 0) {
+            for (int q = 0; q * 8 < dl; ++q) {
+                const int sh = 16 + 8 * q;
+                block_pass(E[cur], E[cur ^ 1], mc, [&](u32 e) { return (e >> sh) & 255u; }, cnt, gsum, scratch);
+                cur ^= 1;
+            }
+        }
+        if (a.dbg) {
+            for (int p = tid; p < mc; p += kSubThreads) a.dbg[(u64)lam * a.n + lb0 + p] = E[cur][p] & 0xffffu;
+        }
+
+        // split: pivots become nodes, the rest move into the child segments
+        const bool last = (lam == a.L - 2);
+        const LevelGeom gn = make_geom(a.n, lam + 1);
+        for (int p = tid; p < mc; p += kSubThreads) {
+            u32 e = E[cur][p];
+            u32 t = e >> 16, lid = e & 0xffffu;
+            u64 J = J0 + t;
+            u64 o = lb0 + (u64)p - seg_begin(g, J);
+            u64 po = pivot_off(g, J);
+            if (o == po) {
+                write_node(g.Fl + J, lid);
+                if (a.mode == kWidest) nplane[nb + t] = P[(int)ndim[nb + t] * M + lid];
+                continue;
+            }
+            u32 right = o > po ? 1u : 0u;
+            if (last) {
+                write_node(gn.Fl + 2 * J + right, lid);
+                continue;
+            }
+            E[cur ^ 1][p - (int)t - (int)right] = ((2u * t + right) << 16) | lid;
+        }
+        cur ^= 1;
+        __syncthreads();
+
+        if (a.mode == kWidest) {
+            // split dims of the children (level lam+1 nodes of this subtree)
+            const u32 nch = (u32)(2 * nloc);
+            const u32 cb = (u32)(2 * nloc - 1);  // local index of the first child
+            for (u32 c = tid; c < nch; c += kSubThreads) {
+                u64 gnode = gn.Fl + 2 * J0 + c;
+                if (gnode >= a.n) continue;
+                float lo[kMaxK], hi[kMaxK];
+                for (int d = 0; d < k; ++d) { lo[d] = rootbox[d]; hi[d] = rootbox[k + d]; }
+                u32 u = cb + c;
+                while (u > 0) {
+                    u32 par = (u - 1) >> 1;
+                    int dp = ndim[par];
+                    float pl = nplane[par];
+                    if (u & 1u) { if (pl < hi[dp]) hi[dp] = pl; }
+                    else { if (pl > lo[dp]) lo[dp] = pl; }
+                    u = par;
+                }
+                int best = 0;
+                double bw = (double)hi[0] - (double)lo[0];
+                for (int d = 1; d < k; ++d) {
+                    double w = (double)hi[d] - (double)lo[d];
+                    if (w > bw) { bw = w; best = d; }
+                }
+                ndim[cb + c] = (unsigned char)best;
+                a.split_dims[gnode] = (uint8_t)best;
+            }
+            __syncthreads();
+        }
+    }
+    if (a.lam0 > a.L - 2) {
+        // the subtree root is a bottom-level node (only when L - 1 == lam0)
+        if (tid == 0 && m == 1) write_node(g0.Fl + j, 0u);
+    }
+}
+
+void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStream_t st) {
+    SubtreeArgs a;
+    a.n = bp.n;
+    a.L = bit_length(bp.n);
+    a.lam0 = lam0;
+    a.k = bp.k;
+    a.mode = bp.mode;
+    a.M = (1 << bp.b) - 1;
+    a.vals[0] = bf.vals[0];
+    a.vals[1] = bf.vals[1];
+    a.plan = bf.plan;
+    a.identity_vals = lam0 == 0;
+    a.pts = bp.pts;
+    a.out_pts = bp.out_pts;
+    a.perm = bp.perm;
+    a.split_dims = bp.split_dims;
+    a.boxes0 = bf.boxes[lam0 & 1];
+    a.dbg = bp.dbg;
+    size_t sm = subtree_smem_bytes(bp.b, bp.k, bp.mode);
+    cudaFuncSetAttribute(subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    unsigned grid = (unsigned)(1ull << lam0);
+    subtree_kernel<<<grid, kSubThreads, sm, st>>>(a);
+}
+
+}  // namespace lbkd

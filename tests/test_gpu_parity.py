@@ -1,0 +1,211 @@
+"""GPU parity: the CUDA build against the reference's golden vectors and the
+CPU oracle (oracle/), bit-exact, through the public API and the C-ABI."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from tests.golden_util import GOLDEN, gen_case, small_cases
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2211_00120_b200 as kd  # noqa: E402
+from paper_2211_00120_b200 import BuildRecorder, build_round_robin, build_widest  # noqa: E402
+from paper_2211_00120_b200 import datagen  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gpu_rr(pts):
+    d = torch.from_numpy(np.ascontiguousarray(pts, dtype=np.float32)).cuda()
+    out, perm = kd.build_round_robin_cuda(d)
+    return out.cpu().numpy(), perm.cpu().numpy().view(np.uint32)
+
+
+def gpu_widest(pts):
+    d = torch.from_numpy(np.ascontiguousarray(pts, dtype=np.float32)).cuda()
+    out, perm, dims = kd.build_widest_cuda(d)
+    return out.cpu().numpy(), perm.cpu().numpy().view(np.uint32), dims.cpu().numpy()
+
+
+def test_walkthrough_every_phase():
+    g = np.load(os.path.join(GOLDEN, "walkthrough.npz"))
+    rec = BuildRecorder(capture=True)
+    tree = build_round_robin(g["points"], recorder=rec)
+    assert len(rec.snapshots) == g["tags"].shape[0]
+    for i, snap in enumerate(rec.snapshots):
+        assert snap.event == str(g["events"][i])
+        assert snap.iteration == int(g["iterations"][i])
+        assert snap.tags.tolist() == g["tags"][i].tolist(), i
+        assert np.array_equal(snap.coords, g["coords"][i].astype(np.float64)), i
+    assert tree.coords[:, 0].tolist() == [46, 15, 53, 40, 44, 68, 62, 10, 45, 25]
+    assert tree.coords[:, 1].tolist() == [63, 43, 67, 33, 58, 21, 69, 15, 40, 54]
+    assert rec.sort_phases == 4 and rec.update_phases == 3 and rec.tag_bytes == 40
+
+
+def test_small_golden_cases_bit_exact():
+    for case in small_cases():
+        pts = gen_case(case)
+        if case["mode"] == "rr":
+            out, perm = gpu_rr(pts)
+            assert np.array_equal(perm, case["perm"]), case["name"]
+        else:
+            out, perm, dims = gpu_widest(pts)
+            assert np.array_equal(perm, case["perm"]), case["name"]
+            assert np.array_equal(dims, case["split_dims"]), case["name"]
+        assert np.array_equal(out, pts[case["perm"].astype(np.int64)]), case["name"]
+
+
+def _hash_cases(max_n):
+    h = json.load(open(os.path.join(GOLDEN, "hashes.json")))
+    return [v for v in h.values() if v["n"] <= max_n]
+
+
+@pytest.mark.parametrize("case", _hash_cases(10**9), ids=lambda c: f"{c['mode']}-{c['kind']}-{c['n']}-k{c['k']}")
+def test_golden_hashes(case):
+    pts = gen_case(case)
+    assert sha(pts) == case["input_sha256"]
+    if case["mode"] == "rr":
+        out, perm = gpu_rr(pts)
+    else:
+        out, perm, dims = gpu_widest(pts)
+        assert sha(dims) == case["split_dims_sha256"]
+    assert perm[:64].tolist() == case["perm_head"]
+    assert sha(perm) == case["perm_sha256"]
+    # the reordered points are the input rows in node order
+    step = max(1, len(perm) // 100000)
+    assert np.array_equal(out[::step], pts[perm[::step].astype(np.int64)])
+
+
+SIZES = [1, 2, 3, 7, 8, 100, 4095, 8191, 8192, 8193, 12287, 16383, 16384, 16385, 40000, 65535, 65536, 65537,
+         131071, 200003, 262144, 300001, 524287, 1 << 20]
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_rr_vs_oracle_sizes(n):
+    rng = np.random.default_rng(n)
+    for kind in ("uniform", "ties", "clustered", "signed_zero"):
+        k = int(rng.integers(1, 6))
+        pts = datagen.make(kind, n, k, seed=n + k)
+        _, perm = gpu_rr(pts)
+        assert np.array_equal(perm, oracle.build_rr(pts)), (kind, n, k)
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_widest_vs_oracle_sizes(n):
+    rng = np.random.default_rng(n + 1)
+    for kind in ("uniform", "ties", "clustered"):
+        k = int(rng.integers(1, 6))
+        pts = datagen.make(kind, n, k, seed=n + 2 * k)
+        _, perm, dims = gpu_widest(pts)
+        want_perm, want_dims = oracle.build_widest(pts)
+        assert np.array_equal(perm, want_perm), (kind, n, k)
+        assert np.array_equal(dims, want_dims), (kind, n, k)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6, 8, 12, 16])
+def test_all_dimension_counts(k):
+    for n in (5000, 70001):
+        pts = datagen.ties(n, k, seed=k)
+        _, perm = gpu_rr(pts)
+        assert np.array_equal(perm, oracle.build_rr(pts)), (n, k)
+        _, perm, dims = gpu_widest(pts)
+        wp, wd = oracle.build_widest(pts)
+        assert np.array_equal(perm, wp), (n, k)
+        assert np.array_equal(dims, wd), (n, k)
+
+
+def test_in_place_and_payload():
+    pts = datagen.uniform(50000, 3, seed=9)
+    d = torch.from_numpy(pts).cuda()
+    ref = oracle.build_rr(pts)
+    out, perm = kd.build_round_robin_cuda(d, out=d)  # in place
+    assert out.data_ptr() == d.data_ptr()
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
+    assert np.array_equal(d.cpu().numpy(), pts[ref.astype(np.int64)])
+    payload = np.arange(50000, dtype=np.int64) * 7 + 3
+    tree = build_round_robin(pts, 3, payload=payload)
+    assert np.array_equal(tree.payload, payload[ref.astype(np.int64)])
+    assert tree.coords.dtype == np.float64
+
+
+def test_edge_cases_and_validation():
+    empty = build_round_robin(np.empty((0, 2), dtype=np.float32), 2)
+    assert empty.n == 0 and empty.k == 2 and empty.levels == 0
+    one = build_round_robin(np.array([[3.5, 2.5]], dtype=np.float32), 2)
+    assert one.coords.tolist() == [[3.5, 2.5]] and one.payload.tolist() == [0]
+    t = build_round_robin([5.0, 1.0, 9.0])
+    assert t.coords[:, 0].tolist() == [5.0, 1.0, 9.0]
+    w = build_widest(np.array([[2.0, 9.0]], dtype=np.float32), 2)
+    assert w.split_dims.tolist() == [0]
+    ew = build_widest(np.empty((0, 4), dtype=np.float32), 4)
+    assert ew.split_dims.shape == (0,)
+    same = build_round_robin(np.full((25, 3), 4.25, dtype=np.float32), 3)
+    assert sorted(same.payload.tolist()) == list(range(25))
+    # reference hand cases (tests/test_verify.py:9-25)
+    assert build_round_robin([[5.0], [1.0]]).coords[:, 0].tolist() == [5.0, 1.0]
+    assert build_round_robin([[3.0], [1.0], [7.0], [5.0]]).coords[:, 0].tolist() == [5.0, 3.0, 7.0, 1.0]
+    with pytest.raises(ValueError):
+        build_round_robin(np.array([[1.0], [np.nan]], dtype=np.float32))
+    # the device flag catches non-finite input that skips host validation
+    bad = torch.tensor([[1.0, 2.0], [float("inf"), 0.0]] * 5000, device="cuda")
+    with pytest.raises(ValueError, match="finite"):
+        kd.build_round_robin_cuda(bad)
+    with pytest.raises(ValueError):
+        build_widest(np.broadcast_to(np.zeros((1, 3), dtype=np.float32), (2**29, 3)))
+
+
+def test_recorder_counts():
+    for n in (1, 2, 3, 10, 100, 1000, 20000):
+        rec = BuildRecorder()
+        build_round_robin(datagen.uniform(n, 2, seed=n), 2, recorder=rec)
+        L = n.bit_length()
+        assert (rec.sort_phases, rec.update_phases, rec.tag_entries, rec.tag_itemsize) == (L, L - 1, n, 4)
+
+
+def test_widest_recorder_capture_matches_oracle_dims():
+    pts = datagen.uniform(300, 3, seed=4)
+    rec = BuildRecorder(capture=True)
+    tree = build_widest(pts, 3, recorder=rec)
+    wp, wd = oracle.build_widest(pts)
+    assert np.array_equal(tree.payload, wp.astype(np.int64))
+    assert np.array_equal(tree.split_dims, wd)
+    assert len(rec.snapshots) == 2 * (300).bit_length()
+
+
+def test_plugin_seam_update_kernels_match_oracle_trace():
+    from paper_2211_00120_b200 import _native
+
+    lib = _native.load()
+    pts = datagen.ties(3000, 3, seed=1)
+    perm, tags, idx = oracle.build_rr(pts, trace=True)
+    n = 3000
+    L = n.bit_length()
+    for l in range(L - 1):
+        before = tags[1 + 2 * l]  # after sort l
+        after = tags[2 + 2 * l]   # after update l
+        d = torch.from_numpy(before.view(np.int32).copy()).cuda()
+        rc = lib.lbkd_update_tags_rr(d.data_ptr(), n, L, l, None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), after), l
+
+
+def test_check_valid_at_scale():
+    for kind in ("uniform", "clustered"):
+        pts = datagen.make(kind, 4_000_000, 3, seed=11)
+        out, perm = gpu_rr(pts)
+        assert np.array_equal(np.sort(perm), np.arange(len(perm), dtype=np.uint32))
+        assert oracle.check_valid(out)
+        out, perm, dims = gpu_widest(pts)
+        assert oracle.check_valid(out, dims)
