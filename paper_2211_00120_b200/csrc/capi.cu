@@ -37,7 +37,7 @@ struct lbkd_ctx {
     u32 epoch = 1;
     int64_t launches = 0;
     // grow-only device allocations
-    size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_ptsb = 0, cap_k = 0;
+    size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_w = 0, cap_copy = 0;
     Buffers bf{};
     float* pts_copy = nullptr;
     u32* perm_scratch = nullptr;
@@ -76,27 +76,32 @@ static int grow(T*& p, size_t& cap_unused, size_t count) {
     return LBKD_OK;
 }
 
-static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0, bool need_pts_copy) {
+static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
     size_t dummy = 0;
     int rc;
+    // W[2] holds k+1 SoA arrays of n words each (only when global levels run)
+    size_t need_w = lam0 > 0 ? (size_t)(k + 1) * n : 0;
+    if (need_w > c->cap_w) {
+        for (int i = 0; i < 2; ++i)
+            if ((rc = grow(c->bf.w[i], dummy, need_w))) return rc;
+        c->cap_w = need_w;
+    }
+    c->bf.stride = n;
     if (n > c->cap_n) {
-        for (int i = 0; i < 2; ++i) {
-            if ((rc = grow(c->bf.keys[i], dummy, n))) return rc;
-            if ((rc = grow(c->bf.vals[i], dummy, n))) return rc;
-        }
         if ((rc = grow(c->perm_scratch, dummy, n))) return rc;
         if ((rc = grow(c->dims_scratch, dummy, n))) return rc;
         c->cap_n = n;
     }
     size_t nseg = (size_t)1 << (lam0 > 0 ? lam0 : 0);
-    if (nseg > c->cap_seg || (size_t)k > c->cap_k) {
+    if (nseg > c->cap_seg) {
         if ((rc = grow(c->bf.hist, dummy, nseg * 1024))) return rc;
         if ((rc = grow(c->bf.seg_and, dummy, nseg))) return rc;
         if ((rc = grow(c->bf.seg_or, dummy, nseg))) return rc;
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 2; ++i) {
             if ((rc = grow(c->bf.boxes[i], dummy, nseg * 2 * (size_t)LBKD_MAX_K))) return rc;
+            if ((rc = grow(c->bf.state[i], dummy, nseg))) return rc;
+        }
         c->cap_seg = nseg;
-        c->cap_k = LBKD_MAX_K;
     }
     size_t T = (size_t)1 << (b - 1);
     size_t tiles = (n + T - 1) / T + 1;
@@ -108,14 +113,9 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0, bool need_pts_copy
     }
     if (!c->bf.tile_ctr) {
         if ((rc = grow(c->bf.tile_ctr, dummy, 4 * 64))) return rc;
-        if ((rc = grow(c->bf.plan, dummy, 1))) return rc;
         if ((rc = grow(c->bf.err, dummy, 4))) return rc;
         if ((rc = grow(c->minmax, dummy, 2 * LBKD_MAX_K))) return rc;
         CK(cudaMallocHost(&c->h_err, sizeof(u32) * 4));
-    }
-    if (need_pts_copy && n * (u64)k > c->cap_ptsb) {
-        if ((rc = grow(c->pts_copy, dummy, n * (u64)k))) return rc;
-        c->cap_ptsb = n * (u64)k;
     }
     return LBKD_OK;
 }
@@ -139,7 +139,7 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     const int lam0 = L - b > 0 ? L - b : 0;
     if (d_trace && lam0 > 0) return LBKD_EUNSUPPORTED;
     const bool inplace = (const void*)d_points == (const void*)d_out;
-    int rc = ensure(c, n, k, b, lam0, inplace);
+    int rc = ensure(c, n, k, b, lam0);
     if (rc) return rc;
 
     BuildParams bp;
@@ -148,7 +148,14 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.mode = mode;
     bp.b = b;
     bp.pts = d_points;
-    if (inplace) {
+    // the global levels read the input only in init (into W), so in-place
+    // reordering needs a private copy only for single-CTA builds
+    if (inplace && lam0 == 0) {
+        if ((u64)k * n > c->cap_copy) {
+            size_t dummy = 0;
+            if ((rc = grow(c->pts_copy, dummy, (size_t)k * n))) return rc;
+            c->cap_copy = (u64)k * n;
+        }
         CK(cudaMemcpyAsync(c->pts_copy, d_points, n * (u64)k * sizeof(float), cudaMemcpyDeviceToDevice, st));
         bp.pts = c->pts_copy;
     }
@@ -159,7 +166,6 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     Buffers& bf = c->bf;
 
     CK(cudaMemsetAsync(bf.tile_ctr, 0, sizeof(u32) * 4 * 64, st));
-    CK(cudaMemsetAsync(bf.plan, 0, sizeof(LevelPlan), st));
     CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
     if (mode == kWidest) {
         CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
@@ -169,12 +175,16 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
         c->launches += 2;
     }
     int ctr = 0;
+    if (lam0 > 0) {
+        launch_init(bp, bf, st);
+        c->launches += 1;
+    }
     for (int l = 0; l < lam0; ++l) {
         const u64 nseg = 1ull << l;
         CK(cudaMemsetAsync(bf.hist, 0, nseg * 1024 * sizeof(u32), st));
         CK(cudaMemsetAsync(bf.seg_and, 0xff, nseg * sizeof(u32), st));
         CK(cudaMemsetAsync(bf.seg_or, 0, nseg * sizeof(u32), st));
-        launch_rekey_hist(bp, bf, l, st);
+        launch_hist(bp, bf, l, st);
         launch_plan(bp, bf, l, st);
         c->launches += 2;
         for (int p = 0; p < 4; ++p) {
@@ -183,6 +193,8 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
             if (c->epoch == 0) c->epoch = 1;
             c->launches += 1;
         }
+        launch_pivots(bp, bf, l, st);
+        c->launches += 1;
         if (mode == kWidest) {
             launch_widest_nodes(bp, l, bf.boxes[l & 1], bf.boxes[(l + 1) & 1], st);
             c->launches += 1;
@@ -208,6 +220,10 @@ int lbkd_create(lbkd_ctx** out, int device) {
         note_cuda(e);
         return LBKD_ECUDA;
     }
+    // Random 4-byte gathers (rekey, subtree load) otherwise pull 128-byte
+    // lines from HBM; 32 bytes is one sector.  Streaming kernels are fully
+    // coalesced, so the smaller fetch granularity costs them nothing.
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
     lbkd_ctx* c = new lbkd_ctx();
     c->device = device;
     *out = c;
@@ -218,16 +234,15 @@ void lbkd_destroy(lbkd_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     for (int i = 0; i < 2; ++i) {
-        cudaFree(c->bf.keys[i]);
-        cudaFree(c->bf.vals[i]);
+        cudaFree(c->bf.w[i]);
         cudaFree(c->bf.boxes[i]);
+        cudaFree(c->bf.state[i]);
     }
     cudaFree(c->bf.hist);
     cudaFree(c->bf.seg_and);
     cudaFree(c->bf.seg_or);
     cudaFree(c->bf.status);
     cudaFree(c->bf.tile_ctr);
-    cudaFree(c->bf.plan);
     cudaFree(c->bf.err);
     cudaFree(c->pts_copy);
     cudaFree(c->perm_scratch);

@@ -115,6 +115,24 @@ __host__ __device__ __forceinline__ u64 pivot_off(const LevelGeom& g, u64 j) {
     return cw - 1ull + on;
 }
 
+// In-order layout (global levels): segment j of level l begins at
+// ib(j) = bw(j) + j -- the compacted begin plus one finished ancestor node
+// between consecutive segments -- which simplifies to
+// min(j * 2^(sh+1), j * 2^sh + B).
+__host__ __device__ __forceinline__ u64 seg_ibegin(const LevelGeom& g, u64 j) {
+    u64 lo = j << g.sh;
+    return lo + (lo < g.B ? lo : g.B);
+}
+
+// segment whose in-order range starts at or before position p (p may be the
+// finished node just after it); inverse of the piecewise-linear ib(j)
+__host__ __device__ __forceinline__ u64 seg_of_inorder(const LevelGeom& g, u64 p) {
+    u64 ja = p >> (g.sh + 1);
+    u64 jb = p >= g.B ? (p - g.B) >> g.sh : 0ull;
+    u64 j = ja > jb ? ja : jb;
+    return j < g.nseg ? j : g.nseg - 1;
+}
+
 // segment containing W_l position p (inverse of seg_begin); O(1) with two
 // integer divisions -- evaluated once per tile, not per element.
 __host__ __device__ inline u64 seg_of(const LevelGeom& g, u64 p) {
@@ -129,6 +147,24 @@ __host__ __device__ inline u64 seg_of(const LevelGeom& g, u64 p) {
     u64 q = p - p1;
     if (q < ps || small == 0) return nf;
     return nf + 1ull + (q - ps) / small;
+}
+
+// Lanes of the warp holding the same NBITS-bit value (the set of "peers"),
+// built from one ballot per bit.  MATCH.ANY runs on the B200's low-rate ADU
+// pipe (measured: the pipe saturates at ~40 cycles per instruction, see
+// DESIGN.md), while VOTE/LOP3 issue at full rate, so the bit-sliced form is
+// several times faster for 8-9 bit digits.  Invalid lanes match only
+// themselves.
+template <int NBITS>
+__device__ __forceinline__ u32 warp_peers(u32 v, bool valid) {
+    u32 m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < NBITS; ++b) {
+        const bool bit = (v >> b) & 1u;
+        const u32 bal = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? bal : ~bal;
+    }
+    return valid ? m : (1u << (threadIdx.x & 31u));
 }
 
 // ---- PTX helpers -----------------------------------------------------------
@@ -146,6 +182,21 @@ __device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
 
 __device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// L2-only (32-byte sector) loads for random gathers: the default LDG path
+// promotes a miss to a full 128-byte line, quadrupling DRAM traffic for
+// scattered 4-byte reads.
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ u32 ld_cg_u32(const u32* p) {
+    u32 v;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
 }
 
 // Decoupled-lookback status word: [63:34] epoch, [33:32] flag, [31:0] count

@@ -1,86 +1,123 @@
-// global_sort.cu -- the per-level "sort phase" of the top (large-segment)
-// levels: a segmented, stable, onesweep LSD radix sort of W_l by the split
-// coordinate, with the updateTags refinement fused into its last digit pass.
+// global_sort.cu -- the per-level sort phase of the top (large-segment)
+// levels: a segmented, stable, onesweep LSD radix sort of every level-l
+// segment by its split coordinate, with the points travelling as payload.
 //
-// Reference semantics (what must come out bit-exact):
+// Reference semantics (bit-exact):
 //   sort_phase   /root/reference/pkg/src/lbkd/builder.py:165-181
 //       np.lexsort((coords[:, l % k], tags)): stable by (tag, coordinate)
 //   update_tags_round_robin  kernels_numba.py:21-46 (pivot arithmetic)
-//   sort_phase_widest        widest.py:119-131 (minor key = own coord in the
-//                            tag's dimension)
+//   sort_phase_widest        widest.py:119-131 (minor key = own coordinate in
+//                            the tag's split dimension)
 //
-// Why segmented: after update pass l-1 every element carries the tag of the
-// level-l node whose contiguous segment it sits in, and tags are already in
-// ascending order along the array (children 2s+1 < 2s+2 < 2(s+1)+1).  The
-// (tag, coord) sort therefore never moves an element across segments: the
-// tag digits of the packed 64-bit key are provably constant-order and their
-// digit passes are skipped entirely; what remains is a stable sort of each
-// segment by its 32-bit order-flipped coordinate.  Segment boundaries come
-// from O(1) treemath arithmetic, not from stored tags.
+// Why segmented: after update pass l-1 the tags along the array are already
+// ascending (children 2s+1 < 2s+2 < 2(s+1)+1) and each level-l node owns one
+// contiguous segment, so the (tag, coord) sort never moves a point across
+// segments: the tag digits of the packed 64-bit key are provably in order
+// and their digit passes are skipped.  What remains is a stable sort of each
+// segment by its 32-bit order-flipped coordinate.
 //
-// Each digit pass is one onesweep kernel: per-tile warp-match ranking into
-// shared memory, decoupled lookback across the tiles of a segment, and a
-// shared-memory-staged coalesced scatter.  Tiles (T = 2^(b-1) keys) are never
-// larger than the smallest segment on the global levels, so a tile spans at
-// most two segments; only the first can have started in an earlier tile.
+// Why in-order layout: the reference moves each finished node to the front
+// (its final tag order).  Here every node stays at its in-order slot; the
+// left child's segment is then exactly the part before the pivot and the
+// right child's the part after it, so updateTags moves nothing -- the pivot
+// is read off in place (pivot kernel) and the children inherit the parent's
+// buffer.  A digit pass runs only for segments whose digit actually varies
+// (per-segment AND/OR), and skipped segments are not touched at all.
+//
+// Why payload: a random 4-byte gather on B200 costs a 128-byte line and is
+// limited to ~50 G gathers/s (measured, tools/micro/gather.cu), so the points
+// move with their keys as SoA arrays and no kernel ever gathers.
 #include "kernels.cuh"
 
 namespace lbkd {
 
-constexpr int kPassThreads = 256;
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
 constexpr int kBuckets = 512;  // 2 segments x 256 digits per tile
 
-int global_items_for_bits(int b) { return (1 << (b - 1)) / kPassThreads; }
+static int items_for_bits(int b) { return (1 << (b - 1)) / kThreads; }
+
+__device__ __forceinline__ u32 parity_out(uint8_t st) {
+    return ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
+}
+
+// split dimension of level-l segment j
+__device__ __forceinline__ int seg_dim(int mode, const uint8_t* split_dims, const LevelGeom& g, int k, u64 j) {
+    return mode == kRoundRobin ? (g.l % k) : (int)split_dims[g.Fl + j];
+}
+
+// parity (buffer) holding level-l segment j at the start of the level
+__device__ __forceinline__ u32 seg_parity_in(const uint8_t* prev_state, int l, u64 j) {
+    return l == 0 ? 0u : parity_out(prev_state[j >> 1]);
+}
 
 // ---------------------------------------------------------------------------
-// rekey + histogram: keys[p] = flip(coord of point vals[p] in the split dim of
-// p's segment); per-(segment, digit-pass, digit) counts; per-segment AND/OR of
-// the keys (digit-pass skipping).  Level 0 reads the points sequentially,
-// writes vals = identity and checks every coordinate is finite.
+// init: AoS float32 input -> W[0] SoA (k coordinate arrays + index array),
+// and the non-finite check of builder.py:134-135.
 // ---------------------------------------------------------------------------
-struct RekeyArgs {
+__global__ void init_kernel(const float* __restrict__ pts, u64 n, int k, u32* w0, u64 stride, u32* err) {
+    bool bad = false;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const float* q = pts + i * k;
+        for (int c = 0; c < k; ++c) {
+            float f = __ldg(q + c);
+            bad |= !isfinite(f);
+            w0[c * stride + i] = __float_as_uint(f);
+        }
+        w0[(u64)k * stride + i] = (u32)i;
+    }
+    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+void launch_init(const BuildParams& bp, const Buffers& bf, cudaStream_t st) {
+    u64 blocks = (bp.n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    init_kernel<<<(unsigned)blocks, 256, 0, st>>>(bp.pts, bp.n, bp.k, bf.w[0], bf.stride, bf.err);
+}
+
+// ---------------------------------------------------------------------------
+// hist: per-(segment, digit pass, digit) counts of the level's keys and the
+// per-segment AND/OR that drive digit-pass skipping.  Each CTA walks a
+// contiguous run of tiles and flushes its shared histogram only when the
+// segment changes, so global atomics stay O(#CTAs + #segments).
+// ---------------------------------------------------------------------------
+struct HistArgs {
     LevelGeom g;
-    int k, mode, level0, items, tiles_per_cta;
+    int k, mode, tiles_per_cta;
     u64 ntiles;
-    const float* pts;
+    Buffers bf;
+    const uint8_t* prev_state;
     const uint8_t* split_dims;
-    u32* keys[2];
-    u32* vals[2];
-    const LevelPlan* plan;
-    u32* hist;
-    u32* seg_and;
-    u32* seg_or;
-    u32* err;
 };
 
+constexpr int kHistThreads = 256;
+
+// warp-private bins, bumped by each match group's highest lane with a plain
+// read-modify-write (the groups of one instruction hit distinct bins, and
+// consecutive rounds are ordered by __syncwarp) -- shared atomics cost
+// ~2 cycles per lane on B200, this costs one bank-conflicted LDS/STS pair
 __device__ __forceinline__ void hist_add(u32* h, u32 d, bool inc) {
-    u32 v = inc ? d : (0x10000u | threadIdx.x);
-    u32 peers = __match_any_sync(kFullMask, v);
-    int leader = __ffs(peers) - 1;
-    if (inc && (int)(threadIdx.x & 31) == leader) atomicAdd(&h[d], (u32)__popc(peers));
+    const u32 lane = threadIdx.x & 31u;
+    u32 peers = warp_peers<8>(d, inc);
+    if (inc && lane == 31u - __clz(peers)) h[d] += (u32)__popc(peers);
+    __syncwarp();
 }
 
 template <int ITEMS>
-__global__ void __launch_bounds__(kPassThreads) rekey_hist_kernel(RekeyArgs a) {
-    __shared__ u32 h[4 * 256];
-    __shared__ u32 s_and[kPassThreads / 32], s_or[kPassThreads / 32];
-    constexpr int T = kPassThreads * ITEMS;
+__global__ void __launch_bounds__(kHistThreads) hist_kernel(HistArgs a) {
+    constexpr int kW = kHistThreads / 32;
+    __shared__ u32 h[kW][4 * 256];
+    __shared__ u32 s_and[kW], s_or[kW];
+    constexpr int T = kHistThreads * ITEMS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const LevelGeom& g = a.g;
-    const u32 sel = a.level0 ? 0u : a.plan->next_sel;
-    const u32* vin = a.vals[sel];
-    u32* kout = a.keys[sel];
-    u32* vout = a.vals[sel];
-    for (int i = threadIdx.x; i < 4 * 256; i += kPassThreads) h[i] = 0;
-
+    for (int i = threadIdx.x; i < kW * 4 * 256; i += kHistThreads) (&h[0][0])[i] = 0;
     u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
     u64 t1 = t0 + a.tiles_per_cta;
     if (t1 > a.ntiles) t1 = a.ntiles;
-    if (t0 >= t1) return;
-    u64 cur = seg_of(g, t0 * T);
+    u64 cur = seg_of_inorder(g, t0 * T);
     u32 acc_and = 0xffffffffu, acc_or = 0u;
-    bool bad = false;
-    int dim_rr = g.l % a.k;
+    u32* hw = h[warp];
     __syncthreads();
 
     auto flush = [&](u64 seg) {
@@ -88,16 +125,18 @@ __global__ void __launch_bounds__(kPassThreads) rekey_hist_kernel(RekeyArgs a) {
         u32 wo = __reduce_or_sync(kFullMask, acc_or);
         if (lane == 0) { s_and[warp] = wa; s_or[warp] = wo; }
         __syncthreads();
-        u32* gh = a.hist + seg * 1024ull;
-        for (int i = threadIdx.x; i < 1024; i += kPassThreads) {
-            u32 v = h[i];
-            if (v) { atomicAdd(&gh[i], v); h[i] = 0; }
+        u32* gh = a.bf.hist + seg * 1024ull;
+        for (int i = threadIdx.x; i < 1024; i += kHistThreads) {
+            u32 v = 0;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) { v += h[w][i]; h[w][i] = 0; }
+            if (v) atomicAdd(&gh[i], v);
         }
         if (threadIdx.x == 0) {
             u32 A = 0xffffffffu, O = 0u;
-            for (int w = 0; w < kPassThreads / 32; ++w) { A &= s_and[w]; O |= s_or[w]; }
-            atomicAnd(&a.seg_and[seg], A);
-            atomicOr(&a.seg_or[seg], O);
+            for (int w = 0; w < kW; ++w) { A &= s_and[w]; O |= s_or[w]; }
+            atomicAnd(&a.bf.seg_and[seg], A);
+            atomicOr(&a.bf.seg_or[seg], O);
         }
         acc_and = 0xffffffffu;
         acc_or = 0u;
@@ -105,410 +144,378 @@ __global__ void __launch_bounds__(kPassThreads) rekey_hist_kernel(RekeyArgs a) {
     };
 
     for (u64 t = t0; t < t1; ++t) {
-        u64 ts = t * T;
-        u64 cnt = g.nl - ts < (u64)T ? g.nl - ts : (u64)T;
-        u64 nb = (cur + 1 < g.nseg) ? seg_begin(g, cur + 1) : ~0ull;
-        u64 bnd = (nb >= ts && nb < ts + cnt) ? nb - ts : cnt;  // first pos of next seg
+        const u64 ts = t * T;
+        const u64 cnt = g.n - ts < (u64)T ? g.n - ts : (u64)T;
+        // segment `cur` occupies [sb, e0); a finished node sits at e0 and
+        // segment cur+1 starts at e0 + 1
+        const u64 sb = seg_ibegin(g, cur);
+        const u64 e0 = sb + seg_size(g, cur);
+        const bool has_next = cur + 1 < g.nseg && e0 + 1 < ts + cnt;
+        const u32 r0a = sb > ts ? (u32)(sb - ts) : 0u;
+        const u32 r0b = e0 > ts ? (u32)((e0 - ts < cnt) ? e0 - ts : cnt) : 0u;
+        const u32 r1a = has_next ? (u32)(e0 + 1 - ts) : (u32)cnt;
+        const u32* k0 = warr(a.bf, seg_parity_in(a.prev_state, g.l, cur), seg_dim(a.mode, a.split_dims, g, a.k, cur));
+        const u32* k1 = has_next ? warr(a.bf, seg_parity_in(a.prev_state, g.l, cur + 1),
+                                        seg_dim(a.mode, a.split_dims, g, a.k, cur + 1))
+                                 : k0;
         u32 key[ITEMS];
-        u32 rel[ITEMS];
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
-            rel[i] = r;
             key[i] = 0;
-            if (r < cnt) {
-                u64 p = ts + r;
-                u32 idx;
-                int d;
-                if (a.level0) {
-                    idx = (u32)p;
-                    vout[p] = idx;
-                    const float* q = a.pts + (u64)idx * a.k;
-                    for (int c = 0; c < a.k; ++c) {
-                        float f = q[c];
-                        if (!isfinite(f)) bad = true;
-                    }
-                } else {
-                    idx = vin[p];
-                }
-                if (a.mode == kRoundRobin) {
-                    d = dim_rr;
-                } else {
-                    u64 seg = (r < bnd) ? cur : cur + 1;
-                    d = a.split_dims[g.Fl + seg];
-                }
-                key[i] = flip_key(__ldg(a.pts + (u64)idx * a.k + d));
-                kout[p] = key[i];
-            }
+            if (r >= r0a && r < r0b) key[i] = flip_key(__uint_as_float(k0[ts + r]));
+            else if (r >= r1a && r < cnt) key[i] = flip_key(__uint_as_float(k1[ts + r]));
         }
-        // phase A: elements of segment `cur`
-#pragma unroll
+#pragma unroll 1
         for (int i = 0; i < ITEMS; ++i) {
-            bool inc = rel[i] < bnd;
+            u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+            bool inc = r >= r0a && r < r0b;
             if (inc) { acc_and &= key[i]; acc_or |= key[i]; }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) hist_add(h + q * 256, (key[i] >> (8 * q)) & 255u, inc);
+            for (int q = 0; q < 4; ++q) hist_add(hw + q * 256, (key[i] >> (8 * q)) & 255u, inc);
         }
-        if (bnd < cnt) {
+        if (has_next) {
             __syncthreads();
             flush(cur);
             ++cur;
-#pragma unroll
+#pragma unroll 1
             for (int i = 0; i < ITEMS; ++i) {
-                bool inc = rel[i] >= bnd && rel[i] < cnt;
+                u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+                bool inc = r >= r1a && r < cnt;
                 if (inc) { acc_and &= key[i]; acc_or |= key[i]; }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) hist_add(h + q * 256, (key[i] >> (8 * q)) & 255u, inc);
+                for (int q = 0; q < 4; ++q) hist_add(hw + q * 256, (key[i] >> (8 * q)) & 255u, inc);
             }
         }
     }
     __syncthreads();
     flush(cur);
-    if (bad) atomicOr(a.err, 1u);
 }
 
-void launch_rekey_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {
-    RekeyArgs a;
+void launch_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {
+    HistArgs a;
     a.g = make_geom(bp.n, l);
     a.k = bp.k;
     a.mode = bp.mode;
-    a.level0 = (l == 0);
-    a.items = global_items_for_bits(bp.b);
-    const u64 T = (u64)kPassThreads * a.items;
-    a.ntiles = (a.g.nl + T - 1) / T;
-    // persistent-ish: ~8 CTAs per SM, each a contiguous run of tiles, so the
-    // per-segment histogram flushes stay O(#CTAs + #segments)
+    int items = (1 << (bp.b - 1)) / kHistThreads;  // tile <= smallest segment
+    if (items > 8) items = 8;
+    const u64 T = (u64)kHistThreads * items;
+    a.ntiles = (bp.n + T - 1) / T;
     u64 target = 148 * 8;
     u64 tpc = (a.ntiles + target - 1) / target;
     if (tpc < 1) tpc = 1;
     a.tiles_per_cta = (int)tpc;
-    a.pts = bp.pts;
+    a.bf = bf;
+    a.prev_state = bf.state[(l + 1) & 1];
     a.split_dims = bp.split_dims;
-    for (int i = 0; i < 2; ++i) { a.keys[i] = bf.keys[i]; a.vals[i] = bf.vals[i]; }
-    a.plan = bf.plan;
-    a.hist = bf.hist;
-    a.seg_and = bf.seg_and;
-    a.seg_or = bf.seg_or;
-    a.err = bf.err;
     unsigned grid = (unsigned)((a.ntiles + tpc - 1) / tpc);
-    switch (a.items) {
-        case 16: rekey_hist_kernel<16><<<grid, kPassThreads, 0, st>>>(a); break;
-        case 8: rekey_hist_kernel<8><<<grid, kPassThreads, 0, st>>>(a); break;
-        default: rekey_hist_kernel<4><<<grid, kPassThreads, 0, st>>>(a); break;
+    switch (items) {
+        case 8: hist_kernel<8><<<grid, kHistThreads, 0, st>>>(a); break;
+        default: hist_kernel<4><<<grid, kHistThreads, 0, st>>>(a); break;
     }
 }
 
 // ---------------------------------------------------------------------------
-// plan: which digit passes are identities (digit constant inside every
-// segment), which pass is last (it carries the updateTags epilogue), and the
-// ping-pong buffer each pass reads.  One CTA.
+// plan: per segment, which digit passes reorder it (digit not constant) and
+// which buffer it starts in (its parent's final buffer).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) plan_kernel(LevelPlan* plan, const u32* seg_and,
-                                                    const u32* seg_or, u64 nseg) {
-    __shared__ u32 s_red[32];
-    u32 x = 0;
-    for (u64 s = threadIdx.x; s < nseg; s += blockDim.x) x |= seg_and[s] ^ seg_or[s];
-    x = __reduce_or_sync(kFullMask, x);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        u32 v = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v |= s_red[w];
-        u32 nontriv[4];
-        for (int p = 0; p < 4; ++p) nontriv[p] = ((v >> (8 * p)) & 255u) != 0;
-        int fin = 0;
-        for (int p = 0; p < 4; ++p)
-            if (nontriv[p]) fin = p;
-        u32 cur = plan->next_sel;
-        LevelPlan np;
-        for (int p = 0; p < 4; ++p) {
-            bool run = (p == fin) || (p < fin && nontriv[p]);
-            np.skip[p] = run ? 0u : 1u;
-            np.src[p] = cur;
-            if (run) cur ^= 1u;
-        }
-        np.final_pass = (u32)fin;
-        np.next_sel = cur;
-        np.pad[0] = np.pad[1] = 0;
-        *plan = np;
-    }
+__global__ void plan_kernel(int l, u64 nseg, const u32* seg_and, const u32* seg_or, const uint8_t* prev_state,
+                            uint8_t* state) {
+    u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    if (j >= nseg) return;
+    u32 vary = seg_and[j] ^ seg_or[j];
+    u32 mask = 0;
+    for (int p = 0; p < 4; ++p)
+        if ((vary >> (8 * p)) & 255u) mask |= 1u << p;
+    u32 par = seg_parity_in(prev_state, l, j);
+    state[j] = (uint8_t)((par << 4) | mask);
 }
 
 void launch_plan(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {
     LevelGeom g = make_geom(bp.n, l);
-    plan_kernel<<<1, 1024, 0, st>>>(bf.plan, bf.seg_and, bf.seg_or, g.nseg);
+    unsigned blocks = (unsigned)((g.nseg + 255) / 256);
+    plan_kernel<<<blocks, 256, 0, st>>>(l, g.nseg, bf.seg_and, bf.seg_or, bf.state[(l + 1) & 1], bf.state[l & 1]);
 }
 
 // ---------------------------------------------------------------------------
 // onesweep digit pass
 // ---------------------------------------------------------------------------
 struct PassArgs {
-    LevelGeom g, gn;  // this level, next level
-    int pass, k;
+    LevelGeom g;
+    int pass, k, mode;
     u32 epoch;
-    u64 ntiles;
-    u32* keys[2];
-    u32* vals[2];
-    const u32* hist;
-    u64* status;
+    Buffers bf;
+    const uint8_t* state;
+    const uint8_t* split_dims;
     u32* tile_ctr;
-    const LevelPlan* plan;
-    const float* pts;
-    float* out_pts;
-    u32* perm;
 };
 
 template <int ITEMS>
 struct PassSmem {
-    static constexpr int T = kPassThreads * ITEMS;
-    u32 keys[T];
-    u32 vals[T];
-    unsigned short cnt[kPassThreads / 32][kBuckets];
-    u32 bstart[kBuckets + 1];
-    u32 gdelta[kBuckets];
+    static constexpr int T = kThreads * ITEMS;
+    unsigned short cnt[kWarps][kBuckets];  // per-warp counts, then warp prefixes
+    u32 bstart[kBuckets];                  // tile-local start of each bucket
+    u32 gdelta[kBuckets];                  // offset-in-segment = gdelta[b] + slot
+    u32 dstoff[T];                         // destination of sorted slot i
+    unsigned short inv[T];                 // tile position of sorted slot i
     u64 scan_tmp[32];
     u64 info[16];
+    // followed by raw[k+1][T] u32 (payload staged by cp.async)
 };
 
-__device__ __forceinline__ void write_node(const PassArgs& a, u64 node, u32 idx) {
-    a.perm[node] = idx;
-    const float* src = a.pts + (u64)idx * a.k;
-    float* dst = a.out_pts + node * a.k;
-    for (int c = 0; c < a.k; ++c) dst[c] = src[c];
+__device__ __forceinline__ void cp_async4(u32* smem_dst, const u32* gsrc) {
+    u32 s = (u32)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int ITEMS>
-__global__ void __launch_bounds__(kPassThreads) onesweep_pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem<ITEMS>& S = *reinterpret_cast<PassSmem<ITEMS>*>(smem_raw);
     constexpr int T = PassSmem<ITEMS>::T;
+    u32* raw = reinterpret_cast<u32*>(smem_raw + sizeof(PassSmem<ITEMS>));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-    const LevelPlan plan = *a.plan;
-    if (plan.skip[a.pass]) return;
-    const bool fin = (u32)a.pass == plan.final_pass;
-    const u32 src = plan.src[a.pass];
-    const u32* kin = a.keys[src];
-    const u32* vin = a.vals[src];
-    u32* kout = a.keys[src ^ 1u];
-    u32* vout = a.vals[src ^ 1u];
     const LevelGeom& g = a.g;
-    const int shift = 8 * a.pass;
+    const int p = a.pass;
+    const int shift = 8 * p;
+    const int A = a.k + 1;
 
-    // --- tile acquisition (in launch order: lookback only waits on earlier
-    // tiles, which are already resident) and segment geometry of the tile
     if (tid == 0) {
         u64 tile = atomicAdd(a.tile_ctr, 1u);
         u64 ts = tile * T;
-        u64 cnt = g.nl - ts < (u64)T ? g.nl - ts : (u64)T;
-        u64 j0 = seg_of(g, ts);
-        u64 b0 = seg_begin(g, j0);
-        u64 b1 = (j0 + 1 < g.nseg) ? seg_begin(g, j0 + 1) : g.nl;
-        u64 bnd = (b1 < ts + cnt) ? b1 - ts : cnt;
+        u64 cnt = g.n - ts < (u64)T ? g.n - ts : (u64)T;
+        u64 j0 = seg_of_inorder(g, ts);
+        u64 s0b = seg_ibegin(g, j0), s0e = s0b + seg_size(g, j0);
+        uint8_t st0 = a.state[j0];
+        u64 r0a = s0b > ts ? s0b - ts : 0ull;
+        u64 r0b = s0e > ts ? ((s0e - ts < cnt) ? s0e - ts : cnt) : 0ull;
+        bool act0 = ((st0 >> p) & 1u) && r0a < r0b;
+        u64 r1a = cnt, r1b = cnt;
+        bool has1 = false, act1 = false;
+        uint8_t st1 = 0;
+        if (j0 + 1 < g.nseg) {
+            u64 s1b = seg_ibegin(g, j0 + 1);
+            if (s1b < ts + cnt) {
+                has1 = true;
+                st1 = a.state[j0 + 1];
+                act1 = (st1 >> p) & 1u;
+                r1a = s1b - ts;
+                u64 s1e = s1b + seg_size(g, j0 + 1);
+                r1b = (s1e - ts < cnt) ? s1e - ts : cnt;
+            }
+        }
+        u32 src0 = ((st0 >> 4) ^ (u32)__popc(st0 & ((1u << p) - 1u))) & 1u;
+        u32 src1 = ((st1 >> 4) ^ (u32)__popc(st1 & ((1u << p) - 1u))) & 1u;
         S.info[0] = tile;
         S.info[1] = ts;
-        S.info[2] = cnt;
-        S.info[3] = j0;
-        S.info[4] = b0;
-        S.info[5] = b1;
-        S.info[6] = bnd;
-        S.info[7] = (b0 < ts) ? 1ull : 0ull;  // first segment continues from earlier tiles
+        S.info[2] = act0 ? r0a : 0;
+        S.info[3] = act0 ? r0b : 0;
+        S.info[4] = act1 ? r1a : cnt;
+        S.info[5] = act1 ? r1b : cnt;
+        S.info[6] = j0;
+        S.info[7] = (act0 ? 1u : 0u) | (act1 ? 2u : 0u) | (has1 ? 4u : 0u) | ((act0 && s0b < ts) ? 8u : 0u) |
+                    (src0 << 4) | (src1 << 5);
+        S.info[9] = s0b;
+        S.info[10] = has1 ? s0e + 1 : 0;  // in-order begin of segment j0+1
+        S.info[11] = (u64)seg_dim(a.mode, a.split_dims, g, a.k, j0) |
+                     ((u64)(has1 ? seg_dim(a.mode, a.split_dims, g, a.k, j0 + 1) : 0) << 8);
     }
-    for (int i = tid; i < (kPassThreads / 32) * kBuckets / 2; i += kPassThreads)
-        reinterpret_cast<u32*>(&S.cnt[0][0])[i] = 0u;
+    for (int i = tid; i < kWarps * kBuckets / 2; i += kThreads) reinterpret_cast<u32*>(&S.cnt[0][0])[i] = 0u;
     __syncthreads();
+    const u32 flags = (u32)S.info[7];
+    if ((flags & 3u) == 0) return;  // neither segment reorders in this pass
     const u64 tile = S.info[0], ts = S.info[1];
-    const u32 cnt = (u32)S.info[2];
-    const u64 j0 = S.info[3];
-    const u32 bnd = (u32)S.info[6];
-    const bool need_lb = S.info[7] != 0;
-    const bool has1 = bnd < cnt;
+    const u32 r0a = (u32)S.info[2], r0b = (u32)S.info[3], r1a = (u32)S.info[4], r1b = (u32)S.info[5];
+    const u64 j0 = S.info[6];
+    const bool act0 = flags & 1u, act1 = flags & 2u, need_lb = flags & 8u;
+    const u32 src0 = (flags >> 4) & 1u, src1 = (flags >> 5) & 1u;
+    const int d0 = (int)(S.info[11] & 255u), d1 = (int)((S.info[11] >> 8) & 255u);
 
-    // --- load (warp-striped, coalesced) and rank within the warp
-    u32 key[ITEMS], val[ITEMS];
-    unsigned short bkt[ITEMS], rnk[ITEMS];
+    // --- stage the payload of the active elements (all k+1 arrays) with
+    // cp.async while the keys are ranked
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+        bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
+        if (in0 || in1) {
+            const u32* base = a.bf.w[in1 ? src1 : src0] + ts + r;
+            for (int c = 0; c < A; ++c) cp_async4(raw + c * T + r, base + (u64)c * a.bf.stride);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+
+    u32 key[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+        bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
+        key[i] = 0u;
+        if (in0) key[i] = a.bf.w[src0][(u64)d0 * a.bf.stride + ts + r];
+        else if (in1) key[i] = a.bf.w[src1][(u64)d1 * a.bf.stride + ts + r];
+    }
+    // --- warp-level stable ranking: all match.any first (independent), then
+    // the per-round counter bumps by each group's highest lane
+    u32 br[ITEMS];  // bucket << 16 | warp-local rank
+    u32 peers[ITEMS];
     const u32 lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
-        bool valid = r < cnt;
-        key[i] = valid ? kin[ts + r] : 0u;
-        val[i] = valid ? vin[ts + r] : 0u;
-        u32 b = valid ? (((key[i] >> shift) & 255u) | (r >= bnd ? 256u : 0u)) : (0x1000u | lane);
-        u32 peers = __match_any_sync(kFullMask, b);
-        int leader = __ffs(peers) - 1;
+        bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
+        u32 dg = (flip_key(__uint_as_float(key[i])) >> shift) & 255u;
+        u32 b = in0 ? dg : (in1 ? (dg | 256u) : (0x1000u | lane));
+        br[i] = b;
+        peers[i] = warp_peers<9>(b, in0 || in1);
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const u32 b = br[i];
+        const int leader = 31 - __clz(peers[i]);
         u32 c = 0;
-        if (lane == leader && valid) {
+        if (lane == leader && b < 1024u) {
             c = S.cnt[warp][b];
-            S.cnt[warp][b] = (unsigned short)(c + __popc(peers));
+            S.cnt[warp][b] = (unsigned short)(c + __popc(peers[i]));
         }
         c = __shfl_sync(kFullMask, c, leader);
-        bkt[i] = (unsigned short)(b & 1023u);
-        rnk[i] = (unsigned short)(c + __popc(peers & lt));
+        br[i] = ((b & 0xffffu) << 16) | (c + __popc(peers[i] & lt));
         __syncwarp();
     }
     __syncthreads();
 
-    // --- per-bucket warp prefixes and tile totals (thread t: buckets t, t+256)
-    u32 tot0 = 0, tot1 = 0;
+    // --- thread t owns bucket t: warp prefixes and the tile count
+    u32 tot = 0;
 #pragma unroll
-    for (int w = 0; w < kPassThreads / 32; ++w) {
-        u32 c0 = S.cnt[w][tid], c1 = S.cnt[w][tid + 256];
-        S.cnt[w][tid] = (unsigned short)tot0;
-        S.cnt[w][tid + 256] = (unsigned short)tot1;
-        tot0 += c0;
-        tot1 += c1;
+    for (int w = 0; w < kWarps; ++w) {
+        u32 c = S.cnt[w][tid];
+        S.cnt[w][tid] = (unsigned short)tot;
+        tot += c;
     }
-    u64 packed_tot;
-    u64 ex = block_exclusive_scan<u64>((u64)tot0 | ((u64)tot1 << 32), S.scan_tmp, &S.info[8]);
-    const u32 seg0_count = (u32)(S.info[8] & 0xffffffffu);
-    S.bstart[tid] = (u32)(ex & 0xffffffffu);
-    S.bstart[tid + 256] = seg0_count + (u32)(ex >> 32);
-    (void)packed_tot;
-
-    // --- per-segment global digit offsets from the level histogram
-    const u32* h0 = a.hist + (j0 * 4ull + a.pass) * 256ull;
-    u64 hv = (u64)h0[tid];
-    if (has1) hv |= (u64)h0[1024 + tid] << 32;  // segment j0+1 is the next 1024 words
-    u64 base = block_exclusive_scan<u64>(hv, S.scan_tmp, nullptr);
-    u32 base0 = (u32)(base & 0xffffffffu), base1 = (u32)(base >> 32);
-
-    // --- decoupled lookback (only the first segment can span earlier tiles)
-    u64* my_status = a.status + tile * 256ull;
-    if (has1) {
-        st_relaxed_u64(my_status + tid, pack_status(a.epoch, kFlagInc, tot1));
-    } else if (!need_lb) {
-        st_relaxed_u64(my_status + tid, pack_status(a.epoch, kFlagInc, tot0));
-    } else {
-        st_relaxed_u64(my_status + tid, pack_status(a.epoch, kFlagAgg, tot0));
+    // --- publish the counts of this tile's LAST segment (if it reorders)
+    u64* my_status = a.bf.status + tile * 256ull;
+    const bool has1 = flags & 4u;
+    if (tid < 256) {
+        if (!has1 && act0) st_relaxed_u64(my_status + tid, pack_status(a.epoch, need_lb ? kFlagAgg : kFlagInc, tot));
+    } else if (act1) {
+        st_relaxed_u64(my_status + (tid - 256), pack_status(a.epoch, kFlagInc, tot));
     }
+    // --- one scan: tile-local bucket starts (low) + per-segment digit bases
+    // from the level histogram (high)
+    u32 hv = 0;
+    if (tid < 256) { if (act0) hv = a.bf.hist[(j0 * 4ull + p) * 256ull + tid]; }
+    else if (act1) hv = a.bf.hist[((j0 + 1) * 4ull + p) * 256ull + (tid - 256)];
+    u64 ex = block_exclusive_scan<u64>((u64)tot | ((u64)hv << 32), S.scan_tmp, nullptr);
+    const u32 bstart = (u32)(ex & 0xffffffffu);
+    u32 base = (u32)(ex >> 32);
+    if (tid == 256) S.info[8] = ex >> 32;  // histogram total of segment j0
+    S.bstart[tid] = bstart;
+    __syncthreads();
+    if (tid >= 256) base -= (u32)S.info[8];
+
+    // --- decoupled lookback for segment j0 (digit = tid), four predecessors
+    // per round trip
     u32 prefix = 0;
-    if (need_lb) {
-        u64 t = tile - 1;
+    if (tid < 256 && need_lb) {
+        long long t = (long long)tile - 1;
         while (true) {
-            u64 w = ld_relaxed_u64(a.status + t * 256ull + tid);
-            u32 ep = (u32)(w >> 34);
-            u64 fl = (w >> 32) & 3ull;
-            if (ep != a.epoch || fl == 0) continue;
-            prefix += (u32)(w & 0xffffffffu);
-            if (fl == kFlagInc) break;
-            --t;
+            u64 w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                w[q] = (t - q >= 0) ? ld_relaxed_u64(a.bf.status + (u64)(t - q) * 256ull + tid) : 0ull;
+            int q = 0;
+            bool done = false;
+#pragma unroll
+            for (; q < 4; ++q) {
+                u64 fl = (w[q] >> 32) & 3ull;
+                if ((u32)(w[q] >> 34) != a.epoch || fl == 0) break;
+                prefix += (u32)(w[q] & 0xffffffffu);
+                if (fl == kFlagInc) { done = true; break; }
+            }
+            if (done) break;
+            t -= q;
         }
-        if (!has1) st_relaxed_u64(my_status + tid, pack_status(a.epoch, kFlagInc, prefix + tot0));
+        if (!has1) st_relaxed_u64(my_status + tid, pack_status(a.epoch, kFlagInc, prefix + tot));
     }
-    // offset-in-segment of sorted tile slot i is gdelta[bucket] + i
-    S.gdelta[tid] = base0 + prefix - S.bstart[tid];
-    S.gdelta[tid + 256] = base1 - S.bstart[tid + 256];
+    S.gdelta[tid] = base + prefix - bstart;
     __syncthreads();
 
-    // --- scatter into shared memory in tile-sorted order
+    // --- sorted slot -> (tile position, destination)
+    const u64 ib0 = S.info[9], ib1 = S.info[10];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
-        if (r < cnt) {
-            u32 b = bkt[i];
-            u32 slot = S.bstart[b] + S.cnt[warp][b] + rnk[i];
-            S.keys[slot] = key[i];
-            S.vals[slot] = val[i];
+        const u32 b = br[i] >> 16;
+        if (b < 1024u) {
+            u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+            u32 slot = S.bstart[b] + S.cnt[warp][b] + (br[i] & 0xffffu);
+            S.inv[slot] = (unsigned short)r;
+            S.dstoff[slot] = (u32)((b & 256u) ? ib1 : ib0) + S.gdelta[b] + slot;
         }
     }
+    cp_async_wait_all();
     __syncthreads();
 
-    // --- coalesced global write-out
-    const u64 sb0 = S.info[4], sb1 = S.info[5];
+    // --- coalesced write-out of every array (runs of one bucket are contiguous)
+    const u32 nact = (r0b - r0a) + (r1b - r1a);
     const u32 split1 = S.bstart[256];
-    if (!fin) {
-#pragma unroll 4
-        for (u32 i = tid; i < cnt; i += kPassThreads) {
-            u32 k = S.keys[i];
-            u32 seg1 = i >= split1 ? 1u : 0u;
-            u32 b = ((k >> shift) & 255u) | (seg1 << 8);
-            u64 dst = (seg1 ? sb1 : sb0) + (u32)(S.gdelta[b] + i);
-            kout[dst] = k;
-            vout[dst] = S.vals[i];
-        }
-        return;
-    }
-    // final pass: fused updateTags (kernels_numba.py:21-46): the element at
-    // the pivot offset becomes node F(l)+j and is written out; the others move
-    // to their child's segment of W_{l+1} (pivots compacted away).
-    const u64 po0 = pivot_off(g, j0);
-    const u64 po1 = has1 ? pivot_off(g, j0 + 1) : 0ull;
-    const bool last = (g.l == g.L - 2);
-    for (u32 i = tid; i < cnt; i += kPassThreads) {
-        u32 k = S.keys[i];
-        u32 v = S.vals[i];
-        u32 seg1 = i >= split1 ? 1u : 0u;
-        u32 b = ((k >> shift) & 255u) | (seg1 << 8);
-        u64 o = (u32)(S.gdelta[b] + i);
-        u64 j = j0 + seg1;
-        u64 po = seg1 ? po1 : po0;
-        if (o == po) {
-            write_node(a, g.Fl + j, v);
-            continue;
-        }
-        u64 right = o > po ? 1ull : 0ull;
-        u64 child = 2ull * j + right;
-        if (last) {
-            write_node(a, a.gn.Fl + child, v);
-            continue;
-        }
-        u64 off = right ? o - po - 1ull : o;
-        vout[seg_begin(a.gn, child) + off] = v;
+    u32* dst0 = a.bf.w[src0 ^ 1u];
+    u32* dst1 = a.bf.w[src1 ^ 1u];
+    for (u32 i = tid; i < nact; i += kThreads) {
+        const u32 r = S.inv[i];
+        const u64 off = S.dstoff[i];
+        u32* dst = (i >= split1) ? dst1 : dst0;
+        for (int c = 0; c < A; ++c) dst[(u64)c * a.bf.stride + off] = raw[c * T + r];
     }
 }
 
-void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch,
-                 u32* tile_ctr, cudaStream_t st) {
+template <int ITEMS>
+static void launch_pass_t(const PassArgs& a, unsigned grid, cudaStream_t st) {
+    size_t sm = sizeof(PassSmem<ITEMS>) + (size_t)(a.k + 1) * PassSmem<ITEMS>::T * sizeof(u32);
+    cudaFuncSetAttribute(pass_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    pass_kernel<ITEMS><<<grid, kThreads, sm, st>>>(a);
+}
+
+void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch, u32* tile_ctr,
+                 cudaStream_t st) {
     PassArgs a;
     a.g = make_geom(bp.n, l);
-    a.gn = make_geom(bp.n, l + 1);
     a.pass = pass;
     a.k = bp.k;
+    a.mode = bp.mode;
     a.epoch = epoch;
-    int items = global_items_for_bits(bp.b);
-    const u64 T = (u64)kPassThreads * items;
-    a.ntiles = (a.g.nl + T - 1) / T;
-    for (int i = 0; i < 2; ++i) { a.keys[i] = bf.keys[i]; a.vals[i] = bf.vals[i]; }
-    a.hist = bf.hist;
-    a.status = bf.status;
+    a.bf = bf;
+    a.state = bf.state[l & 1];
+    a.split_dims = bp.split_dims;
     a.tile_ctr = tile_ctr;
-    a.plan = bf.plan;
-    a.pts = bp.pts;
-    a.out_pts = bp.out_pts;
-    a.perm = bp.perm;
-    unsigned grid = (unsigned)a.ntiles;
+    int items = items_for_bits(bp.b);
+    const u64 T = (u64)kThreads * items;
+    unsigned grid = (unsigned)((bp.n + T - 1) / T);
     switch (items) {
-        case 16: {
-            size_t sm = sizeof(PassSmem<16>);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(onesweep_pass_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                attr = true;
-            }
-            onesweep_pass_kernel<16><<<grid, kPassThreads, sm, st>>>(a);
-            break;
-        }
-        case 8: {
-            size_t sm = sizeof(PassSmem<8>);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(onesweep_pass_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                attr = true;
-            }
-            onesweep_pass_kernel<8><<<grid, kPassThreads, sm, st>>>(a);
-            break;
-        }
-        default: {
-            size_t sm = sizeof(PassSmem<4>);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(onesweep_pass_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                attr = true;
-            }
-            onesweep_pass_kernel<4><<<grid, kPassThreads, sm, st>>>(a);
-            break;
-        }
+        case 8: launch_pass_t<8>(a, grid, st); break;
+        case 4: launch_pass_t<4>(a, grid, st); break;
+        default: launch_pass_t<2>(a, grid, st); break;
     }
+}
+
+// ---------------------------------------------------------------------------
+// pivots: after the level's passes every segment is sorted in place; its
+// pivot (kernels_numba.py:21-46 arithmetic) is node F(l)+j.  One thread per
+// node copies index and point to the level-order output.
+// ---------------------------------------------------------------------------
+__global__ void pivot_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* state, u32* perm, float* out) {
+    u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    if (j >= g.nseg) return;
+    u32 par = parity_out(state[j]);
+    u64 pos = seg_ibegin(g, j) + pivot_off(g, j);
+    u64 node = g.Fl + j;
+    const u32* w = bf.w[par];
+    perm[node] = w[(u64)k * bf.stride + pos];
+    for (int c = 0; c < k; ++c) out[node * k + c] = __uint_as_float(w[(u64)c * bf.stride + pos]);
+}
+
+void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {
+    LevelGeom g = make_geom(bp.n, l);
+    unsigned blocks = (unsigned)((g.nseg + 255) / 256);
+    pivot_kernel<<<blocks, 256, 0, st>>>(g, bp.k, bf, bf.state[l & 1], bp.perm, bp.out_pts);
 }
 
 }  // namespace lbkd

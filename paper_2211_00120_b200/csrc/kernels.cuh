@@ -5,30 +5,26 @@
 
 namespace lbkd {
 
-// Device-resident per-level plan, written by plan_kernel, read by the pass
-// kernels, the next level's rekey and the subtree kernel.  Keeping it on the
-// device lets a whole build be enqueued without host round trips.
-struct LevelPlan {
-    u32 skip[4];      // digit pass p is the identity for every segment
-    u32 src[4];       // ping-pong buffer the pass reads
-    u32 final_pass;   // pass that places pivots and partitions children
-    u32 next_sel;     // buffer holding W_{l+1} after the level (W_0: 0)
-    u32 pad[2];
-};
-
 enum Mode { kRoundRobin = 0, kWidest = 1 };
 
+// Working set of the global levels.
+// Points travel with their sort: W[buf] holds k coordinate arrays and one
+// index array (SoA, `stride` u32 each) in IN-ORDER layout -- the level-l
+// segment of node F(l)+j occupies [ib(j), ib(j) + ss(j)), and every finished
+// node stays at its own in-order slot, so splitting a segment moves nothing.
+// Each segment's data lives in W[parity] and flips buffer only on the digit
+// passes that actually reorder it.
 struct Buffers {
-    u32* keys[2];
-    u32* vals[2];
-    u32* hist;        // [nseg][4][256]
-    u32* seg_and;     // [nseg]
-    u32* seg_or;      // [nseg]
+    u32* w[2];
+    u64 stride;
+    u32* hist;        // [nseg][4][256] digit counts of the level's keys
+    u32* seg_and;     // [nseg] AND of keys  \  digit d of segment j is constant
+    u32* seg_or;      // [nseg] OR of keys   /  iff ((and ^ or) >> 8d) & 255 == 0
+    uint8_t* state[2];  // per level (l & 1): parity_in << 4 | mask of passes to run
     u64* status;      // [tiles][256] decoupled-lookback words
     u32* tile_ctr;    // one counter per pass launch
-    LevelPlan* plan;
     u32* err;         // [0] non-finite flag
-    float* boxes[2];  // widest: per-level node boxes [nseg][2k] (lo..., hi...)
+    float* boxes[2];  // widest: boxes of the level's nodes [nseg][2k]
 };
 
 struct BuildParams {
@@ -43,12 +39,17 @@ struct BuildParams {
     u32* dbg;              // optional per-level trace (single-subtree builds)
 };
 
+__device__ __host__ __forceinline__ u32* warr(const Buffers& bf, u32 buf, int a) {
+    return bf.w[buf] + (u64)a * bf.stride;
+}
+
 // global_sort.cu
-int global_items_for_bits(int b);
-void launch_rekey_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
+void launch_init(const BuildParams& bp, const Buffers& bf, cudaStream_t st);
+void launch_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
 void launch_plan(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
 void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch,
                  u32* tile_ctr, cudaStream_t st);
+void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
 
 // subtree.cu
 size_t subtree_smem_bytes(int b, int k, int mode);

@@ -30,9 +30,9 @@ constexpr int kMaxK = 16;
 struct SubtreeArgs {
     u64 n;
     int L, lam0, k, mode, M;
-    const u32* vals[2];
-    const LevelPlan* plan;
-    int identity_vals;
+    const u32* w[2];          // global-level working set (SoA, in-order)
+    u64 stride;
+    const uint8_t* prev_state;  // plan state of level lam0-1
     const float* pts;
     float* out_pts;
     u32* perm;
@@ -74,7 +74,7 @@ __device__ __forceinline__ void block_pass(const u32* __restrict__ Ein, u32* __r
             bool valid = p < m;
             u32 e = valid ? Ein[p] : 0u;
             u32 d = valid ? digit(e) : (0x1000u | lane);
-            u32 peers = __match_any_sync(kFullMask, d);
+            u32 peers = warp_peers<8>(d, valid);
             int leader = __ffs(peers) - 1;
             u32 c = 0;
             if (lane == leader && valid) {
@@ -166,15 +166,25 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
 
     const u64 j = blockIdx.x;
     const LevelGeom g0 = make_geom(a.n, a.lam0);
-    const u64 base = a.lam0 == 0 ? 0ull : seg_begin(g0, j);
     const int m = (int)(a.lam0 == 0 ? a.n : seg_size(g0, j));
-    const u32* vin = a.identity_vals ? nullptr : a.vals[a.plan->next_sel] + base;
-
-    // gather the subtree's points (one HBM read per point for all levels)
+    // the subtree's points: the whole input for a single-CTA build, else its
+    // in-order range of the global levels' working set (contiguous, so the
+    // load is coalesced -- no gather)
+    const u32* src = nullptr;
+    const u32* vin = nullptr;
+    if (a.lam0 > 0) {
+        const uint8_t st = a.prev_state[j >> 1];
+        const u32 par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
+        src = a.w[par] + seg_ibegin(g0, j);
+        vin = src + (u64)k * a.stride;
+    }
     for (int lid = tid; lid < m; lid += kSubThreads) {
-        u32 idx = vin ? vin[lid] : (u32)lid;
-        const float* q = a.pts + (u64)idx * k;
-        for (int c = 0; c < k; ++c) P[c * M + lid] = __ldg(q + c);
+        if (src) {
+            for (int c = 0; c < k; ++c) P[c * M + lid] = __uint_as_float(src[(u64)c * a.stride + lid]);
+        } else {
+            const float* q = a.pts + (u64)lid * k;
+            for (int c = 0; c < k; ++c) P[c * M + lid] = q[c];
+        }
         E[0][lid] = (u32)lid;
     }
     if (a.mode == kWidest) {
@@ -309,10 +319,10 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStre
     a.k = bp.k;
     a.mode = bp.mode;
     a.M = (1 << bp.b) - 1;
-    a.vals[0] = bf.vals[0];
-    a.vals[1] = bf.vals[1];
-    a.plan = bf.plan;
-    a.identity_vals = lam0 == 0;
+    a.w[0] = bf.w[0];
+    a.w[1] = bf.w[1];
+    a.stride = bf.stride;
+    a.prev_state = bf.state[(lam0 + 1) & 1];
     a.pts = bp.pts;
     a.out_pts = bp.out_pts;
     a.perm = bp.perm;

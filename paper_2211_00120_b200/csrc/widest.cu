@@ -80,8 +80,7 @@ void launch_widest_root(const BuildParams& bp, const u32* d_minmax, float* box0,
 // children of level-lp nodes: box_c = box_parent clipped by the parent's
 // plane (left: hi, right: lo), dim_c = first argmax of f64 widths
 __global__ void widest_nodes_kernel(u64 n, int lp, const float* __restrict__ boxes_in, float* boxes_out,
-                                    uint8_t* split_dims, const u32* __restrict__ perm,
-                                    const float* __restrict__ pts, int k) {
+                                    uint8_t* split_dims, const float* __restrict__ out_pts, int k) {
     u64 nchild = 2ull << lp;
     u64 c = blockIdx.x * (u64)blockDim.x + threadIdx.x;
     if (c >= nchild) return;
@@ -91,7 +90,7 @@ __global__ void widest_nodes_kernel(u64 n, int lp, const float* __restrict__ box
     u64 pj = c >> 1;
     u64 s = Fp + pj;
     int d = split_dims[s];
-    float plane = __ldg(pts + (u64)perm[s] * k + d);
+    float plane = out_pts[s * k + d];  // the parent's point, just placed
     float lo[kMaxKW], hi[kMaxKW];
     for (int q = 0; q < k; ++q) { lo[q] = boxes_in[pj * 2 * k + q]; hi[q] = boxes_in[pj * 2 * k + k + q]; }
     if ((c & 1ull) == 0) { if (plane < hi[d]) hi[d] = plane; }   // left child
@@ -104,8 +103,8 @@ void launch_widest_nodes(const BuildParams& bp, int parent_level, const float* b
                          cudaStream_t st) {
     u64 nchild = 2ull << parent_level;
     unsigned blocks = (unsigned)((nchild + 255) / 256);
-    widest_nodes_kernel<<<blocks, 256, 0, st>>>(bp.n, parent_level, boxes_in, boxes_out, bp.split_dims, bp.perm,
-                                                bp.pts, bp.k);
+    widest_nodes_kernel<<<blocks, 256, 0, st>>>(bp.n, parent_level, boxes_in, boxes_out, bp.split_dims,
+                                                bp.out_pts, bp.k);
 }
 
 }  // namespace lbkd
