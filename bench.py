@@ -1,0 +1,364 @@
+"""Benchmark: Mpoints/s of one full k-d tree build (float3 uniform, N=100M).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" is one complete build of N points (BASELINE.json metric: build
+Mpoints/s for float3 N=100M, round-robin split dims).  Rank 0 prints ONE
+JSON line.
+
+- value: device-resident throughput -- points already in HBM when the timed
+  region starts, level-order points + permutation in HBM when it ends; CUDA
+  events on the build stream around K back-to-back builds (inputs of 1.2 GB
+  and a 3.2 GB working set exceed the 126 MB L2, so no flush is needed).
+- e2e: the same build through the C-ABI with HOST buffers: pinned host points
+  -> H2D -> lbkd_build_rr -> D2H of the level-order points and permutation,
+  all inside the timed region.
+- roofline: the dominant kernel (the onesweep digit pass) -- its algorithmic
+  bytes (each reordered point reads and writes its k coordinates + index)
+  over its device time, both measured inside the library with CUDA events
+  on the build stream during the timed region (lbkd_set_profile).
+- cpu_baseline: the CPU oracle port (oracle/, a C restatement of the
+  reference's tag-and-sort loop) on a bounded sample of the same workload.
+- --impl reference: the reference path on the host cores: the oracle port
+  (the reference is pure Python and does not travel to the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CPU_SAMPLE_N = 4_000_000
+
+
+def survey_model_bytes(n: int, k: int, widest: bool = False) -> float:
+    """SURVEY.md §8(d) fixed algorithmic-byte model of the prescribed
+    tag-and-sort algorithm (u64 key + u32 index LSD radix, 8-bit digits,
+    constant tag digits skipped)."""
+    L = n.bit_length()
+    db = (k - 1).bit_length() if widest else 0
+    B = 0.0
+    for l in range(L - 1):
+        t = 0 if l == 0 else l + 1 + db
+        P = -(-(32 + t) // 8)
+        B += 24.0 * n * P + 8.0 * n + 24.0 * n
+    B += (4 * k + 12) * n + (8 + 8 * k) * n
+    if widest:
+        B += 4 * k * n + 8 * n * (L - 1)
+    return B
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_pass_kernel.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    def __init__(self):
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            local = int(os.environ.get("LOCAL_RANK", "0"))
+            vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+            dev = vis[local] if local < len(vis) else str(local)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", dev,
+                 f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(k: int, dist: str):
+    from oracle import oracle
+    from paper_2211_00120_b200 import datagen
+
+    pts = datagen.make(dist, CPU_SAMPLE_N, k, seed=0)
+    oracle.set_threads(0)
+    oracle.build_rr(pts[:1000])
+    t = oracle.timed_build(pts, "rr")
+    return {
+        "value": round(CPU_SAMPLE_N / t / 1e6, 4),
+        "unit": "Mpoints/s",
+        "cores": oracle.threads(),
+        "kind": "port",
+        "sample": f"one build of {CPU_SAMPLE_N:,} {dist} float{k} points (same generator), "
+                  f"{t:.2f} s; oracle/lbkd_oracle.c (stable merge sort per level like np.lexsort, "
+                  f"single-threaded; OpenMP update pass)",
+    }
+
+
+def run_reference(args):
+    """--impl reference: the reference path on the host cores (oracle port)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    from paper_2211_00120_b200 import datagen
+
+    sample = int(os.environ.get("BENCH_REF_SAMPLE", "1000000"))
+    pts = datagen.make(args.dist, sample, args.k, seed=0)
+    oracle.set_threads(0)
+    for _ in range(args.warmup):
+        oracle.timed_build(pts, "rr" if args.mode == "rr" else "widest")
+    ts = [oracle.timed_build(pts, "rr" if args.mode == "rr" else "widest") for _ in range(args.steps)]
+    total = sum(ts)
+    value = sample * args.steps / total / 1e6
+    line = {
+        "impl": "reference",
+        "metric": "Mpoints/s kd-tree build (float3, N=100M)",
+        "value": round(value, 4),
+        "unit": "Mpoints/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1000 * total / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.dist} float{args.k} {args.mode}, bounded CPU sample of N={sample:,} "
+                               f"(the N={args.n:,} build would take ~20 min on the host)",
+                   "n": sample, "k": args.k, "mode": args.mode},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpoints/s", "cores": oracle.threads(), "kind": "port",
+                         "sample": f"{args.steps} builds of {sample:,} points"},
+        "e2e": {"value": round(value, 4), "unit": "Mpoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=100_000_000)
+    ap.add_argument("--k", type=int, default=3)
+    ap.add_argument("--mode", default="rr", choices=["rr", "widest"])
+    ap.add_argument("--dist", default="uniform")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2211_00120_b200 as kd
+    from paper_2211_00120_b200 import _native, datagen
+
+    n, k = args.n, args.k
+    pts = datagen.make(args.dist, n, k, seed=rank)
+    h_pts = torch.from_numpy(pts).pin_memory()
+    d_pts = h_pts.to(dev)
+    out = torch.empty_like(d_pts)
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    dims = torch.zeros(n, dtype=torch.uint8, device=dev) if args.mode == "widest" else None
+
+    def build(src, dst, pm):
+        if args.mode == "rr":
+            kd.build_round_robin_cuda(src, out=dst, perm=pm, check_finite=False)
+        else:
+            kd.build_widest_cuda(src, out=dst, perm=pm, split_dims=dims, check_finite=False)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        build(d_pts, out, perm)
+    launches = kd.builder.last_launch_count(local)
+
+    # ---- device-resident timed region
+    _native.set_profile(True, local)
+    sampler = ClockSampler()
+    sampler.start()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        build(d_pts, out, perm)
+    t1.record()
+    barrier()
+    clocks = sampler.stop()
+    ms = t0.elapsed_time(t1)
+    n_pass, pass_ms, pass_bytes = _native.profile_read(local)
+    _native.set_profile(False, local)
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+
+    # ---- end to end through the C-ABI with host buffers
+    h_out = torch.empty((n, k), dtype=torch.float32).pin_memory()
+    h_perm = torch.empty(n, dtype=torch.int32).pin_memory()
+    d_in = torch.empty_like(d_pts)
+
+    def e2e_step():
+        d_in.copy_(h_pts, non_blocking=True)
+        build(d_in, out, perm)
+        h_out.copy_(out, non_blocking=True)
+        h_perm.copy_(perm, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_t.item())
+
+    # ---- correctness spot check of the benchmarked output (permutation)
+    p = perm.cpu().numpy().view(np.uint32)
+    ok = bool(np.array_equal(np.bincount(p, minlength=n), np.ones(n, dtype=np.int64)))
+
+    if rank == 0:
+        total_pts = n * world * args.steps
+        value = total_pts / (ms / 1000.0) / 1e6
+        peak, peak_src = measured_peak()
+        achieved = (pass_bytes / (pass_ms / 1000.0)) / 1e9 if pass_ms > 0 else 0.0
+        traffic, _ = ncu_traffic()
+        model_B = survey_model_bytes(n, k, args.mode == "widest")
+        step_s = ms / 1000.0 / args.steps
+        line = {
+            "metric": "Mpoints/s kd-tree build (float3, N=100M)",
+            "value": round(value, 2),
+            "unit": "Mpoints/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {
+                "workload": f"{args.dist} float{k} {'round-robin' if args.mode == 'rr' else 'widest'} build, N={n:,}",
+                "n": n, "k": k, "mode": args.mode, "distribution": f"{args.dist}[0,1) float32, numpy PCG64 seed={rank}",
+                "l2": "inputs 1.2 GB + 3.2 GB working set exceed the 126 MB L2 (no flush needed)",
+                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            },
+            "e2e": {
+                "value": round(total_pts / (e2e_ms / 1000.0) / 1e6, 2),
+                "unit": "Mpoints/s",
+                "h2d_bytes_per_step": n * k * 4,
+                "d2h_bytes_per_step": n * k * 4 + n * 4,
+            },
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "pass_kernel (onesweep digit pass)",
+                "achieved": round(achieved, 1),
+                "peak": peak,
+                "unit": "GB/s",
+                "frac": round(achieved / peak, 4),
+                "traffic": traffic,
+                "peak_source": peak_src,
+                "launches_per_build": n_pass,
+                "kernel_ms_per_build": round(pass_ms, 3),
+                "kernel_share_of_step": round(pass_ms / (ms / args.steps), 4),
+                "algorithmic_bytes_per_build": pass_bytes,
+            },
+            "model": {
+                "note": "SURVEY.md 8(d) fixed byte model of the 64-bit-key tag-and-sort algorithm",
+                "bytes": model_B,
+                "achieved_gbs": round(model_B / step_s / 1e9, 1),
+                "frac": round(model_B / step_s / 1e9 / peak, 4),
+            },
+            "gpu_launches": int(launches * args.steps),
+            "clocks": clocks,
+            "output_is_permutation": ok,
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(k, args.dist)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

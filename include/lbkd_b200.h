@@ -91,6 +91,14 @@ int64_t lbkd_single_cta_capacity(int k, int widest);
 int lbkd_plan_info(int64_t n, int k, int widest, int *b, int *lam0);
 /* Kernel launches enqueued by the last build on this context. */
 int64_t lbkd_last_launch_count(const lbkd_ctx *ctx);
+/* Profiling: with lbkd_set_profile(ctx, 1) every digit-pass launch of the
+ * next builds is bracketed by CUDA events on the build stream and counts the
+ * points it reorders; lbkd_profile_read() returns, for the LAST build, the
+ * number of digit-pass launches, their summed device time and their
+ * algorithmic bytes (each reordered point reads and writes its k coordinates
+ * and its index once).  Synchronises on the events. */
+void lbkd_set_profile(lbkd_ctx *ctx, int on);
+int lbkd_profile_read(lbkd_ctx *ctx, int *n_pass_launches, double *pass_ms, double *pass_bytes);
 const char *lbkd_strerror(int code);
 const char *lbkd_last_cuda_error(void);
 

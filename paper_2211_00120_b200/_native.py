@@ -30,6 +30,7 @@ EXPORTED = (
     "lbkd_update_tags_rr", "lbkd_update_tags_widest",
     "lbkd_num_levels", "lbkd_single_cta_capacity", "lbkd_plan_info",
     "lbkd_last_launch_count", "lbkd_strerror", "lbkd_last_cuda_error",
+    "lbkd_set_profile", "lbkd_profile_read",
 )
 
 _lib = None
@@ -86,6 +87,11 @@ def load():
         lib.lbkd_plan_info.restype = i32
         lib.lbkd_last_launch_count.argtypes = [vp]
         lib.lbkd_last_launch_count.restype = i64
+        lib.lbkd_set_profile.argtypes = [vp, i32]
+        lib.lbkd_set_profile.restype = None
+        dp = ctypes.POINTER(ctypes.c_double)
+        lib.lbkd_profile_read.argtypes = [vp, ctypes.POINTER(i32), dp, dp]
+        lib.lbkd_profile_read.restype = i32
         lib.lbkd_strerror.argtypes = [i32]
         lib.lbkd_strerror.restype = ctypes.c_char_p
         lib.lbkd_last_cuda_error.argtypes = []
@@ -112,6 +118,21 @@ def context(device: int):
 def check(rc: int, where: str) -> None:
     if rc != LBKD_OK:
         raise NativeError(rc, where)
+
+
+def profile_read(device: int = 0):
+    """(digit-pass launches, their device ms, their algorithmic bytes) of the
+    last build on this thread's context for `device` (lbkd_set_profile on)."""
+    lib = load()
+    n = ctypes.c_int()
+    ms = ctypes.c_double()
+    by = ctypes.c_double()
+    check(lib.lbkd_profile_read(context(device), ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)), "lbkd_profile_read")
+    return n.value, ms.value, by.value
+
+
+def set_profile(on: bool, device: int = 0) -> None:
+    load().lbkd_set_profile(context(device), 1 if on else 0)
 
 
 def plan_info(n: int, k: int, widest: bool):

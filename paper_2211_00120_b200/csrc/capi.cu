@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include "../../include/lbkd_b200.h"
 #include "kernels.cuh"
 
@@ -44,6 +45,13 @@ struct lbkd_ctx {
     uint8_t* dims_scratch = nullptr;
     u32* minmax = nullptr;
     u32* h_err = nullptr;  // pinned
+    // profiling (lbkd_set_profile): CUDA events around every digit-pass
+    // launch and the number of points each launch reordered
+    int profile = 0;
+    std::vector<cudaEvent_t> ev;
+    int n_ev_used = 0;
+    u64* d_moved = nullptr;
+    int k_last = 0;
 };
 
 static int choose_bits(int k, int mode) {
@@ -113,6 +121,7 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
     }
     if (!c->bf.tile_ctr) {
         if ((rc = grow(c->bf.tile_ctr, dummy, 4 * 64))) return rc;
+        if ((rc = grow(c->d_moved, dummy, 256))) return rc;
         if ((rc = grow(c->bf.err, dummy, 4))) return rc;
         if ((rc = grow(c->minmax, dummy, 2 * LBKD_MAX_K))) return rc;
         CK(cudaMallocHost(&c->h_err, sizeof(u32) * 4));
@@ -166,6 +175,11 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     Buffers& bf = c->bf;
 
     CK(cudaMemsetAsync(bf.tile_ctr, 0, sizeof(u32) * 4 * 64, st));
+    if (c->profile) {
+        CK(cudaMemsetAsync(c->d_moved, 0, sizeof(u64) * 256, st));
+        c->n_ev_used = 0;
+    }
+    c->k_last = k;
     CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
     if (mode == kWidest) {
         CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
@@ -188,7 +202,22 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
         launch_plan(bp, bf, l, st);
         c->launches += 2;
         for (int p = 0; p < 4; ++p) {
-            launch_pass(bp, bf, l, p, c->epoch, bf.tile_ctr + (ctr++ % 256), st);
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (c->profile) {
+                while ((int)c->ev.size() < c->n_ev_used + 2) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreate(&e));
+                    c->ev.push_back(e);
+                }
+                e0 = c->ev[c->n_ev_used];
+                e1 = c->ev[c->n_ev_used + 1];
+                c->n_ev_used += 2;
+                CK(cudaEventRecord(e0, st));
+            }
+            launch_pass(bp, bf, l, p, c->epoch, bf.tile_ctr + (ctr % 256), c->profile ? c->d_moved + (ctr % 256) : nullptr,
+                        st);
+            ++ctr;
+            if (c->profile) CK(cudaEventRecord(e1, st));
             c->epoch = (c->epoch + 1) & 0x3fffffffu;
             if (c->epoch == 0) c->epoch = 1;
             c->launches += 1;
@@ -248,6 +277,8 @@ void lbkd_destroy(lbkd_ctx* c) {
     cudaFree(c->perm_scratch);
     cudaFree(c->dims_scratch);
     cudaFree(c->minmax);
+    cudaFree(c->d_moved);
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->h_err) cudaFreeHost(c->h_err);
     delete c;
 }
@@ -321,6 +352,34 @@ int lbkd_plan_info(int64_t n, int k, int widest, int* b_out, int* lam0_out) {
 }
 
 int64_t lbkd_last_launch_count(const lbkd_ctx* c) { return c ? c->launches : 0; }
+
+void lbkd_set_profile(lbkd_ctx* c, int on) {
+    if (c) c->profile = on ? 1 : 0;
+}
+
+int lbkd_profile_read(lbkd_ctx* c, int* n_pass_launches, double* pass_ms, double* pass_bytes) {
+    if (!c) return LBKD_EINVAL_SHAPE;
+    int n = c->n_ev_used / 2;
+    double ms = 0.0, bytes = 0.0;
+    if (n > 0) {
+        CK(cudaSetDevice(c->device));
+        std::vector<u64> moved(256, 0);
+        CK(cudaMemcpy(moved.data(), c->d_moved, sizeof(u64) * 256, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n; ++i) {
+            float t = 0.f;
+            CK(cudaEventSynchronize(c->ev[2 * i + 1]));
+            CK(cudaEventElapsedTime(&t, c->ev[2 * i], c->ev[2 * i + 1]));
+            ms += t;
+            // algorithmic bytes: every reordered point reads and writes its
+            // k coordinates and its index once
+            bytes += (double)moved[i % 256] * 2.0 * 4.0 * (double)(c->k_last + 1);
+        }
+    }
+    if (n_pass_launches) *n_pass_launches = n;
+    if (pass_ms) *pass_ms = ms;
+    if (pass_bytes) *pass_bytes = bytes;
+    return LBKD_OK;
+}
 
 const char* lbkd_strerror(int code) {
     switch (code) {

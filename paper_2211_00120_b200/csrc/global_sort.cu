@@ -248,6 +248,7 @@ struct PassArgs {
     const uint8_t* state;
     const uint8_t* split_dims;
     u32* tile_ctr;
+    u64* moved;
 };
 
 template <int ITEMS>
@@ -318,6 +319,8 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
                     (src0 << 4) | (src1 << 5);
         S.info[9] = s0b;
         S.info[10] = has1 ? s0e + 1 : 0;  // in-order begin of segment j0+1
+        u64 nact = (act0 ? r0b - r0a : 0) + (act1 ? r1b - r1a : 0);
+        if (nact && a.moved) atomicAdd(a.moved, nact);
         S.info[11] = (u64)seg_dim(a.mode, a.split_dims, g, a.k, j0) |
                      ((u64)(has1 ? seg_dim(a.mode, a.split_dims, g, a.k, j0 + 1) : 0) << 8);
     }
@@ -475,7 +478,7 @@ static void launch_pass_t(const PassArgs& a, unsigned grid, cudaStream_t st) {
 }
 
 void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch, u32* tile_ctr,
-                 cudaStream_t st) {
+                 u64* moved, cudaStream_t st) {
     PassArgs a;
     a.g = make_geom(bp.n, l);
     a.pass = pass;
@@ -486,6 +489,7 @@ void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 
     a.state = bf.state[l & 1];
     a.split_dims = bp.split_dims;
     a.tile_ctr = tile_ctr;
+    a.moved = moved;
     int items = items_for_bits(bp.b);
     const u64 T = (u64)kThreads * items;
     unsigned grid = (unsigned)((bp.n + T - 1) / T);

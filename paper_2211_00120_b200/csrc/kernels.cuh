@@ -23,6 +23,7 @@ struct Buffers {
     uint8_t* state[2];  // per level (l & 1): parity_in << 4 | mask of passes to run
     u64* status;      // [tiles][256] decoupled-lookback words
     u32* tile_ctr;    // one counter per pass launch
+    u64* moved;       // per pass launch: points the launch reordered (profiling)
     u32* err;         // [0] non-finite flag
     float* boxes[2];  // widest: boxes of the level's nodes [nseg][2k]
 };
@@ -48,7 +49,7 @@ void launch_init(const BuildParams& bp, const Buffers& bf, cudaStream_t st);
 void launch_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
 void launch_plan(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
 void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch,
-                 u32* tile_ctr, cudaStream_t st);
+                 u32* tile_ctr, u64* moved, cudaStream_t st);
 void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
 
 // subtree.cu
