@@ -57,7 +57,9 @@ struct lbkd_ctx {
 static int choose_bits(int k, int mode) {
     const size_t limit = 227 * 1024;
     for (int b = 13; b >= 10; --b)
-        if (subtree_smem_bytes(b, k, mode) <= limit) return b;
+        if (subtree_smem_bytes(b, k, mode) <= limit &&
+            (mode != kRoundRobin || subtree_rr_smem_bytes(b, k) <= limit))
+            return b;
     return -1;
 }
 

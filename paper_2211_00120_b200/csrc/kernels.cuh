@@ -54,6 +54,7 @@ void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t
 
 // subtree.cu
 size_t subtree_smem_bytes(int b, int k, int mode);
+size_t subtree_rr_smem_bytes(int b, int k);
 void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStream_t st);
 
 // widest.cu

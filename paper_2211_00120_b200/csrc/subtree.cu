@@ -55,8 +55,8 @@ size_t subtree_smem_bytes(int b, int k, int mode) {
 
 // One stable block-wide counting pass: Eout[rank(e)] = e for the m elements
 // of Ein, ranked by digit(e) in 0..255 with ties kept in Ein order.
-template <typename DigitFn>
-__device__ __forceinline__ void block_pass(const u32* __restrict__ Ein, u32* __restrict__ Eout, int m,
+template <typename ET, typename DigitFn>
+__device__ __forceinline__ void block_pass(const ET* __restrict__ Ein, ET* __restrict__ Eout, int m,
                                            DigitFn digit, unsigned short (*cnt)[256], u32 (*gsum)[256],
                                            u32* scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
@@ -72,7 +72,7 @@ __device__ __forceinline__ void block_pass(const u32* __restrict__ Ein, u32* __r
         if (r < R) {
             int p = warp * C + r * 32 + lane;
             bool valid = p < m;
-            u32 e = valid ? Ein[p] : 0u;
+            u32 e = valid ? (u32)Ein[p] : 0u;
             u32 d = valid ? digit(e) : (0x1000u | lane);
             u32 peers = warp_peers<8>(d, valid);
             int leader = __ffs(peers) - 1;
@@ -129,7 +129,7 @@ __device__ __forceinline__ void block_pass(const u32* __restrict__ Ein, u32* __r
             if (p < m) {
                 u32 d = dr[r] >> 16;
                 u32 slot = gsum[warp >> 3][d] + cnt[warp][d] + (dr[r] & 0xffffu);
-                Eout[slot] = ev[r];
+                Eout[slot] = (ET)ev[r];
             }
         }
     }
@@ -311,6 +311,227 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
     }
 }
 
+// ===========================================================================
+// Round-robin fast path: presorted lists instead of per-level sorts.
+//
+// Within a subtree entered at level lam0 >= k, the order the reference's
+// stable sorts leave inside every node at level l is a FIXED total order
+//     T_d = (c[d], c[d-1], ..., c[d-k+1], input index),  d = l mod k
+// (each level's stable sort by c[d] starts from the previous level's
+// order, and after k levels all coordinates are in the chain; further
+// repeats of a coordinate never decide a comparison).  The entry order is
+// T_{(lam0-1) mod k}; T_d = stable_sort(T_{d-1}, c[d]), so k-1 block radix
+// sorts give all k orders as lists of local ids.  Each level then only
+// (1) reads the pivot of every segment straight off list T_{l mod k} at the
+// reference's pivot offset (kernels_numba.py:21-46) and (2) stably
+// partitions every list that is still needed into the two child segments
+// (one block scan), instead of re-sorting.
+// ===========================================================================
+size_t subtree_rr_smem_bytes(int b, int k) {
+    size_t M = ((size_t)1 << b) - 1;
+    size_t Mp = (M + 8) & ~(size_t)7;  // 16-byte aligned u16 arrays
+    size_t bytes = sizeof(float) * (size_t)k * Mp;   // P
+    bytes += sizeof(unsigned short) * Mp * (k + 1);   // k lists + partition target
+    bytes += sizeof(unsigned short) * Mp;             // seg of each point
+    bytes += Mp;                                      // side of each point
+    size_t nloc = ((size_t)1 << (b - 2));             // segments at the deepest sort level
+    size_t tables = sizeof(unsigned short) * (2 * nloc + 8) + sizeof(u32) * nloc;
+    size_t sortscr = sizeof(unsigned short) * kSubWarps * 256 + sizeof(u32) * 4 * 256;
+    bytes += tables > sortscr ? tables : sortscr;
+    bytes += sizeof(u32) * 64;
+    return (bytes + 15) & ~(size_t)15;
+}
+
+__global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typedef unsigned short u16;
+    const int M = a.M, k = a.k, tid = threadIdx.x;
+    const int Mp = (M + 8) & ~7;
+    unsigned char* sp = smem_raw;
+    float* P = reinterpret_cast<float*>(sp);
+    sp += sizeof(float) * (size_t)k * Mp;
+    u16* Lst[kMaxK + 1];
+    for (int d = 0; d <= k; ++d) {
+        Lst[d] = reinterpret_cast<u16*>(sp);
+        sp += sizeof(u16) * Mp;
+    }
+    u16* segv = reinterpret_cast<u16*>(sp);
+    sp += sizeof(u16) * Mp;
+    unsigned char* side = sp;
+    sp += Mp;
+    sp = reinterpret_cast<unsigned char*>(((uintptr_t)sp + 15) & ~(uintptr_t)15);
+    // tables (levels) alias the radix-sort scratch (chain sorts)
+    const int nmax = (M + 1) / 4;  // 2^(b-2) segments at the deepest sort level
+    u16* lbt = reinterpret_cast<u16*>(sp);
+    u16* pot = lbt + nmax + 8;
+    u32* segpre = reinterpret_cast<u32*>(pot + nmax);
+    unsigned short(*cnt)[256] = reinterpret_cast<unsigned short(*)[256]>(sp);
+    u32(*gsum)[256] = reinterpret_cast<u32(*)[256]>(sp + sizeof(unsigned short) * kSubWarps * 256);
+    size_t tables = sizeof(u16) * (2 * (size_t)nmax + 8) + sizeof(u32) * nmax;
+    size_t sortscr = sizeof(unsigned short) * kSubWarps * 256 + sizeof(u32) * 4 * 256;
+    u32* scratch = reinterpret_cast<u32*>(sp + (tables > sortscr ? tables : sortscr));
+
+    const u64 j = blockIdx.x;
+    const LevelGeom g0 = make_geom(a.n, a.lam0);
+    const int m = (int)seg_size(g0, j);
+    const uint8_t st = a.prev_state[j >> 1];
+    const u32 par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
+    const u32* src = a.w[par] + seg_ibegin(g0, j);
+    const u32* vin = src + (u64)k * a.stride;
+    const int e = (a.lam0 - 1) % k;  // dimension of the entry order
+    for (int lid = tid; lid < m; lid += kSubThreads) {
+        for (int c = 0; c < k; ++c) P[c * Mp + lid] = __uint_as_float(src[(u64)c * a.stride + lid]);
+        Lst[e][lid] = (u16)lid;
+        segv[lid] = 0;
+    }
+    __syncthreads();
+
+    // ---- chain sorts: T_d = stable_sort(T_{d-1}, c[d]) for the k-1 other dims
+    for (int q = 1; q < k; ++q) {
+        const int d = (e + q) % k;
+        const int dprev = (e + q - 1) % k;
+        const float* Pd = P + d * Mp;
+        u32 x_and = 0xffffffffu, x_or = 0u;
+        for (int p = tid; p < m; p += kSubThreads) {
+            u32 kk = flip_key(Pd[p]);
+            x_and &= kk;
+            x_or |= kk;
+        }
+        x_and = __reduce_and_sync(kFullMask, x_and);
+        x_or = __reduce_or_sync(kFullMask, x_or);
+        if ((tid & 31) == 0) scratch[32 + (tid >> 5)] = x_and ^ x_or;
+        __syncthreads();
+        u32 vary = 0;
+        for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
+        __syncthreads();
+        const u16* in = Lst[dprev];
+        u16* outA = Lst[d];
+        u16* outB = Lst[k];  // spare
+        int npass = 0;
+        for (int b = 0; b < 4; ++b) {
+            if (((vary >> (8 * b)) & 255u) == 0) continue;
+            u16* out = (npass & 1) ? outB : outA;
+            const int sh = 8 * b;
+            block_pass(in, out, m, [&](u32 lid) { return (flip_key(Pd[lid]) >> sh) & 255u; }, cnt, gsum, scratch);
+            in = out;
+            ++npass;
+        }
+        if (npass == 0) {
+            for (int p = tid; p < m; p += kSubThreads) outA[p] = Lst[dprev][p];
+            __syncthreads();
+        } else if (npass & 1) {
+            // result in outA == Lst[d]
+        } else {
+            // result in the spare list: swap roles
+            Lst[k] = outA;
+            Lst[d] = outB;
+        }
+    }
+
+    auto write_node = [&](u64 node, u32 lid) {
+        a.perm[node] = vin[lid];
+        float* dst = a.out_pts + node * (u64)k;
+        for (int c = 0; c < k; ++c) dst[c] = P[c * Mp + lid];
+    };
+
+    for (int lam = a.lam0; lam <= a.L - 2; ++lam) {
+        const LevelGeom g = make_geom(a.n, lam);
+        const int dl = lam - a.lam0;
+        const int nloc = 1 << dl;
+        const u64 J0 = j << dl;
+        const u64 lb0 = seg_begin(g, J0);
+        const int mc = m - (nloc - 1);
+        const int ad = lam % k;
+        const bool last = (lam == a.L - 2);
+        const LevelGeom gn = make_geom(a.n, lam + 1);
+        for (int t = tid; t < nloc; t += kSubThreads) {
+            lbt[t] = (u16)(seg_begin(g, J0 + t) - lb0);
+            pot[t] = (u16)pivot_off(g, J0 + t);
+        }
+        if (tid == 0) lbt[nloc] = (u16)mc;
+        __syncthreads();
+
+        // (1) the active list: pivots, sides, child segments; its own stable
+        // partition needs no scan (left part precedes the pivot)
+        u16* A = Lst[ad];
+        u16* tmp = Lst[k];
+        for (int p = tid; p < mc; p += kSubThreads) {
+            const u32 lid = A[p];
+            const u32 t = segv[lid];
+            const u32 o = (u32)p - lbt[t];
+            const u32 po = pot[t];
+            if (o == po) {
+                side[lid] = 2;
+                segv[lid] = (u16)(2 * t);
+                write_node(g.Fl + J0 + t, lid);
+                continue;
+            }
+            const u32 r = o > po ? 1u : 0u;
+            side[lid] = (unsigned char)r;
+            segv[lid] = (u16)(2 * t + r);
+            if (last) {
+                write_node(gn.Fl + 2 * (J0 + t) + r, lid);
+            } else {
+                tmp[lbt[t] - t + o - r] = (u16)lid;
+            }
+        }
+        __syncthreads();
+        if (last) break;
+        Lst[k] = A;
+        Lst[ad] = tmp;
+
+        // (2) stable partition of every other list still needed later
+        for (int d = 0; d < k; ++d) {
+            if (d == ad) continue;
+            int next_use = lam + ((d - ad + k) % k);
+            if (next_use > a.L - 2) continue;
+            u16* Ld = Lst[d];
+            u16* Tg = Lst[k];
+            // 8 consecutive positions per thread: packed (right, pivot) counts
+            const int p0 = tid * 8;
+            u32 lid8[8];
+            u32 v8 = 0, run[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int p = p0 + i;
+                u32 lid = p < mc ? Ld[p] : 0u;
+                lid8[i] = lid;
+                u32 s = p < mc ? side[lid] : 0u;
+                run[i] = v8;
+                v8 += (s == 1 ? 1u : 0u) | (s == 2 ? 0x10000u : 0u);
+            }
+            u32 ex = block_exclusive_scan<u32>(v8, scratch, nullptr);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int p = p0 + i;
+                if (p < mc) {
+                    const u32 t = segv[lid8[i]] >> 1;
+                    if ((u32)p == lbt[t]) segpre[t] = ex + run[i];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int p = p0 + i;
+                if (p >= mc) break;
+                const u32 lid = lid8[i];
+                const u32 s = side[lid];
+                if (s == 2) continue;
+                const u32 t = segv[lid] >> 1;
+                const u32 pre = ex + run[i] - segpre[t];
+                const u32 rb = pre & 0xffffu, pb = pre >> 16;
+                const u32 base = lbt[t] - t;
+                const u32 dst = s ? base + pot[t] + rb : base + ((u32)p - lbt[t]) - rb - pb;
+                Tg[dst] = (u16)lid;
+            }
+            __syncthreads();
+            Lst[k] = Ld;
+            Lst[d] = Tg;
+        }
+    }
+    if (a.lam0 > a.L - 2 && tid == 0 && m == 1) write_node(g0.Fl + j, 0u);
+}
+
 void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStream_t st) {
     SubtreeArgs a;
     a.n = bp.n;
@@ -329,9 +550,15 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStre
     a.split_dims = bp.split_dims;
     a.boxes0 = bf.boxes[lam0 & 1];
     a.dbg = bp.dbg;
+    unsigned grid = (unsigned)(1ull << lam0);
+    if (bp.mode == kRoundRobin && lam0 >= bp.k) {
+        size_t sm = subtree_rr_smem_bytes(bp.b, bp.k);
+        cudaFuncSetAttribute(subtree_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        subtree_rr_kernel<<<grid, kSubThreads, sm, st>>>(a);
+        return;
+    }
     size_t sm = subtree_smem_bytes(bp.b, bp.k, bp.mode);
     cudaFuncSetAttribute(subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    unsigned grid = (unsigned)(1ull << lam0);
     subtree_kernel<<<grid, kSubThreads, sm, st>>>(a);
 }
 
