@@ -90,13 +90,14 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
     size_t dummy = 0;
     int rc;
     // W[2] holds k+1 SoA arrays of n words each (only when global levels run)
-    size_t need_w = lam0 > 0 ? (size_t)(k + 1) * n : 0;
+    const size_t stride = (n + 3) & ~(size_t)3;  // 16-byte aligned arrays
+    size_t need_w = lam0 > 0 ? (size_t)(k + 1) * stride : 0;
     if (need_w > c->cap_w) {
         for (int i = 0; i < 2; ++i)
             if ((rc = grow(c->bf.w[i], dummy, need_w))) return rc;
         c->cap_w = need_w;
     }
-    c->bf.stride = n;
+    c->bf.stride = stride;
     if (n > c->cap_n) {
         if ((rc = grow(c->perm_scratch, dummy, n))) return rc;
         if ((rc = grow(c->dims_scratch, dummy, n))) return rc;

@@ -268,6 +268,10 @@ __device__ __forceinline__ void cp_async4(u32* smem_dst, const u32* gsrc) {
     u32 s = (u32)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16(u32* smem_dst, const u32* gsrc) {
+    u32 s = (u32)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int ITEMS>
@@ -337,13 +341,23 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
 
     // --- stage the payload of the active elements (all k+1 arrays) with
     // cp.async while the keys are ranked
+    // 16-byte chunks (stride is a multiple of 4 words); only a chunk that
+    // straddles a part boundary falls back to per-word copies
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
-        bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
-        if (in0 || in1) {
-            const u32* base = a.bf.w[in1 ? src1 : src0] + ts + r;
-            for (int c = 0; c < A; ++c) cp_async4(raw + c * T + r, base + (u64)c * a.bf.stride);
+    for (u32 chunk = tid; chunk < (u32)T / 4u; chunk += kThreads) {
+        const u32 r = chunk * 4u;
+        const bool all0 = r >= r0a && r + 4 <= r0b, all1 = r >= r1a && r + 4 <= r1b;
+        const bool any0 = r < r0b && r + 4 > r0a, any1 = r < r1b && r + 4 > r1a;
+        if (all0 || all1) {
+            const u32* g = a.bf.w[all1 ? src1 : src0] + ts + r;
+            for (int c = 0; c < A; ++c) cp_async16(raw + c * T + r, g + (u64)c * a.bf.stride);
+        } else if (any0 || any1) {
+            for (u32 q = r; q < r + 4; ++q) {
+                const bool in0 = q >= r0a && q < r0b, in1 = q >= r1a && q < r1b;
+                if (!(in0 || in1)) continue;
+                const u32* g = a.bf.w[in1 ? src1 : src0] + ts + q;
+                for (int c = 0; c < A; ++c) cp_async4(raw + c * T + q, g + (u64)c * a.bf.stride);
+            }
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -369,7 +383,8 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
         u32 dg = (flip_key(__uint_as_float(key[i])) >> shift) & 255u;
         u32 b = in0 ? dg : (in1 ? (dg | 256u) : (0x1000u | lane));
         br[i] = b;
-        peers[i] = warp_peers<9>(b, in0 || in1);
+        // the segment bit only matters in the (rare) two-segment tiles
+        peers[i] = (flags & 4u) ? warp_peers<9>(b, in0 || in1) : warp_peers<8>(b, in0 || in1);
     }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -462,11 +477,14 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
     const u32 split1 = S.bstart[256];
     u32* dst0 = a.bf.w[src0 ^ 1u];
     u32* dst1 = a.bf.w[src1 ^ 1u];
+    const u64 stride = a.bf.stride;
     for (u32 i = tid; i < nact; i += kThreads) {
-        const u32 r = S.inv[i];
-        const u64 off = S.dstoff[i];
-        u32* dst = (i >= split1) ? dst1 : dst0;
-        for (int c = 0; c < A; ++c) dst[(u64)c * a.bf.stride + off] = raw[c * T + r];
+        const u32* rp = raw + S.inv[i];
+        u32* d = ((i >= split1) ? dst1 : dst0) + S.dstoff[i];
+        for (int c = 0; c < A; ++c) {
+            *d = rp[c * T];
+            d += stride;
+        }
     }
 }
 
