@@ -78,6 +78,25 @@ int lbkd_build_rr_trace(lbkd_ctx *ctx, const float *d_points, float *d_points_ou
 int lbkd_build_widest_trace(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int64_t n, int k,
                             uint32_t *d_perm, uint8_t *d_split_dims, uint32_t *d_trace, void *stream);
 
+/* Multi-device sharding (no reference counterpart -- the
+ * reference is single-process).  After the top `top_levels` levels the
+ * 2^top_levels subtrees are independent:
+ *  - lbkd_build_rr_top: on the device holding the input, build levels
+ *    0..top_levels-1 (nodes written to d_out/d_perm at their global slots) and
+ *    pack subtree j's points into d_sub: array c (c < k: coordinate c as
+ *    float bits, c == k: input row) at d_sub + c*sub_stride + off_j, where
+ *    off_j = segment_begin(F(top)+j) - F(top) (treemath.py:108-126), in the
+ *    order the reference's sort leaves them (needed for its tie-break).
+ *  - lbkd_build_rr_sub: on any device, finish the subtree rooted at
+ *    (root_level, root_index) of an n_total-point tree from its packed
+ *    points; nodes land at their global level-order slots of the full-size
+ *    d_out / d_perm.
+ * Results are bit-identical to lbkd_build_rr. */
+int lbkd_build_rr_top(lbkd_ctx *ctx, const float *d_points, int64_t n, int k, int top_levels, float *d_out,
+                      uint32_t *d_perm, uint32_t *d_sub, int64_t sub_stride, void *stream);
+int lbkd_build_rr_sub(lbkd_ctx *ctx, const uint32_t *d_sub, int64_t sub_stride, int64_t n_total, int k,
+                      int root_level, int64_t root_index, float *d_out, uint32_t *d_perm, void *stream);
+
 /* The accel plugin seam (accel.py:48-58): in-place tag refinement. */
 int lbkd_update_tags_rr(uint32_t *d_tags, int64_t n, int levels, int l, void *stream);
 int lbkd_update_tags_widest(uint32_t *d_tags, const double *d_coords, int k, uint8_t *d_split_dims,

@@ -31,6 +31,7 @@ EXPORTED = (
     "lbkd_num_levels", "lbkd_single_cta_capacity", "lbkd_plan_info",
     "lbkd_last_launch_count", "lbkd_strerror", "lbkd_last_cuda_error",
     "lbkd_set_profile", "lbkd_profile_read",
+    "lbkd_build_rr_top", "lbkd_build_rr_sub",
 )
 
 _lib = None
@@ -75,6 +76,10 @@ def load():
         lib.lbkd_build_rr_trace.restype = i32
         lib.lbkd_build_widest_trace.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp, vp]
         lib.lbkd_build_widest_trace.restype = i32
+        lib.lbkd_build_rr_top.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, i64, vp]
+        lib.lbkd_build_rr_top.restype = i32
+        lib.lbkd_build_rr_sub.argtypes = [vp, vp, i64, i64, i32, i32, i64, vp, vp, vp]
+        lib.lbkd_build_rr_sub.restype = i32
         lib.lbkd_update_tags_rr.argtypes = [vp, i64, i32, i32, vp]
         lib.lbkd_update_tags_rr.restype = i32
         lib.lbkd_update_tags_widest.argtypes = [vp, vp, i32, vp, vp, vp, i64, i32, i32, i32, vp]

@@ -36,6 +36,7 @@ struct lbkd_ctx {
     int device = 0;
     int check = 1;
     u32 epoch = 1;
+    int ctr = 0;
     int64_t launches = 0;
     // grow-only device allocations
     size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_w = 0, cap_copy = 0;
@@ -132,14 +133,86 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
     return LBKD_OK;
 }
 
-static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in, int k, u32* d_perm,
-                 uint8_t* d_dims, u32* d_trace, int mode, cudaStream_t st) {
+// the global levels [lfrom, lto) of the view bp (hist -> plan -> up to four
+// digit passes -> pivots [-> widest child dims])
+static int run_levels(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cudaStream_t st) {
+    Buffers& bf = c->bf;
+    for (int l = lfrom; l < lto; ++l) {
+        const u64 nseg = 1ull << (l - bp.lroot);
+        CK(cudaMemsetAsync(bf.hist, 0, nseg * 1024 * sizeof(u32), st));
+        CK(cudaMemsetAsync(bf.seg_and, 0xff, nseg * sizeof(u32), st));
+        CK(cudaMemsetAsync(bf.seg_or, 0, nseg * sizeof(u32), st));
+        launch_hist(bp, bf, l, st);
+        launch_plan(bp, bf, l, st);
+        c->launches += 2;
+        for (int p = 0; p < 4; ++p) {
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (c->profile) {
+                while ((int)c->ev.size() < c->n_ev_used + 2) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreate(&e));
+                    c->ev.push_back(e);
+                }
+                e0 = c->ev[c->n_ev_used];
+                e1 = c->ev[c->n_ev_used + 1];
+                c->n_ev_used += 2;
+                CK(cudaEventRecord(e0, st));
+            }
+            launch_pass(bp, bf, l, p, c->epoch, bf.tile_ctr + (c->ctr % 256),
+                        c->profile ? c->d_moved + (c->ctr % 256) : nullptr, st);
+            ++c->ctr;
+            if (c->profile) CK(cudaEventRecord(e1, st));
+            c->epoch = (c->epoch + 1) & 0x3fffffffu;
+            if (c->epoch == 0) c->epoch = 1;
+            c->launches += 1;
+        }
+        launch_pivots(bp, bf, l, st);
+        c->launches += 1;
+        if (bp.mode == kWidest) {
+            launch_widest_nodes(bp, l, bf.boxes[l & 1], bf.boxes[(l + 1) & 1], st);
+            c->launches += 1;
+        }
+    }
+    return LBKD_OK;
+}
+
+static int begin_build(lbkd_ctx* c, int k, cudaStream_t st) {
+    Buffers& bf = c->bf;
+    CK(cudaMemsetAsync(bf.tile_ctr, 0, sizeof(u32) * 4 * 64, st));
+    if (c->profile) {
+        CK(cudaMemsetAsync(c->d_moved, 0, sizeof(u64) * 256, st));
+        c->n_ev_used = 0;
+    }
+    c->k_last = k;
+    c->ctr = 0;
+    CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
+    return LBKD_OK;
+}
+
+static int end_build(lbkd_ctx* c, cudaStream_t st) {
+    CK(cudaGetLastError());
+    if (c->check) {
+        CK(cudaMemcpyAsync(c->h_err, c->bf.err, sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (c->h_err[0]) return LBKD_ENONFINITE;
+    }
+    return LBKD_OK;
+}
+
+static int check_args(lbkd_ctx* c, int64_t n_in, int k, int mode) {
     if (!c || n_in < 0 || k < 1 || k > LBKD_MAX_K) return LBKD_EINVAL_SHAPE;
     if (n_in > 0x7fffffffll) return LBKD_ECAPACITY;
     if (mode == kWidest) {
         int db = bit_length((u64)(k - 1));
         if ((n_in << db) > 0x7fffffffll) return LBKD_ECAPACITY;
     }
+    return LBKD_OK;
+}
+
+static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in, int k, u32* d_perm,
+                 uint8_t* d_dims, u32* d_trace, int mode, cudaStream_t st) {
+    int rc = check_args(c, n_in, k, mode);
+    if (rc) return rc;
     c->launches = 0;
     if (n_in == 0) return LBKD_OK;
     if (!d_points || !d_out) return LBKD_EINVAL_SHAPE;
@@ -151,7 +224,7 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     const int lam0 = L - b > 0 ? L - b : 0;
     if (d_trace && lam0 > 0) return LBKD_EUNSUPPORTED;
     const bool inplace = (const void*)d_points == (const void*)d_out;
-    int rc = ensure(c, n, k, b, lam0);
+    rc = ensure(c, n, k, b, lam0);
     if (rc) return rc;
 
     BuildParams bp;
@@ -175,72 +248,101 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.perm = d_perm ? d_perm : c->perm_scratch;
     bp.split_dims = d_dims ? d_dims : c->dims_scratch;
     bp.dbg = d_trace;
-    Buffers& bf = c->bf;
-
-    CK(cudaMemsetAsync(bf.tile_ctr, 0, sizeof(u32) * 4 * 64, st));
-    if (c->profile) {
-        CK(cudaMemsetAsync(c->d_moved, 0, sizeof(u64) * 256, st));
-        c->n_ev_used = 0;
-    }
-    c->k_last = k;
-    CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
+    if ((rc = begin_build(c, k, st))) return rc;
     if (mode == kWidest) {
         CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
         CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
         launch_world_bounds(bp, c->minmax, st);
-        launch_widest_root(bp, c->minmax, bf.boxes[0], st);
+        launch_widest_root(bp, c->minmax, c->bf.boxes[0], st);
         c->launches += 2;
     }
-    int ctr = 0;
     if (lam0 > 0) {
-        launch_init(bp, bf, st);
+        launch_init(bp, c->bf, st);
         c->launches += 1;
     }
-    for (int l = 0; l < lam0; ++l) {
-        const u64 nseg = 1ull << l;
-        CK(cudaMemsetAsync(bf.hist, 0, nseg * 1024 * sizeof(u32), st));
-        CK(cudaMemsetAsync(bf.seg_and, 0xff, nseg * sizeof(u32), st));
-        CK(cudaMemsetAsync(bf.seg_or, 0, nseg * sizeof(u32), st));
-        launch_hist(bp, bf, l, st);
-        launch_plan(bp, bf, l, st);
-        c->launches += 2;
-        for (int p = 0; p < 4; ++p) {
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            if (c->profile) {
-                while ((int)c->ev.size() < c->n_ev_used + 2) {
-                    cudaEvent_t e;
-                    CK(cudaEventCreate(&e));
-                    c->ev.push_back(e);
-                }
-                e0 = c->ev[c->n_ev_used];
-                e1 = c->ev[c->n_ev_used + 1];
-                c->n_ev_used += 2;
-                CK(cudaEventRecord(e0, st));
-            }
-            launch_pass(bp, bf, l, p, c->epoch, bf.tile_ctr + (ctr % 256), c->profile ? c->d_moved + (ctr % 256) : nullptr,
-                        st);
-            ++ctr;
-            if (c->profile) CK(cudaEventRecord(e1, st));
-            c->epoch = (c->epoch + 1) & 0x3fffffffu;
-            if (c->epoch == 0) c->epoch = 1;
-            c->launches += 1;
-        }
-        launch_pivots(bp, bf, l, st);
-        c->launches += 1;
-        if (mode == kWidest) {
-            launch_widest_nodes(bp, l, bf.boxes[l & 1], bf.boxes[(l + 1) & 1], st);
-            c->launches += 1;
-        }
-    }
-    launch_subtree(bp, bf, lam0, st);
+    if ((rc = run_levels(c, bp, 0, lam0, st))) return rc;
+    launch_subtree(bp, c->bf, lam0, st);
     c->launches += 1;
-    CK(cudaGetLastError());
-    if (c->check) {
-        CK(cudaMemcpyAsync(c->h_err, bf.err, sizeof(u32), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (c->h_err[0]) return LBKD_ENONFINITE;
-    }
-    return LBKD_OK;
+    return end_build(c, st);
+}
+
+// multi-device, rank 0: the top `top` levels of the whole tree, then the
+// 2^top subtrees' points (k coordinate arrays + index array, in the
+// reference's entry order) packed back to back into d_sub
+static int build_top(lbkd_ctx* c, const float* d_points, int64_t n_in, int k, int top, float* d_out, u32* d_perm,
+                     u32* d_sub, int64_t sub_stride, cudaStream_t st) {
+    int rc = check_args(c, n_in, k, kRoundRobin);
+    if (rc) return rc;
+    c->launches = 0;
+    if (!d_points || !d_out || !d_perm || !d_sub || top < 1) return LBKD_EINVAL_SHAPE;
+    CK(cudaSetDevice(c->device));
+    const u64 n = (u64)n_in;
+    const int b = choose_bits(k, kRoundRobin);
+    const int L = bit_length(n);
+    const int lam0 = L - b > 0 ? L - b : 0;
+    if (top > lam0) return LBKD_EUNSUPPORTED;  // tree too small to shard
+    if ((u64)sub_stride < n) return LBKD_EINVAL_SHAPE;
+    rc = ensure(c, n, k, b, lam0);
+    if (rc) return rc;
+    BuildParams bp;
+    bp.n = n;
+    bp.k = k;
+    bp.mode = kRoundRobin;
+    bp.b = b;
+    bp.pts = d_points;
+    bp.out_pts = d_out;
+    bp.perm = d_perm;
+    bp.split_dims = c->dims_scratch;
+    bp.dbg = nullptr;
+    if ((rc = begin_build(c, k, st))) return rc;
+    launch_init(bp, c->bf, st);
+    c->launches += 1;
+    if ((rc = run_levels(c, bp, 0, top, st))) return rc;
+    launch_extract(bp, c->bf, top, d_sub, (u64)sub_stride, st);
+    c->launches += 1;
+    return end_build(c, st);
+}
+
+// multi-device, rank j: finish the subtree rooted at (root_level, root_index)
+// of an n_total-point tree from its points in d_sub (as packed by build_top);
+// nodes land at their global level-order slots of d_out / d_perm
+static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t n_total, int k, int root_level,
+                     int64_t root_index, float* d_out, u32* d_perm, cudaStream_t st) {
+    int rc = check_args(c, n_total, k, kRoundRobin);
+    if (rc) return rc;
+    c->launches = 0;
+    if (!d_sub || !d_out || !d_perm || root_level < 0) return LBKD_EINVAL_SHAPE;
+    CK(cudaSetDevice(c->device));
+    const u64 n = (u64)n_total;
+    const int L = bit_length(n);
+    if (root_level > L - 1 || (u64)root_index >= (1ull << root_level)) return LBKD_EINVAL_SHAPE;
+    const int b = choose_bits(k, kRoundRobin);
+    int lam0 = L - b > 0 ? L - b : 0;
+    if (lam0 < root_level) lam0 = root_level;
+    const LevelGeom gr = make_geom(n, root_level);
+    const u64 nview = seg_size(gr, (u64)root_index);
+    if ((u64)sub_stride < nview) return LBKD_EINVAL_SHAPE;
+    rc = ensure(c, nview, k, b, lam0 - root_level + 1);
+    if (rc) return rc;
+    BuildParams bp;
+    bp.n = n;
+    bp.k = k;
+    bp.mode = kRoundRobin;
+    bp.b = b;
+    bp.pts = nullptr;
+    bp.out_pts = d_out;
+    bp.perm = d_perm;
+    bp.split_dims = c->dims_scratch;
+    bp.dbg = nullptr;
+    bp.lroot = root_level;
+    bp.jroot = (u64)root_index;
+    if ((rc = begin_build(c, k, st))) return rc;
+    CK(cudaMemcpy2DAsync(c->bf.w[0], c->bf.stride * sizeof(u32), d_sub, (size_t)sub_stride * sizeof(u32),
+                         nview * sizeof(u32), (size_t)k + 1, cudaMemcpyDeviceToDevice, st));
+    if ((rc = run_levels(c, bp, root_level, lam0, st))) return rc;
+    launch_subtree(bp, c->bf, lam0, st);
+    c->launches += 1;
+    return end_build(c, st);
 }
 
 extern "C" {
@@ -310,6 +412,16 @@ int lbkd_build_widest_trace(lbkd_ctx* c, const float* d_points, float* d_out, in
                             uint32_t* d_perm, uint8_t* d_dims, uint32_t* d_trace, void* stream) {
     if (!d_trace) return LBKD_EINVAL_SHAPE;
     return build(c, d_points, d_out, n, k, d_perm, d_dims, d_trace, kWidest, (cudaStream_t)stream);
+}
+
+int lbkd_build_rr_top(lbkd_ctx* c, const float* d_points, int64_t n, int k, int top_levels, float* d_out,
+                      uint32_t* d_perm, uint32_t* d_sub, int64_t sub_stride, void* stream) {
+    return build_top(c, d_points, n, k, top_levels, d_out, d_perm, d_sub, sub_stride, (cudaStream_t)stream);
+}
+
+int lbkd_build_rr_sub(lbkd_ctx* c, const uint32_t* d_sub, int64_t sub_stride, int64_t n_total, int k,
+                      int root_level, int64_t root_index, float* d_out, uint32_t* d_perm, void* stream) {
+    return build_sub(c, d_sub, sub_stride, n_total, k, root_level, root_index, d_out, d_perm, (cudaStream_t)stream);
 }
 
 int lbkd_update_tags_rr(uint32_t* d_tags, int64_t n, int levels, int l, void* stream) {

@@ -66,7 +66,14 @@ struct LevelGeom {
     u64 B;        // bottom_have = N - F(L-1)
     u64 Fl;       // F(l) = 2^l - 1 (finalized nodes before level l)
     u64 nl;       // N - F(l): elements in W_l
-    u64 nseg;     // 2^l segments
+    u64 nseg;     // segments in the view (2^l for the whole tree)
+    // view of a subtree (multi-GPU shard / sub-build); the whole tree is the
+    // view rooted at level 0.  Local segment t is global segment sbase + t,
+    // local in-order position p is global position pbase + p.
+    u64 sbase;
+    u64 pbase;
+    u64 nview;    // points in the view
+    int lfirst;   // root level of the view (buffers start at parity 0 there)
 };
 
 __host__ __device__ inline int bit_length(u64 v) {
@@ -85,6 +92,10 @@ __host__ __device__ inline LevelGeom make_geom(u64 n, int l) {
     g.Fl = (1ull << l) - 1ull;
     g.nl = n - g.Fl;
     g.nseg = 1ull << l;
+    g.sbase = 0;
+    g.pbase = 0;
+    g.nview = n;
+    g.lfirst = 0;
     return g;
 }
 
@@ -130,6 +141,31 @@ __host__ __device__ __forceinline__ u64 seg_of_inorder(const LevelGeom& g, u64 p
     u64 ja = p >> (g.sh + 1);
     u64 jb = p >= g.B ? (p - g.B) >> g.sh : 0ull;
     u64 j = ja > jb ? ja : jb;
+    const u64 all = 1ull << g.l;
+    return j < all ? j : all - 1;
+}
+
+// View of the subtree rooted at node (level lroot, index jroot) at level l.
+__host__ __device__ inline LevelGeom make_view(u64 n, int l, int lroot, u64 jroot) {
+    LevelGeom g = make_geom(n, l);
+    LevelGeom gr = make_geom(n, lroot);
+    g.nseg = 1ull << (l - lroot);
+    g.sbase = jroot << (l - lroot);
+    g.pbase = seg_ibegin(gr, jroot);
+    g.nview = seg_size(gr, jroot);
+    g.lfirst = lroot;
+    return g;
+}
+
+// local (view) forms of the in-order helpers
+__host__ __device__ __forceinline__ u64 v_ibegin(const LevelGeom& g, u64 t) {
+    return seg_ibegin(g, g.sbase + t) - g.pbase;
+}
+__host__ __device__ __forceinline__ u64 v_size(const LevelGeom& g, u64 t) { return seg_size(g, g.sbase + t); }
+__host__ __device__ __forceinline__ u64 v_pivot(const LevelGeom& g, u64 t) { return pivot_off(g, g.sbase + t); }
+__host__ __device__ __forceinline__ u64 v_seg_of(const LevelGeom& g, u64 p) {
+    u64 j = seg_of_inorder(g, g.pbase + p);
+    j = j > g.sbase ? j - g.sbase : 0ull;
     return j < g.nseg ? j : g.nseg - 1;
 }
 
@@ -138,7 +174,7 @@ __host__ __device__ __forceinline__ u64 seg_of_inorder(const LevelGeom& g, u64 p
 __host__ __device__ inline u64 seg_of(const LevelGeom& g, u64 p) {
     u64 full = (2ull << g.sh) - 1ull;
     u64 nf = g.B >> g.sh;
-    if (nf > g.nseg) nf = g.nseg;
+    if (nf > (1ull << g.l)) nf = 1ull << g.l;
     u64 p1 = nf * full;
     if (p < p1) return p / full;
     u64 rem = g.B - (nf << g.sh);

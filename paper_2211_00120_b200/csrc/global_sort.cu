@@ -43,12 +43,13 @@ __device__ __forceinline__ u32 parity_out(uint8_t st) {
 
 // split dimension of level-l segment j
 __device__ __forceinline__ int seg_dim(int mode, const uint8_t* split_dims, const LevelGeom& g, int k, u64 j) {
-    return mode == kRoundRobin ? (g.l % k) : (int)split_dims[g.Fl + j];
+    return mode == kRoundRobin ? (g.l % k) : (int)split_dims[g.Fl + g.sbase + j];
 }
 
-// parity (buffer) holding level-l segment j at the start of the level
-__device__ __forceinline__ u32 seg_parity_in(const uint8_t* prev_state, int l, u64 j) {
-    return l == 0 ? 0u : parity_out(prev_state[j >> 1]);
+// parity (buffer) holding level-l (local) segment j at the start of the
+// level: its parent's final buffer (sbase is even below the view's root)
+__device__ __forceinline__ u32 seg_parity_in(const uint8_t* prev_state, const LevelGeom& g, u64 j) {
+    return g.l == g.lfirst ? 0u : parity_out(prev_state[j >> 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(HistArgs a) {
     u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
     u64 t1 = t0 + a.tiles_per_cta;
     if (t1 > a.ntiles) t1 = a.ntiles;
-    u64 cur = seg_of_inorder(g, t0 * T);
+    u64 cur = v_seg_of(g, t0 * T);
     u32 acc_and = 0xffffffffu, acc_or = 0u;
     u32* hw = h[warp];
     __syncthreads();
@@ -145,17 +146,17 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(HistArgs a) {
 
     for (u64 t = t0; t < t1; ++t) {
         const u64 ts = t * T;
-        const u64 cnt = g.n - ts < (u64)T ? g.n - ts : (u64)T;
+        const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
         // segment `cur` occupies [sb, e0); a finished node sits at e0 and
         // segment cur+1 starts at e0 + 1
-        const u64 sb = seg_ibegin(g, cur);
-        const u64 e0 = sb + seg_size(g, cur);
+        const u64 sb = v_ibegin(g, cur);
+        const u64 e0 = sb + v_size(g, cur);
         const bool has_next = cur + 1 < g.nseg && e0 + 1 < ts + cnt;
         const u32 r0a = sb > ts ? (u32)(sb - ts) : 0u;
         const u32 r0b = e0 > ts ? (u32)((e0 - ts < cnt) ? e0 - ts : cnt) : 0u;
         const u32 r1a = has_next ? (u32)(e0 + 1 - ts) : (u32)cnt;
-        const u32* k0 = warr(a.bf, seg_parity_in(a.prev_state, g.l, cur), seg_dim(a.mode, a.split_dims, g, a.k, cur));
-        const u32* k1 = has_next ? warr(a.bf, seg_parity_in(a.prev_state, g.l, cur + 1),
+        const u32* k0 = warr(a.bf, seg_parity_in(a.prev_state, g, cur), seg_dim(a.mode, a.split_dims, g, a.k, cur));
+        const u32* k1 = has_next ? warr(a.bf, seg_parity_in(a.prev_state, g, cur + 1),
                                         seg_dim(a.mode, a.split_dims, g, a.k, cur + 1))
                                  : k0;
         u32 key[ITEMS];
@@ -194,13 +195,13 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(HistArgs a) {
 
 void launch_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {
     HistArgs a;
-    a.g = make_geom(bp.n, l);
+    a.g = view_of(bp, l);
     a.k = bp.k;
     a.mode = bp.mode;
     int items = (1 << (bp.b - 1)) / kHistThreads;  // tile <= smallest segment
     if (items > 8) items = 8;
     const u64 T = (u64)kHistThreads * items;
-    a.ntiles = (bp.n + T - 1) / T;
+    a.ntiles = (a.g.nview + T - 1) / T;
     u64 target = 148 * 8;
     u64 tpc = (a.ntiles + target - 1) / target;
     if (tpc < 1) tpc = 1;
@@ -219,22 +220,22 @@ void launch_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t s
 // plan: per segment, which digit passes reorder it (digit not constant) and
 // which buffer it starts in (its parent's final buffer).
 // ---------------------------------------------------------------------------
-__global__ void plan_kernel(int l, u64 nseg, const u32* seg_and, const u32* seg_or, const uint8_t* prev_state,
+__global__ void plan_kernel(LevelGeom g, const u32* seg_and, const u32* seg_or, const uint8_t* prev_state,
                             uint8_t* state) {
     u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-    if (j >= nseg) return;
+    if (j >= g.nseg) return;
     u32 vary = seg_and[j] ^ seg_or[j];
     u32 mask = 0;
     for (int p = 0; p < 4; ++p)
         if ((vary >> (8 * p)) & 255u) mask |= 1u << p;
-    u32 par = seg_parity_in(prev_state, l, j);
+    u32 par = seg_parity_in(prev_state, g, j);
     state[j] = (uint8_t)((par << 4) | mask);
 }
 
 void launch_plan(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {
-    LevelGeom g = make_geom(bp.n, l);
+    LevelGeom g = view_of(bp, l);
     unsigned blocks = (unsigned)((g.nseg + 255) / 256);
-    plan_kernel<<<blocks, 256, 0, st>>>(l, g.nseg, bf.seg_and, bf.seg_or, bf.state[(l + 1) & 1], bf.state[l & 1]);
+    plan_kernel<<<blocks, 256, 0, st>>>(g, bf.seg_and, bf.seg_or, bf.state[(l + 1) & 1], bf.state[l & 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -289,9 +290,9 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
     if (tid == 0) {
         u64 tile = atomicAdd(a.tile_ctr, 1u);
         u64 ts = tile * T;
-        u64 cnt = g.n - ts < (u64)T ? g.n - ts : (u64)T;
-        u64 j0 = seg_of_inorder(g, ts);
-        u64 s0b = seg_ibegin(g, j0), s0e = s0b + seg_size(g, j0);
+        u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
+        u64 j0 = v_seg_of(g, ts);
+        u64 s0b = v_ibegin(g, j0), s0e = s0b + v_size(g, j0);
         uint8_t st0 = a.state[j0];
         u64 r0a = s0b > ts ? s0b - ts : 0ull;
         u64 r0b = s0e > ts ? ((s0e - ts < cnt) ? s0e - ts : cnt) : 0ull;
@@ -300,13 +301,13 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
         bool has1 = false, act1 = false;
         uint8_t st1 = 0;
         if (j0 + 1 < g.nseg) {
-            u64 s1b = seg_ibegin(g, j0 + 1);
+            u64 s1b = v_ibegin(g, j0 + 1);
             if (s1b < ts + cnt) {
                 has1 = true;
                 st1 = a.state[j0 + 1];
                 act1 = (st1 >> p) & 1u;
                 r1a = s1b - ts;
-                u64 s1e = s1b + seg_size(g, j0 + 1);
+                u64 s1e = s1b + v_size(g, j0 + 1);
                 r1b = (s1e - ts < cnt) ? s1e - ts : cnt;
             }
         }
@@ -498,7 +499,7 @@ static void launch_pass_t(const PassArgs& a, unsigned grid, cudaStream_t st) {
 void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch, u32* tile_ctr,
                  u64* moved, cudaStream_t st) {
     PassArgs a;
-    a.g = make_geom(bp.n, l);
+    a.g = view_of(bp, l);
     a.pass = pass;
     a.k = bp.k;
     a.mode = bp.mode;
@@ -510,7 +511,7 @@ void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 
     a.moved = moved;
     int items = items_for_bits(bp.b);
     const u64 T = (u64)kThreads * items;
-    unsigned grid = (unsigned)((bp.n + T - 1) / T);
+    unsigned grid = (unsigned)((a.g.nview + T - 1) / T);
     switch (items) {
         case 8: launch_pass_t<8>(a, grid, st); break;
         case 4: launch_pass_t<4>(a, grid, st); break;
@@ -527,15 +528,40 @@ __global__ void pivot_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* stat
     u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
     if (j >= g.nseg) return;
     u32 par = parity_out(state[j]);
-    u64 pos = seg_ibegin(g, j) + pivot_off(g, j);
-    u64 node = g.Fl + j;
+    u64 pos = v_ibegin(g, j) + v_pivot(g, j);
+    u64 node = g.Fl + g.sbase + j;
     const u32* w = bf.w[par];
     perm[node] = w[(u64)k * bf.stride + pos];
     for (int c = 0; c < k; ++c) out[node * k + c] = __uint_as_float(w[(u64)c * bf.stride + pos]);
 }
 
+// ---------------------------------------------------------------------------
+// extract (multi-device rank 0): after the top levels, subtree j of level
+// `top` is one contiguous in-order range of every SoA array; copy it to the
+// packed send buffer at offset seg_begin(j) (the compacted begin = the sum of
+// the sizes of the subtrees before it).
+// ---------------------------------------------------------------------------
+__global__ void extract_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* prev_state, u32* d_sub,
+                               u64 sub_stride) {
+    const u64 j = blockIdx.y / (u64)(k + 1);
+    const int c = (int)(blockIdx.y % (u64)(k + 1));
+    const u32 par = parity_out(prev_state[j >> 1]);
+    const u32* src = bf.w[par] + (u64)c * bf.stride + seg_ibegin(g, j);
+    u32* dst = d_sub + (u64)c * sub_stride + seg_begin(g, j);
+    const u64 m = seg_size(g, j);
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride,
+                    cudaStream_t st) {
+    LevelGeom g = make_geom(bp.n, top);
+    dim3 grid(148 * 2, (unsigned)(g.nseg * (u64)(bp.k + 1)));
+    extract_kernel<<<grid, 256, 0, st>>>(g, bp.k, bf, bf.state[(top - 1) & 1], d_sub, sub_stride);
+}
+
 void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {
-    LevelGeom g = make_geom(bp.n, l);
+    LevelGeom g = view_of(bp, l);
     unsigned blocks = (unsigned)((g.nseg + 255) / 256);
     pivot_kernel<<<blocks, 256, 0, st>>>(g, bp.k, bf, bf.state[l & 1], bp.perm, bp.out_pts);
 }

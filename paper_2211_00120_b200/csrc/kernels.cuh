@@ -38,7 +38,11 @@ struct BuildParams {
     u32* perm;
     uint8_t* split_dims;   // widest only
     u32* dbg;              // optional per-level trace (single-subtree builds)
+    int lroot = 0;         // sub-build: root node (level, index) of the view;
+    u64 jroot = 0;         // the whole tree is (0, 0)
 };
+
+inline LevelGeom view_of(const BuildParams& bp, int l) { return make_view(bp.n, l, bp.lroot, bp.jroot); }
 
 __device__ __host__ __forceinline__ u32* warr(const Buffers& bf, u32 buf, int a) {
     return bf.w[buf] + (u64)a * bf.stride;
@@ -51,6 +55,8 @@ void launch_plan(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t s
 void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch,
                  u32* tile_ctr, u64* moved, cudaStream_t st);
 void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
+void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride,
+                    cudaStream_t st);
 
 // subtree.cu
 size_t subtree_smem_bytes(int b, int k, int mode);

@@ -39,6 +39,10 @@ struct SubtreeArgs {
     uint8_t* split_dims;
     const float* boxes0;  // widest: boxes of level-lam0 nodes [nseg][2k]
     u32* dbg;
+    u64 jbase;    // global index (level lam0) of the view's first subtree
+    u64 pbase;    // global in-order position of the view's first point
+    int lfirst;   // root level of the view
+    int from_pts; // single-CTA whole-tree build straight from the input
 };
 
 size_t subtree_smem_bytes(int b, int k, int mode) {
@@ -164,18 +168,22 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
         ndim = sp;
     }
 
-    const u64 j = blockIdx.x;
+    const u64 jl = blockIdx.x;      // subtree within the view
+    const u64 j = a.jbase + jl;     // global index at level lam0
     const LevelGeom g0 = make_geom(a.n, a.lam0);
-    const int m = (int)(a.lam0 == 0 ? a.n : seg_size(g0, j));
+    const int m = (int)(a.from_pts ? a.n : seg_size(g0, j));
     // the subtree's points: the whole input for a single-CTA build, else its
     // in-order range of the global levels' working set (contiguous, so the
     // load is coalesced -- no gather)
     const u32* src = nullptr;
     const u32* vin = nullptr;
-    if (a.lam0 > 0) {
-        const uint8_t st = a.prev_state[j >> 1];
-        const u32 par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
-        src = a.w[par] + seg_ibegin(g0, j);
+    if (!a.from_pts) {
+        u32 par = 0;
+        if (a.lam0 != a.lfirst) {
+            const uint8_t st = a.prev_state[jl >> 1];
+            par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
+        }
+        src = a.w[par] + (seg_ibegin(g0, j) - a.pbase);
         vin = src + (u64)k * a.stride;
     }
     for (int lid = tid; lid < m; lid += kSubThreads) {
@@ -188,7 +196,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
         E[0][lid] = (u32)lid;
     }
     if (a.mode == kWidest) {
-        if (tid < 2 * k) rootbox[tid] = a.boxes0[j * 2ull * k + tid];
+        if (tid < 2 * k) rootbox[tid] = a.boxes0[jl * 2ull * k + tid];
         if (tid == 0) ndim[0] = a.split_dims[g0.Fl + j];
     }
     __syncthreads();
@@ -371,12 +379,16 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
     size_t sortscr = sizeof(unsigned short) * kSubWarps * 256 + sizeof(u32) * 4 * 256;
     u32* scratch = reinterpret_cast<u32*>(sp + (tables > sortscr ? tables : sortscr));
 
-    const u64 j = blockIdx.x;
+    const u64 jl = blockIdx.x;      // subtree within the view
+    const u64 j = a.jbase + jl;     // global index at level lam0
     const LevelGeom g0 = make_geom(a.n, a.lam0);
     const int m = (int)seg_size(g0, j);
-    const uint8_t st = a.prev_state[j >> 1];
-    const u32 par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
-    const u32* src = a.w[par] + seg_ibegin(g0, j);
+    u32 par = 0;
+    if (a.lam0 != a.lfirst) {
+        const uint8_t st = a.prev_state[jl >> 1];
+        par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
+    }
+    const u32* src = a.w[par] + (seg_ibegin(g0, j) - a.pbase);
     const u32* vin = src + (u64)k * a.stride;
     const int e = (a.lam0 - 1) % k;  // dimension of the entry order
     for (int lid = tid; lid < m; lid += kSubThreads) {
@@ -550,7 +562,11 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStre
     a.split_dims = bp.split_dims;
     a.boxes0 = bf.boxes[lam0 & 1];
     a.dbg = bp.dbg;
-    unsigned grid = (unsigned)(1ull << lam0);
+    a.jbase = bp.jroot << (lam0 - bp.lroot);
+    a.pbase = seg_ibegin(make_geom(bp.n, bp.lroot), bp.jroot);
+    a.lfirst = bp.lroot;
+    a.from_pts = lam0 == 0 ? 1 : 0;
+    unsigned grid = (unsigned)(1ull << (lam0 - bp.lroot));
     if (bp.mode == kRoundRobin && lam0 >= bp.k) {
         size_t sm = subtree_rr_smem_bytes(bp.b, bp.k);
         cudaFuncSetAttribute(subtree_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -209,3 +209,33 @@ def test_check_valid_at_scale():
         assert oracle.check_valid(out)
         out, perm, dims = gpu_widest(pts)
         assert oracle.check_valid(out, dims)
+
+
+@pytest.mark.parametrize("n,k,world,kind", [(300_000, 3, 2, "uniform"), (1_000_000, 3, 8, "clustered"),
+                                            (2_000_003, 2, 4, "ties"), (500_000, 4, 4, "uniform"),
+                                            (20_000, 3, 4, "uniform"), (70_000, 1, 2, "ties")])
+def test_sharded_build_matches_single_gpu(n, k, world, kind):
+    """The multi-GPU path run rank by rank on one GPU: top levels, then every
+    subtree from its packed points with the global geometry -- bit-identical
+    to the single-device build (the exchange itself is covered by the gloo
+    tests)."""
+    from paper_2211_00120_b200 import multigpu
+
+    pts = datagen.make(kind, n, k, seed=n)
+    d = torch.from_numpy(pts).cuda()
+    want_out, want_perm = kd.build_round_robin_cuda(d)
+    top = multigpu.top_levels_for(world)
+    ops = multigpu.CudaOps(0)
+    out = torch.full_like(d, float("nan"))
+    perm = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    sub = torch.empty((k + 1) * n, dtype=torch.int32, device="cuda")
+    ops.build_top(d, top, out, perm, sub, n)
+    for sh in multigpu.shard_layout(n, top):
+        mine = torch.empty((k + 1) * sh.size, dtype=torch.int32, device="cuda")
+        for c in range(k + 1):
+            mine[c * sh.size:(c + 1) * sh.size] = sub[c * n + sh.offset: c * n + sh.offset + sh.size]
+        ops.build_sub(mine, sh.size, n, k, top, sh.index, out, perm)
+    torch.cuda.synchronize()
+    assert torch.equal(perm, want_perm)
+    assert torch.equal(out, want_out)
+    assert oracle.build_rr(pts).tolist()[:1000] == perm.cpu().numpy().view(np.uint32).tolist()[:1000]
