@@ -203,6 +203,18 @@ __device__ __forceinline__ u32 warp_peers(u32 v, bool valid) {
     return valid ? m : (1u << (threadIdx.x & 31u));
 }
 
+// warp_peers for a warp whose 32 lanes are all valid (no validity ballot)
+template <int NBITS>
+__device__ __forceinline__ u32 warp_peers_full(u32 v) {
+    u32 m = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < NBITS; ++b) {
+        const u32 bal = __ballot_sync(0xffffffffu, (v >> b) & 1u);
+        m &= ((v >> b) & 1u) ? bal : ~bal;
+    }
+    return m;
+}
+
 // ---- PTX helpers -----------------------------------------------------------
 __device__ __forceinline__ u32 lanemask_lt() {
     u32 r;

@@ -97,10 +97,26 @@ constexpr int kHistThreads = 256;
 // read-modify-write (the groups of one instruction hit distinct bins, and
 // consecutive rounds are ordered by __syncwarp) -- shared atomics cost
 // ~2 cycles per lane on B200, this costs one bank-conflicted LDS/STS pair
-__device__ __forceinline__ void hist_add(u32* h, u32 d, bool inc) {
+// All four digit histograms of one warp row: 32 bit ballots give the peer
+// masks of every digit; `full` (warp-uniform) skips the validity ballot.
+__device__ __forceinline__ void hist_round(u32* h, u32 key, bool inc, bool full) {
     const u32 lane = threadIdx.x & 31u;
-    u32 peers = warp_peers<8>(d, inc);
-    if (inc && lane == 31u - __clz(peers)) h[d] += (u32)__popc(peers);
+    const u32 v = full ? 0xffffffffu : __ballot_sync(kFullMask, inc);
+    u32 m[4] = {v, v, v, v};
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 bit = (key >> (8 * q + b)) & 1u;
+            const u32 bal = __ballot_sync(kFullMask, bit);
+            m[q] &= bit ? bal : ~bal;
+        }
+    }
+    if (inc) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (lane == 31u - __clz(m[q])) h[q * 256 + ((key >> (8 * q)) & 255u)] += (u32)__popc(m[q]);
+    }
     __syncwarp();
 }
 
@@ -167,25 +183,27 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(HistArgs a) {
             if (r >= r0a && r < r0b) key[i] = flip_key(__uint_as_float(k0[ts + r]));
             else if (r >= r1a && r < cnt) key[i] = flip_key(__uint_as_float(k1[ts + r]));
         }
-#pragma unroll 1
+#pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+            const u32 row = (u32)(warp * ITEMS * 32 + i * 32);
+            u32 r = row + lane;
             bool inc = r >= r0a && r < r0b;
             if (inc) { acc_and &= key[i]; acc_or |= key[i]; }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) hist_add(hw + q * 256, (key[i] >> (8 * q)) & 255u, inc);
+            const bool full = row >= r0a && row + 32 <= r0b;
+            if (__any_sync(kFullMask, inc)) hist_round(hw, key[i], inc, full);
         }
         if (has_next) {
             __syncthreads();
             flush(cur);
             ++cur;
-#pragma unroll 1
+#pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+                const u32 row = (u32)(warp * ITEMS * 32 + i * 32);
+                u32 r = row + lane;
                 bool inc = r >= r1a && r < cnt;
                 if (inc) { acc_and &= key[i]; acc_or |= key[i]; }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) hist_add(hw + q * 256, (key[i] >> (8 * q)) & 255u, inc);
+                const bool full = row >= r1a && row + 32 <= cnt;
+                if (__any_sync(kFullMask, inc)) hist_round(hw, key[i], inc, full);
             }
         }
     }
@@ -364,28 +382,34 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
     asm volatile("cp.async.commit_group;" ::: "memory");
 
     u32 key[ITEMS];
+    const u32* k0p = a.bf.w[src0] + (u64)d0 * a.bf.stride + ts;
+    const u32* k1p = a.bf.w[src1] + (u64)d1 * a.bf.stride + ts;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
         bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
         key[i] = 0u;
-        if (in0) key[i] = a.bf.w[src0][(u64)d0 * a.bf.stride + ts + r];
-        else if (in1) key[i] = a.bf.w[src1][(u64)d1 * a.bf.stride + ts + r];
+        if (in0) key[i] = k0p[r];
+        else if (in1) key[i] = k1p[r];
     }
-    // --- warp-level stable ranking: all match.any first (independent), then
-    // the per-round counter bumps by each group's highest lane
+    // --- warp-level stable ranking: peers of each element's bucket from
+    // bit-sliced ballots, then the per-round counter bumps by each group's
+    // highest lane
     u32 br[ITEMS];  // bucket << 16 | warp-local rank
     u32 peers[ITEMS];
     const u32 lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+        const u32 row = (u32)(warp * ITEMS * 32 + i * 32);
+        u32 r = row + lane;
         bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
         u32 dg = (flip_key(__uint_as_float(key[i])) >> shift) & 255u;
         u32 b = in0 ? dg : (in1 ? (dg | 256u) : (0x1000u | lane));
         br[i] = b;
-        // the segment bit only matters in the (rare) two-segment tiles
-        peers[i] = (flags & 4u) ? warp_peers<9>(b, in0 || in1) : warp_peers<8>(b, in0 || in1);
+        // a row entirely inside one active part (the common case) needs only
+        // the 8 digit bits; otherwise the segment bit and validity join in
+        const bool full = (row >= r0a && row + 32 <= r0b) || (row >= r1a && row + 32 <= r1b);
+        peers[i] = full ? warp_peers_full<8>(dg) : warp_peers<9>(b, in0 || in1);
     }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -451,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(PassArgs a) {
                 if (fl == kFlagInc) { done = true; break; }
             }
             if (done) break;
+            if (q == 0) __nanosleep(100);  // predecessor not ready: yield issue slots
             t -= q;
         }
         if (!has1) st_relaxed_u64(my_status + tid, pack_status(a.epoch, kFlagInc, prefix + tot));
