@@ -118,6 +118,17 @@ int64_t lbkd_last_launch_count(const lbkd_ctx *ctx);
  * and its index once).  Synchronises on the events. */
 void lbkd_set_profile(lbkd_ctx *ctx, int on);
 int lbkd_profile_read(lbkd_ctx *ctx, int *n_pass_launches, double *pass_ms, double *pass_bytes);
+/* Per kernel class of the last profiled build (cls = -1: all launches):
+ * 0 init, 1 hist, 2 pick, 3 filter, 4 select, 5 partition, 6 subtree,
+ * 7 sort-path digit pass, 8 other.  Same units as lbkd_profile_read. */
+int lbkd_profile_kernel(lbkd_ctx *ctx, int cls, int *n_launches, double *ms, double *bytes);
+/* Global-level algorithm: 0 = pivot selection + stable 3-way partition per
+ * level (default), 1 = the literal per-level segmented LSD radix sort
+ * (onesweep digit passes).  Both are bit-exact; env LBKD_ALGO=sort selects 1
+ * at context creation.  lbkd_profile_read reports the partition (0) or the
+ * digit pass (1) kernel. */
+int lbkd_set_algorithm(lbkd_ctx *ctx, int algo);
+int lbkd_get_algorithm(const lbkd_ctx *ctx);
 const char *lbkd_strerror(int code);
 const char *lbkd_last_cuda_error(void);
 

@@ -32,7 +32,12 @@ EXPORTED = (
     "lbkd_last_launch_count", "lbkd_strerror", "lbkd_last_cuda_error",
     "lbkd_set_profile", "lbkd_profile_read",
     "lbkd_build_rr_top", "lbkd_build_rr_sub",
+    "lbkd_profile_kernel", "lbkd_set_algorithm", "lbkd_get_algorithm",
 )
+
+# kernel classes of lbkd_profile_kernel
+PROFILE_CLASSES = ("init", "hist", "pick", "filter", "select", "partition", "subtree", "sort_pass", "other")
+ALGORITHMS = ("select", "sort")
 
 _lib = None
 _lock = threading.Lock()
@@ -97,6 +102,12 @@ def load():
         dp = ctypes.POINTER(ctypes.c_double)
         lib.lbkd_profile_read.argtypes = [vp, ctypes.POINTER(i32), dp, dp]
         lib.lbkd_profile_read.restype = i32
+        lib.lbkd_profile_kernel.argtypes = [vp, i32, ctypes.POINTER(i32), dp, dp]
+        lib.lbkd_profile_kernel.restype = i32
+        lib.lbkd_set_algorithm.argtypes = [vp, i32]
+        lib.lbkd_set_algorithm.restype = i32
+        lib.lbkd_get_algorithm.argtypes = [vp]
+        lib.lbkd_get_algorithm.restype = i32
         lib.lbkd_strerror.argtypes = [i32]
         lib.lbkd_strerror.restype = ctypes.c_char_p
         lib.lbkd_last_cuda_error.argtypes = []
@@ -134,6 +145,32 @@ def profile_read(device: int = 0):
     by = ctypes.c_double()
     check(lib.lbkd_profile_read(context(device), ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)), "lbkd_profile_read")
     return n.value, ms.value, by.value
+
+
+def profile_kernels(device: int = 0) -> dict:
+    """{class: (launches, device ms, algorithmic bytes)} of the last profiled
+    build on this thread's context for `device`."""
+    lib = load()
+    out = {}
+    for i, name in enumerate(PROFILE_CLASSES):
+        n = ctypes.c_int()
+        ms = ctypes.c_double()
+        by = ctypes.c_double()
+        check(lib.lbkd_profile_kernel(context(device), i, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)),
+              "lbkd_profile_kernel")
+        if n.value:
+            out[name] = (n.value, ms.value, by.value)
+    return out
+
+
+def set_algorithm(algo: str, device: int = 0) -> None:
+    """Global-level algorithm of this thread's context: "select" (pivot
+    selection + stable partition, default) or "sort" (per-level radix sort)."""
+    check(load().lbkd_set_algorithm(context(device), ALGORITHMS.index(algo)), "lbkd_set_algorithm")
+
+
+def get_algorithm(device: int = 0) -> str:
+    return ALGORITHMS[load().lbkd_get_algorithm(context(device))]
 
 
 def set_profile(on: bool, device: int = 0) -> None:

@@ -9,6 +9,7 @@
 // Everything is enqueued on the caller's stream with device-side plans, so
 // the only host synchronisation is the final non-finite check.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -38,6 +39,9 @@ struct lbkd_ctx {
     u32 epoch = 1;
     int ctr = 0;
     int64_t launches = 0;
+    int algo = 0;      // 0: select + partition (default), 1: per-level sort
+    u32 pepoch = 1;    // partition lookback epochs
+    size_t cap_cand = 0, cap_ptiles = 0, cap_piv = 0;
     // grow-only device allocations
     size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_w = 0, cap_copy = 0;
     Buffers bf{};
@@ -46,17 +50,47 @@ struct lbkd_ctx {
     uint8_t* dims_scratch = nullptr;
     u32* minmax = nullptr;
     u32* h_err = nullptr;  // pinned
-    // profiling (lbkd_set_profile): CUDA events around every digit-pass
-    // launch and the number of points each launch reordered
+    // profiling (lbkd_set_profile): CUDA events around every kernel launch
+    // of a build, its kernel class and its algorithmic HBM bytes
     int profile = 0;
     std::vector<cudaEvent_t> ev;
+    std::vector<int> ev_cls;
+    std::vector<double> ev_bytes;
     int n_ev_used = 0;
     u64* d_moved = nullptr;
     int k_last = 0;
 };
 
+// kernel classes of the profile (lbkd_profile_kernel)
+enum { kPInit = 0, kPHist, kPPick, kPFilter, kPSelect, kPPart, kPSubtree, kPSortPass, kPOther, kPClasses };
+
+// open / close a profiled launch: events on the build stream around it
+static int prof_begin(lbkd_ctx* c, cudaStream_t st) {
+    if (!c->profile) return 0;
+    while ((int)c->ev.size() < c->n_ev_used + 2) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return 1;
+        c->ev.push_back(e);
+    }
+    cudaEventRecord(c->ev[c->n_ev_used], st);
+    return 0;
+}
+static void prof_end(lbkd_ctx* c, cudaStream_t st, int cls, double bytes) {
+    c->launches += 1;
+    if (!c->profile) return;
+    cudaEventRecord(c->ev[c->n_ev_used + 1], st);
+    const int i = c->n_ev_used / 2;
+    if ((int)c->ev_cls.size() <= i) {
+        c->ev_cls.resize(i + 1);
+        c->ev_bytes.resize(i + 1);
+    }
+    c->ev_cls[i] = cls;
+    c->ev_bytes[i] = bytes;
+    c->n_ev_used += 2;
+}
+
 static int choose_bits(int k, int mode) {
-    const size_t limit = 227 * 1024;
+    const size_t limit = 227 * 1024 - 256;  // dynamic + a little static smem
     for (int b = 13; b >= 10; --b)
         if (subtree_smem_bytes(b, k, mode) <= limit &&
             (mode != kRoundRobin || subtree_rr_smem_bytes(b, k) <= limit))
@@ -115,6 +149,31 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
         }
         c->cap_seg = nseg;
     }
+    if (lam0 > 0 && c->algo == 0) {
+        const size_t rec = (size_t)(k + 1) * n;
+        if (rec > c->cap_cand) {
+            if ((rc = grow(c->bf.cand, dummy, rec))) return rc;
+            if ((rc = grow(c->bf.cand2, dummy, rec))) return rc;
+            c->cap_cand = rec;
+        }
+        const size_t pv = nseg * (size_t)(LBKD_MAX_K + 1);
+        if (pv > c->cap_piv) {
+            if ((rc = grow(c->bf.piv, dummy, pv))) return rc;
+            if ((rc = grow(c->bf.chains, dummy, nseg))) return rc;
+            if ((rc = grow(c->bf.sel, dummy, nseg * kSelW))) return rc;
+            for (int i = 0; i < 2; ++i) {
+                if ((rc = grow(c->bf.mmn[i], dummy, nseg))) return rc;
+                if ((rc = grow(c->bf.mmx[i], dummy, nseg))) return rc;
+            }
+            c->cap_piv = pv;
+        }
+        const size_t pt = n / 1024 + 2;  // partition tiles are >= 1024 points
+        if (pt > c->cap_ptiles) {
+            if ((rc = grow(c->bf.pstatus, dummy, pt))) return rc;
+            CK(cudaMemset(c->bf.pstatus, 0, pt * sizeof(u64)));
+            c->cap_ptiles = pt;
+        }
+    }
     size_t T = (size_t)1 << (b - 1);
     size_t tiles = (n + T - 1) / T + 1;
     if (tiles > c->cap_tiles) {
@@ -127,52 +186,147 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
         if ((rc = grow(c->bf.tile_ctr, dummy, 4 * 64))) return rc;
         if ((rc = grow(c->d_moved, dummy, 256))) return rc;
         if ((rc = grow(c->bf.err, dummy, 4))) return rc;
+        if ((rc = grow(c->bf.cand_ctr, dummy, 4))) return rc;
         if ((rc = grow(c->minmax, dummy, 2 * LBKD_MAX_K))) return rc;
         CK(cudaMallocHost(&c->h_err, sizeof(u32) * 4));
     }
     return LBKD_OK;
 }
 
-// the global levels [lfrom, lto) of the view bp (hist -> plan -> up to four
-// digit passes -> pivots [-> widest child dims])
-static int run_levels(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cudaStream_t st) {
+// number of points in the segments of level l of the view (the view minus
+// the finished nodes between its segments)
+static u64 level_points(const BuildParams& bp, int l) {
+    const LevelGeom g = view_of(bp, l);
+    return g.nview - (g.nseg - 1);
+}
+
+// sort path: the global levels [lfrom, lto) of the view bp (hist -> plan ->
+// up to four digit passes -> pivots [-> widest child dims])
+static int run_levels_sort(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cudaStream_t st) {
     Buffers& bf = c->bf;
     for (int l = lfrom; l < lto; ++l) {
         const u64 nseg = 1ull << (l - bp.lroot);
+        const double pts = (double)level_points(bp, l);
         CK(cudaMemsetAsync(bf.hist, 0, nseg * 1024 * sizeof(u32), st));
         CK(cudaMemsetAsync(bf.seg_and, 0xff, nseg * sizeof(u32), st));
         CK(cudaMemsetAsync(bf.seg_or, 0, nseg * sizeof(u32), st));
+        if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_hist(bp, bf, l, st);
+        prof_end(c, st, kPHist, 4.0 * pts);
+        if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_plan(bp, bf, l, st);
-        c->launches += 2;
+        prof_end(c, st, kPOther, 0.0);
         for (int p = 0; p < 4; ++p) {
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            if (c->profile) {
-                while ((int)c->ev.size() < c->n_ev_used + 2) {
-                    cudaEvent_t e;
-                    CK(cudaEventCreate(&e));
-                    c->ev.push_back(e);
-                }
-                e0 = c->ev[c->n_ev_used];
-                e1 = c->ev[c->n_ev_used + 1];
-                c->n_ev_used += 2;
-                CK(cudaEventRecord(e0, st));
-            }
-            launch_pass(bp, bf, l, p, c->epoch, bf.tile_ctr + (c->ctr % 256),
-                        c->profile ? c->d_moved + (c->ctr % 256) : nullptr, st);
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            const int slot = c->ctr % 256;
+            launch_pass(bp, bf, l, p, c->epoch, bf.tile_ctr + slot, c->profile ? c->d_moved + slot : nullptr, st);
             ++c->ctr;
-            if (c->profile) CK(cudaEventRecord(e1, st));
+            // bytes: each reordered point reads + writes k coords + index,
+            // counted on the device (resolved in lbkd_profile_read)
+            prof_end(c, st, kPSortPass, -1.0 - slot);
             c->epoch = (c->epoch + 1) & 0x3fffffffu;
             if (c->epoch == 0) c->epoch = 1;
-            c->launches += 1;
         }
+        if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_pivots(bp, bf, l, st);
-        c->launches += 1;
+        prof_end(c, st, kPOther, 0.0);
         if (bp.mode == kWidest) {
+            if (prof_begin(c, st)) return LBKD_ECUDA;
             launch_widest_nodes(bp, l, bf.boxes[l & 1], bf.boxes[(l + 1) & 1], st);
-            c->launches += 1;
+            prof_end(c, st, kPOther, 0.0);
         }
     }
+    return LBKD_OK;
+}
+
+// select path: the global levels [lfrom, lto) of the view bp -- per level
+// hist -> pick -> filter -> select -> partition (select.cu)
+static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cudaStream_t st) {
+    Buffers& bf = c->bf;
+    const int k = bp.k;
+    const double A = 4.0 * (k + 1);
+    for (int l = lfrom; l < lto; ++l) {
+        const LevelGeom g = view_of(bp, l);
+        const u64 nseg = g.nseg;
+        const int D = sel_digit_bits(nseg);
+        const u32 par = (u32)((l - bp.lroot) & 1);
+        const bool last = l == lto - 1;
+        const double pts = (double)level_points(bp, l);
+        CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
+        CK(cudaMemsetAsync(bf.cand_ctr, 0, sizeof(u32), st));
+        if (!last) {
+            CK(cudaMemsetAsync(bf.mmn[par ^ 1], 0xff, 2 * nseg * sizeof(u32), st));
+            CK(cudaMemsetAsync(bf.mmx[par ^ 1], 0, 2 * nseg * sizeof(u32), st));
+        }
+        SelArgs a;
+        memset(&a, 0, sizeof(a));
+        a.g = g;
+        a.k = k;
+        a.mode = bp.mode;
+        a.D = D;
+        a.bf = bf;
+        a.par = par;
+        a.mmn = bf.mmn[par];
+        a.mmx = bf.mmx[par];
+        a.hist = bf.hist;
+        a.sel = bf.sel;
+        a.cand = bf.cand;
+        a.cand2 = bf.cand2;
+        a.cand_ctr = bf.cand_ctr;
+        a.piv = bf.piv;
+        a.chains = bf.chains;
+        a.split_dims = bp.split_dims;
+        a.perm = bp.perm;
+        a.out_pts = bp.out_pts;
+        a.boxes_in = bf.boxes[par];
+        a.boxes_out = bf.boxes[par ^ 1];
+        a.status = bf.pstatus;
+        a.tile_ctr = bf.tile_ctr + (c->ctr % 256);
+        ++c->ctr;
+        a.epoch = c->pepoch;
+        c->pepoch = (c->pepoch + 1) & 0x1fffffffu;
+        if (c->pepoch == 0) {
+            // epoch wrapped: no stale status word may match a future epoch
+            CK(cudaMemsetAsync(bf.pstatus, 0, c->cap_ptiles * sizeof(u64), st));
+            c->pepoch = 1;
+        }
+        a.want_mm = last ? 0 : 1;
+        a.mmn_next = bf.mmn[par ^ 1];
+        a.mmx_next = bf.mmx[par ^ 1];
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_sel_hist(a, bp.b, st);
+        prof_end(c, st, kPHist, 4.0 * pts);
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_sel_pick(a, st);
+        prof_end(c, st, kPPick, 4.0 * (double)(nseg << D));
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_sel_filter(a, bp.b, st);
+        prof_end(c, st, kPFilter, 4.0 * pts);
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_sel_select(a, st);
+        prof_end(c, st, kPSelect, 0.0);
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_sel_part(a, bp.b, st);
+        // reads every point of the level, writes all but the nodes
+        prof_end(c, st, kPPart, A * (2.0 * pts - (double)nseg));
+    }
+    return LBKD_OK;
+}
+
+static int run_levels(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cudaStream_t st) {
+    return c->algo == 0 ? run_levels_select(c, bp, lfrom, lto, st) : run_levels_sort(c, bp, lfrom, lto, st);
+}
+
+// the in-CTA levels from lam0 on
+static int run_subtrees(lbkd_ctx* c, const BuildParams& bp, int lam0, cudaStream_t st) {
+    if (prof_begin(c, st)) return LBKD_ECUDA;
+    const int entry_sorted = c->algo != 0 || lam0 == 0;
+    const int src_par = c->algo == 0 ? ((lam0 - bp.lroot) & 1) : -1;
+    launch_subtree(bp, c->bf, lam0, entry_sorted, src_par, st);
+    // each point of the subtrees is read once (k coords + index) and written
+    // once to its level-order slot (k coords + perm)
+    const u64 pts = lam0 == 0 ? bp.n : level_points(bp, lam0);
+    prof_end(c, st, kPSubtree, 8.0 * (bp.k + 1) * (double)pts);
     return LBKD_OK;
 }
 
@@ -205,6 +359,40 @@ static int check_args(lbkd_ctx* c, int64_t n_in, int k, int mode) {
     if (mode == kWidest) {
         int db = bit_length((u64)(k - 1));
         if ((n_in << db) > 0x7fffffffll) return LBKD_ECAPACITY;
+    }
+    return LBKD_OK;
+}
+
+// input -> working set W[0] (global levels) and the root's key range /
+// widest world box and root dim
+static int prologue(lbkd_ctx* c, const BuildParams& bp, int lam0, cudaStream_t st) {
+    const int k = bp.k;
+    const double pts = (double)bp.n;
+    if (lam0 > 0 && c->algo == 0) {
+        CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
+        CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_init_stats(bp, c->bf, c->minmax, st);
+        prof_end(c, st, kPInit, pts * (4.0 * k + 4.0 * (k + 1)));
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_root(bp, c->bf, c->minmax, st);
+        prof_end(c, st, kPOther, 0.0);
+        return LBKD_OK;
+    }
+    if (bp.mode == kWidest) {
+        CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
+        CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_world_bounds(bp, c->minmax, st);
+        prof_end(c, st, kPOther, pts * 4.0 * k);
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_widest_root(bp, c->minmax, c->bf.boxes[0], st);
+        prof_end(c, st, kPOther, 0.0);
+    }
+    if (lam0 > 0) {
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_init(bp, c->bf, st);
+        prof_end(c, st, kPInit, pts * (4.0 * k + 4.0 * (k + 1)));
     }
     return LBKD_OK;
 }
@@ -249,20 +437,9 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.split_dims = d_dims ? d_dims : c->dims_scratch;
     bp.dbg = d_trace;
     if ((rc = begin_build(c, k, st))) return rc;
-    if (mode == kWidest) {
-        CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
-        CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
-        launch_world_bounds(bp, c->minmax, st);
-        launch_widest_root(bp, c->minmax, c->bf.boxes[0], st);
-        c->launches += 2;
-    }
-    if (lam0 > 0) {
-        launch_init(bp, c->bf, st);
-        c->launches += 1;
-    }
+    if ((rc = prologue(c, bp, lam0, st))) return rc;
     if ((rc = run_levels(c, bp, 0, lam0, st))) return rc;
-    launch_subtree(bp, c->bf, lam0, st);
-    c->launches += 1;
+    if ((rc = run_subtrees(c, bp, lam0, st))) return rc;
     return end_build(c, st);
 }
 
@@ -295,11 +472,11 @@ static int build_top(lbkd_ctx* c, const float* d_points, int64_t n_in, int k, in
     bp.split_dims = c->dims_scratch;
     bp.dbg = nullptr;
     if ((rc = begin_build(c, k, st))) return rc;
-    launch_init(bp, c->bf, st);
-    c->launches += 1;
+    if ((rc = prologue(c, bp, lam0, st))) return rc;
     if ((rc = run_levels(c, bp, 0, top, st))) return rc;
-    launch_extract(bp, c->bf, top, d_sub, (u64)sub_stride, st);
-    c->launches += 1;
+    if (prof_begin(c, st)) return LBKD_ECUDA;
+    launch_extract(bp, c->bf, top, d_sub, (u64)sub_stride, c->algo == 0 ? (top & 1) : -1, st);
+    prof_end(c, st, kPOther, 8.0 * (k + 1) * (double)level_points(bp, top));
     return end_build(c, st);
 }
 
@@ -339,9 +516,15 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     if ((rc = begin_build(c, k, st))) return rc;
     CK(cudaMemcpy2DAsync(c->bf.w[0], c->bf.stride * sizeof(u32), d_sub, (size_t)sub_stride * sizeof(u32),
                          nview * sizeof(u32), (size_t)k + 1, cudaMemcpyDeviceToDevice, st));
+    if (c->algo == 0 && lam0 > root_level) {
+        CK(cudaMemsetAsync(c->bf.mmn[0], 0xff, sizeof(u32), st));
+        CK(cudaMemsetAsync(c->bf.mmx[0], 0, sizeof(u32), st));
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_view_minmax(bp, c->bf, root_level % k, nview, st);
+        prof_end(c, st, kPOther, 4.0 * (double)nview);
+    }
     if ((rc = run_levels(c, bp, root_level, lam0, st))) return rc;
-    launch_subtree(bp, c->bf, lam0, st);
-    c->launches += 1;
+    if ((rc = run_subtrees(c, bp, lam0, st))) return rc;
     return end_build(c, st);
 }
 
@@ -360,6 +543,8 @@ int lbkd_create(lbkd_ctx** out, int device) {
     cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
     lbkd_ctx* c = new lbkd_ctx();
     c->device = device;
+    const char* algo = getenv("LBKD_ALGO");
+    if (algo && strcmp(algo, "sort") == 0) c->algo = 1;
     *out = c;
     return LBKD_OK;
 }
@@ -373,6 +558,17 @@ void lbkd_destroy(lbkd_ctx* c) {
         cudaFree(c->bf.state[i]);
     }
     cudaFree(c->bf.hist);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(c->bf.mmn[i]);
+        cudaFree(c->bf.mmx[i]);
+    }
+    cudaFree(c->bf.sel);
+    cudaFree(c->bf.cand);
+    cudaFree(c->bf.cand2);
+    cudaFree(c->bf.cand_ctr);
+    cudaFree(c->bf.piv);
+    cudaFree(c->bf.chains);
+    cudaFree(c->bf.pstatus);
     cudaFree(c->bf.seg_and);
     cudaFree(c->bf.seg_or);
     cudaFree(c->bf.status);
@@ -472,29 +668,53 @@ void lbkd_set_profile(lbkd_ctx* c, int on) {
     if (c) c->profile = on ? 1 : 0;
 }
 
-int lbkd_profile_read(lbkd_ctx* c, int* n_pass_launches, double* pass_ms, double* pass_bytes) {
+// per-class totals of the last profiled build (device time from the events,
+// algorithmic bytes from the launch geometry or the device counters)
+static int profile_class(lbkd_ctx* c, int cls, int* n_out, double* ms_out, double* bytes_out) {
     if (!c) return LBKD_EINVAL_SHAPE;
-    int n = c->n_ev_used / 2;
+    const int n = c->n_ev_used / 2;
+    int cnt = 0;
     double ms = 0.0, bytes = 0.0;
     if (n > 0) {
         CK(cudaSetDevice(c->device));
         std::vector<u64> moved(256, 0);
         CK(cudaMemcpy(moved.data(), c->d_moved, sizeof(u64) * 256, cudaMemcpyDeviceToHost));
         for (int i = 0; i < n; ++i) {
+            if (cls >= 0 && c->ev_cls[i] != cls) continue;
             float t = 0.f;
             CK(cudaEventSynchronize(c->ev[2 * i + 1]));
             CK(cudaEventElapsedTime(&t, c->ev[2 * i], c->ev[2 * i + 1]));
             ms += t;
-            // algorithmic bytes: every reordered point reads and writes its
-            // k coordinates and its index once
-            bytes += (double)moved[i % 256] * 2.0 * 4.0 * (double)(c->k_last + 1);
+            ++cnt;
+            const double b = c->ev_bytes[i];
+            // sort path digit passes: every reordered point reads and writes
+            // its k coordinates and its index once
+            bytes += b >= 0.0 ? b : (double)moved[(int)(-b - 1.0)] * 2.0 * 4.0 * (double)(c->k_last + 1);
         }
     }
-    if (n_pass_launches) *n_pass_launches = n;
-    if (pass_ms) *pass_ms = ms;
-    if (pass_bytes) *pass_bytes = bytes;
+    if (n_out) *n_out = cnt;
+    if (ms_out) *ms_out = ms;
+    if (bytes_out) *bytes_out = bytes;
     return LBKD_OK;
 }
+
+int lbkd_profile_read(lbkd_ctx* c, int* n_pass_launches, double* pass_ms, double* pass_bytes) {
+    if (!c) return LBKD_EINVAL_SHAPE;
+    return profile_class(c, c->algo == 0 ? kPPart : kPSortPass, n_pass_launches, pass_ms, pass_bytes);
+}
+
+int lbkd_profile_kernel(lbkd_ctx* c, int cls, int* n_launches, double* ms, double* bytes) {
+    if (cls < -1 || cls >= kPClasses) return LBKD_EINVAL_SHAPE;
+    return profile_class(c, cls, n_launches, ms, bytes);
+}
+
+int lbkd_set_algorithm(lbkd_ctx* c, int algo) {
+    if (!c || algo < 0 || algo > 1) return LBKD_EINVAL_SHAPE;
+    c->algo = algo;
+    return LBKD_OK;
+}
+
+int lbkd_get_algorithm(const lbkd_ctx* c) { return c ? c->algo : -1; }
 
 const char* lbkd_strerror(int code) {
     switch (code) {

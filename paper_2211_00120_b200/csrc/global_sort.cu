@@ -566,11 +566,11 @@ __global__ void pivot_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* stat
 // packed send buffer at offset seg_begin(j) (the compacted begin = the sum of
 // the sizes of the subtrees before it).
 // ---------------------------------------------------------------------------
-__global__ void extract_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* prev_state, u32* d_sub,
+__global__ void extract_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* prev_state, int src_par, u32* d_sub,
                                u64 sub_stride) {
     const u64 j = blockIdx.y / (u64)(k + 1);
     const int c = (int)(blockIdx.y % (u64)(k + 1));
-    const u32 par = parity_out(prev_state[j >> 1]);
+    const u32 par = src_par >= 0 ? (u32)src_par : parity_out(prev_state[j >> 1]);
     const u32* src = bf.w[par] + (u64)c * bf.stride + seg_ibegin(g, j);
     u32* dst = d_sub + (u64)c * sub_stride + seg_begin(g, j);
     const u64 m = seg_size(g, j);
@@ -578,11 +578,11 @@ __global__ void extract_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* pr
         dst[i] = src[i];
 }
 
-void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride,
+void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride, int src_par,
                     cudaStream_t st) {
     LevelGeom g = make_geom(bp.n, top);
     dim3 grid(148 * 2, (unsigned)(g.nseg * (u64)(bp.k + 1)));
-    extract_kernel<<<grid, 256, 0, st>>>(g, bp.k, bf, bf.state[(top - 1) & 1], d_sub, sub_stride);
+    extract_kernel<<<grid, 256, 0, st>>>(g, bp.k, bf, bf.state[(top - 1) & 1], src_par, d_sub, sub_stride);
 }
 
 void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st) {

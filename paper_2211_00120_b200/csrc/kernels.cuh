@@ -2,21 +2,69 @@
 #pragma once
 #include <cstdint>
 #include "common.cuh"
+#include "lbkd_b200.h"
 
 namespace lbkd {
 
 enum Mode { kRoundRobin = 0, kWidest = 1 };
+
+// Fields of a node's within-node order T(s) (select.cu): m dimensions, most
+// significant first, then the input index.
+struct Chain {
+    u32 m;
+    uint8_t d[LBKD_MAX_K];
+};
+constexpr int kChainWords = sizeof(Chain) / 4;
+
+// RR: dims l, l-1, ..., max(0, l-k+1) (mod k)
+__host__ __device__ inline void rr_chain(int l, int k, Chain& c) {
+    int m = l + 1 < k ? l + 1 : k;
+    c.m = (u32)m;
+    for (int i = 0; i < m; ++i) c.d[i] = (uint8_t)((l - i) % k);
+}
+
+// widest: node s and its ancestors' split dims, most recent first, repeats
+// dropped (the reference's stable sorts nest: widest.py:119-131)
+__device__ inline void widest_chain(u64 s, int k, const uint8_t* split_dims, Chain& c) {
+    c.m = 0;
+    u32 seen = 0;
+    u64 a = s;
+    while (true) {
+        const int d = split_dims[a];
+        if (!((seen >> d) & 1u)) {
+            seen |= 1u << d;
+            c.d[c.m++] = (uint8_t)d;
+            if ((int)c.m == k) break;
+        }
+        if (a == 0) break;
+        a = (a - 1) >> 1;
+    }
+}
+
+// per-segment pick record of the select path
+enum { kSelLo = 0, kSelShift, kSelB, kSelR, kSelC, kSelOff, kSelFill, kSelW = 8 };
 
 // Working set of the global levels.
 // Points travel with their sort: W[buf] holds k coordinate arrays and one
 // index array (SoA, `stride` u32 each) in IN-ORDER layout -- the level-l
 // segment of node F(l)+j occupies [ib(j), ib(j) + ss(j)), and every finished
 // node stays at its own in-order slot, so splitting a segment moves nothing.
-// Each segment's data lives in W[parity] and flips buffer only on the digit
-// passes that actually reorder it.
+// Sort path: each segment's data lives in W[parity] and flips buffer only on the digit
+// passes that actually reorder it; select path: level l lives in
+// W[(l - lfirst) & 1].
 struct Buffers {
     u32* w[2];
     u64 stride;
+    // select path (select.cu)
+    u32* mmn[2];      // per level parity: [nseg] min of the level's key (flipped)
+    u32* mmx[2];      //                   [nseg] max
+    u32* sel;         // [nseg][kSelW]
+    u32* cand;        // candidate records [n][k+1]
+    u32* cand2;       // compaction buffer  [n][k+1]
+    u32* cand_ctr;    // [1]
+    u32* piv;         // [nseg][k+1] pivot records (coordinate bits + index)
+    Chain* chains;    // [nseg]
+    u64* pstatus;     // [tiles] partition lookback words
     u32* hist;        // [nseg][4][256] digit counts of the level's keys
     u32* seg_and;     // [nseg] AND of keys  \  digit d of segment j is constant
     u32* seg_or;      // [nseg] OR of keys   /  iff ((and ^ or) >> 8d) & 255 == 0
@@ -48,6 +96,45 @@ __device__ __host__ __forceinline__ u32* warr(const Buffers& bf, u32 buf, int a)
     return bf.w[buf] + (u64)a * bf.stride;
 }
 
+// select.cu
+struct SelArgs {
+    LevelGeom g;
+    int k, mode, D;
+    Buffers bf;
+    u32 par;               // W[par] holds the level's data
+    const u32* mmn;        // key range of the level's segments
+    const u32* mmx;
+    u32* hist;             // [nseg][2^D]
+    u32* sel;
+    u32* cand;
+    u32* cand2;
+    u32* cand_ctr;
+    u32* piv;
+    Chain* chains;
+    uint8_t* split_dims;
+    u32* perm;
+    float* out_pts;
+    const float* boxes_in;  // widest: boxes of the level's segments
+    float* boxes_out;       //         boxes of their children
+    u64* status;
+    u32* tile_ctr;
+    u32 epoch;
+    int want_mm;           // partition: record the children's key ranges
+    u32* mmn_next;
+    u32* mmx_next;
+    int tiles_per_cta;
+    u64 ntiles;
+};
+int sel_digit_bits(u64 nseg);
+void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cudaStream_t st);
+void launch_view_minmax(const BuildParams& bp, const Buffers& bf, int dim, u64 m, cudaStream_t st);
+void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cudaStream_t st);
+void launch_sel_hist(const SelArgs& a, int b, cudaStream_t st);
+void launch_sel_pick(const SelArgs& a, cudaStream_t st);
+void launch_sel_filter(const SelArgs& a, int b, cudaStream_t st);
+void launch_sel_select(const SelArgs& a, cudaStream_t st);
+void launch_sel_part(const SelArgs& a, int b, cudaStream_t st);
+
 // global_sort.cu
 void launch_init(const BuildParams& bp, const Buffers& bf, cudaStream_t st);
 void launch_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
@@ -55,13 +142,14 @@ void launch_plan(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t s
 void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 epoch,
                  u32* tile_ctr, u64* moved, cudaStream_t st);
 void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t st);
-void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride,
+void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride, int src_par,
                     cudaStream_t st);
 
 // subtree.cu
 size_t subtree_smem_bytes(int b, int k, int mode);
 size_t subtree_rr_smem_bytes(int b, int k);
-void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStream_t st);
+void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entry_sorted, int src_par,
+                    cudaStream_t st);
 
 // widest.cu
 void launch_world_bounds(const BuildParams& bp, u32* d_minmax, cudaStream_t st);

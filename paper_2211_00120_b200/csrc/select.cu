@@ -1,0 +1,837 @@
+// select.cu -- the global (large-segment) levels as pivot SELECTION plus one
+// stable 3-way PARTITION per level, instead of a full per-level sort.
+//
+// Why this is bit-exact: the reference sorts every level
+// stably by (tag, coord[dim]) (builder.py:165-181 / widest.py:119-131), so
+// inside a level-l node the order it leaves is a FIXED total order
+//     T(s) = (c[dim(s)], c[dim(parent)], ..., c[dim(root)], input index)
+// (later repeats of a dimension dropped; RR: dims l, l-1, ..., l-k+1 mod k).
+// The node's point is the element of rank pivot_off(s) under T(s)
+// (kernels_numba.py:21-46 arithmetic); the left child gets every element
+// below it, the right child every element above it.  Nothing else about the
+// reference's arrangement is observable: the next level orders its nodes by
+// a total order of its own.  So one level is
+//   hist   : per-segment histogram of the key c[dim] in 2^D equal-width
+//            buckets over the segment's exact [min, max] (HBM read 4 B/pt)
+//   pick   : bucket holding rank pivot_off, rank inside it     (per segment)
+//   filter : the elements of that bucket -> candidate records  (4 B/pt)
+//   select : radix select over the candidates' composite key (k coords +
+//            index) -> the node's point, written to its level-order slot
+//   part   : stable 3-way partition of every segment around its pivot
+//            (read + write k coords + index = 8(k+1) B/pt, decoupled
+//            lookback for the per-segment prefix), fused with the exact
+//            [min, max] of the children's next key
+// The partition is stable, so every segment keeps the INPUT order of its
+// points; the in-CTA phase (subtree.cu) derives its chain orders from that.
+//
+// Layout: in-order SoA as in global_sort.cu -- segment j of level l occupies
+// [ib(j), ib(j) + ss(j)) of W[(l - lfirst) & 1]; finished nodes leave a hole.
+#include "kernels.cuh"
+
+namespace lbkd {
+
+__device__ __forceinline__ int seg_key_dim(const SelArgs& a, u64 t) {
+    return a.mode == kRoundRobin ? (a.g.l % a.k) : (int)a.split_dims[a.g.Fl + a.g.sbase + t];
+}
+
+__device__ __forceinline__ int bitlen32(u32 v) { return v ? 32 - __clz(v) : 0; }
+
+// equal-width buckets of [lo, hi]: shift such that (hi - lo) >> shift < 2^D
+__device__ __forceinline__ u32 bucket_shift(u32 lo, u32 hi, int D) {
+    int b = bitlen32(hi - lo) - D;
+    return b > 0 ? (u32)b : 0u;
+}
+
+// Equal-width buckets of a segment's VALUE range [min, max] (the exact key
+// range, order-flipped u32).  Float keys are exponential in their bits, so
+// equal widths in key space would put half of a [0, 1) segment into the few
+// buckets of [0.5, 1); equal widths in value space split it evenly.  The map
+// is monotone (IEEE subtraction, multiplication by a positive scale and the
+// truncation are monotone) and identical in hist and filter, which is all
+// the selection needs.  -0.0 and +0.0 land in the same bucket.
+struct Bucketer {
+    double lo, scale;
+    u32 top;
+};
+
+__device__ __forceinline__ Bucketer make_bucketer(u32 kmin, u32 kmax, int D) {
+    Bucketer b;
+    b.lo = (double)unflip_key(kmin);
+    const double w = (double)unflip_key(kmax) - b.lo;
+    b.scale = w > 0.0 ? (double)(1u << D) / w : 0.0;
+    b.top = (1u << D) - 1u;
+    return b;
+}
+
+__device__ __forceinline__ u32 bucket_of(const Bucketer& b, u32 bits) {
+    const double x = ((double)__uint_as_float(bits) - b.lo) * b.scale;
+    return x >= (double)b.top ? b.top : (u32)x;
+}
+
+// tile -> (first segment part, second segment part) of the view; a tile
+// holds at most two segment parts (tile <= smallest segment)
+struct TileParts {
+    u64 j0;
+    u32 r0a, r0b, r1a, r1b;  // tile-relative [a, b) of the parts
+    bool has1;
+    u64 ib0, ib1;            // in-order (view) begins of segments j0, j0+1
+};
+
+__device__ __forceinline__ TileParts tile_parts(const LevelGeom& g, u64 ts, u64 cnt) {
+    TileParts p;
+    p.j0 = v_seg_of(g, ts);
+    const u64 s0b = v_ibegin(g, p.j0), s0e = s0b + v_size(g, p.j0);
+    p.ib0 = s0b;
+    p.r0a = s0b > ts ? (u32)(s0b - ts) : 0u;
+    p.r0b = s0e > ts ? (u32)((s0e - ts < cnt) ? s0e - ts : cnt) : 0u;
+    if (p.r0b < p.r0a) p.r0b = p.r0a;
+    p.has1 = false;
+    p.r1a = p.r1b = (u32)cnt;
+    p.ib1 = 0;
+    if (p.j0 + 1 < g.nseg) {
+        const u64 s1b = v_ibegin(g, p.j0 + 1);
+        if (s1b < ts + cnt) {
+            p.has1 = true;
+            p.ib1 = s1b;
+            p.r1a = (u32)(s1b - ts);
+            const u64 s1e = s1b + v_size(g, p.j0 + 1);
+            p.r1b = (u32)((s1e - ts < cnt) ? s1e - ts : cnt);
+        }
+    }
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// init: AoS float32 input -> W[0] SoA (k coordinate arrays + index array),
+// the non-finite check of builder.py:134-135 and the per-dimension min/max
+// (world_bounds, widest.py:84-88; the root's key range) as order-flipped
+// u32 so plain atomics are exact.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) init_stats_kernel(const float* __restrict__ pts, u64 n, int k, u32* w0,
+                                                         u64 stride, u32* err, u32* minmax) {
+    __shared__ u32 smn[LBKD_MAX_K], smx[LBKD_MAX_K];
+    if (threadIdx.x < LBKD_MAX_K) { smn[threadIdx.x] = 0xffffffffu; smx[threadIdx.x] = 0u; }
+    __syncthreads();
+    u32 mn[LBKD_MAX_K], mx[LBKD_MAX_K];
+#pragma unroll
+    for (int c = 0; c < LBKD_MAX_K; ++c) { mn[c] = 0xffffffffu; mx[c] = 0u; }
+    bool bad = false;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const float* q = pts + i * k;
+#pragma unroll
+        for (int c = 0; c < LBKD_MAX_K; ++c) {
+            if (c < k) {
+                const float f = __ldg(q + c);
+                bad |= !isfinite(f);
+                const u32 key = flip_key(f);
+                mn[c] = min(mn[c], key);
+                mx[c] = max(mx[c], key);
+                w0[c * stride + i] = __float_as_uint(f);
+            }
+        }
+        w0[(u64)k * stride + i] = (u32)i;
+    }
+    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+#pragma unroll
+    for (int c = 0; c < LBKD_MAX_K; ++c) {
+        if (c < k) {
+            const u32 a = __reduce_min_sync(kFullMask, mn[c]);
+            const u32 b = __reduce_max_sync(kFullMask, mx[c]);
+            if ((threadIdx.x & 31) == 0) { atomicMin(&smn[c], a); atomicMax(&smx[c], b); }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)k) {
+        atomicMin(&minmax[threadIdx.x], smn[threadIdx.x]);
+        atomicMax(&minmax[k + threadIdx.x], smx[threadIdx.x]);
+    }
+}
+
+void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cudaStream_t st) {
+    u64 blocks = (bp.n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    init_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(bp.pts, bp.n, bp.k, bf.w[0], bf.stride, bf.err, minmax);
+}
+
+// key range of the view's root segment from a W[0] array (sub-builds)
+__global__ void view_minmax_kernel(const u32* __restrict__ keys, u64 m, u32* mn_out, u32* mx_out) {
+    u32 mn = 0xffffffffu, mx = 0u;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+        const u32 key = flip_key(__uint_as_float(keys[i]));
+        mn = min(mn, key);
+        mx = max(mx, key);
+    }
+    mn = __reduce_min_sync(kFullMask, mn);
+    mx = __reduce_max_sync(kFullMask, mx);
+    if ((threadIdx.x & 31) == 0) { atomicMin(mn_out, mn); atomicMax(mx_out, mx); }
+}
+
+void launch_view_minmax(const BuildParams& bp, const Buffers& bf, int dim, u64 m, cudaStream_t st) {
+    u64 blocks = (m + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    if (blocks < 1) blocks = 1;
+    view_minmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(bf.w[0] + (u64)dim * bf.stride, m, bf.mmn[0], bf.mmx[0]);
+}
+
+// root: RR key range = dim 0 of the world box; widest: world box, root dim
+// = first argmax of the float64 widths (widest.py:91-93, :164-166)
+__global__ void root_kernel(const u32* minmax, int k, int mode, int root_dim, u32* mmn0, u32* mmx0, float* box0,
+                            uint8_t* split_dims) {
+    if (threadIdx.x != 0) return;
+    int d0 = root_dim;
+    if (mode == kWidest) {
+        double bw = 0.0;
+        for (int d = 0; d < k; ++d) {
+            const float lo = unflip_key(minmax[d]), hi = unflip_key(minmax[k + d]);
+            box0[d] = lo;
+            box0[k + d] = hi;
+            const double w = (double)hi - (double)lo;
+            if (d == 0 || w > bw) { bw = w; d0 = d; }
+        }
+        split_dims[0] = (uint8_t)d0;
+    }
+    mmn0[0] = minmax[d0];
+    mmx0[0] = minmax[k + d0];
+}
+
+void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cudaStream_t st) {
+    root_kernel<<<1, 32, 0, st>>>(minmax, bp.k, bp.mode, 0, bf.mmn[0], bf.mmx[0], bf.boxes[0], bp.split_dims);
+}
+
+// ---------------------------------------------------------------------------
+// hist: per segment, 2^D equal-width buckets of the key over [min, max].
+// Each CTA walks a contiguous run of tiles and flushes its shared histogram
+// when the segment changes (global atomics O(#CTAs + #segments) x 2^D).
+// ---------------------------------------------------------------------------
+constexpr int kHThreads = 256;
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
+    extern __shared__ u32 h[];
+    constexpr int T = kHThreads * ITEMS;
+    const int nb = 1 << a.D;
+    const LevelGeom& g = a.g;
+    for (int i = threadIdx.x; i < nb; i += kHThreads) h[i] = 0u;
+    const u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
+    u64 t1 = t0 + a.tiles_per_cta;
+    if (t1 > a.ntiles) t1 = a.ntiles;
+    u64 cur = v_seg_of(g, t0 * T);
+    __syncthreads();
+    auto flush = [&](u64 seg) {
+        __syncthreads();
+        u32* gh = a.hist + seg * (u64)nb;
+        for (int i = threadIdx.x; i < nb; i += kHThreads) {
+            const u32 v = h[i];
+            if (v) { atomicAdd(&gh[i], v); h[i] = 0u; }
+        }
+        __syncthreads();
+    };
+    const u32* W = a.bf.w[a.par];
+    for (u64 t = t0; t < t1; ++t) {
+        const u64 ts = t * T;
+        const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
+        TileParts tp = tile_parts(g, ts, cnt);
+        if (tp.j0 != cur) {  // the previous tile ended exactly at a segment end
+            flush(cur);
+            cur = tp.j0;
+        }
+        const u32* k0 = W + (u64)seg_key_dim(a, tp.j0) * a.bf.stride + ts;
+        const Bucketer b0 = make_bucketer(a.mmn[tp.j0], a.mmx[tp.j0], a.D);
+        u32 key[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const u32 r = (u32)(i * kHThreads + threadIdx.x);
+            key[i] = 0u;
+            if (r >= tp.r0a && r < tp.r0b) key[i] = k0[r];
+        }
+        if (tp.has1) {
+            const u32* k1 = W + (u64)seg_key_dim(a, tp.j0 + 1) * a.bf.stride + ts;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const u32 r = (u32)(i * kHThreads + threadIdx.x);
+                if (r >= tp.r1a && r < tp.r1b) key[i] = k1[r];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const u32 r = (u32)(i * kHThreads + threadIdx.x);
+            if (r >= tp.r0a && r < tp.r0b) atomicAdd(&h[bucket_of(b0, key[i])], 1u);
+        }
+        if (tp.has1) {
+            flush(cur);
+            cur = tp.j0 + 1;
+            const Bucketer b1 = make_bucketer(a.mmn[cur], a.mmx[cur], a.D);
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const u32 r = (u32)(i * kHThreads + threadIdx.x);
+                if (r >= tp.r1a && r < tp.r1b) atomicAdd(&h[bucket_of(b1, key[i])], 1u);
+            }
+        }
+    }
+    flush(cur);
+}
+
+// ---------------------------------------------------------------------------
+// pick: one CTA per segment -- the bucket b* holding rank pivot_off and the
+// rank r inside it; reserves the segment's candidate range.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
+    __shared__ u32 wtot[32];
+    const u64 j = blockIdx.x;
+    const int nb = 1 << a.D;
+    const int per = nb / 256;
+    const u32* h = a.hist + j * (u64)nb;
+    const u32 po = (u32)v_pivot(a.g, j);
+    u32 s = 0;
+    for (int i = 0; i < per; ++i) s += h[threadIdx.x * per + i];
+    const u32 ex = block_exclusive_scan<u32>(s, wtot, nullptr);
+    if (po >= ex && po < ex + s) {
+        u32 cum = ex;
+        int b = threadIdx.x * per;
+        while (cum + h[b] <= po) { cum += h[b]; ++b; }
+        u32* sel = a.sel + j * kSelW;
+        const u32 C = h[b];
+        sel[kSelLo] = a.mmn[j];
+        sel[kSelShift] = a.mmx[j];  // (hi) the bucketer is rebuilt from [lo, hi]
+        sel[kSelB] = (u32)b;
+        sel[kSelR] = po - cum;
+        sel[kSelC] = C;
+        sel[kSelOff] = atomicAdd(a.cand_ctr, C);
+        sel[kSelFill] = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// filter: every element in its segment's bucket b* -> a candidate record
+// (k coordinate bits + index) in the segment's candidate range.
+// ---------------------------------------------------------------------------
+template <int ITEMS>
+__global__ void __launch_bounds__(kHThreads) sel_filter_kernel(SelArgs a) {
+    __shared__ u32 wtot[32];
+    __shared__ u32 s_base;
+    constexpr int T = kHThreads * ITEMS;
+    const LevelGeom& g = a.g;
+    const u32* W = a.bf.w[a.par];
+    const int R = a.k + 1;
+    for (u64 t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const u64 ts = t * T;
+        const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
+        const TileParts tp = tile_parts(g, ts, cnt);
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+            if (part == 1 && !tp.has1) break;
+            const u64 j = tp.j0 + part;
+            const u32 ra = part ? tp.r1a : tp.r0a, rb = part ? tp.r1b : tp.r0b;
+            if (ra >= rb) continue;
+            u32* sel = a.sel + j * kSelW;
+            const Bucketer bk = make_bucketer(sel[kSelLo], sel[kSelShift], a.D);
+            const u32 bs = sel[kSelB], off = sel[kSelOff];
+            const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
+            // thread-contiguous items so one block scan orders the hits
+            u32 hits = 0;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const u32 r = (u32)(threadIdx.x * ITEMS + i);
+                if (r >= ra && r < rb && bucket_of(bk, kp[r]) == bs) hits |= 1u << i;
+            }
+            const u32 ex = block_exclusive_scan<u32>((u32)__popc(hits), wtot, nullptr);
+            if (threadIdx.x == kHThreads - 1) s_base = atomicAdd(&sel[kSelFill], ex + __popc(hits));
+            __syncthreads();
+            u32 slot = off + s_base + ex;
+            while (hits) {
+                const int i = __ffs(hits) - 1;
+                hits &= hits - 1;
+                const u32 r = (u32)(threadIdx.x * ITEMS + i);
+                u32* rec = a.cand + (u64)slot * R;
+                for (int c = 0; c < R; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
+                ++slot;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// select: one CTA per segment.  Radix select of rank r among the segment's
+// candidates under the composite key (chain coords order-flipped, then the
+// input index): per field, equal-width buckets over the live [min, max],
+// narrowing until one candidate is left.  Writes the node (level-order
+// output), the pivot record and chain the partition compares against, and
+// for widest the children's boxes and split dims (kernels_numba.py:80-110).
+// ---------------------------------------------------------------------------
+constexpr int kSThreads = 256;
+
+__device__ __forceinline__ u32 rec_field(const u32* rec, const Chain& ch, int f, int k) {
+    return f < ch.m ? flip_key(__uint_as_float(rec[ch.d[f]])) : rec[k];
+}
+
+__global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a) {
+    __shared__ u32 hist[256];
+    __shared__ u32 red[2][32];
+    __shared__ u32 s_misc[4];
+    __shared__ Chain s_ch;
+    const u64 j = blockIdx.x;
+    const int k = a.k, R = k + 1, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const LevelGeom& g = a.g;
+    const u64 node = g.Fl + g.sbase + j;
+    u32* sel = a.sel + j * kSelW;
+    if (tid == 0) {
+        if (a.mode == kRoundRobin) rr_chain(g.l, k, s_ch);
+        else widest_chain(node, k, a.split_dims, s_ch);
+    }
+    __syncthreads();
+    const Chain ch = s_ch;
+    u32 n = sel[kSelC];
+    u32 r = sel[kSelR];
+    const u64 off = sel[kSelOff];
+    const u32* src = a.cand + off * R;
+    u32* bufs[2] = {a.cand2 + off * R, a.cand + off * R};
+    int nb_flip = 0;
+    for (int f = 0; f <= ch.m && n > 1; ++f) {
+        while (n > 1) {
+            // live range of field f
+            u32 mn = 0xffffffffu, mx = 0u;
+            for (u32 i = tid; i < n; i += kSThreads) {
+                const u32 v = rec_field(src + (u64)i * R, ch, f, k);
+                mn = min(mn, v);
+                mx = max(mx, v);
+            }
+            mn = __reduce_min_sync(kFullMask, mn);
+            mx = __reduce_max_sync(kFullMask, mx);
+            if (lane == 0) { red[0][warp] = mn; red[1][warp] = mx; }
+            hist[tid] = 0u;
+            __syncthreads();
+            if (tid == 0) {
+                u32 a0 = 0xffffffffu, b0 = 0u;
+                for (int w = 0; w < kSThreads / 32; ++w) { a0 = min(a0, red[0][w]); b0 = max(b0, red[1][w]); }
+                s_misc[0] = a0;
+                s_misc[1] = b0;
+            }
+            __syncthreads();
+            mn = s_misc[0];
+            mx = s_misc[1];
+            if (mn == mx) break;  // field constant over the candidates
+            const u32 sh = bucket_shift(mn, mx, 8);
+            for (u32 i = tid; i < n; i += kSThreads)
+                atomicAdd(&hist[(rec_field(src + (u64)i * R, ch, f, k) - mn) >> sh], 1u);
+            __syncthreads();
+            if (tid == 0) {
+                u32 cum = 0;
+                int b = 0;
+                while (cum + hist[b] <= r) { cum += hist[b]; ++b; }
+                s_misc[2] = (u32)b;
+                s_misc[3] = cum;
+                s_misc[0] = 0u;  // compaction counter
+            }
+            __syncthreads();
+            const u32 bsel = s_misc[2];
+            r -= s_misc[3];
+            const u32 cnt = hist[bsel];
+            u32* dst = bufs[nb_flip];
+            for (u32 i0 = 0; i0 < n; i0 += kSThreads) {
+                const u32 i = i0 + tid;
+                bool hit = false;
+                if (i < n) hit = ((rec_field(src + (u64)i * R, ch, f, k) - mn) >> sh) == bsel;
+                const u32 m = __ballot_sync(kFullMask, hit);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    u32 base = 0;
+                    if (lane == leader) base = atomicAdd(&s_misc[0], (u32)__popc(m));
+                    base = __shfl_sync(kFullMask, base, leader);
+                    if (hit) {
+                        const u32* s = src + (u64)i * R;
+                        u32* d = dst + (u64)(base + __popc(m & lanemask_lt())) * R;
+                        for (int c = 0; c < R; ++c) d[c] = s[c];
+                    }
+                }
+            }
+            __syncthreads();
+            src = dst;
+            nb_flip ^= 1;
+            n = cnt;
+        }
+    }
+    // src[0] is the node's point
+    if (tid < R) a.piv[j * R + tid] = src[tid];
+    if (tid == 0) {
+        for (int c = 0; c < kChainWords; ++c) reinterpret_cast<u32*>(a.chains + j)[c] = reinterpret_cast<const u32*>(&ch)[c];
+        a.perm[node] = src[k];
+    }
+    if (tid < k) a.out_pts[node * k + tid] = __uint_as_float(src[tid]);
+    if (a.mode == kWidest && tid < 2) {
+        // child tid of node: box = node box clipped by the node's plane
+        const int d = ch.d[0];
+        const float plane = __uint_as_float(src[d]);
+        const float* bin = a.boxes_in + j * 2ull * k;
+        float lo[LBKD_MAX_K], hi[LBKD_MAX_K];
+        for (int q = 0; q < k; ++q) { lo[q] = bin[q]; hi[q] = bin[k + q]; }
+        if (tid == 0) { if (plane < hi[d]) hi[d] = plane; }
+        else { if (plane > lo[d]) lo[d] = plane; }
+        const u64 c = 2 * j + tid;
+        float* bout = a.boxes_out + c * 2ull * k;
+        int best = 0;
+        double bw = 0.0;
+        for (int q = 0; q < k; ++q) {
+            bout[q] = lo[q];
+            bout[k + q] = hi[q];
+            const double w = (double)hi[q] - (double)lo[q];
+            if (q == 0 || w > bw) { bw = w; best = q; }
+        }
+        const u64 cnode = 2 * node + 1 + tid;
+        if (cnode < g.n) a.split_dims[cnode] = (uint8_t)best;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// part: stable 3-way partition of every segment around its pivot.  Tile of
+// T = 512 x ITEMS in-order positions (at most two segment parts), payload
+// (k coords + index) staged in shared memory by cp.async, ranks from warp
+// ballots, per-segment prefix (elements below the pivot, pivot seen) by
+// decoupled lookback, coalesced write-out of the four runs (left/right of
+// each part).  Fused: exact [min, max] of each child's next key.
+// ---------------------------------------------------------------------------
+constexpr int kPThreads = 512;
+constexpr int kPWarps = kPThreads / 32;
+
+template <int ITEMS>
+struct PartSmem {
+    static constexpr int T = kPThreads * ITEMS;
+    unsigned short inv[T];
+    u32 wcnt[kPWarps][4];
+    u32 run_start[5];
+    u32 cmin[4], cmax[4];
+    u32 flags;
+    u32 piv[2][LBKD_MAX_K + 1];
+    Chain ch[2];
+    long long dbase[4];
+    u64 info[8];
+    int cdim[4];
+    // followed by raw[k+1][T] u32
+};
+
+__device__ __forceinline__ void cp_async4_(u32* smem_dst, const u32* gsrc) {
+    u32 s = (u32)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16_(u32* smem_dst, const u32* gsrc) {
+    u32 s = (u32)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+
+// status word: [63:35] epoch, [34:33] flag, [32] pivot seen, [31:0] #below
+__device__ __forceinline__ u64 pstatus(u32 epoch, u64 flag, u32 pseen, u32 cnt) {
+    return ((u64)epoch << 35) | (flag << 33) | ((u64)pseen << 32) | (u64)cnt;
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kPThreads, 2) sel_part_kernel(SelArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PartSmem<ITEMS>& S = *reinterpret_cast<PartSmem<ITEMS>*>(smem_raw);
+    constexpr int T = PartSmem<ITEMS>::T;
+    u32* raw = reinterpret_cast<u32*>(smem_raw + ((sizeof(PartSmem<ITEMS>) + 15) & ~(size_t)15));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const LevelGeom& g = a.g;
+    const int k = a.k, A = k + 1;
+
+    if (tid == 0) {
+        const u64 tile = atomicAdd(a.tile_ctr, 1u);
+        const u64 ts = tile * T;
+        const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
+        const TileParts tp = tile_parts(g, ts, cnt);
+        S.info[0] = tile;
+        S.info[1] = ts;
+        S.info[2] = tp.j0;
+        S.info[3] = ((u64)tp.r0a) | ((u64)tp.r0b << 32);
+        S.info[4] = ((u64)tp.r1a) | ((u64)tp.r1b << 32);
+        S.info[5] = tp.ib0;
+        S.info[6] = tp.ib1;
+        S.info[7] = tp.has1 ? 1u : 0u;
+        S.flags = 0u;
+        for (int q = 0; q < 4; ++q) { S.cmin[q] = 0xffffffffu; S.cmax[q] = 0u; }
+        if (a.want_mm) {
+            for (int q = 0; q < 4; ++q) {
+                const u64 child = 2 * (tp.j0 + (q >> 1)) + (q & 1);  // local child index
+                int d = (g.l + 1) % k;
+                if (a.mode == kWidest) {
+                    const u64 cnode = 2 * (g.Fl + g.sbase + tp.j0 + (q >> 1)) + 1 + (q & 1);
+                    d = (cnode < g.n && child < 2 * g.nseg) ? (int)a.split_dims[cnode] : 0;
+                }
+                S.cdim[q] = d;
+            }
+        }
+    }
+    __syncthreads();
+    const u64 tile = S.info[0], ts = S.info[1], j0 = S.info[2];
+    const u32 r0a = (u32)S.info[3], r0b = (u32)(S.info[3] >> 32);
+    const u32 r1a = (u32)S.info[4], r1b = (u32)(S.info[4] >> 32);
+    const bool has1 = S.info[7] != 0;
+    const u32* Wsrc = a.bf.w[a.par];
+    u32* Wdst = a.bf.w[a.par ^ 1u];
+
+    // --- stage the payload of both parts (16-byte chunks; ragged chunks per word)
+    for (u32 chunk = tid; chunk < (u32)T / 4u; chunk += kPThreads) {
+        const u32 r = chunk * 4u;
+        const bool all0 = r >= r0a && r + 4 <= r0b, all1 = r >= r1a && r + 4 <= r1b;
+        const bool any0 = r < r0b && r + 4 > r0a, any1 = r < r1b && r + 4 > r1a;
+        if (all0 || all1) {
+            const u32* gp = Wsrc + ts + r;
+            for (int c = 0; c < A; ++c) cp_async16_(raw + c * T + r, gp + (u64)c * a.bf.stride);
+        } else if (any0 || any1) {
+            for (u32 q = r; q < r + 4; ++q) {
+                const bool in = (q >= r0a && q < r0b) || (q >= r1a && q < r1b);
+                if (!in) continue;
+                const u32* gp = Wsrc + ts + q;
+                for (int c = 0; c < A; ++c) cp_async4_(raw + c * T + q, gp + (u64)c * a.bf.stride);
+            }
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (tid < 2 * A) {
+        const int p = tid / A, c = tid % A;
+        if (p == 0 || has1) S.piv[p][c] = a.piv[(j0 + p) * A + c];
+    }
+    if (tid < 2 * kChainWords) {
+        const int p = tid / kChainWords, c = tid % kChainWords;
+        if (p == 0 || has1) reinterpret_cast<u32*>(&S.ch[p])[c] = reinterpret_cast<const u32*>(a.chains + j0 + p)[c];
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+
+    // --- classify: -1 none, 0 left, 1 pivot, 2 right; q = part*2 + side
+    const u32 lt = lanemask_lt();
+    u32 run[4] = {0u, 0u, 0u, 0u};
+    u32 qr[ITEMS];  // q << 16 | warp-local rank, 0xffffffff = no slot
+    u32 mn[4], mx[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { mn[q] = 0xffffffffu; mx[q] = 0u; }
+    bool pseen0 = false, pseen1 = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+        const bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
+        int cls = -1;
+        if (in0 || in1) {
+            const int p = in1 ? 1 : 0;
+            const Chain& ch = S.ch[p];
+            const u32* pv = S.piv[p];
+            cls = 1;
+            for (int f = 0; f < ch.m; ++f) {
+                const int d = ch.d[f];
+                const u32 x = flip_key(__uint_as_float(raw[d * T + r]));
+                const u32 y = flip_key(__uint_as_float(pv[d]));
+                if (x != y) { cls = x < y ? 0 : 2; break; }
+            }
+            if (cls == 1) {
+                const u32 x = raw[k * T + r], y = pv[k];
+                cls = x < y ? 0 : (x > y ? 2 : 1);
+            }
+            if (cls == 1) { if (p) pseen1 = true; else pseen0 = true; }
+        }
+        const int q = (cls == 0 || cls == 2) ? ((in1 ? 2 : 0) + (cls == 2 ? 1 : 0)) : -1;
+        u32 myrank = 0;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const u32 b = __ballot_sync(kFullMask, q == qq);
+            if (q == qq) myrank = run[qq] + __popc(b & lt);
+            run[qq] += __popc(b);
+        }
+        qr[i] = q >= 0 ? (((u32)q << 16) | myrank) : 0xffffffffu;
+        if (a.want_mm && q >= 0) {
+            const u32 v = flip_key(__uint_as_float(raw[S.cdim[q] * T + r]));
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                if (q == qq) {
+                    mn[qq] = min(mn[qq], v);
+                    mx[qq] = max(mx[qq], v);
+                }
+            }
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S.wcnt[warp][q] = run[q];
+    }
+    if (__any_sync(kFullMask, pseen0) && lane == 0) atomicOr(&S.flags, 1u);
+    if (__any_sync(kFullMask, pseen1) && lane == 0) atomicOr(&S.flags, 2u);
+    if (a.want_mm) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 x = __reduce_min_sync(kFullMask, mn[q]);
+            const u32 y = __reduce_max_sync(kFullMask, mx[q]);
+            if (lane == 0 && x <= y) { atomicMin(&S.cmin[q], x); atomicMax(&S.cmax[q], y); }
+        }
+    }
+    __syncthreads();
+
+    // --- warp prefixes (warp 0), run starts, status publication + lookback
+    if (warp == 0) {
+        u32 tot[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 v = lane < kPWarps ? S.wcnt[lane][q] : 0u;
+            u32 x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(kFullMask, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane < kPWarps) S.wcnt[lane][q] = x - v;
+            tot[q] = __shfl_sync(kFullMask, x, 31);
+        }
+        const u32 fl = S.flags;
+        const u32 ps0 = fl & 1u, ps1 = (fl >> 1) & 1u;
+        const bool act0 = r0a < r0b;
+        const bool need_lb = act0 && S.info[5] < ts;  // segment j0 began before this tile
+        u64* my = a.status + tile;
+        if (lane == 0) {
+            if (has1) st_relaxed_u64(my, pstatus(a.epoch, kFlagInc, ps1, tot[2]));
+            else if (act0) st_relaxed_u64(my, pstatus(a.epoch, need_lb ? kFlagAgg : kFlagInc, ps0, tot[0]));
+        }
+        u32 below = 0, pb = 0;
+        if (need_lb) {
+            long long t = (long long)tile - 1;
+            while (true) {
+                const long long tt = t - lane;
+                const u64 w = tt >= 0 ? ld_relaxed_u64(a.status + tt) : 0ull;
+                const bool ready = (u32)(w >> 35) == a.epoch && ((w >> 33) & 3ull) != 0ull;
+                const bool inc = ready && ((w >> 33) & 3ull) == kFlagInc;
+                const u32 incm = __ballot_sync(kFullMask, inc);
+                const u32 nrm = __ballot_sync(kFullMask, !ready);
+                const int f = incm ? __ffs(incm) - 1 : 32;
+                const u32 need = f == 32 ? 0xffffffffu : (0xffffffffu >> (31 - f));
+                if (nrm & need) {
+                    __nanosleep(64);
+                    continue;
+                }
+                const bool use = lane <= f;
+                below += __reduce_add_sync(kFullMask, use ? (u32)(w & 0xffffffffull) : 0u);
+                pb |= __reduce_or_sync(kFullMask, use ? (u32)((w >> 32) & 1ull) : 0u);
+                if (f < 32) break;
+                t -= 32;
+            }
+            if (!has1 && lane == 0) st_relaxed_u64(my, pstatus(a.epoch, kFlagInc, pb | ps0, below + tot[0]));
+        }
+        if (lane == 0) {
+            const u64 ib0 = S.info[5], ib1 = S.info[6];
+            const u64 po0 = v_pivot(g, j0);
+            const u64 before = need_lb ? ts - ib0 : 0ull;
+            const u64 rb = before - below - pb;
+            S.dbase[0] = (long long)(ib0 + below);
+            S.dbase[1] = (long long)(ib0 + po0 + 1 + rb);
+            if (has1) {
+                const u64 po1 = v_pivot(g, j0 + 1);
+                S.dbase[2] = (long long)ib1;
+                S.dbase[3] = (long long)(ib1 + po1 + 1);
+            } else {
+                S.dbase[2] = S.dbase[3] = 0;
+            }
+            S.run_start[0] = 0u;
+            S.run_start[1] = tot[0];
+            S.run_start[2] = tot[0] + tot[1];
+            S.run_start[3] = tot[0] + tot[1] + tot[2];
+            S.run_start[4] = tot[0] + tot[1] + tot[2] + tot[3];
+        }
+    }
+    __syncthreads();
+
+    // --- slots (stable: warp order, then row, then lane)
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        if (qr[i] != 0xffffffffu) {
+            const u32 q = qr[i] >> 16;
+            const u32 slot = S.run_start[q] + S.wcnt[warp][q] + (qr[i] & 0xffffu);
+            S.inv[slot] = (unsigned short)(warp * ITEMS * 32 + i * 32 + lane);
+        }
+    }
+    if (a.want_mm && tid < 4) {
+        const int q = tid;
+        if (S.cmin[q] <= S.cmax[q]) {
+            const u64 child = 2 * (j0 + (q >> 1)) + (q & 1);
+            atomicMin(&a.mmn_next[child], S.cmin[q]);
+            atomicMax(&a.mmx_next[child], S.cmax[q]);
+        }
+    }
+    __syncthreads();
+
+    // --- coalesced write-out of the four runs
+    const u32 nslots = S.run_start[4];
+    const u64 stride = a.bf.stride;
+    for (u32 s = tid; s < nslots; s += kPThreads) {
+        const int q = (s >= S.run_start[1]) + (s >= S.run_start[2]) + (s >= S.run_start[3]);
+        const u64 dst = (u64)S.dbase[q] + (s - S.run_start[q]);
+        const u32 src = S.inv[s];
+        u32* d = Wdst + dst;
+        for (int c = 0; c < A; ++c) d[(u64)c * stride] = raw[c * T + src];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int sel_items(int b) {
+    int items = (1 << (b - 1)) / kPThreads;
+    return items > 8 ? 8 : items;
+}
+
+int sel_digit_bits(u64 nseg) {
+    int lg = 0;
+    while ((1ull << lg) < nseg) ++lg;
+    int D = 20 - lg;
+    return D < 8 ? 8 : (D > 11 ? 11 : D);
+}
+
+void launch_sel_hist(const SelArgs& a0, int b, cudaStream_t st) {
+    SelArgs a = a0;
+    int items = (1 << (b - 1)) / kHThreads;
+    if (items > 8) items = 8;
+    const u64 T = (u64)kHThreads * items;
+    a.ntiles = (a.g.nview + T - 1) / T;
+    const u64 target = 148 * 8;
+    u64 tpc = (a.ntiles + target - 1) / target;
+    if (tpc < 1) tpc = 1;
+    a.tiles_per_cta = (int)tpc;
+    const unsigned grid = (unsigned)((a.ntiles + tpc - 1) / tpc);
+    const size_t sm = sizeof(u32) << a.D;
+    if (items >= 8) sel_hist_kernel<8><<<grid, kHThreads, sm, st>>>(a);
+    else sel_hist_kernel<4><<<grid, kHThreads, sm, st>>>(a);
+}
+
+void launch_sel_pick(const SelArgs& a, cudaStream_t st) {
+    sel_pick_kernel<<<(unsigned)a.g.nseg, 256, 0, st>>>(a);
+}
+
+void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
+    SelArgs a = a0;
+    int items = (1 << (b - 1)) / kHThreads;
+    if (items > 8) items = 8;
+    const u64 T = (u64)kHThreads * items;
+    a.ntiles = (a.g.nview + T - 1) / T;
+    u64 grid = a.ntiles < 148 * 8 ? a.ntiles : 148 * 8;
+    if (items >= 8) sel_filter_kernel<8><<<(unsigned)grid, kHThreads, 0, st>>>(a);
+    else sel_filter_kernel<4><<<(unsigned)grid, kHThreads, 0, st>>>(a);
+}
+
+void launch_sel_select(const SelArgs& a, cudaStream_t st) {
+    sel_select_kernel<<<(unsigned)a.g.nseg, kSThreads, 0, st>>>(a);
+}
+
+template <int ITEMS>
+static void launch_part_t(const SelArgs& a, unsigned grid, cudaStream_t st) {
+    const size_t sm = ((sizeof(PartSmem<ITEMS>) + 15) & ~(size_t)15) +
+                      (size_t)(a.k + 1) * PartSmem<ITEMS>::T * sizeof(u32);
+    cudaFuncSetAttribute(sel_part_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    sel_part_kernel<ITEMS><<<grid, kPThreads, sm, st>>>(a);
+}
+
+void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
+    const int items = sel_items(b);
+    const u64 T = (u64)kPThreads * items;
+    const unsigned grid = (unsigned)((a.g.nview + T - 1) / T);
+    switch (items) {
+        case 8: launch_part_t<8>(a, grid, st); break;
+        case 4: launch_part_t<4>(a, grid, st); break;
+        default: launch_part_t<2>(a, grid, st); break;
+    }
+}
+
+}  // namespace lbkd

@@ -43,6 +43,9 @@ struct SubtreeArgs {
     u64 pbase;    // global in-order position of the view's first point
     int lfirst;   // root level of the view
     int from_pts; // single-CTA whole-tree build straight from the input
+    int entry_sorted;  // sort path: each subtree arrives in the reference's
+                       // order T(parent); select path: in input order
+    int src_par;       // select path: W[src_par] holds the subtree (else prev_state)
 };
 
 size_t subtree_smem_bytes(int b, int k, int mode) {
@@ -140,6 +143,96 @@ __device__ __forceinline__ void block_pass(const ET* __restrict__ Ein, ET* __res
     __syncthreads();
 }
 
+// Stable sort of the list in buf[cur] (m entries, local id in the low 16
+// bits) by the coordinate array Pd, ping-ponging between buf0 and buf1;
+// digits constant over the list are skipped.  Returns the new cur.
+template <typename ET>
+__device__ int list_sort_dim(ET* buf0, ET* buf1, int cur, int m, const float* Pd, unsigned short (*cnt)[256],
+                             u32 (*gsum)[256], u32* scratch) {
+    const int tid = threadIdx.x;
+    u32 x_and = 0xffffffffu, x_or = 0u;
+    for (int p = tid; p < m; p += kSubThreads) {
+        const u32 kk = flip_key(Pd[p]);
+        x_and &= kk;
+        x_or |= kk;
+    }
+    x_and = __reduce_and_sync(kFullMask, x_and);
+    x_or = __reduce_or_sync(kFullMask, x_or);
+    scratch[32 + (tid >> 5)] = x_and ^ x_or;  // every lane stores the warp-uniform value: a
+    // lane-0 guard here was miscompiled by NVVM 12.9 (it reused the guarded
+    // (tid >> 3) == 4 * warp for every lane in the next cnt[warp] address)
+    __syncthreads();
+    u32 vary = 0;
+    for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
+    __syncthreads();
+    for (int q = 0; q < 4; ++q) {
+        if (((vary >> (8 * q)) & 255u) == 0) continue;
+        const int sh = 8 * q;
+        block_pass(cur ? buf1 : buf0, cur ? buf0 : buf1, m,
+                   [&](u32 e) { return (flip_key(Pd[e & 0xffffu]) >> sh) & 255u; }, cnt, gsum, scratch);
+        cur ^= 1;
+    }
+    return cur;
+}
+
+// Entry order of a subtree that arrives in INPUT order (select path): the
+// reference's order inside the subtree root's parent, i.e. the lexicographic
+// order of (c[ch.d[0]], ..., c[ch.d[m-1]], input index).  One stable sort by
+// the leading field leaves every run of equal leading keys in input order;
+// runs of at most kTieRun elements (float data: almost always pairs) are then
+// re-ordered by the remaining fields in place, one thread per run (insertion
+// sort).  Only when a longer run exists are the remaining fields sorted in
+// LSD order from the input order again.  buf0 holds the identity on entry;
+// returns the buffer (0/1) holding the result.
+constexpr int kTieRun = 32;
+
+__device__ __forceinline__ bool chain_less(u32 a, u32 b, const float* P, int ldP, const Chain& ch) {
+    for (u32 f = 1; f < ch.m; ++f) {
+        const float* Pd = P + (size_t)ch.d[f] * ldP;
+        const u32 x = flip_key(Pd[a]), y = flip_key(Pd[b]);
+        if (x != y) return x < y;
+    }
+    return a < b;  // local ids are in input order
+}
+
+template <typename ET>
+__device__ int entry_order(ET* buf0, ET* buf1, int m, const float* P, int ldP, const Chain& ch,
+                           unsigned short (*cnt)[256], u32 (*gsum)[256], u32* scratch) {
+    if (ch.m == 0) return 0;
+    const float* P0 = P + (size_t)ch.d[0] * ldP;
+    int cur = list_sort_dim(buf0, buf1, 0, m, P0, cnt, gsum, scratch);
+    if (ch.m == 1) return cur;
+    ET* L = cur ? buf1 : buf0;
+    int longrun = 0;
+    for (int p = threadIdx.x; p + 1 < m; p += kSubThreads) {
+        const u32 kp = flip_key(P0[L[p] & 0xffffu]);
+        if (flip_key(P0[L[p + 1] & 0xffffu]) != kp) continue;           // no tie at p
+        if (p > 0 && flip_key(P0[L[p - 1] & 0xffffu]) == kp) continue;  // not the run's start
+        int q = p + 2;
+        while (q < m && q - p <= kTieRun && flip_key(P0[L[q] & 0xffffu]) == kp) ++q;
+        if (q - p > kTieRun) {
+            longrun = 1;
+            continue;
+        }
+        for (int i = p + 1; i < q; ++i) {  // insertion sort of L[p, q)
+            const ET v = L[i];
+            int t = i - 1;
+            while (t >= p && chain_less((u32)v & 0xffffu, (u32)L[t] & 0xffffu, P, ldP, ch)) {
+                L[t + 1] = L[t];
+                --t;
+            }
+            L[t + 1] = v;
+        }
+    }
+    if (!__syncthreads_or(longrun)) return cur;
+    for (int p = threadIdx.x; p < m; p += kSubThreads) buf0[p] = (ET)p;
+    __syncthreads();
+    cur = 0;
+    for (int f = (int)ch.m - 1; f >= 0; --f)
+        cur = list_sort_dim(buf0, buf1, cur, m, P + (size_t)ch.d[f] * ldP, cnt, gsum, scratch);
+    return cur;
+}
+
 __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M = a.M, k = a.k, tid = threadIdx.x;
@@ -179,7 +272,9 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
     const u32* vin = nullptr;
     if (!a.from_pts) {
         u32 par = 0;
-        if (a.lam0 != a.lfirst) {
+        if (a.src_par >= 0) {
+            par = (u32)a.src_par;
+        } else if (a.lam0 != a.lfirst) {
             const uint8_t st = a.prev_state[jl >> 1];
             par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
         }
@@ -208,6 +303,15 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
     };
 
     int cur = 0;
+    if (!a.entry_sorted && !a.from_pts && a.lam0 > 0) {
+        // input order -> the reference's order inside the subtree's parent
+        // (no static shared memory here: it would misalign the dynamic
+        // region, so every thread derives the chain itself)
+        Chain ch;
+        if (a.mode == kRoundRobin) rr_chain(a.lam0 - 1, k, ch);
+        else widest_chain(make_geom(a.n, a.lam0 - 1).Fl + (j >> 1), k, a.split_dims, ch);
+        cur = entry_order(E[0], E[1], m, P, M, ch, cnt, gsum, scratch);
+    }
     for (int lam = a.lam0; lam <= a.L - 2; ++lam) {
         const LevelGeom g = make_geom(a.n, lam);
         const int dl = lam - a.lam0;
@@ -233,7 +337,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
         }
         x_and = __reduce_and_sync(kFullMask, x_and);
         x_or = __reduce_or_sync(kFullMask, x_or);
-        if ((tid & 31) == 0) { scratch[32 + (tid >> 5)] = x_and ^ x_or; }
+        scratch[32 + (tid >> 5)] = x_and ^ x_or;  // all lanes: same value
         __syncthreads();
         u32 vary = 0;
         for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
@@ -384,19 +488,38 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
     const LevelGeom g0 = make_geom(a.n, a.lam0);
     const int m = (int)seg_size(g0, j);
     u32 par = 0;
-    if (a.lam0 != a.lfirst) {
+    if (a.src_par >= 0) {
+        par = (u32)a.src_par;
+    } else if (a.lam0 != a.lfirst) {
         const uint8_t st = a.prev_state[jl >> 1];
         par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
     }
     const u32* src = a.w[par] + (seg_ibegin(g0, j) - a.pbase);
     const u32* vin = src + (u64)k * a.stride;
     const int e = (a.lam0 - 1) % k;  // dimension of the entry order
+    u16* ident = a.entry_sorted ? Lst[e] : Lst[0];
     for (int lid = tid; lid < m; lid += kSubThreads) {
         for (int c = 0; c < k; ++c) P[c * Mp + lid] = __uint_as_float(src[(u64)c * a.stride + lid]);
-        Lst[e][lid] = (u16)lid;
+        ident[lid] = (u16)lid;
         segv[lid] = 0;
     }
     __syncthreads();
+    if (!a.entry_sorted) {
+        // input order -> T_e (full chain: lam0 >= k), then hand the k other
+        // buffers out as the remaining lists and the spare
+        Chain ch;
+        rr_chain(a.lam0 - 1, k, ch);
+        const int r = entry_order(Lst[0], Lst[1], m, P, Mp, ch, cnt, gsum, scratch);
+        u16* pool[kMaxK + 1];
+        for (int d = 0; d <= k; ++d) pool[d] = Lst[d];
+        u16* res = pool[r];
+        int q = 0;
+        for (int d = 0; d <= k; ++d) {
+            if (d == e) { Lst[d] = res; continue; }
+            if (pool[q] == res) ++q;
+            Lst[d] = pool[q++];
+        }
+    }
 
     // ---- chain sorts: T_d = stable_sort(T_{d-1}, c[d]) for the k-1 other dims
     for (int q = 1; q < k; ++q) {
@@ -411,7 +534,9 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         }
         x_and = __reduce_and_sync(kFullMask, x_and);
         x_or = __reduce_or_sync(kFullMask, x_or);
-        if ((tid & 31) == 0) scratch[32 + (tid >> 5)] = x_and ^ x_or;
+        scratch[32 + (tid >> 5)] = x_and ^ x_or;  // every lane stores the warp-uniform value: a
+    // lane-0 guard here was miscompiled by NVVM 12.9 (it reused the guarded
+    // (tid >> 3) == 4 * warp for every lane in the next cnt[warp] address)
         __syncthreads();
         u32 vary = 0;
         for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
@@ -544,7 +669,8 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
     if (a.lam0 > a.L - 2 && tid == 0 && m == 1) write_node(g0.Fl + j, 0u);
 }
 
-void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStream_t st) {
+void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entry_sorted, int src_par,
+                    cudaStream_t st) {
     SubtreeArgs a;
     a.n = bp.n;
     a.L = bit_length(bp.n);
@@ -566,6 +692,8 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, cudaStre
     a.pbase = seg_ibegin(make_geom(bp.n, bp.lroot), bp.jroot);
     a.lfirst = bp.lroot;
     a.from_pts = lam0 == 0 ? 1 : 0;
+    a.entry_sorted = entry_sorted;
+    a.src_par = src_par;
     unsigned grid = (unsigned)(1ull << (lam0 - bp.lroot));
     if (bp.mode == kRoundRobin && lam0 >= bp.k) {
         size_t sm = subtree_rr_smem_bytes(bp.b, bp.k);
