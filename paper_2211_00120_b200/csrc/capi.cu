@@ -40,7 +40,6 @@ struct lbkd_ctx {
     int ctr = 0;
     int64_t launches = 0;
     int algo = 0;      // 0: select + partition (default), 1: per-level sort
-    u32 pepoch = 1;    // partition lookback epochs
     size_t cap_cand = 0, cap_ptiles = 0, cap_piv = 0;
     // grow-only device allocations
     size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_w = 0, cap_copy = 0;
@@ -150,7 +149,7 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
         c->cap_seg = nseg;
     }
     if (lam0 > 0 && c->algo == 0) {
-        const size_t rec = (size_t)(k + 1) * n;
+        const size_t rec = (size_t)(k + 2) * n;
         if (rec > c->cap_cand) {
             if ((rc = grow(c->bf.cand, dummy, rec))) return rc;
             if ((rc = grow(c->bf.cand2, dummy, rec))) return rc;
@@ -161,16 +160,16 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
             if ((rc = grow(c->bf.piv, dummy, pv))) return rc;
             if ((rc = grow(c->bf.chains, dummy, nseg))) return rc;
             if ((rc = grow(c->bf.sel, dummy, nseg * kSelW))) return rc;
+            if ((rc = grow(c->bf.ppos, dummy, nseg))) return rc;
             for (int i = 0; i < 2; ++i) {
                 if ((rc = grow(c->bf.mmn[i], dummy, nseg))) return rc;
                 if ((rc = grow(c->bf.mmx[i], dummy, nseg))) return rc;
             }
             c->cap_piv = pv;
         }
-        const size_t pt = n / 1024 + 2;  // partition tiles are >= 1024 points
+        const size_t pt = 2 * (n / (size_t)sel_tile(b) + 2);
         if (pt > c->cap_ptiles) {
-            if ((rc = grow(c->bf.pstatus, dummy, pt))) return rc;
-            CK(cudaMemset(c->bf.pstatus, 0, pt * sizeof(u64)));
+            if ((rc = grow(c->bf.tile_lt, dummy, pt))) return rc;
             c->cap_ptiles = pt;
         }
     }
@@ -280,16 +279,8 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.out_pts = bp.out_pts;
         a.boxes_in = bf.boxes[par];
         a.boxes_out = bf.boxes[par ^ 1];
-        a.status = bf.pstatus;
-        a.tile_ctr = bf.tile_ctr + (c->ctr % 256);
-        ++c->ctr;
-        a.epoch = c->pepoch;
-        c->pepoch = (c->pepoch + 1) & 0x1fffffffu;
-        if (c->pepoch == 0) {
-            // epoch wrapped: no stale status word may match a future epoch
-            CK(cudaMemsetAsync(bf.pstatus, 0, c->cap_ptiles * sizeof(u64), st));
-            c->pepoch = 1;
-        }
+        a.tile_lt = bf.tile_lt;
+        a.ppos = bf.ppos;
         a.want_mm = last ? 0 : 1;
         a.mmn_next = bf.mmn[par ^ 1];
         a.mmx_next = bf.mmx[par ^ 1];
@@ -303,7 +294,7 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         launch_sel_filter(a, bp.b, st);
         prof_end(c, st, kPFilter, 4.0 * pts);
         if (prof_begin(c, st)) return LBKD_ECUDA;
-        launch_sel_select(a, st);
+        launch_sel_select(a, bp.b, st);
         prof_end(c, st, kPSelect, 0.0);
         if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_sel_part(a, bp.b, st);
@@ -568,7 +559,8 @@ void lbkd_destroy(lbkd_ctx* c) {
     cudaFree(c->bf.cand_ctr);
     cudaFree(c->bf.piv);
     cudaFree(c->bf.chains);
-    cudaFree(c->bf.pstatus);
+    cudaFree(c->bf.tile_lt);
+    cudaFree(c->bf.ppos);
     cudaFree(c->bf.seg_and);
     cudaFree(c->bf.seg_or);
     cudaFree(c->bf.status);

@@ -64,7 +64,8 @@ struct Buffers {
     u32* cand_ctr;    // [1]
     u32* piv;         // [nseg][k+1] pivot records (coordinate bits + index)
     Chain* chains;    // [nseg]
-    u64* pstatus;     // [tiles] partition lookback words
+    u32* tile_lt;     // [tiles][2] per (tile, segment part) counts below the pivot
+    u32* ppos;        // [nseg] pivot positions
     u32* hist;        // [nseg][4][256] digit counts of the level's keys
     u32* seg_and;     // [nseg] AND of keys  \  digit d of segment j is constant
     u32* seg_or;      // [nseg] OR of keys   /  iff ((and ^ or) >> 8d) & 255 == 0
@@ -116,9 +117,8 @@ struct SelArgs {
     float* out_pts;
     const float* boxes_in;  // widest: boxes of the level's segments
     float* boxes_out;       //         boxes of their children
-    u64* status;
-    u32* tile_ctr;
-    u32 epoch;
+    u32* tile_lt;          // [tiles][2] below-pivot counts -> exclusive prefixes
+    u32* ppos;             // [nseg] in-order position of each segment's pivot
     int want_mm;           // partition: record the children's key ranges
     u32* mmn_next;
     u32* mmx_next;
@@ -132,7 +132,9 @@ void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cu
 void launch_sel_hist(const SelArgs& a, int b, cudaStream_t st);
 void launch_sel_pick(const SelArgs& a, cudaStream_t st);
 void launch_sel_filter(const SelArgs& a, int b, cudaStream_t st);
-void launch_sel_select(const SelArgs& a, cudaStream_t st);
+void launch_sel_select(const SelArgs& a, int b, cudaStream_t st);
+int sel_items(int b);
+int sel_tile(int b);
 void launch_sel_part(const SelArgs& a, int b, cudaStream_t st);
 
 // global_sort.cu

@@ -65,7 +65,7 @@ __device__ __forceinline__ Bucketer make_bucketer(u32 kmin, u32 kmax, int D) {
 
 __device__ __forceinline__ u32 bucket_of(const Bucketer& b, u32 bits) {
     const double x = ((double)__uint_as_float(bits) - b.lo) * b.scale;
-    return x >= (double)b.top ? b.top : (u32)x;
+    return x < (double)b.top ? (u32)x : b.top;  // NaN (non-finite input, reported later) -> top
 }
 
 // tile -> (first segment part, second segment part) of the view; a tile
@@ -302,17 +302,22 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// filter: every element in its segment's bucket b* -> a candidate record
-// (k coordinate bits + index) in the segment's candidate range.
+// filter: per (tile, part) the number of elements in buckets below b*, and
+// every element of bucket b* -> a candidate record (k coordinate bits, input
+// index, in-order position) in the segment's candidate range.  Tiles are the
+// partition's tiles (kPThreads x ITEMS positions).
 // ---------------------------------------------------------------------------
+constexpr int kPThreads = 256;
+constexpr int kPWarps = kPThreads / 32;
+
 template <int ITEMS>
-__global__ void __launch_bounds__(kHThreads) sel_filter_kernel(SelArgs a) {
+__global__ void __launch_bounds__(kPThreads) sel_filter_kernel(SelArgs a) {
     __shared__ u32 wtot[32];
     __shared__ u32 s_base;
-    constexpr int T = kHThreads * ITEMS;
+    constexpr int T = kPThreads * ITEMS;
     const LevelGeom& g = a.g;
     const u32* W = a.bf.w[a.par];
-    const int R = a.k + 1;
+    const int k = a.k, R = k + 2;
     for (u64 t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         const u64 ts = t * T;
         const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
@@ -328,22 +333,33 @@ __global__ void __launch_bounds__(kHThreads) sel_filter_kernel(SelArgs a) {
             const u32 bs = sel[kSelB], off = sel[kSelOff];
             const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
             // thread-contiguous items so one block scan orders the hits
-            u32 hits = 0;
+            u32 hits = 0, nlt = 0;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const u32 r = (u32)(threadIdx.x * ITEMS + i);
-                if (r >= ra && r < rb && bucket_of(bk, kp[r]) == bs) hits |= 1u << i;
+                if (r >= ra && r < rb) {
+                    const u32 b = bucket_of(bk, kp[r]);
+                    if (b == bs) hits |= 1u << i;
+                    nlt += b < bs ? 1u : 0u;
+                }
             }
-            const u32 ex = block_exclusive_scan<u32>((u32)__popc(hits), wtot, nullptr);
-            if (threadIdx.x == kHThreads - 1) s_base = atomicAdd(&sel[kSelFill], ex + __popc(hits));
+            // one scan: hits (low 16 bits) and below-b* counts (high 16)
+            const u32 v = (u32)__popc(hits) | (nlt << 16);
+            const u32 ex = block_exclusive_scan<u32>(v, wtot, nullptr);
+            if (threadIdx.x == kPThreads - 1) {
+                const u32 tot = ex + v;
+                s_base = atomicAdd(&sel[kSelFill], tot & 0xffffu);
+                a.tile_lt[t * 2 + part] = tot >> 16;
+            }
             __syncthreads();
-            u32 slot = off + s_base + ex;
+            u32 slot = off + s_base + (ex & 0xffffu);
             while (hits) {
                 const int i = __ffs(hits) - 1;
                 hits &= hits - 1;
                 const u32 r = (u32)(threadIdx.x * ITEMS + i);
                 u32* rec = a.cand + (u64)slot * R;
-                for (int c = 0; c < R; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
+                for (int c = 0; c <= k; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
+                rec[k + 1] = (u32)(ts + r);
                 ++slot;
             }
             __syncthreads();
@@ -355,23 +371,28 @@ __global__ void __launch_bounds__(kHThreads) sel_filter_kernel(SelArgs a) {
 // select: one CTA per segment.  Radix select of rank r among the segment's
 // candidates under the composite key (chain coords order-flipped, then the
 // input index): per field, equal-width buckets over the live [min, max],
-// narrowing until one candidate is left.  Writes the node (level-order
-// output), the pivot record and chain the partition compares against, and
-// for widest the children's boxes and split dims (kernels_numba.py:80-110).
+// narrowing until one candidate is left.  Every candidate that falls below
+// the narrowing bucket is below the pivot: it is added to its tile's count,
+// after which the segment's per-tile counts are turned into exclusive
+// prefixes (the partition's destinations, no lookback).  Writes the node
+// (level-order output), the pivot record / position / chain the partition
+// compares against, and for widest the children's boxes and split dims
+// (kernels_numba.py:80-110).
 // ---------------------------------------------------------------------------
 constexpr int kSThreads = 256;
 
 __device__ __forceinline__ u32 rec_field(const u32* rec, const Chain& ch, int f, int k) {
-    return f < ch.m ? flip_key(__uint_as_float(rec[ch.d[f]])) : rec[k];
+    return f < (int)ch.m ? flip_key(__uint_as_float(rec[ch.d[f]])) : rec[k];
 }
 
-__global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a) {
+__global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T) {
     __shared__ u32 hist[256];
     __shared__ u32 red[2][32];
     __shared__ u32 s_misc[4];
+    __shared__ u32 wtot[32];
     __shared__ Chain s_ch;
     const u64 j = blockIdx.x;
-    const int k = a.k, R = k + 1, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = a.k, R = k + 2, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const LevelGeom& g = a.g;
     const u64 node = g.Fl + g.sbase + j;
     u32* sel = a.sel + j * kSelW;
@@ -381,13 +402,23 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a) {
     }
     __syncthreads();
     const Chain ch = s_ch;
+    // the segment's tiles: the first one holds it as part 1 unless the
+    // segment starts exactly at the tile start
+    const u64 ib = v_ibegin(g, j);
+    const u64 tfirst = ib / (u64)T;
+    const u64 tlast = (ib + v_size(g, j) - 1) / (u64)T;
+    const u32 pfirst = (ib == tfirst * (u64)T) ? 0u : 1u;
+    auto count_below = [&](const u32* rec) {
+        const u64 t = rec[k + 1] / (u64)T;
+        atomicAdd(&a.tile_lt[t * 2 + (t == tfirst ? pfirst : 0u)], 1u);
+    };
     u32 n = sel[kSelC];
     u32 r = sel[kSelR];
     const u64 off = sel[kSelOff];
     const u32* src = a.cand + off * R;
     u32* bufs[2] = {a.cand2 + off * R, a.cand + off * R};
     int nb_flip = 0;
-    for (int f = 0; f <= ch.m && n > 1; ++f) {
+    for (int f = 0; f <= (int)ch.m && n > 1; ++f) {
         while (n > 1) {
             // live range of field f
             u32 mn = 0xffffffffu, mx = 0u;
@@ -431,7 +462,11 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a) {
             for (u32 i0 = 0; i0 < n; i0 += kSThreads) {
                 const u32 i = i0 + tid;
                 bool hit = false;
-                if (i < n) hit = ((rec_field(src + (u64)i * R, ch, f, k) - mn) >> sh) == bsel;
+                if (i < n) {
+                    const u32 b = (rec_field(src + (u64)i * R, ch, f, k) - mn) >> sh;
+                    hit = b == bsel;
+                    if (b < bsel) count_below(src + (u64)i * R);
+                }
                 const u32 m = __ballot_sync(kFullMask, hit);
                 if (m) {
                     const int leader = __ffs(m) - 1;
@@ -452,10 +487,11 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a) {
         }
     }
     // src[0] is the node's point
-    if (tid < R) a.piv[j * R + tid] = src[tid];
+    if (tid <= k) a.piv[j * (k + 1) + tid] = src[tid];
     if (tid == 0) {
         for (int c = 0; c < kChainWords; ++c) reinterpret_cast<u32*>(a.chains + j)[c] = reinterpret_cast<const u32*>(&ch)[c];
         a.perm[node] = src[k];
+        a.ppos[j] = src[k + 1];
     }
     if (tid < k) a.out_pts[node * k + tid] = __uint_as_float(src[tid]);
     if (a.mode == kWidest && tid < 2) {
@@ -480,298 +516,296 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a) {
         const u64 cnode = 2 * node + 1 + tid;
         if (cnode < g.n) a.split_dims[cnode] = (uint8_t)best;
     }
+    // per-tile counts below the pivot -> exclusive prefixes in tile order
+    __syncthreads();
+    u32 carry = 0;
+    for (u64 t0 = tfirst; t0 <= tlast; t0 += kSThreads) {
+        const u64 t = t0 + tid;
+        u32* slot = t <= tlast ? &a.tile_lt[t * 2 + (t == tfirst ? pfirst : 0u)] : nullptr;
+        const u32 v = slot ? *slot : 0u;
+        const u32 ex = block_exclusive_scan<u32>(v, wtot, nullptr);
+        if (slot) *slot = carry + ex;
+        // chunk total: last thread's inclusive value
+        if (tid == kSThreads - 1) s_misc[1] = ex + v;
+        __syncthreads();
+        carry += s_misc[1];
+        __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------------------
-// part: stable 3-way partition of every segment around its pivot.  Tile of
-// T = 512 x ITEMS in-order positions (at most two segment parts), payload
-// (k coords + index) staged in shared memory by cp.async, ranks from warp
-// ballots, per-segment prefix (elements below the pivot, pivot seen) by
-// decoupled lookback, coalesced write-out of the four runs (left/right of
-// each part).  Fused: exact [min, max] of each child's next key.
+// part: stable 3-way partition of every segment around its pivot.  Persistent
+// CTAs walk tiles of T = 256 x ITEMS in-order positions (at most two segment
+// parts); each tile's k+1 arrays arrive in shared memory by bulk async copies
+// (cp.async.bulk + mbarrier, double-buffered so tile i+1 loads while tile i
+// is split), ranks come from warp ballots, the per-segment prefix of elements
+// below the pivot from select (no lookback), and the four runs (left / right
+// of each part) are written out coalesced.  Fused: exact [min, max] of each
+// child's next key.
 // ---------------------------------------------------------------------------
-constexpr int kPThreads = 512;
-constexpr int kPWarps = kPThreads / 32;
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
 
 template <int ITEMS>
 struct PartSmem {
     static constexpr int T = kPThreads * ITEMS;
+    u64 bar[2];
     unsigned short inv[T];
     u32 wcnt[kPWarps][4];
     u32 run_start[5];
     u32 cmin[4], cmax[4];
-    u32 flags;
     u32 piv[2][LBKD_MAX_K + 1];
     Chain ch[2];
     long long dbase[4];
-    u64 info[8];
     int cdim[4];
-    // followed by raw[k+1][T] u32
+    // followed by raw[2][k+1][T] u32 (two stages)
 };
 
-__device__ __forceinline__ void cp_async4_(u32* smem_dst, const u32* gsrc) {
-    u32 s = (u32)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async16_(u32* smem_dst, const u32* gsrc) {
-    u32 s = (u32)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
-}
-
-// status word: [63:35] epoch, [34:33] flag, [32] pivot seen, [31:0] #below
-__device__ __forceinline__ u64 pstatus(u32 epoch, u64 flag, u32 pseen, u32 cnt) {
-    return ((u64)epoch << 35) | (flag << 33) | ((u64)pseen << 32) | (u64)cnt;
-}
-
 template <int ITEMS>
-__global__ void __launch_bounds__(kPThreads, 2) sel_part_kernel(SelArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(kPThreads) sel_part_kernel(SelArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     PartSmem<ITEMS>& S = *reinterpret_cast<PartSmem<ITEMS>*>(smem_raw);
     constexpr int T = PartSmem<ITEMS>::T;
-    u32* raw = reinterpret_cast<u32*>(smem_raw + ((sizeof(PartSmem<ITEMS>) + 15) & ~(size_t)15));
+    const int k = a.k, A = k + 1;
+    u32* raw0 = reinterpret_cast<u32*>(smem_raw + ((sizeof(PartSmem<ITEMS>) + 127) & ~(size_t)127));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
     const LevelGeom& g = a.g;
-    const int k = a.k, A = k + 1;
+    const u32* Wsrc = a.bf.w[a.par];
+    u32* Wdst = a.bf.w[a.par ^ 1u];
+    const u64 stride = a.bf.stride;
+
+    auto issue = [&](u64 tile, int stage) {
+        // one elected thread: the tile's k+1 slices, rounded up to 16 bytes
+        // (the arrays are padded to a multiple of 4 words)
+        const u64 ts = tile * T;
+        const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
+        const u32 bytes = (u32)(((cnt + 3) & ~3ull) * 4);
+        mbar_expect_tx(&S.bar[stage], bytes * A);
+        u32* dst = raw0 + (size_t)stage * A * T;
+        for (int c = 0; c < A; ++c) bulk_g2s(dst + c * T, Wsrc + (u64)c * stride + ts, bytes, &S.bar[stage]);
+    };
 
     if (tid == 0) {
-        const u64 tile = atomicAdd(a.tile_ctr, 1u);
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (blockIdx.x < a.ntiles) issue(blockIdx.x, 0);
+    }
+    __syncthreads();
+    u32 phases = 0u;  // mbarrier parity of each stage (bit per stage)
+    int stage = 0;
+    for (u64 tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, stage ^= 1) {
+        // prefetch the next tile into the other stage (freed by the barrier
+        // at the end of the previous iteration)
+        if (tid == 0 && tile + gridDim.x < a.ntiles) issue(tile + gridDim.x, stage ^ 1);
         const u64 ts = tile * T;
         const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
         const TileParts tp = tile_parts(g, ts, cnt);
-        S.info[0] = tile;
-        S.info[1] = ts;
-        S.info[2] = tp.j0;
-        S.info[3] = ((u64)tp.r0a) | ((u64)tp.r0b << 32);
-        S.info[4] = ((u64)tp.r1a) | ((u64)tp.r1b << 32);
-        S.info[5] = tp.ib0;
-        S.info[6] = tp.ib1;
-        S.info[7] = tp.has1 ? 1u : 0u;
-        S.flags = 0u;
-        for (int q = 0; q < 4; ++q) { S.cmin[q] = 0xffffffffu; S.cmax[q] = 0u; }
-        if (a.want_mm) {
-            for (int q = 0; q < 4; ++q) {
-                const u64 child = 2 * (tp.j0 + (q >> 1)) + (q & 1);  // local child index
-                int d = (g.l + 1) % k;
-                if (a.mode == kWidest) {
-                    const u64 cnode = 2 * (g.Fl + g.sbase + tp.j0 + (q >> 1)) + 1 + (q & 1);
-                    d = (cnode < g.n && child < 2 * g.nseg) ? (int)a.split_dims[cnode] : 0;
+        const u64 j0 = tp.j0;
+        const u32 r0a = tp.r0a, r0b = tp.r0b, r1a = tp.r1a, r1b = tp.r1b;
+        const bool has1 = tp.has1;
+        if (tid < 2 * A) {
+            const int p = tid / A, c = tid % A;
+            if (p == 0 || has1) S.piv[p][c] = a.piv[(j0 + p) * A + c];
+        }
+        if (tid < 2 * kChainWords) {
+            const int p = tid / kChainWords, c = tid % kChainWords;
+            if (p == 0 || has1)
+                reinterpret_cast<u32*>(&S.ch[p])[c] = reinterpret_cast<const u32*>(a.chains + j0 + p)[c];
+        }
+        if (tid < 4) {
+            S.cmin[tid] = 0xffffffffu;
+            S.cmax[tid] = 0u;
+            int d = (g.l + 1) % k;
+            if (a.mode == kWidest) {
+                const u64 child = 2 * (j0 + (tid >> 1)) + (tid & 1);
+                const u64 cnode = 2 * (g.Fl + g.sbase + j0 + (tid >> 1)) + 1 + (tid & 1);
+                d = (a.want_mm && cnode < g.n && child < 2 * g.nseg) ? (int)a.split_dims[cnode] : 0;
+            }
+            S.cdim[tid] = d;
+        }
+        mbar_wait(&S.bar[stage], (phases >> stage) & 1u);
+        phases ^= 1u << stage;
+        __syncthreads();
+        const u32* raw = raw0 + (size_t)stage * A * T;
+
+        // --- classify: q = part*2 + side (0 left, 1 right), -1 none / pivot
+        const u32 lt = lanemask_lt();
+        u32 run[4] = {0u, 0u, 0u, 0u};
+        u32 qr[ITEMS];  // q << 16 | warp-local rank, 0xffffffff = no slot
+        u32 mn[4], mx[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { mn[q] = 0xffffffffu; mx[q] = 0u; }
+        const int d00 = S.ch[0].d[0], d10 = S.ch[1].d[0];
+        const u32 y00 = flip_key(__uint_as_float(S.piv[0][d00]));
+        const u32 y10 = flip_key(__uint_as_float(S.piv[1][d10]));
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+            const bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
+            int side = -1;
+            if (in0 || in1) {
+                const int p = in1 ? 1 : 0;
+                const u32 x = flip_key(__uint_as_float(raw[(p ? d10 : d00) * T + r]));
+                const u32 y = p ? y10 : y00;
+                if (x != y) {
+                    side = x < y ? 0 : 1;
+                } else {  // tie in the leading field: the rest of the chain, then the index
+                    const Chain& ch = S.ch[p];
+                    const u32* pv = S.piv[p];
+                    side = 2;
+                    for (u32 f = 1; f < ch.m; ++f) {
+                        const int d = ch.d[f];
+                        const u32 xx = flip_key(__uint_as_float(raw[d * T + r]));
+                        const u32 yy = flip_key(__uint_as_float(pv[d]));
+                        if (xx != yy) { side = xx < yy ? 0 : 1; break; }
+                    }
+                    if (side == 2) {
+                        const u32 xx = raw[k * T + r], yy = pv[k];
+                        side = xx < yy ? 0 : (xx > yy ? 1 : 2);
+                    }
                 }
-                S.cdim[q] = d;
             }
-        }
-    }
-    __syncthreads();
-    const u64 tile = S.info[0], ts = S.info[1], j0 = S.info[2];
-    const u32 r0a = (u32)S.info[3], r0b = (u32)(S.info[3] >> 32);
-    const u32 r1a = (u32)S.info[4], r1b = (u32)(S.info[4] >> 32);
-    const bool has1 = S.info[7] != 0;
-    const u32* Wsrc = a.bf.w[a.par];
-    u32* Wdst = a.bf.w[a.par ^ 1u];
-
-    // --- stage the payload of both parts (16-byte chunks; ragged chunks per word)
-    for (u32 chunk = tid; chunk < (u32)T / 4u; chunk += kPThreads) {
-        const u32 r = chunk * 4u;
-        const bool all0 = r >= r0a && r + 4 <= r0b, all1 = r >= r1a && r + 4 <= r1b;
-        const bool any0 = r < r0b && r + 4 > r0a, any1 = r < r1b && r + 4 > r1a;
-        if (all0 || all1) {
-            const u32* gp = Wsrc + ts + r;
-            for (int c = 0; c < A; ++c) cp_async16_(raw + c * T + r, gp + (u64)c * a.bf.stride);
-        } else if (any0 || any1) {
-            for (u32 q = r; q < r + 4; ++q) {
-                const bool in = (q >= r0a && q < r0b) || (q >= r1a && q < r1b);
-                if (!in) continue;
-                const u32* gp = Wsrc + ts + q;
-                for (int c = 0; c < A; ++c) cp_async4_(raw + c * T + q, gp + (u64)c * a.bf.stride);
-            }
-        }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    if (tid < 2 * A) {
-        const int p = tid / A, c = tid % A;
-        if (p == 0 || has1) S.piv[p][c] = a.piv[(j0 + p) * A + c];
-    }
-    if (tid < 2 * kChainWords) {
-        const int p = tid / kChainWords, c = tid % kChainWords;
-        if (p == 0 || has1) reinterpret_cast<u32*>(&S.ch[p])[c] = reinterpret_cast<const u32*>(a.chains + j0 + p)[c];
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-
-    // --- classify: -1 none, 0 left, 1 pivot, 2 right; q = part*2 + side
-    const u32 lt = lanemask_lt();
-    u32 run[4] = {0u, 0u, 0u, 0u};
-    u32 qr[ITEMS];  // q << 16 | warp-local rank, 0xffffffff = no slot
-    u32 mn[4], mx[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) { mn[q] = 0xffffffffu; mx[q] = 0u; }
-    bool pseen0 = false, pseen1 = false;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
-        const bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
-        int cls = -1;
-        if (in0 || in1) {
-            const int p = in1 ? 1 : 0;
-            const Chain& ch = S.ch[p];
-            const u32* pv = S.piv[p];
-            cls = 1;
-            for (int f = 0; f < ch.m; ++f) {
-                const int d = ch.d[f];
-                const u32 x = flip_key(__uint_as_float(raw[d * T + r]));
-                const u32 y = flip_key(__uint_as_float(pv[d]));
-                if (x != y) { cls = x < y ? 0 : 2; break; }
-            }
-            if (cls == 1) {
-                const u32 x = raw[k * T + r], y = pv[k];
-                cls = x < y ? 0 : (x > y ? 2 : 1);
-            }
-            if (cls == 1) { if (p) pseen1 = true; else pseen0 = true; }
-        }
-        const int q = (cls == 0 || cls == 2) ? ((in1 ? 2 : 0) + (cls == 2 ? 1 : 0)) : -1;
-        u32 myrank = 0;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-            const u32 b = __ballot_sync(kFullMask, q == qq);
-            if (q == qq) myrank = run[qq] + __popc(b & lt);
-            run[qq] += __popc(b);
-        }
-        qr[i] = q >= 0 ? (((u32)q << 16) | myrank) : 0xffffffffu;
-        if (a.want_mm && q >= 0) {
-            const u32 v = flip_key(__uint_as_float(raw[S.cdim[q] * T + r]));
+            const int q = (side == 0 || side == 1) ? ((in1 ? 2 : 0) + side) : -1;
+            u32 myrank = 0;
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
-                if (q == qq) {
-                    mn[qq] = min(mn[qq], v);
-                    mx[qq] = max(mx[qq], v);
+                const u32 b = __ballot_sync(kFullMask, q == qq);
+                if (q == qq) myrank = run[qq] + __popc(b & lt);
+                run[qq] += __popc(b);
+            }
+            qr[i] = q >= 0 ? (((u32)q << 16) | myrank) : 0xffffffffu;
+            if (a.want_mm && q >= 0) {
+                const u32 v = flip_key(__uint_as_float(raw[S.cdim[q] * T + r]));
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    if (q == qq) {
+                        mn[qq] = min(mn[qq], v);
+                        mx[qq] = max(mx[qq], v);
+                    }
                 }
             }
         }
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) S.wcnt[warp][q] = run[q];
-    }
-    if (__any_sync(kFullMask, pseen0) && lane == 0) atomicOr(&S.flags, 1u);
-    if (__any_sync(kFullMask, pseen1) && lane == 0) atomicOr(&S.flags, 2u);
-    if (a.want_mm) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const u32 x = __reduce_min_sync(kFullMask, mn[q]);
-            const u32 y = __reduce_max_sync(kFullMask, mx[q]);
-            if (lane == 0 && x <= y) { atomicMin(&S.cmin[q], x); atomicMax(&S.cmax[q], y); }
-        }
-    }
-    __syncthreads();
-
-    // --- warp prefixes (warp 0), run starts, status publication + lookback
-    if (warp == 0) {
-        u32 tot[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const u32 v = lane < kPWarps ? S.wcnt[lane][q] : 0u;
-            u32 x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 y = __shfl_up_sync(kFullMask, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane < kPWarps) S.wcnt[lane][q] = x - v;
-            tot[q] = __shfl_sync(kFullMask, x, 31);
-        }
-        const u32 fl = S.flags;
-        const u32 ps0 = fl & 1u, ps1 = (fl >> 1) & 1u;
-        const bool act0 = r0a < r0b;
-        const bool need_lb = act0 && S.info[5] < ts;  // segment j0 began before this tile
-        u64* my = a.status + tile;
         if (lane == 0) {
-            if (has1) st_relaxed_u64(my, pstatus(a.epoch, kFlagInc, ps1, tot[2]));
-            else if (act0) st_relaxed_u64(my, pstatus(a.epoch, need_lb ? kFlagAgg : kFlagInc, ps0, tot[0]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) S.wcnt[warp][q] = run[q];
         }
-        u32 below = 0, pb = 0;
-        if (need_lb) {
-            long long t = (long long)tile - 1;
-            while (true) {
-                const long long tt = t - lane;
-                const u64 w = tt >= 0 ? ld_relaxed_u64(a.status + tt) : 0ull;
-                const bool ready = (u32)(w >> 35) == a.epoch && ((w >> 33) & 3ull) != 0ull;
-                const bool inc = ready && ((w >> 33) & 3ull) == kFlagInc;
-                const u32 incm = __ballot_sync(kFullMask, inc);
-                const u32 nrm = __ballot_sync(kFullMask, !ready);
-                const int f = incm ? __ffs(incm) - 1 : 32;
-                const u32 need = f == 32 ? 0xffffffffu : (0xffffffffu >> (31 - f));
-                if (nrm & need) {
-                    __nanosleep(64);
-                    continue;
+        if (a.want_mm) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const u32 x = __reduce_min_sync(kFullMask, mn[q]);
+                const u32 y = __reduce_max_sync(kFullMask, mx[q]);
+                if (lane == 0 && x <= y) { atomicMin(&S.cmin[q], x); atomicMax(&S.cmax[q], y); }
+            }
+        }
+        __syncthreads();
+
+        // --- warp prefixes, run starts and destinations (warp 0)
+        if (warp == 0) {
+            u32 tot[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const u32 v = lane < kPWarps ? S.wcnt[lane][q] : 0u;
+                u32 x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 y = __shfl_up_sync(kFullMask, x, o);
+                    if (lane >= o) x += y;
                 }
-                const bool use = lane <= f;
-                below += __reduce_add_sync(kFullMask, use ? (u32)(w & 0xffffffffull) : 0u);
-                pb |= __reduce_or_sync(kFullMask, use ? (u32)((w >> 32) & 1ull) : 0u);
-                if (f < 32) break;
-                t -= 32;
+                if (lane < kPWarps) S.wcnt[lane][q] = x - v;
+                tot[q] = __shfl_sync(kFullMask, x, 31);
             }
-            if (!has1 && lane == 0) st_relaxed_u64(my, pstatus(a.epoch, kFlagInc, pb | ps0, below + tot[0]));
-        }
-        if (lane == 0) {
-            const u64 ib0 = S.info[5], ib1 = S.info[6];
-            const u64 po0 = v_pivot(g, j0);
-            const u64 before = need_lb ? ts - ib0 : 0ull;
-            const u64 rb = before - below - pb;
-            S.dbase[0] = (long long)(ib0 + below);
-            S.dbase[1] = (long long)(ib0 + po0 + 1 + rb);
-            if (has1) {
-                const u64 po1 = v_pivot(g, j0 + 1);
-                S.dbase[2] = (long long)ib1;
-                S.dbase[3] = (long long)(ib1 + po1 + 1);
-            } else {
-                S.dbase[2] = S.dbase[3] = 0;
+            if (lane == 0) {
+                // elements of segment j0 before this tile: below / pivot / above
+                const bool began = r0a < r0b && tp.ib0 < ts;
+                const u64 before = began ? ts - tp.ib0 : 0ull;
+                const u64 below = began ? a.tile_lt[tile * 2] : 0ull;
+                const u64 pb = (began && a.ppos[j0] < ts) ? 1ull : 0ull;
+                const u64 po0 = v_pivot(g, j0);
+                S.dbase[0] = (long long)(tp.ib0 + below);
+                S.dbase[1] = (long long)(tp.ib0 + po0 + 1 + (before - below - pb));
+                if (has1) {
+                    S.dbase[2] = (long long)tp.ib1;
+                    S.dbase[3] = (long long)(tp.ib1 + v_pivot(g, j0 + 1) + 1);
+                } else {
+                    S.dbase[2] = S.dbase[3] = 0;
+                }
+                S.run_start[0] = 0u;
+                S.run_start[1] = tot[0];
+                S.run_start[2] = tot[0] + tot[1];
+                S.run_start[3] = tot[0] + tot[1] + tot[2];
+                S.run_start[4] = tot[0] + tot[1] + tot[2] + tot[3];
             }
-            S.run_start[0] = 0u;
-            S.run_start[1] = tot[0];
-            S.run_start[2] = tot[0] + tot[1];
-            S.run_start[3] = tot[0] + tot[1] + tot[2];
-            S.run_start[4] = tot[0] + tot[1] + tot[2] + tot[3];
         }
-    }
-    __syncthreads();
+        __syncthreads();
 
-    // --- slots (stable: warp order, then row, then lane)
+        // --- slots (stable: warp order, then row, then lane)
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        if (qr[i] != 0xffffffffu) {
-            const u32 q = qr[i] >> 16;
-            const u32 slot = S.run_start[q] + S.wcnt[warp][q] + (qr[i] & 0xffffu);
-            S.inv[slot] = (unsigned short)(warp * ITEMS * 32 + i * 32 + lane);
+        for (int i = 0; i < ITEMS; ++i) {
+            if (qr[i] != 0xffffffffu) {
+                const u32 q = qr[i] >> 16;
+                const u32 slot = S.run_start[q] + S.wcnt[warp][q] + (qr[i] & 0xffffu);
+                S.inv[slot] = (unsigned short)(warp * ITEMS * 32 + i * 32 + lane);
+            }
         }
-    }
-    if (a.want_mm && tid < 4) {
-        const int q = tid;
-        if (S.cmin[q] <= S.cmax[q]) {
-            const u64 child = 2 * (j0 + (q >> 1)) + (q & 1);
-            atomicMin(&a.mmn_next[child], S.cmin[q]);
-            atomicMax(&a.mmx_next[child], S.cmax[q]);
+        if (a.want_mm && tid < 4) {
+            const int q = tid;
+            if (S.cmin[q] <= S.cmax[q]) {
+                const u64 child = 2 * (j0 + (q >> 1)) + (q & 1);
+                atomicMin(&a.mmn_next[child], S.cmin[q]);
+                atomicMax(&a.mmx_next[child], S.cmax[q]);
+            }
         }
-    }
-    __syncthreads();
+        __syncthreads();
 
-    // --- coalesced write-out of the four runs
-    const u32 nslots = S.run_start[4];
-    const u64 stride = a.bf.stride;
-    for (u32 s = tid; s < nslots; s += kPThreads) {
-        const int q = (s >= S.run_start[1]) + (s >= S.run_start[2]) + (s >= S.run_start[3]);
-        const u64 dst = (u64)S.dbase[q] + (s - S.run_start[q]);
-        const u32 src = S.inv[s];
-        u32* d = Wdst + dst;
-        for (int c = 0; c < A; ++c) d[(u64)c * stride] = raw[c * T + src];
+        // --- coalesced write-out, run by run
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 s0 = S.run_start[q], s1 = S.run_start[q + 1];
+            u32* d = Wdst + ((u64)S.dbase[q] - s0);
+            for (u32 sl = s0 + tid; sl < s1; sl += kPThreads) {
+                const u32 src = S.inv[sl];
+                for (int c = 0; c < A; ++c) d[(u64)c * stride + sl] = raw[c * T + src];
+            }
+        }
+        __syncthreads();  // the stage is free for the prefetch two tiles ahead
     }
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static int sel_items(int b) {
+int sel_items(int b) {
     int items = (1 << (b - 1)) / kPThreads;
     return items > 8 ? 8 : items;
 }
+
+int sel_tile(int b) { return kPThreads * sel_items(b); }
 
 int sel_digit_bits(u64 nseg) {
     int lg = 0;
@@ -802,35 +836,40 @@ void launch_sel_pick(const SelArgs& a, cudaStream_t st) {
 
 void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
     SelArgs a = a0;
-    int items = (1 << (b - 1)) / kHThreads;
-    if (items > 8) items = 8;
-    const u64 T = (u64)kHThreads * items;
+    const int items = sel_items(b);
+    const u64 T = (u64)kPThreads * items;
     a.ntiles = (a.g.nview + T - 1) / T;
-    u64 grid = a.ntiles < 148 * 8 ? a.ntiles : 148 * 8;
-    if (items >= 8) sel_filter_kernel<8><<<(unsigned)grid, kHThreads, 0, st>>>(a);
-    else sel_filter_kernel<4><<<(unsigned)grid, kHThreads, 0, st>>>(a);
+    const u64 grid = a.ntiles < 148 * 8 ? a.ntiles : 148 * 8;
+    switch (items) {
+        case 8: sel_filter_kernel<8><<<(unsigned)grid, kPThreads, 0, st>>>(a); break;
+        case 4: sel_filter_kernel<4><<<(unsigned)grid, kPThreads, 0, st>>>(a); break;
+        default: sel_filter_kernel<2><<<(unsigned)grid, kPThreads, 0, st>>>(a); break;
+    }
 }
 
-void launch_sel_select(const SelArgs& a, cudaStream_t st) {
-    sel_select_kernel<<<(unsigned)a.g.nseg, kSThreads, 0, st>>>(a);
+void launch_sel_select(const SelArgs& a, int b, cudaStream_t st) {
+    sel_select_kernel<<<(unsigned)a.g.nseg, kSThreads, 0, st>>>(a, sel_tile(b));
 }
 
 template <int ITEMS>
-static void launch_part_t(const SelArgs& a, unsigned grid, cudaStream_t st) {
-    const size_t sm = ((sizeof(PartSmem<ITEMS>) + 15) & ~(size_t)15) +
-                      (size_t)(a.k + 1) * PartSmem<ITEMS>::T * sizeof(u32);
+static void launch_part_t(SelArgs a, cudaStream_t st) {
+    const int T = PartSmem<ITEMS>::T;
+    a.ntiles = (a.g.nview + T - 1) / T;
+    const size_t sm = ((sizeof(PartSmem<ITEMS>) + 127) & ~(size_t)127) + 2 * (size_t)(a.k + 1) * T * sizeof(u32);
     cudaFuncSetAttribute(sel_part_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    sel_part_kernel<ITEMS><<<grid, kPThreads, sm, st>>>(a);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sel_part_kernel<ITEMS>, kPThreads, sm);
+    if (per_sm < 1) per_sm = 1;
+    u64 grid = (u64)per_sm * 148;
+    if (grid > a.ntiles) grid = a.ntiles;
+    sel_part_kernel<ITEMS><<<(unsigned)grid, kPThreads, sm, st>>>(a);
 }
 
 void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
-    const int items = sel_items(b);
-    const u64 T = (u64)kPThreads * items;
-    const unsigned grid = (unsigned)((a.g.nview + T - 1) / T);
-    switch (items) {
-        case 8: launch_part_t<8>(a, grid, st); break;
-        case 4: launch_part_t<4>(a, grid, st); break;
-        default: launch_part_t<2>(a, grid, st); break;
+    switch (sel_items(b)) {
+        case 8: launch_part_t<8>(a, st); break;
+        case 4: launch_part_t<4>(a, st); break;
+        default: launch_part_t<2>(a, st); break;
     }
 }
 
