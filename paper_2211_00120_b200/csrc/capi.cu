@@ -161,15 +161,12 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
             if ((rc = grow(c->bf.chains, dummy, nseg))) return rc;
             if ((rc = grow(c->bf.sel, dummy, nseg * kSelW))) return rc;
             if ((rc = grow(c->bf.ppos, dummy, nseg))) return rc;
-            for (int i = 0; i < 2; ++i) {
-                if ((rc = grow(c->bf.mmn[i], dummy, nseg))) return rc;
-                if ((rc = grow(c->bf.mmx[i], dummy, nseg))) return rc;
-            }
             c->cap_piv = pv;
         }
-        const size_t pt = 2 * (n / (size_t)sel_tile(b) + 2);
+        const size_t pt = 2 * (n / 256 + 16);  // per 256-position subtile (tiles are coarser)
         if (pt > c->cap_ptiles) {
             if ((rc = grow(c->bf.tile_lt, dummy, pt))) return rc;
+            if ((rc = grow(c->bf.sub_lt, dummy, pt))) return rc;
             c->cap_ptiles = pt;
         }
     }
@@ -249,14 +246,9 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         const u64 nseg = g.nseg;
         const int D = sel_digit_bits(nseg);
         const u32 par = (u32)((l - bp.lroot) & 1);
-        const bool last = l == lto - 1;
         const double pts = (double)level_points(bp, l);
         CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
         CK(cudaMemsetAsync(bf.cand_ctr, 0, sizeof(u32), st));
-        if (!last) {
-            CK(cudaMemsetAsync(bf.mmn[par ^ 1], 0xff, 2 * nseg * sizeof(u32), st));
-            CK(cudaMemsetAsync(bf.mmx[par ^ 1], 0, 2 * nseg * sizeof(u32), st));
-        }
         SelArgs a;
         memset(&a, 0, sizeof(a));
         a.g = g;
@@ -265,8 +257,6 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.D = D;
         a.bf = bf;
         a.par = par;
-        a.mmn = bf.mmn[par];
-        a.mmx = bf.mmx[par];
         a.hist = bf.hist;
         a.sel = bf.sel;
         a.cand = bf.cand;
@@ -280,10 +270,8 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.boxes_in = bf.boxes[par];
         a.boxes_out = bf.boxes[par ^ 1];
         a.tile_lt = bf.tile_lt;
+        a.sub_lt = bf.sub_lt;
         a.ppos = bf.ppos;
-        a.want_mm = last ? 0 : 1;
-        a.mmn_next = bf.mmn[par ^ 1];
-        a.mmx_next = bf.mmx[par ^ 1];
         if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_sel_hist(a, bp.b, st);
         prof_end(c, st, kPHist, 4.0 * pts);
@@ -508,11 +496,14 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     CK(cudaMemcpy2DAsync(c->bf.w[0], c->bf.stride * sizeof(u32), d_sub, (size_t)sub_stride * sizeof(u32),
                          nview * sizeof(u32), (size_t)k + 1, cudaMemcpyDeviceToDevice, st));
     if (c->algo == 0 && lam0 > root_level) {
-        CK(cudaMemsetAsync(c->bf.mmn[0], 0xff, sizeof(u32), st));
-        CK(cudaMemsetAsync(c->bf.mmx[0], 0, sizeof(u32), st));
+        CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
+        CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
         if (prof_begin(c, st)) return LBKD_ECUDA;
-        launch_view_minmax(bp, c->bf, root_level % k, nview, st);
-        prof_end(c, st, kPOther, 4.0 * (double)nview);
+        launch_view_minmax(bp, c->bf, c->minmax, nview, st);
+        prof_end(c, st, kPOther, 4.0 * k * (double)nview);
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_root(bp, c->bf, c->minmax, st);
+        prof_end(c, st, kPOther, 0.0);
     }
     if ((rc = run_levels(c, bp, root_level, lam0, st))) return rc;
     if ((rc = run_subtrees(c, bp, lam0, st))) return rc;
@@ -549,10 +540,6 @@ void lbkd_destroy(lbkd_ctx* c) {
         cudaFree(c->bf.state[i]);
     }
     cudaFree(c->bf.hist);
-    for (int i = 0; i < 2; ++i) {
-        cudaFree(c->bf.mmn[i]);
-        cudaFree(c->bf.mmx[i]);
-    }
     cudaFree(c->bf.sel);
     cudaFree(c->bf.cand);
     cudaFree(c->bf.cand2);
@@ -560,6 +547,7 @@ void lbkd_destroy(lbkd_ctx* c) {
     cudaFree(c->bf.piv);
     cudaFree(c->bf.chains);
     cudaFree(c->bf.tile_lt);
+    cudaFree(c->bf.sub_lt);
     cudaFree(c->bf.ppos);
     cudaFree(c->bf.seg_and);
     cudaFree(c->bf.seg_or);

@@ -56,8 +56,6 @@ struct Buffers {
     u32* w[2];
     u64 stride;
     // select path (select.cu)
-    u32* mmn[2];      // per level parity: [nseg] min of the level's key (flipped)
-    u32* mmx[2];      //                   [nseg] max
     u32* sel;         // [nseg][kSelW]
     u32* cand;        // candidate records [n][k+1]
     u32* cand2;       // compaction buffer  [n][k+1]
@@ -65,6 +63,7 @@ struct Buffers {
     u32* piv;         // [nseg][k+1] pivot records (coordinate bits + index)
     Chain* chains;    // [nseg]
     u32* tile_lt;     // [tiles][2] per (tile, segment part) counts below the pivot
+    u32* sub_lt;      // [subtiles][2] the same per 256-position warp subtile
     u32* ppos;        // [nseg] pivot positions
     u32* hist;        // [nseg][4][256] digit counts of the level's keys
     u32* seg_and;     // [nseg] AND of keys  \  digit d of segment j is constant
@@ -103,8 +102,6 @@ struct SelArgs {
     int k, mode, D;
     Buffers bf;
     u32 par;               // W[par] holds the level's data
-    const u32* mmn;        // key range of the level's segments
-    const u32* mmx;
     u32* hist;             // [nseg][2^D]
     u32* sel;
     u32* cand;
@@ -118,16 +115,14 @@ struct SelArgs {
     const float* boxes_in;  // widest: boxes of the level's segments
     float* boxes_out;       //         boxes of their children
     u32* tile_lt;          // [tiles][2] below-pivot counts -> exclusive prefixes
+    u32* sub_lt;           // [subtiles][2] below-pivot counts per 256-position warp subtile
     u32* ppos;             // [nseg] in-order position of each segment's pivot
-    int want_mm;           // partition: record the children's key ranges
-    u32* mmn_next;
-    u32* mmx_next;
     int tiles_per_cta;
     u64 ntiles;
 };
 int sel_digit_bits(u64 nseg);
 void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cudaStream_t st);
-void launch_view_minmax(const BuildParams& bp, const Buffers& bf, int dim, u64 m, cudaStream_t st);
+void launch_view_minmax(const BuildParams& bp, const Buffers& bf, u32* minmax, u64 m, cudaStream_t st);
 void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cudaStream_t st);
 void launch_sel_hist(const SelArgs& a, int b, cudaStream_t st);
 void launch_sel_pick(const SelArgs& a, cudaStream_t st);

@@ -42,8 +42,9 @@ __device__ __forceinline__ u32 bucket_shift(u32 lo, u32 hi, int D) {
     return b > 0 ? (u32)b : 0u;
 }
 
-// Equal-width buckets of a segment's VALUE range [min, max] (the exact key
-// range, order-flipped u32).  Float keys are exponential in their bits, so
+// Equal-width buckets of a segment's VALUE range [lo, hi] in its split
+// dimension: its node's box (the world box clipped by the ancestors' planes,
+// a valid bound of every point of the node).  Float keys are exponential in their bits, so
 // equal widths in key space would put half of a [0, 1) segment into the few
 // buckets of [0.5, 1); equal widths in value space split it evenly.  The map
 // is monotone (IEEE subtraction, multiplication by a positive scale and the
@@ -54,10 +55,10 @@ struct Bucketer {
     u32 top;
 };
 
-__device__ __forceinline__ Bucketer make_bucketer(u32 kmin, u32 kmax, int D) {
+__device__ __forceinline__ Bucketer make_bucketer(float lo, float hi, int D) {
     Bucketer b;
-    b.lo = (double)unflip_key(kmin);
-    const double w = (double)unflip_key(kmax) - b.lo;
+    b.lo = (double)lo;
+    const double w = (double)hi - b.lo;
     b.scale = w > 0.0 ? (double)(1u << D) / w : 0.0;
     b.top = (1u << D) - 1u;
     return b;
@@ -153,8 +154,11 @@ void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cu
     init_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(bp.pts, bp.n, bp.k, bf.w[0], bf.stride, bf.err, minmax);
 }
 
-// key range of the view's root segment from a W[0] array (sub-builds)
-__global__ void view_minmax_kernel(const u32* __restrict__ keys, u64 m, u32* mn_out, u32* mx_out) {
+// bounding box of a sub-build's points (W[0], blockIdx.y = dimension): the
+// view root's box (any valid bound of its points works)
+__global__ void view_minmax_kernel(const u32* __restrict__ w0, u64 stride, u64 m, int k, u32* minmax) {
+    const int d = blockIdx.y;
+    const u32* keys = w0 + (u64)d * stride;
     u32 mn = 0xffffffffu, mx = 0u;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
         const u32 key = flip_key(__uint_as_float(keys[i]));
@@ -163,39 +167,39 @@ __global__ void view_minmax_kernel(const u32* __restrict__ keys, u64 m, u32* mn_
     }
     mn = __reduce_min_sync(kFullMask, mn);
     mx = __reduce_max_sync(kFullMask, mx);
-    if ((threadIdx.x & 31) == 0) { atomicMin(mn_out, mn); atomicMax(mx_out, mx); }
+    if ((threadIdx.x & 31) == 0) { atomicMin(&minmax[d], mn); atomicMax(&minmax[k + d], mx); }
 }
 
-void launch_view_minmax(const BuildParams& bp, const Buffers& bf, int dim, u64 m, cudaStream_t st) {
+void launch_view_minmax(const BuildParams& bp, const Buffers& bf, u32* minmax, u64 m, cudaStream_t st) {
     u64 blocks = (m + 255) / 256;
-    if (blocks > 148 * 4) blocks = 148 * 4;
+    if (blocks > 148 * 2) blocks = 148 * 2;
     if (blocks < 1) blocks = 1;
-    view_minmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(bf.w[0] + (u64)dim * bf.stride, m, bf.mmn[0], bf.mmx[0]);
+    view_minmax_kernel<<<dim3((unsigned)blocks, (unsigned)bp.k), 256, 0, st>>>(bf.w[0], bf.stride, m, bp.k, minmax);
 }
 
-// root: RR key range = dim 0 of the world box; widest: world box, root dim
-// = first argmax of the float64 widths (widest.py:91-93, :164-166)
-__global__ void root_kernel(const u32* minmax, int k, int mode, int root_dim, u32* mmn0, u32* mmx0, float* box0,
-                            uint8_t* split_dims) {
+// root box = world box (widest.py:84-88); widest: root dim = first argmax
+// of the float64 widths (widest.py:91-93, :164-166)
+__global__ void root_kernel(const u32* minmax, int k, int mode, float* box0, uint8_t* split_dims) {
     if (threadIdx.x != 0) return;
-    int d0 = root_dim;
-    if (mode == kWidest) {
-        double bw = 0.0;
-        for (int d = 0; d < k; ++d) {
-            const float lo = unflip_key(minmax[d]), hi = unflip_key(minmax[k + d]);
-            box0[d] = lo;
-            box0[k + d] = hi;
-            const double w = (double)hi - (double)lo;
-            if (d == 0 || w > bw) { bw = w; d0 = d; }
-        }
-        split_dims[0] = (uint8_t)d0;
+    int d0 = 0;
+    double bw = 0.0;
+    for (int d = 0; d < k; ++d) {
+        const float lo = unflip_key(minmax[d]), hi = unflip_key(minmax[k + d]);
+        box0[d] = lo;
+        box0[k + d] = hi;
+        const double w = (double)hi - (double)lo;
+        if (d == 0 || w > bw) { bw = w; d0 = d; }
     }
-    mmn0[0] = minmax[d0];
-    mmx0[0] = minmax[k + d0];
+    if (mode == kWidest) split_dims[0] = (uint8_t)d0;
 }
 
 void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cudaStream_t st) {
-    root_kernel<<<1, 32, 0, st>>>(minmax, bp.k, bp.mode, 0, bf.mmn[0], bf.mmx[0], bf.boxes[0], bp.split_dims);
+    root_kernel<<<1, 32, 0, st>>>(minmax, bp.k, bp.mode, bf.boxes[0], bp.split_dims);
+}
+
+__device__ __forceinline__ Bucketer seg_bucketer(const SelArgs& a, u64 t, int d) {
+    const float* box = a.boxes_in + t * 2ull * a.k;
+    return make_bucketer(box[d], box[a.k + d], a.D);
 }
 
 // ---------------------------------------------------------------------------
@@ -235,8 +239,9 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
             flush(cur);
             cur = tp.j0;
         }
-        const u32* k0 = W + (u64)seg_key_dim(a, tp.j0) * a.bf.stride + ts;
-        const Bucketer b0 = make_bucketer(a.mmn[tp.j0], a.mmx[tp.j0], a.D);
+        const int dk0 = seg_key_dim(a, tp.j0);
+        const u32* k0 = W + (u64)dk0 * a.bf.stride + ts;
+        const Bucketer b0 = seg_bucketer(a, tp.j0, dk0);
         u32 key[ITEMS];
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
         if (tp.has1) {
             flush(cur);
             cur = tp.j0 + 1;
-            const Bucketer b1 = make_bucketer(a.mmn[cur], a.mmx[cur], a.D);
+            const Bucketer b1 = seg_bucketer(a, cur, seg_key_dim(a, cur));
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const u32 r = (u32)(i * kHThreads + threadIdx.x);
@@ -291,8 +296,10 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
         while (cum + h[b] <= po) { cum += h[b]; ++b; }
         u32* sel = a.sel + j * kSelW;
         const u32 C = h[b];
-        sel[kSelLo] = a.mmn[j];
-        sel[kSelShift] = a.mmx[j];  // (hi) the bucketer is rebuilt from [lo, hi]
+        const int d = seg_key_dim(a, j);
+        const float* box = a.boxes_in + j * 2ull * a.k;
+        sel[kSelLo] = __float_as_uint(box[d]);  // the filter rebuilds the bucketer
+        sel[kSelShift] = __float_as_uint(box[a.k + d]);
         sel[kSelB] = (u32)b;
         sel[kSelR] = po - cum;
         sel[kSelC] = C;
@@ -302,51 +309,62 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// filter: per (tile, part) the number of elements in buckets below b*, and
-// every element of bucket b* -> a candidate record (k coordinate bits, input
-// index, in-order position) in the segment's candidate range.  Tiles are the
-// partition's tiles (kPThreads x ITEMS positions).
+// filter: per (tile, part) and per (warp subtile, part) the number of
+// elements in buckets below b*, and every element of bucket b* -> a
+// candidate record (k coordinate bits, input index, in-order position) in
+// the segment's candidate range.  A tile is T = 8 x blockDim positions, a
+// warp subtile kSub = 256 positions (8 per thread, thread-contiguous); the
+// part index of both is relative to the TILE's first segment.
 // ---------------------------------------------------------------------------
-constexpr int kPThreads = 256;
-constexpr int kPWarps = kPThreads / 32;
+constexpr int kSub = 256;  // positions per warp subtile (32 lanes x 8 rows)
 
-template <int ITEMS>
-__global__ void __launch_bounds__(kPThreads) sel_filter_kernel(SelArgs a) {
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
+    constexpr int ITEMS = 8;
+    constexpr int T = THREADS * ITEMS;
+    constexpr int NSUB = T / kSub;
     __shared__ u32 wtot[32];
     __shared__ u32 s_base;
-    constexpr int T = kPThreads * ITEMS;
     const LevelGeom& g = a.g;
     const u32* W = a.bf.w[a.par];
     const int k = a.k, R = k + 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (u64 t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         const u64 ts = t * T;
         const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
         const TileParts tp = tile_parts(g, ts, cnt);
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
-            if (part == 1 && !tp.has1) break;
             const u64 j = tp.j0 + part;
             const u32 ra = part ? tp.r1a : tp.r0a, rb = part ? tp.r1b : tp.r0b;
-            if (ra >= rb) continue;
-            u32* sel = a.sel + j * kSelW;
-            const Bucketer bk = make_bucketer(sel[kSelLo], sel[kSelShift], a.D);
-            const u32 bs = sel[kSelB], off = sel[kSelOff];
-            const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
-            // thread-contiguous items so one block scan orders the hits
+            const bool present = (part == 0 || tp.has1) && ra < rb;
             u32 hits = 0, nlt = 0;
+            u32 off = 0;
+            u32* sel = a.sel + j * kSelW;
+            if (present) {
+                const Bucketer bk =
+                    make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D);
+                const u32 bs = sel[kSelB];
+                off = sel[kSelOff];
+                const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
 #pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const u32 r = (u32)(threadIdx.x * ITEMS + i);
-                if (r >= ra && r < rb) {
-                    const u32 b = bucket_of(bk, kp[r]);
-                    if (b == bs) hits |= 1u << i;
-                    nlt += b < bs ? 1u : 0u;
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 r = (u32)(threadIdx.x * ITEMS + i);
+                    if (r >= ra && r < rb) {
+                        const u32 b = bucket_of(bk, kp[r]);
+                        if (b == bs) hits |= 1u << i;
+                        nlt += b < bs ? 1u : 0u;
+                    }
                 }
             }
+            // per warp subtile (zero for absent parts: the partition sums them)
+            const u32 wl = __reduce_add_sync(kFullMask, nlt);
+            if (lane == 0) a.sub_lt[(t * NSUB + warp) * 2 + part] = wl;
+            if (!present) continue;  // uniform over the block
             // one scan: hits (low 16 bits) and below-b* counts (high 16)
             const u32 v = (u32)__popc(hits) | (nlt << 16);
             const u32 ex = block_exclusive_scan<u32>(v, wtot, nullptr);
-            if (threadIdx.x == kPThreads - 1) {
+            if (threadIdx.x == THREADS - 1) {
                 const u32 tot = ex + v;
                 s_base = atomicAdd(&sel[kSelFill], tot & 0xffffu);
                 a.tile_lt[t * 2 + part] = tot >> 16;
@@ -409,8 +427,11 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
     const u64 tlast = (ib + v_size(g, j) - 1) / (u64)T;
     const u32 pfirst = (ib == tfirst * (u64)T) ? 0u : 1u;
     auto count_below = [&](const u32* rec) {
-        const u64 t = rec[k + 1] / (u64)T;
-        atomicAdd(&a.tile_lt[t * 2 + (t == tfirst ? pfirst : 0u)], 1u);
+        const u64 pos = rec[k + 1];
+        const u64 t = pos / (u64)T;
+        const u32 pt = t == tfirst ? pfirst : 0u;
+        atomicAdd(&a.tile_lt[t * 2 + pt], 1u);
+        atomicAdd(&a.sub_lt[(pos / (u64)kSub) * 2 + pt], 1u);
     };
     u32 n = sel[kSelC];
     u32 r = sel[kSelR];
@@ -494,8 +515,9 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
         a.ppos[j] = src[k + 1];
     }
     if (tid < k) a.out_pts[node * k + tid] = __uint_as_float(src[tid]);
-    if (a.mode == kWidest && tid < 2) {
-        // child tid of node: box = node box clipped by the node's plane
+    if (tid < 2) {
+        // child tid of node: box = node box clipped by the node's plane (the
+        // next level's bucket range; widest: its split dim)
         const int d = ch.d[0];
         const float plane = __uint_as_float(src[d]);
         const float* bin = a.boxes_in + j * 2ull * k;
@@ -514,7 +536,7 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
             if (q == 0 || w > bw) { bw = w; best = q; }
         }
         const u64 cnode = 2 * node + 1 + tid;
-        if (cnode < g.n) a.split_dims[cnode] = (uint8_t)best;
+        if (a.mode == kWidest && cnode < g.n) a.split_dims[cnode] = (uint8_t)best;
     }
     // per-tile counts below the pivot -> exclusive prefixes in tile order
     __syncthreads();
@@ -534,266 +556,135 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
 }
 
 // ---------------------------------------------------------------------------
-// part: stable 3-way partition of every segment around its pivot.  Persistent
-// CTAs walk tiles of T = 256 x ITEMS in-order positions (at most two segment
-// parts); each tile's k+1 arrays arrive in shared memory by bulk async copies
-// (cp.async.bulk + mbarrier, double-buffered so tile i+1 loads while tile i
-// is split), ranks come from warp ballots, the per-segment prefix of elements
-// below the pivot from select (no lookback), and the four runs (left / right
-// of each part) are written out coalesced.  Fused: exact [min, max] of each
-// child's next key.
+// part: stable 3-way partition of every segment around its pivot.  Each
+// warp owns one 256-position subtile at a time and needs no other warp:
+// the number of elements below the pivot in everything before its subtile
+// comes from select (per-tile exclusive prefix) plus the filter's counts of
+// the earlier subtiles of the same tile.  The warp loads its subtile's k+1
+// arrays with coalesced loads (all rows in flight at once), classifies
+// against the pivot (chain fields only on a tie), ranks with warp ballots
+// and stores every element straight from registers into its child run --
+// no shared-memory staging and no block barrier.  Stability: rows in
+// position order, lanes in order inside a row.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+constexpr int kPThreads = 256;
+constexpr int kPRows = kSub / 32;
 
-__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
-template <int ITEMS>
-struct PartSmem {
-    static constexpr int T = kPThreads * ITEMS;
-    u64 bar[2];
-    unsigned short inv[T];
-    u32 wcnt[kPWarps][4];
-    u32 run_start[5];
-    u32 cmin[4], cmax[4];
-    u32 piv[2][LBKD_MAX_K + 1];
-    Chain ch[2];
-    long long dbase[4];
-    int cdim[4];
-    // followed by raw[2][k+1][T] u32 (two stages)
-};
-
-template <int ITEMS>
-__global__ void __launch_bounds__(kPThreads) sel_part_kernel(SelArgs a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    PartSmem<ITEMS>& S = *reinterpret_cast<PartSmem<ITEMS>*>(smem_raw);
-    constexpr int T = PartSmem<ITEMS>::T;
+template <int KMAX>
+__global__ void __launch_bounds__(kPThreads) sel_part_kernel(SelArgs a, int T) {
+    const int lane = threadIdx.x & 31;
     const int k = a.k, A = k + 1;
-    u32* raw0 = reinterpret_cast<u32*>(smem_raw + ((sizeof(PartSmem<ITEMS>) + 127) & ~(size_t)127));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
     const LevelGeom& g = a.g;
     const u32* Wsrc = a.bf.w[a.par];
     u32* Wdst = a.bf.w[a.par ^ 1u];
     const u64 stride = a.bf.stride;
-
-    auto issue = [&](u64 tile, int stage) {
-        // one elected thread: the tile's k+1 slices, rounded up to 16 bytes
-        // (the arrays are padded to a multiple of 4 words)
-        const u64 ts = tile * T;
-        const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
-        const u32 bytes = (u32)(((cnt + 3) & ~3ull) * 4);
-        mbar_expect_tx(&S.bar[stage], bytes * A);
-        u32* dst = raw0 + (size_t)stage * A * T;
-        for (int c = 0; c < A; ++c) bulk_g2s(dst + c * T, Wsrc + (u64)c * stride + ts, bytes, &S.bar[stage]);
-    };
-
-    if (tid == 0) {
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (blockIdx.x < a.ntiles) issue(blockIdx.x, 0);
-    }
-    __syncthreads();
-    u32 phases = 0u;  // mbarrier parity of each stage (bit per stage)
-    int stage = 0;
-    for (u64 tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, stage ^= 1) {
-        // prefetch the next tile into the other stage (freed by the barrier
-        // at the end of the previous iteration)
-        if (tid == 0 && tile + gridDim.x < a.ntiles) issue(tile + gridDim.x, stage ^ 1);
-        const u64 ts = tile * T;
-        const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
-        const TileParts tp = tile_parts(g, ts, cnt);
-        const u64 j0 = tp.j0;
-        const u32 r0a = tp.r0a, r0b = tp.r0b, r1a = tp.r1a, r1b = tp.r1b;
-        const bool has1 = tp.has1;
-        if (tid < 2 * A) {
-            const int p = tid / A, c = tid % A;
-            if (p == 0 || has1) S.piv[p][c] = a.piv[(j0 + p) * A + c];
-        }
-        if (tid < 2 * kChainWords) {
-            const int p = tid / kChainWords, c = tid % kChainWords;
-            if (p == 0 || has1)
-                reinterpret_cast<u32*>(&S.ch[p])[c] = reinterpret_cast<const u32*>(a.chains + j0 + p)[c];
-        }
-        if (tid < 4) {
-            S.cmin[tid] = 0xffffffffu;
-            S.cmax[tid] = 0u;
-            int d = (g.l + 1) % k;
-            if (a.mode == kWidest) {
-                const u64 child = 2 * (j0 + (tid >> 1)) + (tid & 1);
-                const u64 cnode = 2 * (g.Fl + g.sbase + j0 + (tid >> 1)) + 1 + (tid & 1);
-                d = (a.want_mm && cnode < g.n && child < 2 * g.nseg) ? (int)a.split_dims[cnode] : 0;
+    const u64 nsub = (g.nview + kSub - 1) / kSub;
+    const int nsub_tile = T / kSub;
+    const u32 lt = lanemask_lt();
+    for (u64 s = (u64)blockIdx.x * (kPThreads / 32) + (threadIdx.x >> 5); s < nsub;
+         s += (u64)gridDim.x * (kPThreads / 32)) {
+        const u64 ss = s * kSub;
+        const u64 cnt = g.nview - ss < (u64)kSub ? g.nview - ss : (u64)kSub;
+        // issue every load of the subtile first
+        u32 v[KMAX + 1][kPRows];
+#pragma unroll
+        for (int c = 0; c <= KMAX; ++c) {
+            if (c < A) {
+                const u32* src = Wsrc + (u64)c * stride + ss;
+#pragma unroll
+                for (int i = 0; i < kPRows; ++i) {
+                    const u32 r = (u32)(i * 32 + lane);
+                    v[c][i] = r < cnt ? src[r] : 0u;
+                }
             }
-            S.cdim[tid] = d;
         }
-        mbar_wait(&S.bar[stage], (phases >> stage) & 1u);
-        phases ^= 1u << stage;
-        __syncthreads();
-        const u32* raw = raw0 + (size_t)stage * A * T;
-
-        // --- classify: q = part*2 + side (0 left, 1 right), -1 none / pivot
-        const u32 lt = lanemask_lt();
-        u32 run[4] = {0u, 0u, 0u, 0u};
-        u32 qr[ITEMS];  // q << 16 | warp-local rank, 0xffffffff = no slot
-        u32 mn[4], mx[4];
+        // geometry (warp-uniform)
+        const TileParts tp = tile_parts(g, ss, cnt);
+        const u64 t = ss / (u64)T;
+        const u64 j0t = v_seg_of(g, t * (u64)T);  // the tile's first segment
+        const int sin = (int)(s - t * (u64)nsub_tile);  // subtile inside the tile
+        long long bL0 = 0, bR0 = 0, bL1 = 0, bR1 = 0;
+        int d00 = 0, d01 = 0;
+        u32 y00 = 0, y01 = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { mn[q] = 0xffffffffu; mx[q] = 0u; }
-        const int d00 = S.ch[0].d[0], d10 = S.ch[1].d[0];
-        const u32 y00 = flip_key(__uint_as_float(S.piv[0][d00]));
-        const u32 y10 = flip_key(__uint_as_float(S.piv[1][d10]));
+        for (int p = 0; p < 2; ++p) {
+            if (p == 1 && !tp.has1) continue;
+            const u64 j = tp.j0 + p;
+            const u32 pt = j == j0t ? 0u : 1u;
+            // below-pivot elements of segment j before this subtile
+            u32 below = lane < sin ? a.sub_lt[(t * (u64)nsub_tile + lane) * 2 + pt] : 0u;
+            below = __reduce_add_sync(kFullMask, below) + a.tile_lt[t * 2 + pt];
+            const u64 ib = p ? tp.ib1 : tp.ib0;
+            const u64 before = ss > ib ? ss - ib : 0ull;
+            const u64 pb = (before > 0 && a.ppos[j] < ss) ? 1ull : 0ull;
+            const long long l = (long long)(ib + below);
+            const long long rr = (long long)(ib + v_pivot(g, j) + 1 + (before - below - pb));
+            const int d = a.chains[j].d[0];
+            const u32 y = flip_key(__uint_as_float(a.piv[j * A + d]));
+            if (p == 0) { bL0 = l; bR0 = rr; d00 = d; y00 = y; }
+            else { bL1 = l; bR1 = rr; d01 = d; y01 = y; }
+        }
+        const u32 r0a = tp.r0a, r0b = tp.r0b, r1a = tp.r1a, r1b = tp.r1b;
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const u32 r = (u32)(warp * ITEMS * 32 + i * 32 + lane);
+        for (int i = 0; i < kPRows; ++i) {
+            const u32 r = (u32)(i * 32 + lane);
             const bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
-            int side = -1;
+            int side = 2;  // 2: pivot or outside the parts
             if (in0 || in1) {
-                const int p = in1 ? 1 : 0;
-                const u32 x = flip_key(__uint_as_float(raw[(p ? d10 : d00) * T + r]));
-                const u32 y = p ? y10 : y00;
+                const int dd = in1 ? d01 : d00;
+                u32 x = 0;
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c)
+                    if (c == dd) x = v[c][i];
+                x = flip_key(__uint_as_float(x));
+                const u32 y = in1 ? y01 : y00;
                 if (x != y) {
                     side = x < y ? 0 : 1;
                 } else {  // tie in the leading field: the rest of the chain, then the index
-                    const Chain& ch = S.ch[p];
-                    const u32* pv = S.piv[p];
-                    side = 2;
-                    for (u32 f = 1; f < ch.m; ++f) {
-                        const int d = ch.d[f];
-                        const u32 xx = flip_key(__uint_as_float(raw[d * T + r]));
+                    const u64 j = tp.j0 + (in1 ? 1 : 0);
+                    const Chain* ch = a.chains + j;
+                    const u32* pv = a.piv + j * A;
+                    const u32 mm = ch->m;
+                    for (u32 f = 1; f < mm && side == 2; ++f) {
+                        const int d = ch->d[f];
+                        u32 xx = 0;
+#pragma unroll
+                        for (int c = 0; c < KMAX; ++c)
+                            if (c == d) xx = v[c][i];
+                        xx = flip_key(__uint_as_float(xx));
                         const u32 yy = flip_key(__uint_as_float(pv[d]));
-                        if (xx != yy) { side = xx < yy ? 0 : 1; break; }
+                        if (xx != yy) side = xx < yy ? 0 : 1;
                     }
                     if (side == 2) {
-                        const u32 xx = raw[k * T + r], yy = pv[k];
+                        u32 xx = 0;
+#pragma unroll
+                        for (int c = 0; c <= KMAX; ++c)
+                            if (c == k) xx = v[c][i];
+                        const u32 yy = pv[k];
                         side = xx < yy ? 0 : (xx > yy ? 1 : 2);
                     }
                 }
             }
-            const int q = (side == 0 || side == 1) ? ((in1 ? 2 : 0) + side) : -1;
-            u32 myrank = 0;
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-                const u32 b = __ballot_sync(kFullMask, q == qq);
-                if (q == qq) myrank = run[qq] + __popc(b & lt);
-                run[qq] += __popc(b);
+            const u32 ml = __ballot_sync(kFullMask, side == 0);
+            const u32 mr = __ballot_sync(kFullMask, side == 1);
+            const u32 pm = __ballot_sync(kFullMask, in1);
+            long long dst = -1;
+            if (side < 2) {
+                const u32 m = (side == 0 ? ml : mr) & (in1 ? pm : ~pm);
+                const long long base = side == 0 ? (in1 ? bL1 : bL0) : (in1 ? bR1 : bR0);
+                dst = base + __popc(m & lt);
             }
-            qr[i] = q >= 0 ? (((u32)q << 16) | myrank) : 0xffffffffu;
-            if (a.want_mm && q >= 0) {
-                const u32 v = flip_key(__uint_as_float(raw[S.cdim[q] * T + r]));
+            // advance the four run bases by this row's counts
+            bL0 += __popc(ml & ~pm);
+            bR0 += __popc(mr & ~pm);
+            bL1 += __popc(ml & pm);
+            bR1 += __popc(mr & pm);
+            if (dst >= 0) {
 #pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    if (q == qq) {
-                        mn[qq] = min(mn[qq], v);
-                        mx[qq] = max(mx[qq], v);
-                    }
-                }
-            }
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) S.wcnt[warp][q] = run[q];
-        }
-        if (a.want_mm) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const u32 x = __reduce_min_sync(kFullMask, mn[q]);
-                const u32 y = __reduce_max_sync(kFullMask, mx[q]);
-                if (lane == 0 && x <= y) { atomicMin(&S.cmin[q], x); atomicMax(&S.cmax[q], y); }
+                for (int c = 0; c <= KMAX; ++c)
+                    if (c < A) Wdst[(u64)c * stride + (u64)dst] = v[c][i];
             }
         }
-        __syncthreads();
-
-        // --- warp prefixes, run starts and destinations (warp 0)
-        if (warp == 0) {
-            u32 tot[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const u32 v = lane < kPWarps ? S.wcnt[lane][q] : 0u;
-                u32 x = v;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const u32 y = __shfl_up_sync(kFullMask, x, o);
-                    if (lane >= o) x += y;
-                }
-                if (lane < kPWarps) S.wcnt[lane][q] = x - v;
-                tot[q] = __shfl_sync(kFullMask, x, 31);
-            }
-            if (lane == 0) {
-                // elements of segment j0 before this tile: below / pivot / above
-                const bool began = r0a < r0b && tp.ib0 < ts;
-                const u64 before = began ? ts - tp.ib0 : 0ull;
-                const u64 below = began ? a.tile_lt[tile * 2] : 0ull;
-                const u64 pb = (began && a.ppos[j0] < ts) ? 1ull : 0ull;
-                const u64 po0 = v_pivot(g, j0);
-                S.dbase[0] = (long long)(tp.ib0 + below);
-                S.dbase[1] = (long long)(tp.ib0 + po0 + 1 + (before - below - pb));
-                if (has1) {
-                    S.dbase[2] = (long long)tp.ib1;
-                    S.dbase[3] = (long long)(tp.ib1 + v_pivot(g, j0 + 1) + 1);
-                } else {
-                    S.dbase[2] = S.dbase[3] = 0;
-                }
-                S.run_start[0] = 0u;
-                S.run_start[1] = tot[0];
-                S.run_start[2] = tot[0] + tot[1];
-                S.run_start[3] = tot[0] + tot[1] + tot[2];
-                S.run_start[4] = tot[0] + tot[1] + tot[2] + tot[3];
-            }
-        }
-        __syncthreads();
-
-        // --- slots (stable: warp order, then row, then lane)
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            if (qr[i] != 0xffffffffu) {
-                const u32 q = qr[i] >> 16;
-                const u32 slot = S.run_start[q] + S.wcnt[warp][q] + (qr[i] & 0xffffu);
-                S.inv[slot] = (unsigned short)(warp * ITEMS * 32 + i * 32 + lane);
-            }
-        }
-        if (a.want_mm && tid < 4) {
-            const int q = tid;
-            if (S.cmin[q] <= S.cmax[q]) {
-                const u64 child = 2 * (j0 + (q >> 1)) + (q & 1);
-                atomicMin(&a.mmn_next[child], S.cmin[q]);
-                atomicMax(&a.mmx_next[child], S.cmax[q]);
-            }
-        }
-        __syncthreads();
-
-        // --- coalesced write-out, run by run
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const u32 s0 = S.run_start[q], s1 = S.run_start[q + 1];
-            u32* d = Wdst + ((u64)S.dbase[q] - s0);
-            for (u32 sl = s0 + tid; sl < s1; sl += kPThreads) {
-                const u32 src = S.inv[sl];
-                for (int c = 0; c < A; ++c) d[(u64)c * stride + sl] = raw[c * T + src];
-            }
-        }
-        __syncthreads();  // the stage is free for the prefetch two tiles ahead
     }
 }
 
@@ -801,11 +692,12 @@ __global__ void __launch_bounds__(kPThreads) sel_part_kernel(SelArgs a) {
 // host side
 // ---------------------------------------------------------------------------
 int sel_items(int b) {
-    int items = (1 << (b - 1)) / kPThreads;
+    int items = (1 << (b - 1)) / 256;
     return items > 8 ? 8 : items;
 }
 
-int sel_tile(int b) { return kPThreads * sel_items(b); }
+// tile of the filter / select scan: at most two segment parts per tile
+int sel_tile(int b) { return 256 * sel_items(b); }
 
 int sel_digit_bits(u64 nseg) {
     int lg = 0;
@@ -836,14 +728,13 @@ void launch_sel_pick(const SelArgs& a, cudaStream_t st) {
 
 void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
     SelArgs a = a0;
-    const int items = sel_items(b);
-    const u64 T = (u64)kPThreads * items;
+    const int T = sel_tile(b);
     a.ntiles = (a.g.nview + T - 1) / T;
     const u64 grid = a.ntiles < 148 * 8 ? a.ntiles : 148 * 8;
-    switch (items) {
-        case 8: sel_filter_kernel<8><<<(unsigned)grid, kPThreads, 0, st>>>(a); break;
-        case 4: sel_filter_kernel<4><<<(unsigned)grid, kPThreads, 0, st>>>(a); break;
-        default: sel_filter_kernel<2><<<(unsigned)grid, kPThreads, 0, st>>>(a); break;
+    switch (T) {
+        case 2048: sel_filter_kernel<256><<<(unsigned)grid, 256, 0, st>>>(a); break;
+        case 1024: sel_filter_kernel<128><<<(unsigned)grid, 128, 0, st>>>(a); break;
+        default: sel_filter_kernel<64><<<(unsigned)grid, 64, 0, st>>>(a); break;
     }
 }
 
@@ -851,26 +742,16 @@ void launch_sel_select(const SelArgs& a, int b, cudaStream_t st) {
     sel_select_kernel<<<(unsigned)a.g.nseg, kSThreads, 0, st>>>(a, sel_tile(b));
 }
 
-template <int ITEMS>
-static void launch_part_t(SelArgs a, cudaStream_t st) {
-    const int T = PartSmem<ITEMS>::T;
-    a.ntiles = (a.g.nview + T - 1) / T;
-    const size_t sm = ((sizeof(PartSmem<ITEMS>) + 127) & ~(size_t)127) + 2 * (size_t)(a.k + 1) * T * sizeof(u32);
-    cudaFuncSetAttribute(sel_part_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sel_part_kernel<ITEMS>, kPThreads, sm);
-    if (per_sm < 1) per_sm = 1;
-    u64 grid = (u64)per_sm * 148;
-    if (grid > a.ntiles) grid = a.ntiles;
-    sel_part_kernel<ITEMS><<<(unsigned)grid, kPThreads, sm, st>>>(a);
-}
-
 void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
-    switch (sel_items(b)) {
-        case 8: launch_part_t<8>(a, st); break;
-        case 4: launch_part_t<4>(a, st); break;
-        default: launch_part_t<2>(a, st); break;
-    }
+    const int T = sel_tile(b);
+    const u64 nsub = (a.g.nview + kSub - 1) / kSub;
+    const u64 per_cta = kPThreads / 32;
+    u64 grid = (nsub + per_cta - 1) / per_cta;
+    const u64 cap = 148ull * 8;
+    if (grid > cap) grid = cap;
+    if (a.k <= 4) sel_part_kernel<4><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
+    else if (a.k <= 8) sel_part_kernel<8><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
+    else sel_part_kernel<16><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
 }
 
 }  // namespace lbkd

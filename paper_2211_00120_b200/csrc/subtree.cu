@@ -147,7 +147,7 @@ __device__ __forceinline__ void block_pass(const ET* __restrict__ Ein, ET* __res
 // bits) by the coordinate array Pd, ping-ponging between buf0 and buf1;
 // digits constant over the list are skipped.  Returns the new cur.
 template <typename ET>
-__device__ int list_sort_dim(ET* buf0, ET* buf1, int cur, int m, const float* Pd, unsigned short (*cnt)[256],
+__device__ __forceinline__ int list_sort_dim(ET* buf0, ET* buf1, int cur, int m, const float* Pd, unsigned short (*cnt)[256],
                              u32 (*gsum)[256], u32* scratch) {
     const int tid = threadIdx.x;
     u32 x_and = 0xffffffffu, x_or = 0u;
@@ -196,7 +196,7 @@ __device__ __forceinline__ bool chain_less(u32 a, u32 b, const float* P, int ldP
 }
 
 template <typename ET>
-__device__ int entry_order(ET* buf0, ET* buf1, int m, const float* P, int ldP, const Chain& ch,
+__device__ __forceinline__ int entry_order(ET* buf0, ET* buf1, int m, const float* P, int ldP, const Chain& ch,
                            unsigned short (*cnt)[256], u32 (*gsum)[256], u32* scratch) {
     if (ch.m == 0) return 0;
     const float* P0 = P + (size_t)ch.d[0] * ldP;
@@ -433,55 +433,68 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
 // order, and after k levels all coordinates are in the chain; further
 // repeats of a coordinate never decide a comparison).  The entry order is
 // T_{(lam0-1) mod k}; T_d = stable_sort(T_{d-1}, c[d]), so k-1 block radix
-// sorts give all k orders as lists of local ids.  Each level then only
-// (1) reads the pivot of every segment straight off list T_{l mod k} at the
-// reference's pivot offset (kernels_numba.py:21-46) and (2) stably
-// partitions every list that is still needed into the two child segments
-// (one block scan), instead of re-sorting.
+// sorts give all k orders as lists of local ids.
+//
+// Block phase (segments > 31 points), per level:
+//   (1) the active list T_{l mod k}: the element at each segment's pivot
+//       offset (kernels_numba.py:21-46) is the node; every element records
+//       (child segment, side) in one packed state word; the list itself
+//       splits without a scan (left part precedes the pivot);
+//   (2) every other list still needed later is split stably into the child
+//       segments -- up to two lists share ONE block scan of packed
+//       (right, pivot) counts; destinations come from per-segment tables
+//       (right elements of the earlier segments: one scan per level).
+// Warp phase (segments <= 31 points, the last <= 5 levels): the position of
+// every point in each list is its rank under T_d; one warp per segment
+// finishes the segment's subtree in registers -- each level a point's rank
+// inside its node is a count over the warp's lanes -- without barriers.
 // ===========================================================================
+constexpr int kWarpSegBits = 5;  // warp phase once segments hold <= 2^5 - 1 points
+
 size_t subtree_rr_smem_bytes(int b, int k) {
     size_t M = ((size_t)1 << b) - 1;
     size_t Mp = (M + 8) & ~(size_t)7;  // 16-byte aligned u16 arrays
     size_t bytes = sizeof(float) * (size_t)k * Mp;   // P
-    bytes += sizeof(unsigned short) * Mp * (k + 1);   // k lists + partition target
-    bytes += sizeof(unsigned short) * Mp;             // seg of each point
-    bytes += Mp;                                      // side of each point
-    size_t nloc = ((size_t)1 << (b - 2));             // segments at the deepest sort level
-    size_t tables = sizeof(unsigned short) * (2 * nloc + 8) + sizeof(u32) * nloc;
+    bytes += sizeof(unsigned short) * Mp * (k + 2);   // k lists + two partition targets
+    bytes += sizeof(unsigned short) * Mp;             // packed state of each point
+    size_t nloc = ((size_t)1 << (b - 2));             // segments at the deepest block level
+    // level tables + node table (after the chain sorts) alias the sort scratch
+    size_t tables = sizeof(unsigned short) * 3 * (nloc + 8) + sizeof(unsigned short) * Mp;
     size_t sortscr = sizeof(unsigned short) * kSubWarps * 256 + sizeof(u32) * 4 * 256;
     bytes += tables > sortscr ? tables : sortscr;
-    bytes += sizeof(u32) * 64;
+    bytes += sizeof(u64) * 64;
     return (bytes + 15) & ~(size_t)15;
 }
 
 __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef unsigned short u16;
-    const int M = a.M, k = a.k, tid = threadIdx.x;
+    const int M = a.M, k = a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int Mp = (M + 8) & ~7;
     unsigned char* sp = smem_raw;
     float* P = reinterpret_cast<float*>(sp);
     sp += sizeof(float) * (size_t)k * Mp;
-    u16* Lst[kMaxK + 1];
-    for (int d = 0; d <= k; ++d) {
-        Lst[d] = reinterpret_cast<u16*>(sp);
-        sp += sizeof(u16) * Mp;
-    }
-    u16* segv = reinterpret_cast<u16*>(sp);
+    // the k + 2 lists as offsets from one shared base: pointers kept in a
+    // local array would lose their address space (generic LD/ST)
+    u16* const LB = reinterpret_cast<u16*>(sp);
+    int Lo[kMaxK + 2];
+    for (int d = 0; d <= k + 1; ++d) Lo[d] = d * Mp;
+    sp += sizeof(u16) * Mp * (k + 2);
+    u16* state = reinterpret_cast<u16*>(sp);  // (next-level segment << 2) | side (0 L, 1 R, 2 node)
     sp += sizeof(u16) * Mp;
-    unsigned char* side = sp;
-    sp += Mp;
-    sp = reinterpret_cast<unsigned char*>(((uintptr_t)sp + 15) & ~(uintptr_t)15);
-    // tables (levels) alias the radix-sort scratch (chain sorts)
-    const int nmax = (M + 1) / 4;  // 2^(b-2) segments at the deepest sort level
-    u16* lbt = reinterpret_cast<u16*>(sp);
-    u16* pot = lbt + nmax + 8;
-    u32* segpre = reinterpret_cast<u32*>(pot + nmax);
+    sp = smem_raw + (((size_t)(sp - smem_raw) + 15) & ~(size_t)15);  // keep the shared base (no uintptr_t round trip)
+    // per-level tables alias the radix-sort scratch (chain sorts)
+    const int nmax = (M + 1) / 4;  // 2^(b-2) segments at the deepest block level
+    u16* lbt = reinterpret_cast<u16*>(sp);   // segment begin in the lists
+    u16* pot = lbt + nmax + 8;               // pivot offset
+    u16* rtb = pot + nmax + 8;               // right elements of the earlier segments
+    u16* ntab = rtb + nmax + 8;              // local id of the point of every node, heap order
     unsigned short(*cnt)[256] = reinterpret_cast<unsigned short(*)[256]>(sp);
     u32(*gsum)[256] = reinterpret_cast<u32(*)[256]>(sp + sizeof(unsigned short) * kSubWarps * 256);
-    size_t tables = sizeof(u16) * (2 * (size_t)nmax + 8) + sizeof(u32) * nmax;
+    size_t tables = sizeof(u16) * 3 * ((size_t)nmax + 8) + sizeof(u16) * Mp;
     size_t sortscr = sizeof(unsigned short) * kSubWarps * 256 + sizeof(u32) * 4 * 256;
     u32* scratch = reinterpret_cast<u32*>(sp + (tables > sortscr ? tables : sortscr));
+    u64* scratch64 = reinterpret_cast<u64*>(scratch);
 
     const u64 jl = blockIdx.x;      // subtree within the view
     const u64 j = a.jbase + jl;     // global index at level lam0
@@ -497,27 +510,25 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
     const u32* src = a.w[par] + (seg_ibegin(g0, j) - a.pbase);
     const u32* vin = src + (u64)k * a.stride;
     const int e = (a.lam0 - 1) % k;  // dimension of the entry order
-    u16* ident = a.entry_sorted ? Lst[e] : Lst[0];
+    u16* ident = LB + (a.entry_sorted ? Lo[e] : Lo[0]);
     for (int lid = tid; lid < m; lid += kSubThreads) {
         for (int c = 0; c < k; ++c) P[c * Mp + lid] = __uint_as_float(src[(u64)c * a.stride + lid]);
         ident[lid] = (u16)lid;
-        segv[lid] = 0;
+        state[lid] = 0;
     }
     __syncthreads();
     if (!a.entry_sorted) {
-        // input order -> T_e (full chain: lam0 >= k), then hand the k other
-        // buffers out as the remaining lists and the spare
+        // input order -> T_e (full chain: lam0 >= k), then hand the other
+        // buffers out as the remaining lists and the spares
         Chain ch;
         rr_chain(a.lam0 - 1, k, ch);
-        const int r = entry_order(Lst[0], Lst[1], m, P, Mp, ch, cnt, gsum, scratch);
-        u16* pool[kMaxK + 1];
-        for (int d = 0; d <= k; ++d) pool[d] = Lst[d];
-        u16* res = pool[r];
+        const int r = entry_order(LB + Lo[0], LB + Lo[1], m, P, Mp, ch, cnt, gsum, scratch);
+        const int res = r * Mp;  // list buffers are still in order here
         int q = 0;
-        for (int d = 0; d <= k; ++d) {
-            if (d == e) { Lst[d] = res; continue; }
-            if (pool[q] == res) ++q;
-            Lst[d] = pool[q++];
+        for (int d = 0; d <= k + 1; ++d) {
+            if (d == e) { Lo[d] = res; continue; }
+            if (q * Mp == res) ++q;
+            Lo[d] = (q++) * Mp;
         }
     }
 
@@ -534,16 +545,14 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         }
         x_and = __reduce_and_sync(kFullMask, x_and);
         x_or = __reduce_or_sync(kFullMask, x_or);
-        scratch[32 + (tid >> 5)] = x_and ^ x_or;  // every lane stores the warp-uniform value: a
-    // lane-0 guard here was miscompiled by NVVM 12.9 (it reused the guarded
-    // (tid >> 3) == 4 * warp for every lane in the next cnt[warp] address)
+        scratch[32 + (tid >> 5)] = x_and ^ x_or;  // every lane stores the warp-uniform value (NVVM 12.9, above)
         __syncthreads();
         u32 vary = 0;
         for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
         __syncthreads();
-        const u16* in = Lst[dprev];
-        u16* outA = Lst[d];
-        u16* outB = Lst[k];  // spare
+        const u16* in = LB + Lo[dprev];
+        u16* outA = LB + Lo[d];
+        u16* outB = LB + Lo[k];  // spare
         int npass = 0;
         for (int b = 0; b < 4; ++b) {
             if (((vary >> (8 * b)) & 255u) == 0) continue;
@@ -554,119 +563,290 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
             ++npass;
         }
         if (npass == 0) {
-            for (int p = tid; p < m; p += kSubThreads) outA[p] = Lst[dprev][p];
+            for (int p = tid; p < m; p += kSubThreads) outA[p] = in[p];
             __syncthreads();
         } else if (npass & 1) {
             // result in outA == Lst[d]
         } else {
             // result in the spare list: swap roles
-            Lst[k] = outA;
-            Lst[d] = outB;
+            const int t = Lo[k];
+            Lo[k] = Lo[d];
+            Lo[d] = t;
         }
     }
 
-    auto write_node = [&](u64 node, u32 lid) {
-        a.perm[node] = vin[lid];
-        float* dst = a.out_pts + node * (u64)k;
-        for (int c = 0; c < k; ++c) dst[c] = P[c * Mp + lid];
+    // geometry without per-level bit_length loops: B = bottom slots in use
+    const int L = a.L;
+    const u64 Bn = a.n - ((1ull << (L - 1)) - 1ull);
+    auto seg_size_l = [&](int sh, u64 J) -> u32 {
+        const u64 w = 1ull << sh, lo = J << sh;
+        u64 on = Bn > lo ? Bn - lo : 0ull;
+        if (on > w) on = w;
+        return (u32)(w - 1ull + on);
+    };
+    auto seg_begin_l = [&](int sh, u64 J) -> u64 {
+        const u64 lo = J << sh;
+        return J * ((1ull << sh) - 1ull) + (lo < Bn ? lo : Bn);
+    };
+    auto pivot_off_l = [&](int sh, u64 J) -> u32 {
+        if (sh <= 0) return 0u;
+        const u64 cw = 1ull << (sh - 1), lo = (2ull * J) * cw;
+        u64 on = Bn > lo ? Bn - lo : 0ull;
+        if (on > cw) on = cw;
+        return (u32)(cw - 1ull + on);
     };
 
-    for (int lam = a.lam0; lam <= a.L - 2; ++lam) {
-        const LevelGeom g = make_geom(a.n, lam);
+    int lam = a.lam0;
+    // ================= block phase =================
+    for (; lam <= L - 2 && (L - lam - 1) > kWarpSegBits - 1; ++lam) {
+        const int sh = L - lam - 1;
         const int dl = lam - a.lam0;
         const int nloc = 1 << dl;
         const u64 J0 = j << dl;
-        const u64 lb0 = seg_begin(g, J0);
+        const u64 lb0 = seg_begin_l(sh, J0);
         const int mc = m - (nloc - 1);
         const int ad = lam % k;
-        const bool last = (lam == a.L - 2);
-        const LevelGeom gn = make_geom(a.n, lam + 1);
-        for (int t = tid; t < nloc; t += kSubThreads) {
-            lbt[t] = (u16)(seg_begin(g, J0 + t) - lb0);
-            pot[t] = (u16)pivot_off(g, J0 + t);
+        const u64 Fl = (1ull << lam) - 1ull;
+        const bool last = (lam == L - 2);
+        // tables + right elements of the earlier segments (one scan)
+        {
+            u32 v = 0;
+            const int per = (nloc + kSubThreads - 1) / kSubThreads;  // <= 2
+            u32 rs[2] = {0u, 0u};
+            for (int i = 0; i < per; ++i) {
+                const int t = tid * per + i;
+                if (t < nloc) {
+                    const u32 sz = seg_size_l(sh, J0 + t);
+                    const u32 po = pivot_off_l(sh, J0 + t);
+                    lbt[t] = (u16)(seg_begin_l(sh, J0 + t) - lb0);
+                    pot[t] = (u16)po;
+                    rs[i] = sz - po - 1u;
+                    v += rs[i];
+                }
+            }
+            const u32 ex = block_exclusive_scan<u32>(v, scratch, nullptr);
+            u32 run = ex;
+            for (int i = 0; i < per; ++i) {
+                const int t = tid * per + i;
+                if (t < nloc) { rtb[t] = (u16)run; run += rs[i]; }
+            }
+            if (tid == 0) lbt[nloc] = (u16)mc;
         }
-        if (tid == 0) lbt[nloc] = (u16)mc;
         __syncthreads();
 
-        // (1) the active list: pivots, sides, child segments; its own stable
-        // partition needs no scan (left part precedes the pivot)
-        u16* A = Lst[ad];
-        u16* tmp = Lst[k];
+        // (1) the active list: nodes, sides, child segments; its own split
+        u16* A = LB + Lo[ad];
+        u16* tmpA = LB + Lo[k];
         for (int p = tid; p < mc; p += kSubThreads) {
             const u32 lid = A[p];
-            const u32 t = segv[lid];
-            const u32 o = (u32)p - lbt[t];
+            const u32 t = state[lid] >> 2;
+            const u32 lb = lbt[t];
+            const u32 o = (u32)p - lb;
             const u32 po = pot[t];
             if (o == po) {
-                side[lid] = 2;
-                segv[lid] = (u16)(2 * t);
-                write_node(g.Fl + J0 + t, lid);
+                state[lid] = (u16)(((2u * t) << 2) | 2u);
+                ntab[nloc - 1 + t] = (u16)lid;
                 continue;
             }
             const u32 r = o > po ? 1u : 0u;
-            side[lid] = (unsigned char)r;
-            segv[lid] = (u16)(2 * t + r);
-            if (last) {
-                write_node(gn.Fl + 2 * (J0 + t) + r, lid);
-            } else {
-                tmp[lbt[t] - t + o - r] = (u16)lid;
-            }
+            state[lid] = (u16)(((2u * t + r) << 2) | r);
+            if (last) ntab[2 * nloc - 1 + 2 * t + r] = (u16)lid;
+            else tmpA[lb - t + o - r] = (u16)lid;
         }
         __syncthreads();
-        if (last) break;
-        Lst[k] = A;
-        Lst[ad] = tmp;
+        if (last) {  // (only for tiny subtrees) the bottom level is written too
+            lam = L;
+            break;
+        }
+        {
+            const int t = Lo[k];
+            Lo[k] = Lo[ad];
+            Lo[ad] = t;
+        }
 
-        // (2) stable partition of every other list still needed later
+        // (2) the passive lists still needed later, two per block scan
+        int todo[kMaxK];
+        int nt = 0;
         for (int d = 0; d < k; ++d) {
             if (d == ad) continue;
-            int next_use = lam + ((d - ad + k) % k);
-            if (next_use > a.L - 2) continue;
-            u16* Ld = Lst[d];
-            u16* Tg = Lst[k];
-            // 8 consecutive positions per thread: packed (right, pivot) counts
+            const int next_use = lam + ((d - ad + k) % k);
+            if (next_use <= L - 2) todo[nt++] = d;
+        }
+        for (int i0 = 0; i0 < nt; i0 += 2) {
+            const int dA = todo[i0];
+            const int dB = i0 + 1 < nt ? todo[i0 + 1] : -1;
+            const u16* XA = LB + Lo[dA];
+            const bool hasB = dB >= 0;
+            const u16* XB = LB + (hasB ? Lo[dB] : Lo[dA]);
+            u16* YA = LB + Lo[k];
+            u16* YB = LB + Lo[k + 1];
+            // 8 consecutive positions per thread, one 16-byte load per list
             const int p0 = tid * 8;
-            u32 lid8[8];
-            u32 v8 = 0, run[8];
+            u32 la[8], lb8[8], sa[8], sb[8];
+            u64 v = 0;
+            if (p0 < mc) {
+                const uint4 qa = *reinterpret_cast<const uint4*>(XA + p0);
+                const u32 wa[4] = {qa.x, qa.y, qa.z, qa.w};
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int p = p0 + i;
-                u32 lid = p < mc ? Ld[p] : 0u;
-                lid8[i] = lid;
-                u32 s = p < mc ? side[lid] : 0u;
-                run[i] = v8;
-                v8 += (s == 1 ? 1u : 0u) | (s == 2 ? 0x10000u : 0u);
+                for (int i = 0; i < 8; ++i) {
+                    la[i] = (wa[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+                    sa[i] = p0 + i < mc ? (u32)state[la[i]] : 3u;
+                }
+                if (hasB) {
+                    const uint4 qb = *reinterpret_cast<const uint4*>(XB + p0);
+                    const u32 wb[4] = {qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        lb8[i] = (wb[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+                        sb[i] = p0 + i < mc ? (u32)state[lb8[i]] : 3u;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const u32 ca = sa[i] & 3u;
+                    v += (u64)(ca == 1u) | ((u64)(ca == 2u) << 16);
+                    if (hasB) {
+                        const u32 cb = sb[i] & 3u;
+                        v += ((u64)(cb == 1u) << 32) | ((u64)(cb == 2u) << 48);
+                    }
+                }
             }
-            u32 ex = block_exclusive_scan<u32>(v8, scratch, nullptr);
+            u64 ex = block_exclusive_scan<u64>(v, scratch64, nullptr);
+            if (p0 < mc) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int p = p0 + i;
-                if (p < mc) {
-                    const u32 t = segv[lid8[i]] >> 1;
-                    if ((u32)p == lbt[t]) segpre[t] = ex + run[i];
+                for (int i = 0; i < 8; ++i) {
+                    const int p = p0 + i;
+                    const u32 ca = sa[i] & 3u;
+                    if (ca < 2u) {
+                        const u32 t = sa[i] >> 3;
+                        const u32 Rex = (u32)(ex & 0xffffu), Pex = (u32)((ex >> 16) & 0xffffu);
+                        const u32 dst = ca ? (u32)lbt[t] - t + pot[t] + Rex - rtb[t] : (u32)p - Rex - Pex + rtb[t];
+                        YA[dst] = (u16)la[i];
+                    }
+                    ex += (u64)(ca == 1u) | ((u64)(ca == 2u) << 16);
+                    if (hasB) {
+                        const u32 cb = sb[i] & 3u;
+                        if (cb < 2u) {
+                            const u32 t = sb[i] >> 3;
+                            const u32 Rex = (u32)((ex >> 32) & 0xffffu), Pex = (u32)(ex >> 48);
+                            const u32 dst = cb ? (u32)lbt[t] - t + pot[t] + Rex - rtb[t] : (u32)p - Rex - Pex + rtb[t];
+                            YB[dst] = (u16)lb8[i];
+                        }
+                        ex += ((u64)(cb == 1u) << 32) | ((u64)(cb == 2u) << 48);
+                    }
                 }
             }
             __syncthreads();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int p = p0 + i;
-                if (p >= mc) break;
-                const u32 lid = lid8[i];
-                const u32 s = side[lid];
-                if (s == 2) continue;
-                const u32 t = segv[lid] >> 1;
-                const u32 pre = ex + run[i] - segpre[t];
-                const u32 rb = pre & 0xffffu, pb = pre >> 16;
-                const u32 base = lbt[t] - t;
-                const u32 dst = s ? base + pot[t] + rb : base + ((u32)p - lbt[t]) - rb - pb;
-                Tg[dst] = (u16)lid;
+            {
+                const int t = Lo[k];
+                Lo[k] = Lo[dA];
+                Lo[dA] = t;
             }
-            __syncthreads();
-            Lst[k] = Ld;
-            Lst[d] = Tg;
+            if (hasB) {
+                const int t = Lo[k + 1];
+                Lo[k + 1] = Lo[dB];
+                Lo[dB] = t;
+            }
         }
     }
-    if (a.lam0 > a.L - 2 && tid == 0 && m == 1) write_node(g0.Fl + j, 0u);
+
+    // ================= warp phase =================
+    if (lam <= L - 1) {
+        const int dl = lam - a.lam0;
+        const int nloc = 1 << dl;
+        const u64 J0 = j << dl;
+        const int sh = L - lam - 1;
+        const u64 lb0 = seg_begin_l(sh, J0);
+        // rank of every point in each list that is used again = its rank
+        // under T_d inside its segment; the spare buffers receive them
+        int rko[kMaxK];
+        int freeb[kMaxK + 2];
+        int nfree = 0;
+        freeb[nfree++] = Lo[k];
+        freeb[nfree++] = Lo[k + 1];
+        const int memo = Lo[lam % k];
+        const u16* member = LB + memo;
+        for (int d = 0; d < k; ++d) {
+            rko[d] = -1;
+            const int first_use = lam + ((d - lam % k + k) % k);
+            if (first_use > L - 2) continue;
+            const int dsto = freeb[--nfree];
+            u16* dst = LB + dsto;
+            const u16* X = LB + Lo[d];
+            for (int p = tid; p < m - (nloc - 1); p += kSubThreads) dst[X[p]] = (u16)p;
+            rko[d] = dsto;
+            if (Lo[d] != memo) freeb[nfree++] = Lo[d];
+            __syncthreads();
+        }
+        for (int t = warp; t < nloc; t += kSubWarps) {
+            const u64 Jt = J0 + t;
+            const u32 sb = (u32)(seg_begin_l(sh, Jt) - lb0);
+            const u32 sz = seg_size_l(sh, Jt);
+            bool act = (u32)lane < sz;
+            const u32 lid = act ? member[sb + lane] : 0u;
+            u32 nd = 0;  // heap index of the point's node inside segment t's subtree (< 31)
+            for (int l2 = lam; l2 <= L - 1; ++l2) {
+                const int dd = l2 - lam;
+                const int sh2 = L - l2 - 1;
+                // local rank under T_d inside the segment (< 31): the segment
+                // begins at sb in every list
+                const u32 key = (act && l2 <= L - 2) ? (u32)LB[rko[l2 % k] + lid] - sb : 0u;
+                // rank inside the node from bit-sliced ballots: lanes of the
+                // same node (5 node bits), then those with a smaller key
+                u32 eq = __ballot_sync(kFullMask, act);
+#pragma unroll
+                for (int b = 0; b < kWarpSegBits; ++b) {
+                    const u32 bit = (nd >> b) & 1u;
+                    const u32 bal = __ballot_sync(kFullMask, bit);
+                    eq &= bit ? bal : ~bal;
+                }
+                u32 lt = 0u;
+#pragma unroll
+                for (int b = kWarpSegBits - 1; b >= 0; --b) {
+                    const u32 bit = (key >> b) & 1u;
+                    const u32 bal = __ballot_sync(kFullMask, bit);
+                    if (bit) {
+                        lt |= eq & ~bal;
+                        eq &= bal;
+                    } else {
+                        eq &= ~bal;
+                    }
+                }
+                const u32 rank = (u32)__popc(lt);
+                if (act) {
+                    const u32 off = nd + 1u - (1u << dd);  // node's index among depth dd
+                    const u64 J = (Jt << dd) + off;
+                    const u32 po = pivot_off_l(sh2, J);
+                    if (rank == po) {
+                        ntab[(1u << (dl + dd)) - 1u + ((u32)t << dd) + off] = (u16)lid;
+                        act = false;
+                    } else {
+                        nd = 2u * nd + 1u + (rank > po ? 1u : 0u);
+                    }
+                }
+                if (!__any_sync(kFullMask, act)) break;
+            }
+        }
+    }
+
+    // ================= output =================
+    // each level's nodes of this subtree are one contiguous range of the
+    // level-order arrays: coalesced stores of points and input rows
+    __syncthreads();
+    for (int dl = 0; a.lam0 + dl <= L - 1; ++dl) {
+        const int l2 = a.lam0 + dl;
+        const u64 first = ((1ull << l2) - 1ull) + (j << dl);
+        if (first >= a.n) break;
+        u64 cntn = 1ull << dl;
+        if (first + cntn > a.n) cntn = a.n - first;
+        const u32 h0 = (1u << dl) - 1u;
+        for (u32 i = tid; i < (u32)cntn; i += kSubThreads) a.perm[first + i] = vin[ntab[h0 + i]];
+        float* dst = a.out_pts + first * (u64)k;
+        for (u32 i = tid; i < (u32)cntn * (u32)k; i += kSubThreads) {
+            const u32 t = i / (u32)k, c = i - t * (u32)k;
+            dst[i] = P[c * Mp + ntab[h0 + t]];
+        }
+    }
 }
 
 void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entry_sorted, int src_par,

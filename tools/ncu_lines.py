@@ -1,30 +1,27 @@
-"""Per-source-line stall samples / executed instructions from an ncu report."""
-import collections, csv, subprocess, sys
+"""Per-CUDA-source-line instruction / stall shares of an ncu report (needs -lineinfo)."""
+import csv, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
-rows = list(csv.reader(txt.splitlines()))
-cur = None
-hdr = None
-agg = collections.defaultdict(lambda: [0, 0, ""])
+rows = list(csv.reader(out.splitlines()))
+data, f = [], None
 for r in rows:
-    if len(r) == 2 and r[0] == "File Path":
-        cur = r[1].split("/")[-1]
+    if not r:
         continue
-    if r and r[0] == "Line No":
-        hdr = r
+    if r[0] == "File Path":
+        f = r[1].split("/")[-1]
         continue
-    if hdr and len(r) == len(hdr) and r[0].isdigit():
-        s = int(r[4]) if r[4].isdigit() else 0
-        ie = int(r[7]) if r[7].isdigit() else 0
-        a = agg[(cur, int(r[0]))]
-        a[0] += s
-        a[1] += ie
-        a[2] = r[1][:80]
-ts = sum(v[0] for v in agg.values()) or 1
-ti = sum(v[1] for v in agg.values()) or 1
-print("samples", ts, "instr", ti)
-for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
-    print(f"{k[0]:14s}{k[1]:5d} instr {100*v[1]/ti:5.1f}% stall {100*v[0]/ts:5.1f}%  {v[2]}")
+    if r[0] in ("Function Name", "Line No") or len(r) < 8:
+        continue
+    if r[2] == "-":
+        try:
+            data.append((float(r[7] or 0), float(r[4] or 0), f, r[0], r[1][:100]))
+        except ValueError:
+            pass
+ti = sum(d[0] for d in data) or 1
+ts = sum(d[1] for d in data) or 1
+print(f"total warp instructions {ti:.3e}, stall samples {ts:.0f}")
+for d in sorted(data, key=lambda x: -x[1])[:top]:
+    print(f"{d[0] / ti * 100:5.1f}% inst {d[1] / ts * 100:5.1f}% stall {d[2]}:{d[3]:>4} {d[4]}")
