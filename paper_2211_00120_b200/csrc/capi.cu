@@ -90,9 +90,12 @@ static void prof_end(lbkd_ctx* c, cudaStream_t st, int cls, double bytes) {
 
 static int choose_bits(int k, int mode) {
     const size_t limit = 227 * 1024 - 256;  // dynamic + a little static smem
-    for (int b = 13; b >= 10; --b)
+    // round-robin: two CTAs of the presorted-list kernel per SM (<= 8 x 512
+    // points each); widest: one CTA of the general kernel per SM
+    const size_t rr_limit = 113 * 1024;
+    for (int b = (mode == kRoundRobin ? 12 : 13); b >= 9; --b)
         if (subtree_smem_bytes(b, k, mode) <= limit &&
-            (mode != kRoundRobin || subtree_rr_smem_bytes(b, k) <= limit))
+            (mode != kRoundRobin || subtree_rr_smem_bytes(b, k) <= rr_limit))
             return b;
     return -1;
 }
@@ -293,6 +296,8 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
 }
 
 static int run_levels(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cudaStream_t st) {
+    // the digit-pass tiles (512 x items) need segments of >= 2^9 - 1 points
+    if (c->algo != 0 && lto > lfrom && bp.b < 10) return LBKD_EUNSUPPORTED;
     return c->algo == 0 ? run_levels_select(c, bp, lfrom, lto, st) : run_levels_sort(c, bp, lfrom, lto, st);
 }
 

@@ -230,7 +230,8 @@ void launch_hist(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t s
     unsigned grid = (unsigned)((a.ntiles + tpc - 1) / tpc);
     switch (items) {
         case 8: hist_kernel<8><<<grid, kHistThreads, 0, st>>>(a); break;
-        default: hist_kernel<4><<<grid, kHistThreads, 0, st>>>(a); break;
+        case 4: hist_kernel<4><<<grid, kHistThreads, 0, st>>>(a); break;
+        default: hist_kernel<2><<<grid, kHistThreads, 0, st>>>(a); break;
     }
 }
 
@@ -537,10 +538,11 @@ void launch_pass(const BuildParams& bp, const Buffers& bf, int l, int pass, u32 
     int items = items_for_bits(bp.b);
     const u64 T = (u64)kThreads * items;
     unsigned grid = (unsigned)((a.g.nview + T - 1) / T);
-    switch (items) {
+    switch (items) {  // the sort path requires b >= 10 (capi.cu)
         case 8: launch_pass_t<8>(a, grid, st); break;
         case 4: launch_pass_t<4>(a, grid, st); break;
-        default: launch_pass_t<2>(a, grid, st); break;
+        case 2: launch_pass_t<2>(a, grid, st); break;
+        default: launch_pass_t<1>(a, grid, st); break;
     }
 }
 

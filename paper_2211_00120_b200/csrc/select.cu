@@ -718,8 +718,13 @@ void launch_sel_hist(const SelArgs& a0, int b, cudaStream_t st) {
     a.tiles_per_cta = (int)tpc;
     const unsigned grid = (unsigned)((a.ntiles + tpc - 1) / tpc);
     const size_t sm = sizeof(u32) << a.D;
-    if (items >= 8) sel_hist_kernel<8><<<grid, kHThreads, sm, st>>>(a);
-    else sel_hist_kernel<4><<<grid, kHThreads, sm, st>>>(a);
+    // tile <= 2^(b-1) <= the smallest segment: at most two parts per tile
+    switch (items) {
+        case 8: sel_hist_kernel<8><<<grid, kHThreads, sm, st>>>(a); break;
+        case 4: sel_hist_kernel<4><<<grid, kHThreads, sm, st>>>(a); break;
+        case 2: sel_hist_kernel<2><<<grid, kHThreads, sm, st>>>(a); break;
+        default: sel_hist_kernel<1><<<grid, kHThreads, sm, st>>>(a); break;
+    }
 }
 
 void launch_sel_pick(const SelArgs& a, cudaStream_t st) {
@@ -734,7 +739,8 @@ void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
     switch (T) {
         case 2048: sel_filter_kernel<256><<<(unsigned)grid, 256, 0, st>>>(a); break;
         case 1024: sel_filter_kernel<128><<<(unsigned)grid, 128, 0, st>>>(a); break;
-        default: sel_filter_kernel<64><<<(unsigned)grid, 64, 0, st>>>(a); break;
+        case 512: sel_filter_kernel<64><<<(unsigned)grid, 64, 0, st>>>(a); break;
+        default: sel_filter_kernel<32><<<(unsigned)grid, 32, 0, st>>>(a); break;
     }
 }
 

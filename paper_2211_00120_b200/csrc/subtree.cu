@@ -22,9 +22,11 @@
 
 namespace lbkd {
 
-constexpr int kSubThreads = 1024;
+constexpr int kSubThreads = 1024;  // general kernel (widest, small trees)
 constexpr int kSubWarps = kSubThreads / 32;
-constexpr int kMaxRounds = 8;  // M <= 8191 -> at most 8 rounds of 1024
+constexpr int kRRThreads = 512;    // round-robin kernel: two CTAs per SM
+constexpr int kRRWarps = kRRThreads / 32;
+constexpr int kMaxRounds = 8;  // M <= 8 x threads -> at most 8 rounds
 constexpr int kMaxK = 16;
 
 struct SubtreeArgs {
@@ -62,14 +64,14 @@ size_t subtree_smem_bytes(int b, int k, int mode) {
 
 // One stable block-wide counting pass: Eout[rank(e)] = e for the m elements
 // of Ein, ranked by digit(e) in 0..255 with ties kept in Ein order.
-template <typename ET, typename DigitFn>
+template <int NT, typename ET, typename DigitFn>
 __device__ __forceinline__ void block_pass(const ET* __restrict__ Ein, ET* __restrict__ Eout, int m,
                                            DigitFn digit, unsigned short (*cnt)[256], u32 (*gsum)[256],
                                            u32* scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-    const int C = ((m + kSubThreads - 1) / kSubThreads) * 32;  // per-warp chunk
+    const int C = ((m + NT - 1) / NT) * 32;  // per-warp chunk
     const int R = C / 32;
-    for (int i = tid; i < kSubWarps * 256 / 2; i += kSubThreads) reinterpret_cast<u32*>(&cnt[0][0])[i] = 0u;
+    for (int i = tid; i < (NT / 32) * 256 / 2; i += NT) reinterpret_cast<u32*>(&cnt[0][0])[i] = 0u;
     __syncthreads();
     const u32 lt = lanemask_lt();
     u32 ev[kMaxRounds];
@@ -109,7 +111,10 @@ __device__ __forceinline__ void block_pass(const ET* __restrict__ Ein, ET* __res
     }
     __syncthreads();
     if (tid < 256) {
-        u32 g0 = gsum[0][tid], g1 = gsum[1][tid], g2 = gsum[2][tid], g3 = gsum[3][tid];
+        // NT / 256 groups (the unused ones count zero)
+        constexpr int NG = NT / 256;
+        u32 g0 = gsum[0][tid], g1 = NG > 1 ? gsum[1][tid] : 0u, g2 = NG > 2 ? gsum[2][tid] : 0u,
+            g3 = NG > 3 ? gsum[3][tid] : 0u;
         u32 tot = g0 + g1 + g2 + g3;
         // exclusive scan over 256 digit totals within the first 8 warps
         u32 x = tot;
@@ -146,12 +151,12 @@ __device__ __forceinline__ void block_pass(const ET* __restrict__ Ein, ET* __res
 // Stable sort of the list in buf[cur] (m entries, local id in the low 16
 // bits) by the coordinate array Pd, ping-ponging between buf0 and buf1;
 // digits constant over the list are skipped.  Returns the new cur.
-template <typename ET>
+template <int NT, typename ET>
 __device__ __forceinline__ int list_sort_dim(ET* buf0, ET* buf1, int cur, int m, const float* Pd, unsigned short (*cnt)[256],
                              u32 (*gsum)[256], u32* scratch) {
     const int tid = threadIdx.x;
     u32 x_and = 0xffffffffu, x_or = 0u;
-    for (int p = tid; p < m; p += kSubThreads) {
+    for (int p = tid; p < m; p += NT) {
         const u32 kk = flip_key(Pd[p]);
         x_and &= kk;
         x_or |= kk;
@@ -163,12 +168,12 @@ __device__ __forceinline__ int list_sort_dim(ET* buf0, ET* buf1, int cur, int m,
     // (tid >> 3) == 4 * warp for every lane in the next cnt[warp] address)
     __syncthreads();
     u32 vary = 0;
-    for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
+    for (int w = 0; w < (NT / 32); ++w) vary |= scratch[32 + w];
     __syncthreads();
     for (int q = 0; q < 4; ++q) {
         if (((vary >> (8 * q)) & 255u) == 0) continue;
         const int sh = 8 * q;
-        block_pass(cur ? buf1 : buf0, cur ? buf0 : buf1, m,
+        block_pass<NT>(cur ? buf1 : buf0, cur ? buf0 : buf1, m,
                    [&](u32 e) { return (flip_key(Pd[e & 0xffffu]) >> sh) & 255u; }, cnt, gsum, scratch);
         cur ^= 1;
     }
@@ -195,16 +200,16 @@ __device__ __forceinline__ bool chain_less(u32 a, u32 b, const float* P, int ldP
     return a < b;  // local ids are in input order
 }
 
-template <typename ET>
+template <int NT, typename ET>
 __device__ __forceinline__ int entry_order(ET* buf0, ET* buf1, int m, const float* P, int ldP, const Chain& ch,
                            unsigned short (*cnt)[256], u32 (*gsum)[256], u32* scratch) {
     if (ch.m == 0) return 0;
     const float* P0 = P + (size_t)ch.d[0] * ldP;
-    int cur = list_sort_dim(buf0, buf1, 0, m, P0, cnt, gsum, scratch);
+    int cur = list_sort_dim<NT>(buf0, buf1, 0, m, P0, cnt, gsum, scratch);
     if (ch.m == 1) return cur;
     ET* L = cur ? buf1 : buf0;
     int longrun = 0;
-    for (int p = threadIdx.x; p + 1 < m; p += kSubThreads) {
+    for (int p = threadIdx.x; p + 1 < m; p += NT) {
         const u32 kp = flip_key(P0[L[p] & 0xffffu]);
         if (flip_key(P0[L[p + 1] & 0xffffu]) != kp) continue;           // no tie at p
         if (p > 0 && flip_key(P0[L[p - 1] & 0xffffu]) == kp) continue;  // not the run's start
@@ -225,11 +230,11 @@ __device__ __forceinline__ int entry_order(ET* buf0, ET* buf1, int m, const floa
         }
     }
     if (!__syncthreads_or(longrun)) return cur;
-    for (int p = threadIdx.x; p < m; p += kSubThreads) buf0[p] = (ET)p;
+    for (int p = threadIdx.x; p < m; p += NT) buf0[p] = (ET)p;
     __syncthreads();
     cur = 0;
     for (int f = (int)ch.m - 1; f >= 0; --f)
-        cur = list_sort_dim(buf0, buf1, cur, m, P + (size_t)ch.d[f] * ldP, cnt, gsum, scratch);
+        cur = list_sort_dim<NT>(buf0, buf1, cur, m, P + (size_t)ch.d[f] * ldP, cnt, gsum, scratch);
     return cur;
 }
 
@@ -310,7 +315,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
         Chain ch;
         if (a.mode == kRoundRobin) rr_chain(a.lam0 - 1, k, ch);
         else widest_chain(make_geom(a.n, a.lam0 - 1).Fl + (j >> 1), k, a.split_dims, ch);
-        cur = entry_order(E[0], E[1], m, P, M, ch, cnt, gsum, scratch);
+        cur = entry_order<kSubThreads>(E[0], E[1], m, P, M, ch, cnt, gsum, scratch);
     }
     for (int lam = a.lam0; lam <= a.L - 2; ++lam) {
         const LevelGeom g = make_geom(a.n, lam);
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
         for (int q = 0; q < 4; ++q) {
             if (((vary >> (8 * q)) & 255u) == 0) continue;
             const int sh = 8 * q;
-            block_pass(E[cur], E[cur ^ 1], mc, [&](u32 e) { return (key_of(e) >> sh) & 255u; }, cnt, gsum,
+            block_pass<kSubThreads>(E[cur], E[cur ^ 1], mc, [&](u32 e) { return (key_of(e) >> sh) & 255u; }, cnt, gsum,
                        scratch);
             cur ^= 1;
             moved = true;
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
         if (moved && dl > 0) {
             for (int q = 0; q * 8 < dl; ++q) {
                 const int sh = 16 + 8 * q;
-                block_pass(E[cur], E[cur ^ 1], mc, [&](u32 e) { return (e >> sh) & 255u; }, cnt, gsum, scratch);
+                block_pass<kSubThreads>(E[cur], E[cur ^ 1], mc, [&](u32 e) { return (e >> sh) & 255u; }, cnt, gsum, scratch);
                 cur ^= 1;
             }
         }
@@ -460,13 +465,13 @@ size_t subtree_rr_smem_bytes(int b, int k) {
     size_t nloc = ((size_t)1 << (b - 2));             // segments at the deepest block level
     // level tables + node table (after the chain sorts) alias the sort scratch
     size_t tables = sizeof(unsigned short) * 3 * (nloc + 8) + sizeof(unsigned short) * Mp;
-    size_t sortscr = sizeof(unsigned short) * kSubWarps * 256 + sizeof(u32) * 4 * 256;
+    size_t sortscr = sizeof(unsigned short) * kRRWarps * 256 + sizeof(u32) * 4 * 256;
     bytes += tables > sortscr ? tables : sortscr;
     bytes += sizeof(u64) * 64;
     return (bytes + 15) & ~(size_t)15;
 }
 
-__global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs a) {
+__global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef unsigned short u16;
     const int M = a.M, k = a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -490,9 +495,9 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
     u16* rtb = pot + nmax + 8;               // right elements of the earlier segments
     u16* ntab = rtb + nmax + 8;              // local id of the point of every node, heap order
     unsigned short(*cnt)[256] = reinterpret_cast<unsigned short(*)[256]>(sp);
-    u32(*gsum)[256] = reinterpret_cast<u32(*)[256]>(sp + sizeof(unsigned short) * kSubWarps * 256);
+    u32(*gsum)[256] = reinterpret_cast<u32(*)[256]>(sp + sizeof(unsigned short) * kRRWarps * 256);
     size_t tables = sizeof(u16) * 3 * ((size_t)nmax + 8) + sizeof(u16) * Mp;
-    size_t sortscr = sizeof(unsigned short) * kSubWarps * 256 + sizeof(u32) * 4 * 256;
+    size_t sortscr = sizeof(unsigned short) * kRRWarps * 256 + sizeof(u32) * 4 * 256;
     u32* scratch = reinterpret_cast<u32*>(sp + (tables > sortscr ? tables : sortscr));
     u64* scratch64 = reinterpret_cast<u64*>(scratch);
 
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
     const u32* vin = src + (u64)k * a.stride;
     const int e = (a.lam0 - 1) % k;  // dimension of the entry order
     u16* ident = LB + (a.entry_sorted ? Lo[e] : Lo[0]);
-    for (int lid = tid; lid < m; lid += kSubThreads) {
+    for (int lid = tid; lid < m; lid += kRRThreads) {
         for (int c = 0; c < k; ++c) P[c * Mp + lid] = __uint_as_float(src[(u64)c * a.stride + lid]);
         ident[lid] = (u16)lid;
         state[lid] = 0;
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         // buffers out as the remaining lists and the spares
         Chain ch;
         rr_chain(a.lam0 - 1, k, ch);
-        const int r = entry_order(LB + Lo[0], LB + Lo[1], m, P, Mp, ch, cnt, gsum, scratch);
+        const int r = entry_order<kRRThreads>(LB + Lo[0], LB + Lo[1], m, P, Mp, ch, cnt, gsum, scratch);
         const int res = r * Mp;  // list buffers are still in order here
         int q = 0;
         for (int d = 0; d <= k + 1; ++d) {
@@ -538,7 +543,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         const int dprev = (e + q - 1) % k;
         const float* Pd = P + d * Mp;
         u32 x_and = 0xffffffffu, x_or = 0u;
-        for (int p = tid; p < m; p += kSubThreads) {
+        for (int p = tid; p < m; p += kRRThreads) {
             u32 kk = flip_key(Pd[p]);
             x_and &= kk;
             x_or |= kk;
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         scratch[32 + (tid >> 5)] = x_and ^ x_or;  // every lane stores the warp-uniform value (NVVM 12.9, above)
         __syncthreads();
         u32 vary = 0;
-        for (int w = 0; w < kSubWarps; ++w) vary |= scratch[32 + w];
+        for (int w = 0; w < kRRWarps; ++w) vary |= scratch[32 + w];
         __syncthreads();
         const u16* in = LB + Lo[dprev];
         u16* outA = LB + Lo[d];
@@ -558,12 +563,12 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
             if (((vary >> (8 * b)) & 255u) == 0) continue;
             u16* out = (npass & 1) ? outB : outA;
             const int sh = 8 * b;
-            block_pass(in, out, m, [&](u32 lid) { return (flip_key(Pd[lid]) >> sh) & 255u; }, cnt, gsum, scratch);
+            block_pass<kRRThreads>(in, out, m, [&](u32 lid) { return (flip_key(Pd[lid]) >> sh) & 255u; }, cnt, gsum, scratch);
             in = out;
             ++npass;
         }
         if (npass == 0) {
-            for (int p = tid; p < m; p += kSubThreads) outA[p] = in[p];
+            for (int p = tid; p < m; p += kRRThreads) outA[p] = in[p];
             __syncthreads();
         } else if (npass & 1) {
             // result in outA == Lst[d]
@@ -611,7 +616,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         // tables + right elements of the earlier segments (one scan)
         {
             u32 v = 0;
-            const int per = (nloc + kSubThreads - 1) / kSubThreads;  // <= 2
+            const int per = (nloc + kRRThreads - 1) / kRRThreads;  // <= 2
             u32 rs[2] = {0u, 0u};
             for (int i = 0; i < per; ++i) {
                 const int t = tid * per + i;
@@ -637,7 +642,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         // (1) the active list: nodes, sides, child segments; its own split
         u16* A = LB + Lo[ad];
         u16* tmpA = LB + Lo[k];
-        for (int p = tid; p < mc; p += kSubThreads) {
+        for (int p = tid; p < mc; p += kRRThreads) {
             const u32 lid = A[p];
             const u32 t = state[lid] >> 2;
             const u32 lb = lbt[t];
@@ -773,12 +778,12 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
             const int dsto = freeb[--nfree];
             u16* dst = LB + dsto;
             const u16* X = LB + Lo[d];
-            for (int p = tid; p < m - (nloc - 1); p += kSubThreads) dst[X[p]] = (u16)p;
+            for (int p = tid; p < m - (nloc - 1); p += kRRThreads) dst[X[p]] = (u16)p;
             rko[d] = dsto;
             if (Lo[d] != memo) freeb[nfree++] = Lo[d];
             __syncthreads();
         }
-        for (int t = warp; t < nloc; t += kSubWarps) {
+        for (int t = warp; t < nloc; t += kRRWarps) {
             const u64 Jt = J0 + t;
             const u32 sb = (u32)(seg_begin_l(sh, Jt) - lb0);
             const u32 sz = seg_size_l(sh, Jt);
@@ -840,9 +845,9 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_rr_kernel(SubtreeArgs 
         u64 cntn = 1ull << dl;
         if (first + cntn > a.n) cntn = a.n - first;
         const u32 h0 = (1u << dl) - 1u;
-        for (u32 i = tid; i < (u32)cntn; i += kSubThreads) a.perm[first + i] = vin[ntab[h0 + i]];
+        for (u32 i = tid; i < (u32)cntn; i += kRRThreads) a.perm[first + i] = vin[ntab[h0 + i]];
         float* dst = a.out_pts + first * (u64)k;
-        for (u32 i = tid; i < (u32)cntn * (u32)k; i += kSubThreads) {
+        for (u32 i = tid; i < (u32)cntn * (u32)k; i += kRRThreads) {
             const u32 t = i / (u32)k, c = i - t * (u32)k;
             dst[i] = P[c * Mp + ntab[h0 + t]];
         }
@@ -878,7 +883,7 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entr
     if (bp.mode == kRoundRobin && lam0 >= bp.k) {
         size_t sm = subtree_rr_smem_bytes(bp.b, bp.k);
         cudaFuncSetAttribute(subtree_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        subtree_rr_kernel<<<grid, kSubThreads, sm, st>>>(a);
+        subtree_rr_kernel<<<grid, kRRThreads, sm, st>>>(a);
         return;
     }
     size_t sm = subtree_smem_bytes(bp.b, bp.k, bp.mode);

@@ -239,3 +239,44 @@ def test_sharded_build_matches_single_gpu(n, k, world, kind):
     assert torch.equal(perm, want_perm)
     assert torch.equal(out, want_out)
     assert oracle.build_rr(pts).tolist()[:1000] == perm.cpu().numpy().view(np.uint32).tolist()[:1000]
+
+
+@pytest.mark.parametrize("n", [8193, 70001, 300001, 1 << 20])
+def test_sort_algorithm_matches_oracle(n):
+    """The literal per-level radix-sort path (LBKD_ALGO=sort: onesweep digit
+    passes over every segment) is bit-exact too."""
+    from paper_2211_00120_b200 import _native
+
+    _native.set_algorithm("sort")
+    try:
+        assert _native.get_algorithm() == "sort"
+        for kind, k in (("uniform", 3), ("ties", 2), ("clustered", 4)):
+            pts = datagen.make(kind, n, k, seed=n + k)
+            _, perm = gpu_rr(pts)
+            assert np.array_equal(perm, oracle.build_rr(pts)), (kind, n, k)
+            _, perm, dims = gpu_widest(pts)
+            wp, wd = oracle.build_widest(pts)
+            assert np.array_equal(perm, wp) and np.array_equal(dims, wd), (kind, n, k)
+    finally:
+        _native.set_algorithm("select")
+
+
+def test_profile_classes_cover_the_build():
+    """lbkd_profile_kernel accounts every kernel of a profiled build."""
+    from paper_2211_00120_b200 import _native
+
+    pts = datagen.uniform(1 << 20, 3, seed=5)
+    d = torch.from_numpy(pts).cuda()
+    kd.build_round_robin_cuda(d)
+    _native.set_profile(True)
+    try:
+        kd.build_round_robin_cuda(d)
+        torch.cuda.synchronize()
+        prof = _native.profile_kernels()
+    finally:
+        _native.set_profile(False)
+    assert {"init", "hist", "pick", "filter", "select", "partition", "subtree"} <= set(prof)
+    n_launch = sum(v[0] for v in prof.values())
+    assert n_launch == kd.builder.last_launch_count(0)
+    part = prof["partition"]
+    assert part[1] > 0 and part[2] > 0
