@@ -571,7 +571,7 @@ constexpr int kPThreads = 256;
 constexpr int kPRows = kSub / 32;
 
 template <int KMAX>
-__global__ void __launch_bounds__(kPThreads) sel_part_kernel(SelArgs a, int T) {
+__global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 3 : 1) sel_part_kernel(SelArgs a, int T) {
     const int lane = threadIdx.x & 31;
     const int k = a.k, A = k + 1;
     const LevelGeom& g = a.g;
@@ -755,9 +755,17 @@ void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
     u64 grid = (nsub + per_cta - 1) / per_cta;
     const u64 cap = 148ull * 8;
     if (grid > cap) grid = cap;
-    if (a.k <= 4) sel_part_kernel<4><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
-    else if (a.k <= 8) sel_part_kernel<8><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
-    else sel_part_kernel<16><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
+    // register-resident subtile: (KMAX + 1) x 8 words per lane
+    switch (a.k) {
+        case 1: sel_part_kernel<1><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
+        case 2: sel_part_kernel<2><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
+        case 3: sel_part_kernel<3><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
+        case 4: sel_part_kernel<4><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
+        default:
+            if (a.k <= 8) sel_part_kernel<8><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
+            else sel_part_kernel<16><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
+            break;
+    }
 }
 
 }  // namespace lbkd
