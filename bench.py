@@ -291,29 +291,44 @@ def main():
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
 
-    # ---- end to end through the C-ABI with host buffers
+    # ---- end to end through the C-ABI with HOST buffers: every step copies
+    # its pinned input to the device, builds, and copies the level-order
+    # points + permutation back (lbkd_build_rr_host: consecutive steps overlap
+    # their copies with the neighbouring builds on separate copy engines)
     h_out = torch.empty((n, k), dtype=torch.float32).pin_memory() if have_input else None
     h_perm = torch.empty(n, dtype=torch.int32).pin_memory() if have_input else None
     d_in = torch.empty_like(d_pts) if have_input else None
 
     def e2e_step():
-        if have_input:
+        if sharded:
+            if have_input:
+                d_in.copy_(h_pts, non_blocking=True)
+            build(d_in, out, perm)
+            if have_input:
+                h_out.copy_(shard_bufs["out"], non_blocking=True)
+                h_perm.copy_(shard_bufs["perm"], non_blocking=True)
+        elif args.mode == "rr":
+            kd.builder.build_round_robin_host(h_pts, h_out, h_perm, device=local)
+        else:
             d_in.copy_(h_pts, non_blocking=True)
-        build(d_in, out, perm)
-        if have_input:
-            res_out = shard_bufs["out"] if sharded else out
-            res_perm = shard_bufs["perm"] if sharded else perm
-            h_out.copy_(res_out, non_blocking=True)
-            h_perm.copy_(res_perm, non_blocking=True)
+            build(d_in, out, perm)
+            h_out.copy_(out, non_blocking=True)
+            h_perm.copy_(perm, non_blocking=True)
+
+    def e2e_join():
+        if not sharded and args.mode == "rr":
+            kd.builder.host_join(device=local, sync=False)
 
     for _ in range(args.warmup):
         e2e_step()
+    e2e_join()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
         e2e_step()
+    e2e_join()
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -322,12 +337,15 @@ def main():
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_t.item())
 
-    # ---- correctness spot check of the benchmarked output (permutation)
+    # ---- correctness spot check of the benchmarked output (the host copy
+    # of the last e2e step: a permutation, and the same as the device build)
     ok = None
     if rank == 0:
         res_perm = shard_bufs["perm"] if sharded else perm
         p = res_perm.cpu().numpy().view(np.uint32)
         ok = bool(np.array_equal(np.bincount(p, minlength=n), np.ones(n, dtype=np.int64)))
+        if h_perm is not None:
+            ok = ok and bool(np.array_equal(h_perm.numpy().view(np.uint32), p))
 
     if rank == 0:
         total_pts = n * args.steps

@@ -78,6 +78,20 @@ int lbkd_build_rr_trace(lbkd_ctx *ctx, const float *d_points, float *d_points_ou
 int lbkd_build_widest_trace(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int64_t n, int k,
                             uint32_t *d_perm, uint8_t *d_split_dims, uint32_t *d_trace, void *stream);
 
+/* Pipelined builds from / to HOST memory (pinned for overlap): the same
+ * contract as lbkd_build_rr / lbkd_build_widest with host pointers.  Each
+ * call enqueues H2D -> build -> D2H on three internal streams forked from
+ * `stream` and returns; consecutive calls overlap (two device buffer sets
+ * alternate).  Host buffers of a call must stay untouched until
+ * lbkd_host_join, which makes `stream` wait for every outstanding call and,
+ * with sync != 0, waits on the host and returns LBKD_ENONFINITE if any input
+ * since the last join held a NaN or infinity. */
+int lbkd_build_rr_host(lbkd_ctx *ctx, const float *h_points, float *h_points_out, int64_t n, int k,
+                       uint32_t *h_perm, void *stream);
+int lbkd_build_widest_host(lbkd_ctx *ctx, const float *h_points, float *h_points_out, int64_t n, int k,
+                           uint32_t *h_perm, uint8_t *h_split_dims, void *stream);
+int lbkd_host_join(lbkd_ctx *ctx, void *stream, int sync);
+
 /* Multi-device sharding (no reference counterpart -- the
  * reference is single-process).  After the top `top_levels` levels the
  * 2^top_levels subtrees are independent:

@@ -33,6 +33,7 @@ EXPORTED = (
     "lbkd_set_profile", "lbkd_profile_read",
     "lbkd_build_rr_top", "lbkd_build_rr_sub",
     "lbkd_profile_kernel", "lbkd_set_algorithm", "lbkd_get_algorithm",
+    "lbkd_build_rr_host", "lbkd_build_widest_host", "lbkd_host_join",
 )
 
 # kernel classes of lbkd_profile_kernel
@@ -108,6 +109,12 @@ def load():
         lib.lbkd_set_algorithm.restype = i32
         lib.lbkd_get_algorithm.argtypes = [vp]
         lib.lbkd_get_algorithm.restype = i32
+        lib.lbkd_build_rr_host.argtypes = [vp, vp, vp, i64, i32, vp, vp]
+        lib.lbkd_build_rr_host.restype = i32
+        lib.lbkd_build_widest_host.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp]
+        lib.lbkd_build_widest_host.restype = i32
+        lib.lbkd_host_join.argtypes = [vp, vp, i32]
+        lib.lbkd_host_join.restype = i32
         lib.lbkd_strerror.argtypes = [i32]
         lib.lbkd_strerror.restype = ctypes.c_char_p
         lib.lbkd_last_cuda_error.argtypes = []

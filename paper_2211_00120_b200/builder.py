@@ -189,6 +189,37 @@ def build_round_robin_cuda(points, *, out=None, perm=None, stream=None, check_fi
     return out, perm
 
 
+def build_round_robin_host(points, out, perm, *, device: int = 0, stream=None) -> None:
+    """Pipelined build from HOST memory through lbkd_build_rr_host.
+
+    ``points`` / ``out``: (n, k) float32 CPU tensors, ``perm``: (n,) int32 CPU
+    tensor, all pinned for overlap.  The call only enqueues H2D -> build ->
+    D2H; consecutive calls overlap their copies with the previous build.  The
+    buffers are valid after :func:`host_join`.
+    """
+    torch = _torch()
+    for t in (points, out, perm):
+        if t.device.type != "cpu" or not t.is_contiguous():
+            raise ValueError("host buffers must be contiguous CPU tensors")
+    n, k = points.shape
+    lib = _native.load()
+    ctx = _native.context(device)
+    with torch.cuda.device(device):
+        rc = lib.lbkd_build_rr_host(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(),
+                                    _stream_ptr(torch, stream))
+    _raise_for(rc, "lbkd_build_rr_host", n, k)
+
+
+def host_join(*, device: int = 0, stream=None, sync: bool = True) -> None:
+    """Wait for every pipelined host build (lbkd_host_join); raises the
+    reference's ValueError if any of their inputs was non-finite."""
+    torch = _torch()
+    lib = _native.load()
+    with torch.cuda.device(device):
+        rc = lib.lbkd_host_join(_native.context(device), _stream_ptr(torch, stream), 1 if sync else 0)
+    _raise_for(rc, "lbkd_host_join", 0, 0)
+
+
 def _raise_for(rc: int, where: str, n: int, k: int, widest: bool = False) -> None:
     if rc == _native.LBKD_OK:
         return

@@ -40,6 +40,19 @@ struct lbkd_ctx {
     int ctr = 0;
     int64_t launches = 0;
     int algo = 0;      // 0: select + partition (default), 1: per-level sort
+    int err_sticky = 0;  // pipelined host builds: the non-finite flag accumulates until lbkd_host_join
+    // pipelined host-buffer builds (lbkd_build_*_host): two device buffer
+    // sets alternate, H2D / build / D2H run on three streams
+    struct HostPipe {
+        float* d_in[2] = {nullptr, nullptr};
+        float* d_out[2] = {nullptr, nullptr};
+        u32* d_perm[2] = {nullptr, nullptr};
+        uint8_t* d_dims[2] = {nullptr, nullptr};
+        size_t cap = 0;
+        cudaStream_t s_h2d = nullptr, s_build = nullptr, s_d2h = nullptr;
+        cudaEvent_t start = nullptr, h2d_done[2], build_done[2], d2h_done[2];
+        int slot = 0, pending = 0;
+    } hp;
     size_t cap_cand = 0, cap_ptiles = 0, cap_piv = 0;
     // grow-only device allocations
     size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_w = 0, cap_copy = 0;
@@ -323,7 +336,7 @@ static int begin_build(lbkd_ctx* c, int k, cudaStream_t st) {
     }
     c->k_last = k;
     c->ctr = 0;
-    CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
+    if (!c->err_sticky) CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
     return LBKD_OK;
 }
 
@@ -515,7 +528,114 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     return end_build(c, st);
 }
 
+// ---------------------------------------------------------------------------
+// pipelined builds from / to HOST buffers (pinned for overlap): call i's
+// H2D runs while build i-1 computes and D2H of call i-1 drains while build i
+// computes; a build only waits for the buffers it reuses
+// ---------------------------------------------------------------------------
+static int host_pipe_ensure(lbkd_ctx* c, size_t n, int k) {
+    auto& h = c->hp;
+    if (!h.s_h2d) {
+        CK(cudaStreamCreateWithFlags(&h.s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h.s_build, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h.s_d2h, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h.start, cudaEventDisableTiming));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&h.h2d_done[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h.build_done[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h.d2h_done[i], cudaEventDisableTiming));
+            CK(cudaEventRecord(h.build_done[i], h.s_build));
+            CK(cudaEventRecord(h.d2h_done[i], h.s_d2h));
+        }
+    }
+    const size_t need = n * (size_t)k;
+    if (need > h.cap) {
+        CK(cudaDeviceSynchronize());
+        size_t dummy = 0;
+        int rc;
+        for (int i = 0; i < 2; ++i) {
+            if ((rc = grow(h.d_in[i], dummy, need))) return rc;
+            if ((rc = grow(h.d_out[i], dummy, need))) return rc;
+            if ((rc = grow(h.d_perm[i], dummy, n))) return rc;
+            if ((rc = grow(h.d_dims[i], dummy, n))) return rc;
+        }
+        h.cap = need;
+    }
+    return LBKD_OK;
+}
+
+static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in, int k, u32* d_perm,
+                 uint8_t* d_dims, u32* d_trace, int mode, cudaStream_t st);
+
+static int build_host(lbkd_ctx* c, const float* h_points, float* h_out, int64_t n_in, int k, u32* h_perm,
+                      uint8_t* h_dims, int mode, cudaStream_t st) {
+    int rc = check_args(c, n_in, k, mode);
+    if (rc) return rc;
+    if (n_in == 0) return LBKD_OK;
+    if (!h_points || !h_out) return LBKD_EINVAL_SHAPE;
+    CK(cudaSetDevice(c->device));
+    const size_t n = (size_t)n_in;
+    if ((rc = host_pipe_ensure(c, n, k))) return rc;
+    auto& h = c->hp;
+    const int s = h.slot;
+    h.slot ^= 1;
+    // fork from the caller's stream
+    CK(cudaEventRecord(h.start, st));
+    CK(cudaStreamWaitEvent(h.s_h2d, h.start, 0));
+    // d_in[s] is free once the build that read it (two calls ago) is done
+    CK(cudaStreamWaitEvent(h.s_h2d, h.build_done[s], 0));
+    CK(cudaMemcpyAsync(h.d_in[s], h_points, n * k * sizeof(float), cudaMemcpyHostToDevice, h.s_h2d));
+    CK(cudaEventRecord(h.h2d_done[s], h.s_h2d));
+    CK(cudaStreamWaitEvent(h.s_build, h.h2d_done[s], 0));
+    CK(cudaStreamWaitEvent(h.s_build, h.d2h_done[s], 0));  // d_out[s] drained
+    const int check = c->check;
+    c->check = 0;
+    c->err_sticky = 1;
+    rc = build(c, h.d_in[s], h.d_out[s], n_in, k, h.d_perm[s], h.d_dims[s], nullptr, mode, h.s_build);
+    c->check = check;
+    if (rc) return rc;
+    CK(cudaEventRecord(h.build_done[s], h.s_build));
+    CK(cudaStreamWaitEvent(h.s_d2h, h.build_done[s], 0));
+    CK(cudaMemcpyAsync(h_out, h.d_out[s], n * k * sizeof(float), cudaMemcpyDeviceToHost, h.s_d2h));
+    if (h_perm) CK(cudaMemcpyAsync(h_perm, h.d_perm[s], n * sizeof(u32), cudaMemcpyDeviceToHost, h.s_d2h));
+    if (h_dims && mode == kWidest)
+        CK(cudaMemcpyAsync(h_dims, h.d_dims[s], n * sizeof(uint8_t), cudaMemcpyDeviceToHost, h.s_d2h));
+    CK(cudaEventRecord(h.d2h_done[s], h.s_d2h));
+    h.pending = 1;
+    return LBKD_OK;
+}
+
+// join: the caller's stream waits for every pipelined build; with sync != 0
+// also waits on the host and reports non-finite input seen since the last join
+static int host_join(lbkd_ctx* c, cudaStream_t st, int sync) {
+    auto& h = c->hp;
+    if (!h.s_h2d) return LBKD_OK;
+    CK(cudaSetDevice(c->device));
+    for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(st, h.d2h_done[i], 0));
+    if (!sync) return LBKD_OK;
+    CK(cudaMemcpyAsync(c->h_err, c->bf.err, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const u32 e = c->h_err[0];
+    CK(cudaMemsetAsync(c->bf.err, 0, sizeof(u32) * 4, st));
+    CK(cudaStreamSynchronize(st));
+    c->err_sticky = 0;
+    h.pending = 0;
+    return e ? LBKD_ENONFINITE : LBKD_OK;
+}
+
 extern "C" {
+
+int lbkd_build_rr_host(lbkd_ctx* c, const float* h_points, float* h_out, int64_t n, int k, uint32_t* h_perm,
+                       void* stream) {
+    return build_host(c, h_points, h_out, n, k, h_perm, nullptr, kRoundRobin, (cudaStream_t)stream);
+}
+
+int lbkd_build_widest_host(lbkd_ctx* c, const float* h_points, float* h_out, int64_t n, int k, uint32_t* h_perm,
+                           uint8_t* h_split_dims, void* stream) {
+    return build_host(c, h_points, h_out, n, k, h_perm, h_split_dims, kWidest, (cudaStream_t)stream);
+}
+
+int lbkd_host_join(lbkd_ctx* c, void* stream, int sync) { return c ? host_join(c, (cudaStream_t)stream, sync) : LBKD_EINVAL_SHAPE; }
 
 int lbkd_create(lbkd_ctx** out, int device) {
     if (!out) return LBKD_EINVAL_SHAPE;
@@ -539,6 +659,22 @@ int lbkd_create(lbkd_ctx** out, int device) {
 void lbkd_destroy(lbkd_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->hp.s_h2d) {
+        cudaDeviceSynchronize();
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(c->hp.d_in[i]);
+            cudaFree(c->hp.d_out[i]);
+            cudaFree(c->hp.d_perm[i]);
+            cudaFree(c->hp.d_dims[i]);
+            cudaEventDestroy(c->hp.h2d_done[i]);
+            cudaEventDestroy(c->hp.build_done[i]);
+            cudaEventDestroy(c->hp.d2h_done[i]);
+        }
+        cudaEventDestroy(c->hp.start);
+        cudaStreamDestroy(c->hp.s_h2d);
+        cudaStreamDestroy(c->hp.s_build);
+        cudaStreamDestroy(c->hp.s_d2h);
+    }
     for (int i = 0; i < 2; ++i) {
         cudaFree(c->bf.w[i]);
         cudaFree(c->bf.boxes[i]);

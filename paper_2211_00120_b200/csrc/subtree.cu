@@ -471,11 +471,14 @@ size_t subtree_rr_smem_bytes(int b, int k) {
     return (bytes + 15) & ~(size_t)15;
 }
 
+// KT, MPT: compile-time k and padded capacity for the common shapes (all
+// shared-memory offsets become immediates); 0 = taken from the arguments
+template <int KT, int MPT>
 __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef unsigned short u16;
-    const int M = a.M, k = a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int Mp = (M + 8) & ~7;
+    const int M = MPT ? MPT - 1 : a.M, k = KT ? KT : a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int Mp = MPT ? MPT : (M + 8) & ~7;
     unsigned char* sp = smem_raw;
     float* P = reinterpret_cast<float*>(sp);
     sp += sizeof(float) * (size_t)k * Mp;
@@ -882,8 +885,15 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entr
     unsigned grid = (unsigned)(1ull << (lam0 - bp.lroot));
     if (bp.mode == kRoundRobin && lam0 >= bp.k) {
         size_t sm = subtree_rr_smem_bytes(bp.b, bp.k);
-        cudaFuncSetAttribute(subtree_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        subtree_rr_kernel<<<grid, kRRThreads, sm, st>>>(a);
+        const int Mp = (a.M + 8) & ~7;
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            kern<<<grid, kRRThreads, sm, st>>>(a);
+        };
+        if (bp.k == 3 && Mp == 4096) go(subtree_rr_kernel<3, 4096>);
+        else if (bp.k == 2 && Mp == 4096) go(subtree_rr_kernel<2, 4096>);
+        else if (bp.k == 4 && Mp == 2048) go(subtree_rr_kernel<4, 2048>);
+        else go(subtree_rr_kernel<0, 0>);
         return;
     }
     size_t sm = subtree_smem_bytes(bp.b, bp.k, bp.mode);

@@ -280,3 +280,30 @@ def test_profile_classes_cover_the_build():
     assert n_launch == kd.builder.last_launch_count(0)
     part = prof["partition"]
     assert part[1] > 0 and part[2] > 0
+
+
+def test_pipelined_host_builds():
+    """lbkd_build_rr_host: consecutive host-buffer builds overlap and each
+    returns its own exact result; a non-finite input is reported at join."""
+    from paper_2211_00120_b200.builder import build_round_robin_host, host_join
+
+    n, k = 300001, 3
+    inputs = [datagen.make(kind, n, k, seed=s) for s, kind in enumerate(("uniform", "ties", "clustered"))]
+    hin = [torch.from_numpy(p).pin_memory() for p in inputs]
+    hout = [torch.empty((n, k), dtype=torch.float32).pin_memory() for _ in inputs]
+    hperm = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in inputs]
+    for i in range(len(inputs)):
+        build_round_robin_host(hin[i], hout[i], hperm[i])
+    host_join()
+    for i, p in enumerate(inputs):
+        want = oracle.build_rr(p)
+        assert np.array_equal(hperm[i].numpy().view(np.uint32), want), i
+        assert np.array_equal(hout[i].numpy(), p[want.astype(np.int64)]), i
+    bad = inputs[0].copy()
+    bad[7, 1] = np.nan
+    hb = torch.from_numpy(bad).pin_memory()
+    build_round_robin_host(hb, hout[0], hperm[0])
+    with pytest.raises(ValueError, match="finite"):
+        host_join()
+    build_round_robin_host(hin[1], hout[1], hperm[1])  # the flag was cleared
+    host_join()
