@@ -40,6 +40,7 @@ struct lbkd_ctx {
     int ctr = 0;
     int64_t launches = 0;
     int algo = 0;      // 0: select + partition (default), 1: per-level sort
+    int subtree_sel = -1;  // in-CTA phase: -1 default per mode, 1 selection (subtree_sel.cu), 0 lists
     int err_sticky = 0;  // pipelined host builds: the non-finite flag accumulates until lbkd_host_join
     // pipelined host-buffer builds (lbkd_build_*_host): two device buffer
     // sets alternate, H2D / build / D2H run on three streams
@@ -102,14 +103,19 @@ static void prof_end(lbkd_ctx* c, cudaStream_t st, int cls, double bytes) {
 }
 
 static int choose_bits(int k, int mode) {
-    const size_t limit = 227 * 1024 - 256;  // dynamic + a little static smem
-    // round-robin: two CTAs of the presorted-list kernel per SM (<= 8 x 512
-    // points each); widest: one CTA of the general kernel per SM
-    const size_t rr_limit = 113 * 1024;
-    for (int b = (mode == kRoundRobin ? 12 : 13); b >= 9; --b)
-        if (subtree_smem_bytes(b, k, mode) <= limit &&
-            (mode != kRoundRobin || subtree_rr_smem_bytes(b, k) <= rr_limit))
-            return b;
+    const size_t limit = 227 * 1024 - 256;  // one CTA per SM (general / trace kernel)
+    const size_t two = 113 * 1024;           // two CTAs per SM
+    const size_t four = 56 * 1024;           // four CTAs per SM
+    // round-robin: presorted-list kernel, 2 CTAs/SM (b <= 12); widest k <= 4:
+    // selection kernel, 4 CTAs/SM (b <= 11); widest k > 4: general kernel.
+    // Every kernel that may run for (b, k, mode) must fit.
+    const bool wsel = mode == kWidest && k <= 4;
+    for (int b = wsel ? 11 : 12; b >= 9; --b) {
+        if (subtree_smem_bytes(b, k, mode) > limit) continue;
+        if (mode == kRoundRobin && subtree_rr_smem_bytes(b, k) > two) continue;
+        if (subtree_sel_smem_bytes(b, k) > (wsel ? four : limit)) continue;
+        return b;
+    }
     return -1;
 }
 
@@ -433,6 +439,7 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.perm = d_perm ? d_perm : c->perm_scratch;
     bp.split_dims = d_dims ? d_dims : c->dims_scratch;
     bp.dbg = d_trace;
+    bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : (mode == kWidest ? 1 : 0);
     if ((rc = begin_build(c, k, st))) return rc;
     if ((rc = prologue(c, bp, lam0, st))) return rc;
     if ((rc = run_levels(c, bp, 0, lam0, st))) return rc;
@@ -509,6 +516,7 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     bp.split_dims = c->dims_scratch;
     bp.dbg = nullptr;
     bp.lroot = root_level;
+    bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : 0;
     bp.jroot = (u64)root_index;
     if ((rc = begin_build(c, k, st))) return rc;
     CK(cudaMemcpy2DAsync(c->bf.w[0], c->bf.stride * sizeof(u32), d_sub, (size_t)sub_stride * sizeof(u32),
@@ -652,6 +660,9 @@ int lbkd_create(lbkd_ctx** out, int device) {
     c->device = device;
     const char* algo = getenv("LBKD_ALGO");
     if (algo && strcmp(algo, "sort") == 0) c->algo = 1;
+    const char* sub = getenv("LBKD_SUBTREE");
+    if (sub && strcmp(sub, "lists") == 0) c->subtree_sel = 0;
+    if (sub && strcmp(sub, "sel") == 0) c->subtree_sel = 1;
     *out = c;
     return LBKD_OK;
 }

@@ -86,6 +86,7 @@ struct BuildParams {
     u32* perm;
     uint8_t* split_dims;   // widest only
     u32* dbg;              // optional per-level trace (single-subtree builds)
+    int subtree_sel = 1;   // in-CTA levels by selection (subtree_sel.cu) or by presorted lists
     int lroot = 0;         // sub-build: root node (level, index) of the view;
     u64 jroot = 0;         // the whole tree is (0, 0)
 };
@@ -142,11 +143,34 @@ void launch_pivots(const BuildParams& bp, const Buffers& bf, int l, cudaStream_t
 void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride, int src_par,
                     cudaStream_t st);
 
-// subtree.cu
+// subtree.cu / subtree_sel.cu
+struct SubtreeArgs {
+    u64 n;
+    int L, lam0, k, mode, M;
+    const u32* w[2];          // global-level working set (SoA, in-order)
+    u64 stride;
+    const uint8_t* prev_state;  // plan state of level lam0-1
+    const float* pts;
+    float* out_pts;
+    u32* perm;
+    uint8_t* split_dims;
+    const float* boxes0;  // widest: boxes of level-lam0 nodes [nseg][2k]
+    u32* dbg;
+    u64 jbase;    // global index (level lam0) of the view's first subtree
+    u64 pbase;    // global in-order position of the view's first point
+    int lfirst;   // root level of the view
+    int from_pts; // single-CTA whole-tree build straight from the input
+    int entry_sorted;  // sort path: each subtree arrives in the reference's
+                       // order T(parent); select path: in input order
+    int src_par;       // select path: W[src_par] holds the subtree (else prev_state)
+};
+
 size_t subtree_smem_bytes(int b, int k, int mode);
 size_t subtree_rr_smem_bytes(int b, int k);
 void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entry_sorted, int src_par,
                     cudaStream_t st);
+size_t subtree_sel_smem_bytes(int b, int k);
+void launch_subtree_sel(const SubtreeArgs& a, unsigned grid, int b, cudaStream_t st);
 
 // widest.cu
 void launch_world_bounds(const BuildParams& bp, u32* d_minmax, cudaStream_t st);

@@ -29,26 +29,6 @@ constexpr int kRRWarps = kRRThreads / 32;
 constexpr int kMaxRounds = 8;  // M <= 8 x threads -> at most 8 rounds
 constexpr int kMaxK = 16;
 
-struct SubtreeArgs {
-    u64 n;
-    int L, lam0, k, mode, M;
-    const u32* w[2];          // global-level working set (SoA, in-order)
-    u64 stride;
-    const uint8_t* prev_state;  // plan state of level lam0-1
-    const float* pts;
-    float* out_pts;
-    u32* perm;
-    uint8_t* split_dims;
-    const float* boxes0;  // widest: boxes of level-lam0 nodes [nseg][2k]
-    u32* dbg;
-    u64 jbase;    // global index (level lam0) of the view's first subtree
-    u64 pbase;    // global in-order position of the view's first point
-    int lfirst;   // root level of the view
-    int from_pts; // single-CTA whole-tree build straight from the input
-    int entry_sorted;  // sort path: each subtree arrives in the reference's
-                       // order T(parent); select path: in input order
-    int src_par;       // select path: W[src_par] holds the subtree (else prev_state)
-};
 
 size_t subtree_smem_bytes(int b, int k, int mode) {
     size_t M = ((size_t)1 << b) - 1;
@@ -883,6 +863,12 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entr
     a.entry_sorted = entry_sorted;
     a.src_par = src_par;
     unsigned grid = (unsigned)(1ull << (lam0 - bp.lroot));
+    const bool sel_ok = !bp.dbg && (bp.mode == kRoundRobin || bp.k <= 4);
+    if (sel_ok && (bp.subtree_sel || (bp.mode == kRoundRobin && lam0 < bp.k))) {
+        // per-level selection in shared memory (subtree_sel.cu): any entry order
+        launch_subtree_sel(a, grid, bp.b, st);
+        return;
+    }
     if (bp.mode == kRoundRobin && lam0 >= bp.k) {
         size_t sm = subtree_rr_smem_bytes(bp.b, bp.k);
         const int Mp = (a.M + 8) & ~7;

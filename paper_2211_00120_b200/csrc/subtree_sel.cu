@@ -1,0 +1,625 @@
+// subtree_sel.cu -- the in-CTA levels (lam0 .. L-1) of every level-lam0
+// subtree as per-level pivot SELECTION inside one CTA's shared memory, for
+// both split rules.  Same argument as the global levels (select.cu, DESIGN.md
+// §2): a node's point is the element of rank pivot_off(s) under the node's
+// fixed within-node order T(s) = (c[dim(s)], c[dim(parent)], ..., input
+// index); where its children's points sit is unobservable.  So no list is
+// ever sorted:
+//
+// block phase (segments > 31 points), per level, all threads:
+//   setup   per segment: size, pivot offset (kernels_numba.py:21-46), split
+//           dim (RR: l mod k; widest: first f64 argmax of the node box,
+//           kernels_numba.py:80-110), NB equal-width buckets of the box
+//   hist    every live point -> its segment's bucket (shared atomics)
+//   pick    warp per segment: bucket b* holding rank pivot_off
+//   gather  points of b* -> the segment's candidate list
+//   resolve warp per segment: rank of every candidate under T(s) by
+//           comparison (chain fields and the input index only on ties)
+//           -> the node; children boxes = box clipped by the node's plane
+//   split   every live point -> left / right child by one comparison
+// warp phase (segments <= 31 points): one warp per segment holds its points
+// in registers and finishes the segment's subtree: each level a point's rank
+// inside its node is a 32-lane comparison count.
+// Finally the nodes of each level (one contiguous range of the level-order
+// output) are written coalesced.
+#include "kernels.cuh"
+
+namespace lbkd {
+
+constexpr int kSelThreads = 256;  // four CTAs per SM (b = 11: <= 2047 points each)
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelPerSM = 4;
+constexpr int kNB = 64;              // buckets per segment (block phase)
+constexpr int kWarpSegMax = 31;      // warp phase once segments hold <= 31 points
+constexpr int kBoxK = 4;             // widest: per-lane boxes in the warp phase (k <= 4)
+
+struct SelLayout {
+    int Mp, nsb, nsw;  // padded capacity, max segments in block / warp phase
+    size_t off_P, off_seg, off_cand, off_ntab, off_hist, off_box0, off_box1, off_segv, off_ndim, off_wpv, off_wrk,
+        total;
+};
+
+// per-segment scalar arrays (u32 each): size, po, dim, bstar, rank, coff,
+// ccnt, cfill, piv, lo bits, hi bits -> 11 words
+constexpr int kSegWords = 12;
+
+__host__ __device__ inline SelLayout sel_layout(int b, int k) {
+    SelLayout s;
+    const int M = (1 << b) - 1;
+    s.Mp = (M + 8) & ~7;
+    s.nsb = b >= 7 ? 1 << (b - 6) : 1;  // segments of the deepest block level
+    s.nsw = b >= 6 ? 1 << (b - 5) : 1;  // segments when the warp phase starts
+    size_t o = 0;
+    s.off_P = o;
+    o += sizeof(float) * (size_t)k * s.Mp;
+    s.off_seg = o;
+    o += 2 * (size_t)s.Mp;
+    s.off_cand = o;
+    o += 2 * (size_t)s.Mp;
+    s.off_ntab = o;
+    o += 2 * (size_t)s.Mp;
+    o = (o + 15) & ~(size_t)15;
+    s.off_hist = o;
+    o += sizeof(u32) * (size_t)s.nsb * (kNB / 2);
+    s.off_box0 = o;
+    o += sizeof(float) * 2 * (size_t)k * s.nsw;
+    s.off_box1 = o;
+    o += sizeof(float) * 2 * (size_t)k * s.nsw;
+    s.off_segv = o;
+    o += sizeof(u32) * kSegWords * (size_t)s.nsw;
+    s.off_ndim = o;  // widest: split dim of every subtree node (heap order)
+    o += (size_t)s.Mp;
+    o = (o + 15) & ~(size_t)15;
+    s.off_wpv = o;   // warp phase: per warp, pivot plane + dim of each node
+    o += (sizeof(float) + sizeof(u32)) * 32 * kSelWarps;
+    s.off_wrk = o;   // warp phase: per warp, [k][32] ranks
+    o += (size_t)k * 32 * kSelWarps;
+    s.total = (o + 127) & ~(size_t)127;
+    return s;
+}
+
+size_t subtree_sel_smem_bytes(int b, int k) { return sel_layout(b, k).total; }
+
+enum { kSgSize = 0, kSgPo, kSgDim, kSgB, kSgR, kSgOff, kSgCnt, kSgFill, kSgPiv, kSgLo, kSgHi };
+
+template <int KT>
+__global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(SubtreeArgs a, int b) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typedef unsigned short u16;
+    const int k = KT ? KT : a.k;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const SelLayout Ly = sel_layout(b, k);
+    const int Mp = Ly.Mp;
+    float* P = reinterpret_cast<float*>(smem_raw + Ly.off_P);
+    u16* seg = reinterpret_cast<u16*>(smem_raw + Ly.off_seg);
+    u16* cand = reinterpret_cast<u16*>(smem_raw + Ly.off_cand);
+    u16* ntab = reinterpret_cast<u16*>(smem_raw + Ly.off_ntab);
+    u32* hist = reinterpret_cast<u32*>(smem_raw + Ly.off_hist);
+    float* boxA = reinterpret_cast<float*>(smem_raw + Ly.off_box0);
+    float* boxB = reinterpret_cast<float*>(smem_raw + Ly.off_box1);
+    u32* sv = reinterpret_cast<u32*>(smem_raw + Ly.off_segv);
+    uint8_t* ndim = reinterpret_cast<uint8_t*>(smem_raw + Ly.off_ndim);
+    float* wplane = reinterpret_cast<float*>(smem_raw + Ly.off_wpv) + warp * 32;
+    u32* wpdim = reinterpret_cast<u32*>(smem_raw + Ly.off_wpv + sizeof(float) * 32 * kSelWarps) + warp * 32;
+    const u16 kFin = 0xffffu;
+
+    const int L = a.L;
+    const u64 j = a.jbase + blockIdx.x;  // global index of the subtree root at level lam0
+    const u64 Bn = a.n - ((1ull << (L - 1)) - 1ull);
+    auto seg_size_l = [&](int sh, u64 J) -> u32 {
+        const u64 w = 1ull << sh, lo = J << sh;
+        u64 on = Bn > lo ? Bn - lo : 0ull;
+        if (on > w) on = w;
+        return (u32)(w - 1ull + on);
+    };
+    auto pivot_off_l = [&](int sh, u64 J) -> u32 {
+        if (sh <= 0) return 0u;
+        const u64 cw = 1ull << (sh - 1), lo = (2ull * J) * cw;
+        u64 on = Bn > lo ? Bn - lo : 0ull;
+        if (on > cw) on = cw;
+        return (u32)(cw - 1ull + on);
+    };
+    const int lam0 = a.lam0;
+    const int m = (int)(a.from_pts ? a.n : seg_size_l(L - lam0 - 1, j));
+
+    // ---- load the subtree's points (coalesced; input order = local id order)
+    const u32* src = nullptr;
+    const u32* vin = nullptr;
+    if (!a.from_pts) {
+        u32 par = 0;
+        if (a.src_par >= 0) {
+            par = (u32)a.src_par;
+        } else if (lam0 != a.lfirst) {
+            const uint8_t st = a.prev_state[blockIdx.x >> 1];
+            par = ((st >> 4) ^ (u32)__popc(st & 15u)) & 1u;
+        }
+        const LevelGeom g0 = make_geom(a.n, lam0);
+        src = a.w[par] + (seg_ibegin(g0, j) - a.pbase);
+        vin = src + (u64)k * a.stride;
+    }
+    if (src) {
+        // all loads in flight at once: 4-byte cp.async straight into shared
+        // memory (the subtree's slice starts at an arbitrary word)
+        for (int c = 0; c < k; ++c) {
+            const u32* g = src + (u64)c * a.stride;
+            for (int lid = tid; lid < m; lid += kSelThreads) {
+                const u32 sa = (u32)__cvta_generic_to_shared(P + c * Mp + lid);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g + lid) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int lid = tid; lid < m; lid += kSelThreads) {
+        if (!src) {
+            const float* q = a.pts + (u64)lid * k;
+            for (int c = 0; c < k; ++c) P[c * Mp + lid] = q[c];
+        }
+        seg[lid] = 0;
+    }
+    if (src) asm volatile("cp.async.wait_all;" ::: "memory");
+    // input row of a local id (the final tie-break of every chain)
+    auto idx_of = [&](u32 lid) -> u32 { return vin ? vin[lid] : lid; };
+    // subtree root box (global phase: boxes of level lam0; single-CTA build:
+    // reduced here) and, for widest, the dims of the ancestors above the root
+    if (a.from_pts) {
+        // world box of the whole input (widest.py:84-88)
+        for (int c = 0; c < k; ++c) {
+            float lo = INFINITY, hi = -INFINITY;
+            for (int p = tid; p < m; p += kSelThreads) {
+                const float v = P[c * Mp + p];
+                lo = fminf(lo, v);
+                hi = fmaxf(hi, v);
+            }
+            // fminf/fmaxf ignore NaN; non-finite input is reported elsewhere
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = fminf(lo, __shfl_xor_sync(kFullMask, lo, o));
+                hi = fmaxf(hi, __shfl_xor_sync(kFullMask, hi, o));
+            }
+            if (lane == 0) {
+                reinterpret_cast<float*>(cand)[2 * warp] = lo;  // cand is free until the first gather
+                reinterpret_cast<float*>(cand)[2 * warp + 1] = hi;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                float l2 = INFINITY, h2 = -INFINITY;
+                for (int w = 0; w < kSelWarps; ++w) {
+                    l2 = fminf(l2, reinterpret_cast<float*>(cand)[2 * w]);
+                    h2 = fmaxf(h2, reinterpret_cast<float*>(cand)[2 * w + 1]);
+                }
+                boxA[c] = l2;
+                boxA[k + c] = h2;
+            }
+            __syncthreads();
+        }
+    } else if (tid < 2 * k) {
+        boxA[tid] = a.boxes0[blockIdx.x * 2ull * k + tid];
+    }
+    __syncthreads();
+
+    // composite order of the chain of a node: c[d0], then the chain fields,
+    // then the input row.  chain_at(i) gives the i-th chain dim (i >= 1).
+    auto less_tie = [&](u32 x, u32 y, int nchain, auto chain_at) -> bool {
+        for (int f = 1; f < nchain; ++f) {
+            const int d = chain_at(f);
+            const u32 kx = flip_key(P[d * Mp + x]), ky = flip_key(P[d * Mp + y]);
+            if (kx != ky) return kx < ky;
+        }
+        return idx_of(x) < idx_of(y);
+    };
+    // widest: chain of a node = its dim, then its ancestors' dims (repeats
+    // dropped).  Ancestors inside the subtree come from ndim (heap order),
+    // above it from the global split dims.
+    auto widest_chain_of = [&](u32 heap, int depth, Chain& ch) {
+        ch.m = 0;
+        u32 seen = 0;
+        u32 h = heap;
+        int dd = depth;
+        while (true) {
+            const int d = ndim[h];
+            if (!((seen >> d) & 1u)) {
+                seen |= 1u << d;
+                ch.d[ch.m++] = (uint8_t)d;
+                if ((int)ch.m == k) return;
+            }
+            if (dd == 0) break;
+            h = (h - 1) >> 1;
+            --dd;
+        }
+        if (lam0 == 0) return;
+        u64 s = ((1ull << (lam0 - 1)) - 1ull) + (j >> 1);  // parent of the subtree root
+        while (true) {
+            const int d = a.split_dims[s];
+            if (!((seen >> d) & 1u)) {
+                seen |= 1u << d;
+                ch.d[ch.m++] = (uint8_t)d;
+                if ((int)ch.m == k) return;
+            }
+            if (s == 0) return;
+            s = (s - 1) >> 1;
+        }
+    };
+    auto first_argmax = [&](const float* box) -> int {
+        int best = 0;
+        double bw = (double)box[k] - (double)box[0];
+        for (int d = 1; d < k; ++d) {
+            const double w = (double)box[k + d] - (double)box[d];
+            if (w > bw) { bw = w; best = d; }
+        }
+        return best;
+    };
+
+    int lam = lam0;
+    // ======================= block phase =======================
+    for (; lam <= L - 1 && (L - lam - 1) >= 5; ++lam) {
+        const int sh = L - lam - 1;
+        const int dl = lam - lam0;
+        const int nloc = 1 << dl;
+        const u64 J0 = j << dl;
+        const u32 hbase = (1u << dl) - 1u;  // heap index of segment 0
+        // ---- setup
+        for (int t = tid; t < nloc; t += kSelThreads) {
+            u32* s = sv + t * kSegWords;
+            const float* box = boxA + t * 2 * k;
+            const int d = a.mode == kRoundRobin ? lam % k : first_argmax(box);
+            if (a.mode == kWidest) {
+                ndim[hbase + t] = (uint8_t)d;
+                const u64 node = ((1ull << lam) - 1ull) + J0 + t;
+                if (node < a.n) a.split_dims[node] = (uint8_t)d;
+            }
+            s[kSgSize] = seg_size_l(sh, J0 + t);
+            s[kSgPo] = pivot_off_l(sh, J0 + t);
+            s[kSgDim] = (u32)d;
+            s[kSgLo] = __float_as_uint(box[d]);
+            s[kSgHi] = __float_as_uint(box[k + d]);
+            s[kSgFill] = 0u;
+        }
+        for (int i = tid; i < nloc * (kNB / 2); i += kSelThreads) hist[i] = 0u;
+        __syncthreads();
+        // ---- hist (two 16-bit bins per word)
+        for (int p = tid; p < m; p += kSelThreads) {
+            const u32 t = seg[p];
+            if (t == kFin) continue;
+            const u32* s = sv + t * kSegWords;
+            const float lo = __uint_as_float(s[kSgLo]), hi = __uint_as_float(s[kSgHi]);
+            const int d = (int)s[kSgDim];
+            const double w = (double)hi - (double)lo;
+            const double x = w > 0.0 ? ((double)P[d * Mp + p] - (double)lo) * ((double)kNB / w) : 0.0;
+            const u32 bk = x < (double)(kNB - 1) ? (u32)x : (u32)(kNB - 1);
+            atomicAdd(&hist[t * (kNB / 2) + (bk >> 1)], (bk & 1u) ? 0x10000u : 1u);
+        }
+        __syncthreads();
+        // ---- pick: warp per segment
+        for (int t = warp; t < nloc; t += kSelWarps) {
+            u32* s = sv + t * kSegWords;
+            const u32 hw = hist[t * (kNB / 2) + lane];  // kNB == 64: one word per lane
+            const u32 c0 = hw & 0xffffu, c1 = hw >> 16;
+            u32 x = c0 + c1;
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(kFullMask, x, o);
+                if (lane >= o) x += y;
+            }
+            const u32 ex = x - c0 - c1;  // elements before bucket 2*lane
+            const u32 po = s[kSgPo];
+            int bsel = -1;
+            u32 cum = 0, cnt = 0;
+            if (po >= ex && po < ex + c0) { bsel = 2 * lane; cum = ex; cnt = c0; }
+            else if (po >= ex + c0 && po < ex + c0 + c1) { bsel = 2 * lane + 1; cum = ex + c0; cnt = c1; }
+            const u32 who = __ballot_sync(kFullMask, bsel >= 0);
+            const int src_l = __ffs(who) - 1;
+            const int bs = __shfl_sync(kFullMask, bsel, src_l);
+            cum = __shfl_sync(kFullMask, cum, src_l);
+            cnt = __shfl_sync(kFullMask, cnt, src_l);
+            if (lane == 0) {
+                s[kSgB] = (u32)bs;
+                s[kSgR] = po - cum;
+                s[kSgCnt] = cnt;
+            }
+        }
+        __syncthreads();
+        // candidate ranges: exclusive scan of the counts (thread 0; nloc is small)
+        if (tid == 0) {
+            u32 o = 0;
+            for (int t = 0; t < nloc; ++t) {
+                sv[t * kSegWords + kSgOff] = o;
+                o += sv[t * kSegWords + kSgCnt];
+            }
+        }
+        __syncthreads();
+        // ---- gather the candidates
+        for (int p = tid; p < m; p += kSelThreads) {
+            const u32 t = seg[p];
+            if (t == kFin) continue;
+            u32* s = sv + t * kSegWords;
+            const float lo = __uint_as_float(s[kSgLo]), hi = __uint_as_float(s[kSgHi]);
+            const int d = (int)s[kSgDim];
+            const double w = (double)hi - (double)lo;
+            const double x = w > 0.0 ? ((double)P[d * Mp + p] - (double)lo) * ((double)kNB / w) : 0.0;
+            const u32 bk = x < (double)(kNB - 1) ? (u32)x : (u32)(kNB - 1);
+            if (bk == s[kSgB]) cand[s[kSgOff] + atomicAdd(&s[kSgFill], 1u)] = (u16)p;
+        }
+        __syncthreads();
+        // ---- resolve: warp per segment, rank of each candidate by comparison
+        for (int t = warp; t < nloc; t += kSelWarps) {
+            u32* s = sv + t * kSegWords;
+            const u32 C = s[kSgCnt], r = s[kSgR], off = s[kSgOff];
+            const int d = (int)s[kSgDim];
+            Chain wch;
+            if (a.mode == kWidest) widest_chain_of(hbase + t, dl, wch);
+            else rr_chain(lam, k, wch);
+            auto chain_at = [&](int f) -> int { return wch.d[f]; };
+            for (u32 i0 = 0; i0 < C; i0 += 32) {
+                const u32 i = i0 + lane;
+                bool mine = false;
+                u32 ci = 0;
+                if (i < C) {
+                    ci = cand[off + i];
+                    const u32 ki = flip_key(P[d * Mp + ci]);
+                    u32 rank = 0;
+                    for (u32 jj = 0; jj < C; ++jj) {
+                        const u32 cj = cand[off + jj];
+                        const u32 kj = flip_key(P[d * Mp + cj]);
+                        rank += (kj < ki || (kj == ki && cj != ci && less_tie(cj, ci, (int)wch.m, chain_at))) ? 1u : 0u;
+                    }
+                    mine = rank == r;
+                }
+                if (mine) s[kSgPiv] = ci;
+            }
+        }
+        __syncthreads();
+        // children boxes, nodes
+        for (int t = tid; t < nloc; t += kSelThreads) {
+            const u32* s = sv + t * kSegWords;
+            const u32 piv = s[kSgPiv];
+            const int d = (int)s[kSgDim];
+            ntab[hbase + t] = (u16)piv;
+            const float plane = P[d * Mp + piv];
+            const float* box = boxA + t * 2 * k;
+            float* bl = boxB + (2 * t) * 2 * k;
+            float* br = boxB + (2 * t + 1) * 2 * k;
+            for (int c = 0; c < 2 * k; ++c) { bl[c] = box[c]; br[c] = box[c]; }
+            if (plane < bl[k + d]) bl[k + d] = plane;  // left child: hi = min(hi, plane)
+            if (plane > br[d]) br[d] = plane;          // right child: lo = max(lo, plane)
+        }
+        // ---- split: every live point -> left / right child
+        for (int p = tid; p < m; p += kSelThreads) {
+            const u32 t = seg[p];
+            if (t == kFin) continue;
+            const u32* s = sv + t * kSegWords;
+            const u32 piv = s[kSgPiv];
+            if ((u32)p == piv) {
+                seg[p] = kFin;
+                continue;
+            }
+            const int d = (int)s[kSgDim];
+            const u32 kp = flip_key(P[d * Mp + p]), kv = flip_key(P[d * Mp + piv]);
+            bool lt;
+            if (kp != kv) {
+                lt = kp < kv;
+            } else {
+                Chain wch;
+                if (a.mode == kWidest) widest_chain_of(hbase + t, dl, wch);
+                else rr_chain(lam, k, wch);
+                lt = less_tie((u32)p, piv, (int)wch.m, [&](int f) -> int { return wch.d[f]; });
+            }
+            seg[p] = (u16)(2 * t + (lt ? 0u : 1u));
+        }
+        __syncthreads();
+        float* tb = boxA;
+        boxA = boxB;
+        boxB = tb;
+    }
+
+    // ======================= warp phase =======================
+    if (lam <= L - 1) {
+        const int dl = lam - lam0;
+        const int nloc = 1 << dl;
+        const u64 J0 = j << dl;
+        const int sh = L - lam - 1;
+        // per-segment lists (any order): counts, offsets, scatter
+        for (int t = tid; t < nloc; t += kSelThreads) {
+            sv[t * kSegWords + kSgCnt] = 0u;
+            sv[t * kSegWords + kSgFill] = 0u;
+        }
+        __syncthreads();
+        for (int p = tid; p < m; p += kSelThreads) {
+            const u32 t = seg[p];
+            if (t != kFin) atomicAdd(&sv[t * kSegWords + kSgCnt], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            u32 o = 0;
+            for (int t = 0; t < nloc; ++t) {
+                sv[t * kSegWords + kSgOff] = o;
+                o += sv[t * kSegWords + kSgCnt];
+            }
+        }
+        __syncthreads();
+        for (int p = tid; p < m; p += kSelThreads) {
+            const u32 t = seg[p];
+            if (t == kFin) continue;
+            u32* s = sv + t * kSegWords;
+            cand[s[kSgOff] + atomicAdd(&s[kSgFill], 1u)] = (u16)p;
+        }
+        __syncthreads();
+        uint8_t* wrk = reinterpret_cast<uint8_t*>(smem_raw + Ly.off_wrk) + warp * 32 * k;  // [k][32] ranks
+        for (int t = warp; t < nloc; t += kSelWarps) {
+            const u64 Jt = J0 + t;
+            const u32* s = sv + t * kSegWords;
+            const u32 sz = s[kSgCnt];
+            bool act = (u32)lane < sz;
+            const u32 lid = act ? cand[s[kSgOff] + lane] : 0u;
+            const u32 actm = __ballot_sync(kFullMask, act);
+            // ---- rank of every point of the segment under each dimension's
+            // order, once: RR: the full chain T_d (exact for every level of
+            // the warp phase when lam >= k-1); widest: (c[d], input row),
+            // with a per-dim flag for equal coordinates (then the level falls
+            // back to full chain comparisons)
+            const bool rr_exact = a.mode == kRoundRobin && lam >= k - 1;
+            u32 tiemask = 0;  // widest: dims with equal coordinates in the segment
+            for (int d = 0; d < k; ++d) {
+                const u32 key = act ? flip_key(P[d * Mp + lid]) : 0u;
+                u32 rank = 0;
+                bool tie = false;
+                for (int i = 0; i < 32; ++i) {
+                    const u32 ok = __shfl_sync(kFullMask, key, i);
+                    if (((actm >> i) & 1u) && i != lane) {
+                        rank += ok < key ? 1u : 0u;
+                        tie |= ok == key;
+                    }
+                }
+                const u32 tiem = __ballot_sync(kFullMask, act && tie);
+                if (tiem) {
+                    tiemask |= 1u << d;
+                    Chain ch;
+                    if (rr_exact) rr_chain(d + ((lam - d + k - 1) / k) * k, k, ch);  // a level with dim d
+                    for (int i = 0; i < 32; ++i) {
+                        const u32 ok = __shfl_sync(kFullMask, key, i);
+                        const u32 ol = __shfl_sync(kFullMask, lid, i);
+                        if (act && tie && ((actm >> i) & 1u) && i != lane && ok == key) {
+                            const bool lt = rr_exact ? less_tie(ol, lid, (int)ch.m, [&](int f) -> int { return ch.d[f]; })
+                                                     : idx_of(ol) < idx_of(lid);
+                            rank += lt ? 1u : 0u;
+                        }
+                    }
+                }
+                wrk[d * 32 + lane] = (uint8_t)rank;
+            }
+            __syncwarp();
+            u32 nd = 0;  // heap index of the point's node inside the segment's subtree (< 31)
+            // widest: the point's node box (k <= kBoxK)
+            float blo[kBoxK], bhi[kBoxK];
+            if (a.mode == kWidest) {
+                for (int c = 0; c < kBoxK; ++c)
+                    if (c < k) { blo[c] = boxA[t * 2 * k + c]; bhi[c] = boxA[t * 2 * k + k + c]; }
+            }
+            for (int l2 = lam; l2 <= L - 1; ++l2) {
+                const int dd = l2 - lam;
+                const int sh2 = L - l2 - 1;
+                const u32 off = nd + 1u - (1u << dd);  // node's index among its level inside the segment
+                const u64 J = (Jt << dd) + off;
+                const u32 heap = (1u << (dl + dd)) - 1u + ((u32)t << dd) + off;  // heap index in the subtree
+                int d = l2 % k;
+                if (a.mode == kWidest && act) {
+                    int best = 0;
+                    double bw = (double)bhi[0] - (double)blo[0];
+                    for (int c = 1; c < kBoxK; ++c) {
+                        if (c < k) {
+                            const double w = (double)bhi[c] - (double)blo[c];
+                            if (w > bw) { bw = w; best = c; }
+                        }
+                    }
+                    d = best;
+                }
+                u32 rank;
+                const bool exact = rr_exact || !__any_sync(kFullMask, act && ((tiemask >> d) & 1u));
+                if (exact) {
+                    // bit-sliced ballots: lanes of my node (5 node bits), then
+                    // those with a smaller precomputed rank (5 rank bits)
+                    const u32 key = act ? (u32)wrk[d * 32 + lane] : 0u;
+                    u32 eq = actm & __ballot_sync(kFullMask, act);
+#pragma unroll
+                    for (int bb = 0; bb < 5; ++bb) {
+                        const u32 bit = (nd >> bb) & 1u;
+                        const u32 bal = __ballot_sync(kFullMask, bit);
+                        eq &= bit ? bal : ~bal;
+                    }
+                    u32 lt = 0u;
+#pragma unroll
+                    for (int bb = 4; bb >= 0; --bb) {
+                        const u32 bit = (key >> bb) & 1u;
+                        const u32 bal = __ballot_sync(kFullMask, bit);
+                        if (bit) { lt |= eq & ~bal; eq &= bal; }
+                        else eq &= ~bal;
+                    }
+                    rank = (u32)__popc(lt);
+                } else {
+                    // widest with equal coordinates in this dim: full chain comparisons
+                    const u32 key = act ? flip_key(P[d * Mp + lid]) : 0u;
+                    Chain ch;
+                    if (a.mode == kRoundRobin) {
+                        rr_chain(l2, k, ch);  // (tiny trees: truncated chains near the root)
+                    } else if (act) {
+                        ndim[heap] = (uint8_t)d;  // the node's own dim heads its chain
+                        widest_chain_of(heap, dl + dd, ch);
+                    }
+                    rank = 0;
+                    for (int i = 0; i < 32; ++i) {
+                        const u32 ok = __shfl_sync(kFullMask, key, i);
+                        const u32 on = __shfl_sync(kFullMask, act ? nd : 0xffffffffu, i);
+                        const u32 ol = __shfl_sync(kFullMask, lid, i);
+                        if (act && on == nd && i != lane) {
+                            if (ok < key) ++rank;
+                            else if (ok == key && less_tie(ol, lid, (int)ch.m, [&](int f) -> int { return ch.d[f]; }))
+                                ++rank;
+                        }
+                    }
+                }
+                const u32 po = pivot_off_l(sh2, J);
+                const bool is_piv = act && rank == po;
+                if (is_piv) {
+                    ntab[heap] = (u16)lid;
+                    if (a.mode == kWidest) {
+                        ndim[heap] = (uint8_t)d;
+                        const u64 node = ((1ull << l2) - 1ull) + J;
+                        if (node < a.n) a.split_dims[node] = (uint8_t)d;
+                        wplane[nd] = P[d * Mp + lid];
+                        wpdim[nd] = (u32)d;
+                    }
+                }
+                __syncwarp();
+                if (act && !is_piv) {
+                    const bool right = rank > po;
+                    if (a.mode == kWidest) {
+                        const float pl = wplane[nd];
+                        const int pd = (int)wpdim[nd];
+                        for (int c = 0; c < kBoxK; ++c) {
+                            if (c == pd) {
+                                if (right) { if (pl > blo[c]) blo[c] = pl; }
+                                else { if (pl < bhi[c]) bhi[c] = pl; }
+                            }
+                        }
+                    }
+                    nd = 2u * nd + 1u + (right ? 1u : 0u);
+                }
+                act = act && !is_piv;
+                __syncwarp();
+                if (!__any_sync(kFullMask, act)) break;
+            }
+            __syncwarp();
+        }
+        (void)sh;
+    }
+
+    // ======================= output =======================
+    __syncthreads();
+    for (int dl = 0; lam0 + dl <= L - 1; ++dl) {
+        const int l2 = lam0 + dl;
+        const u64 first = ((1ull << l2) - 1ull) + (j << dl);
+        if (first >= a.n) break;
+        u64 cntn = 1ull << dl;
+        if (first + cntn > a.n) cntn = a.n - first;
+        const u32 h0 = (1u << dl) - 1u;
+        for (u32 i = tid; i < (u32)cntn; i += kSelThreads) a.perm[first + i] = idx_of(ntab[h0 + i]);
+        float* dst = a.out_pts + first * (u64)k;
+        for (u32 i = tid; i < (u32)cntn * (u32)k; i += kSelThreads) {
+            const u32 t = i / (u32)k, c = i - t * (u32)k;
+            dst[i] = P[c * Mp + ntab[h0 + t]];
+        }
+    }
+}
+
+void launch_subtree_sel(const SubtreeArgs& a, unsigned grid, int b, cudaStream_t st) {
+    const size_t sm = subtree_sel_smem_bytes(b, a.k);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kern<<<grid, kSelThreads, sm, st>>>(a, b);
+    };
+    switch (a.k) {
+        case 2: go(subtree_sel_kernel<2>); break;
+        case 3: go(subtree_sel_kernel<3>); break;
+        case 4: go(subtree_sel_kernel<4>); break;
+        default: go(subtree_sel_kernel<0>); break;
+    }
+}
+
+}  // namespace lbkd
