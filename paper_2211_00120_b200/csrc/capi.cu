@@ -271,6 +271,10 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         const double pts = (double)level_points(bp, l);
         CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
         CK(cudaMemsetAsync(bf.cand_ctr, 0, sizeof(u32), st));
+        {  // per-tile below-pivot counts accumulate atomically in the filter
+            const u64 T = (u64)sel_tile(bp.b);
+            CK(cudaMemsetAsync(bf.tile_lt, 0, 2 * ((g.nview + T - 1) / T) * sizeof(u32), st));
+        }
         SelArgs a;
         memset(&a, 0, sizeof(a));
         a.g = g;

@@ -51,23 +51,54 @@ __device__ __forceinline__ u32 bucket_shift(u32 lo, u32 hi, int D) {
 // truncation are monotone) and identical in hist and filter, which is all
 // the selection needs.  -0.0 and +0.0 land in the same bucket.
 struct Bucketer {
-    double lo, scale;
+    float hlo, scale;  // halves: no overflow of hi - lo for any finite box
     u32 top;
 };
 
 __device__ __forceinline__ Bucketer make_bucketer(float lo, float hi, int D) {
     Bucketer b;
-    b.lo = (double)lo;
-    const double w = (double)hi - b.lo;
-    b.scale = w > 0.0 ? (double)(1u << D) / w : 0.0;
+    b.hlo = 0.5f * lo;
+    const float w = 0.5f * hi - b.hlo;
+    b.scale = w > 0.0f ? __fdiv_rn((float)(1u << D), w) : 0.0f;
     b.top = (1u << D) - 1u;
     return b;
 }
 
 __device__ __forceinline__ u32 bucket_of(const Bucketer& b, u32 bits) {
-    const double x = ((double)__uint_as_float(bits) - b.lo) * b.scale;
-    return x < (double)b.top ? (u32)x : b.top;  // NaN (non-finite input, reported later) -> top
+    // fp32, round-to-nearest each step: monotone in the key
+    const float x = __fmul_rn(__fsub_rn(0.5f * __uint_as_float(bits), b.hlo), b.scale);
+    return x < (float)b.top ? (u32)x : b.top;  // NaN (non-finite input, reported later) -> top
 }
+
+// Incremental segment cursor over the view's in-order positions for a CTA
+// that walks consecutive tiles (each tile <= the smallest segment, so a tile
+// holds at most two segment parts); 64-bit geometry only at segment changes.
+struct SegCursor {
+    u64 cur, sb, se;  // current segment and its [sb, se) positions
+    __device__ void init(const LevelGeom& g, u64 p) {
+        cur = v_seg_of(g, p);
+        sb = v_ibegin(g, cur);
+        se = sb + v_size(g, cur);
+    }
+    // parts of tile [ts, ts + cnt): [r0a, r0b) of cur, [r1a, r1b) of cur + 1
+    __device__ void parts(const LevelGeom& g, u64 ts, u64 cnt, u32& r0a, u32& r0b, u32& r1a, u32& r1b, bool& has1) {
+        while (se + 1 <= ts && cur + 1 < g.nseg) {  // past cur and the finished node after it
+            ++cur;
+            sb = se + 1;
+            se = sb + v_size(g, cur);
+        }
+        r0a = sb > ts ? (u32)(sb - ts) : 0u;
+        r0b = se > ts ? (u32)((se - ts < cnt) ? se - ts : cnt) : 0u;
+        if (r0b < r0a) r0b = r0a;
+        has1 = cur + 1 < g.nseg && se + 1 < ts + cnt;
+        r1a = r1b = (u32)cnt;
+        if (has1) {
+            r1a = (u32)(se + 1 - ts);
+            const u64 e1 = se + 1 + v_size(g, cur + 1);
+            r1b = (u32)((e1 - ts < cnt) ? e1 - ts : cnt);
+        }
+    }
+};
 
 // tile -> (first segment part, second segment part) of the view; a tile
 // holds at most two segment parts (tile <= smallest segment)
@@ -219,7 +250,9 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
     const u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
     u64 t1 = t0 + a.tiles_per_cta;
     if (t1 > a.ntiles) t1 = a.ntiles;
-    u64 cur = v_seg_of(g, t0 * T);
+    SegCursor sc;
+    sc.init(g, t0 * T);
+    u64 cur = sc.cur;  // segment the shared histogram currently counts
     __syncthreads();
     auto flush = [&](u64 seg) {
         __syncthreads();
@@ -231,45 +264,54 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
         __syncthreads();
     };
     const u32* W = a.bf.w[a.par];
+    int dk = -1;
+    Bucketer bk{};
+    const u32* kp = nullptr;
     for (u64 t = t0; t < t1; ++t) {
         const u64 ts = t * T;
         const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
-        TileParts tp = tile_parts(g, ts, cnt);
-        if (tp.j0 != cur) {  // the previous tile ended exactly at a segment end
+        u32 r0a, r0b, r1a, r1b;
+        bool has1;
+        sc.parts(g, ts, cnt, r0a, r0b, r1a, r1b, has1);
+        if (sc.cur != cur) {  // the previous tile ended exactly at a segment end
             flush(cur);
-            cur = tp.j0;
+            cur = sc.cur;
+            dk = -1;
         }
-        const int dk0 = seg_key_dim(a, tp.j0);
-        const u32* k0 = W + (u64)dk0 * a.bf.stride + ts;
-        const Bucketer b0 = seg_bucketer(a, tp.j0, dk0);
+        if (dk < 0) {
+            dk = seg_key_dim(a, cur);
+            bk = seg_bucketer(a, cur, dk);
+            kp = W + (u64)dk * a.bf.stride;
+        }
         u32 key[ITEMS];
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const u32 r = (u32)(i * kHThreads + threadIdx.x);
-            key[i] = 0u;
-            if (r >= tp.r0a && r < tp.r0b) key[i] = k0[r];
+            key[i] = (r < (u32)cnt) ? kp[ts + r] : 0u;
         }
-        if (tp.has1) {
-            const u32* k1 = W + (u64)seg_key_dim(a, tp.j0 + 1) * a.bf.stride + ts;
+        if (has1 && seg_key_dim(a, cur + 1) != dk) {  // widest: the next segment splits another dim
+            const u32* k1 = W + (u64)seg_key_dim(a, cur + 1) * a.bf.stride;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const u32 r = (u32)(i * kHThreads + threadIdx.x);
-                if (r >= tp.r1a && r < tp.r1b) key[i] = k1[r];
+                if (r >= r1a && r < r1b) key[i] = k1[ts + r];
             }
         }
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const u32 r = (u32)(i * kHThreads + threadIdx.x);
-            if (r >= tp.r0a && r < tp.r0b) atomicAdd(&h[bucket_of(b0, key[i])], 1u);
+            if (r >= r0a && r < r0b) atomicAdd(&h[bucket_of(bk, key[i])], 1u);
         }
-        if (tp.has1) {
+        if (has1) {
             flush(cur);
-            cur = tp.j0 + 1;
-            const Bucketer b1 = seg_bucketer(a, cur, seg_key_dim(a, cur));
+            cur = cur + 1;
+            dk = seg_key_dim(a, cur);
+            bk = seg_bucketer(a, cur, dk);
+            kp = W + (u64)dk * a.bf.stride;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const u32 r = (u32)(i * kHThreads + threadIdx.x);
-                if (r >= tp.r1a && r < tp.r1b) atomicAdd(&h[bucket_of(b1, key[i])], 1u);
+                if (r >= r1a && r < r1b) atomicAdd(&h[bucket_of(bk, key[i])], 1u);
             }
         }
     }
@@ -320,68 +362,86 @@ constexpr int kSub = 256;  // positions per warp subtile (32 lanes x 8 rows)
 
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
+    // CTA = a contiguous run of tiles; per tile every warp owns one 256-
+    // position subtile (8 items per thread, thread-contiguous).  Counts of
+    // elements below b*: per (subtile, part) one plain store by the warp,
+    // per (tile, part) one global atomic per warp (tile_lt is zeroed per
+    // level).  The rare hits (1 / 2^D of the points) append their candidate
+    // record through a warp-aggregated atomic.  No block barrier.
     constexpr int ITEMS = 8;
     constexpr int T = THREADS * ITEMS;
     constexpr int NSUB = T / kSub;
-    __shared__ u32 wtot[32];
-    __shared__ u32 s_base;
     const LevelGeom& g = a.g;
     const u32* W = a.bf.w[a.par];
     const int k = a.k, R = k + 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (u64 t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    const u32 ltm = lanemask_lt();
+    const u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
+    u64 t1 = t0 + a.tiles_per_cta;
+    if (t1 > a.ntiles) t1 = a.ntiles;
+    if (t0 >= t1) return;
+    SegCursor sc;
+    sc.init(g, t0 * T);
+    for (u64 t = t0; t < t1; ++t) {
         const u64 ts = t * T;
         const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
-        const TileParts tp = tile_parts(g, ts, cnt);
+        u32 r0a, r0b, r1a, r1b;
+        bool has1;
+        sc.parts(g, ts, cnt, r0a, r0b, r1a, r1b, has1);
+        const u64 s = t * NSUB + warp;
+        u32 nlt_s[2] = {0u, 0u};
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
-            const u64 j = tp.j0 + part;
-            const u32 ra = part ? tp.r1a : tp.r0a, rb = part ? tp.r1b : tp.r0b;
-            const bool present = (part == 0 || tp.has1) && ra < rb;
-            u32 hits = 0, nlt = 0;
-            u32 off = 0;
+            const u64 j = sc.cur + part;
+            const u32 ra = part ? r1a : r0a, rb = part ? r1b : r0b;
+            if (!((part == 0 || has1) && ra < rb)) continue;
             u32* sel = a.sel + j * kSelW;
-            if (present) {
-                const Bucketer bk =
-                    make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D);
-                const u32 bs = sel[kSelB];
-                off = sel[kSelOff];
-                const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
+            const Bucketer bk = make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D);
+            const u32 bs = sel[kSelB];
+            const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
+            u32 hits = 0, nlt = 0;
 #pragma unroll
-                for (int i = 0; i < ITEMS; ++i) {
-                    const u32 r = (u32)(threadIdx.x * ITEMS + i);
-                    if (r >= ra && r < rb) {
-                        const u32 b = bucket_of(bk, kp[r]);
-                        if (b == bs) hits |= 1u << i;
-                        nlt += b < bs ? 1u : 0u;
-                    }
+            for (int i = 0; i < ITEMS; ++i) {
+                const u32 r = (u32)(threadIdx.x * ITEMS + i);
+                if (r >= ra && r < rb) {
+                    const u32 b = bucket_of(bk, kp[r]);
+                    if (b == bs) hits |= 1u << i;
+                    nlt += b < bs ? 1u : 0u;
                 }
             }
-            // per warp subtile (zero for absent parts: the partition sums them)
-            const u32 wl = __reduce_add_sync(kFullMask, nlt);
-            if (lane == 0) a.sub_lt[(t * NSUB + warp) * 2 + part] = wl;
-            if (!present) continue;  // uniform over the block
-            // one scan: hits (low 16 bits) and below-b* counts (high 16)
-            const u32 v = (u32)__popc(hits) | (nlt << 16);
-            const u32 ex = block_exclusive_scan<u32>(v, wtot, nullptr);
-            if (threadIdx.x == THREADS - 1) {
-                const u32 tot = ex + v;
-                s_base = atomicAdd(&sel[kSelFill], tot & 0xffffu);
-                a.tile_lt[t * 2 + part] = tot >> 16;
+            nlt = __reduce_add_sync(kFullMask, nlt);
+            nlt_s[part] = nlt;
+            if (lane == 0 && nlt) atomicAdd(&a.tile_lt[t * 2 + part], nlt);
+            // candidates: warp-aggregated slot reservation
+            const u32 nh = (u32)__popc(hits);
+            u32 x = nh;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(kFullMask, x, o);
+                if (lane >= o) x += y;
             }
-            __syncthreads();
-            u32 slot = off + s_base + (ex & 0xffffu);
-            while (hits) {
-                const int i = __ffs(hits) - 1;
-                hits &= hits - 1;
-                const u32 r = (u32)(threadIdx.x * ITEMS + i);
-                u32* rec = a.cand + (u64)slot * R;
-                for (int c = 0; c <= k; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
-                rec[k + 1] = (u32)(ts + r);
-                ++slot;
+            const u32 wtot = __shfl_sync(kFullMask, x, 31);
+            if (wtot) {
+                u32 base = 0;
+                if (lane == 31) base = atomicAdd(&sel[kSelFill], wtot);
+                base = __shfl_sync(kFullMask, base, 31);
+                u32 slot = sel[kSelOff] + base + x - nh;
+                while (hits) {
+                    const int i = __ffs(hits) - 1;
+                    hits &= hits - 1;
+                    const u32 r = (u32)(threadIdx.x * ITEMS + i);
+                    u32* rec = a.cand + (u64)slot * R;
+                    for (int c = 0; c <= k; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
+                    rec[k + 1] = (u32)(ts + r);
+                    ++slot;
+                }
             }
-            __syncthreads();
         }
+        if (lane == 0) {
+            a.sub_lt[s * 2] = nlt_s[0];
+            a.sub_lt[s * 2 + 1] = nlt_s[1];
+        }
+        (void)ltm;
     }
 }
 
@@ -736,11 +796,18 @@ void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
     const int T = sel_tile(b);
     a.ntiles = (a.g.nview + T - 1) / T;
     const u64 grid = a.ntiles < 148 * 8 ? a.ntiles : 148 * 8;
+    // contiguous runs of tiles per CTA (the segment cursor advances locally)
+    const u64 target = 148 * 16;
+    u64 tpc = (a.ntiles + target - 1) / target;
+    if (tpc < 1) tpc = 1;
+    a.tiles_per_cta = (int)tpc;
+    const unsigned g2 = (unsigned)((a.ntiles + tpc - 1) / tpc);
+    (void)grid;
     switch (T) {
-        case 2048: sel_filter_kernel<256><<<(unsigned)grid, 256, 0, st>>>(a); break;
-        case 1024: sel_filter_kernel<128><<<(unsigned)grid, 128, 0, st>>>(a); break;
-        case 512: sel_filter_kernel<64><<<(unsigned)grid, 64, 0, st>>>(a); break;
-        default: sel_filter_kernel<32><<<(unsigned)grid, 32, 0, st>>>(a); break;
+        case 2048: sel_filter_kernel<256><<<g2, 256, 0, st>>>(a); break;
+        case 1024: sel_filter_kernel<128><<<g2, 128, 0, st>>>(a); break;
+        case 512: sel_filter_kernel<64><<<g2, 64, 0, st>>>(a); break;
+        default: sel_filter_kernel<32><<<g2, 32, 0, st>>>(a); break;
     }
 }
 
