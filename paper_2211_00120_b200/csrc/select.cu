@@ -630,8 +630,28 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
 constexpr int kPThreads = 256;
 constexpr int kPRows = kSub / 32;
 
-template <int KMAX>
-__global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 3 : 1) sel_part_kernel(SelArgs a, int T) {
+// equal leading coordinates: compare the rest of the node's chain, then the
+// input row (rare; re-reads the point from the source arrays)
+__device__ __noinline__ int part_tie_side(const SelArgs& a, u64 j, u64 pos) {
+    const int k = a.k, A = k + 1;
+    const u32* W = a.bf.w[a.par];
+    const Chain* ch = a.chains + j;
+    const u32* pv = a.piv + j * A;
+    const u32 mm = ch->m;
+    for (u32 f = 1; f < mm; ++f) {
+        const int d = ch->d[f];
+        const u32 xx = flip_key(__uint_as_float(W[(u64)d * a.bf.stride + pos]));
+        const u32 yy = flip_key(__uint_as_float(pv[d]));
+        if (xx != yy) return xx < yy ? 0 : 1;
+    }
+    const u32 xx = W[(u64)k * a.bf.stride + pos], yy = pv[k];
+    return xx < yy ? 0 : (xx > yy ? 1 : 2);
+}
+
+// D0 >= 0: every segment's leading key is coordinate D0 (round-robin): full
+// single-part subtiles take a lean path (float compares, no part masks)
+template <int KMAX, int D0>
+__global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 2 : 1) sel_part_kernel(SelArgs a, int T) {
     const int lane = threadIdx.x & 31;
     const int k = a.k, A = k + 1;
     const LevelGeom& g = a.g;
@@ -641,23 +661,39 @@ __global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 3 : 1) sel_part_kernel(
     const u64 nsub = (g.nview + kSub - 1) / kSub;
     const int nsub_tile = T / kSub;
     const u32 lt = lanemask_lt();
-    for (u64 s = (u64)blockIdx.x * (kPThreads / 32) + (threadIdx.x >> 5); s < nsub;
-         s += (u64)gridDim.x * (kPThreads / 32)) {
-        const u64 ss = s * kSub;
-        const u64 cnt = g.nview - ss < (u64)kSub ? g.nview - ss : (u64)kSub;
-        // issue every load of the subtile first
-        u32 v[KMAX + 1][kPRows];
+    const u64 sstep = (u64)gridDim.x * (kPThreads / 32);
+    // software pipeline: the next subtile's loads are in flight while this
+    // one is split (the kernel is load-latency bound otherwise)
+    u32 vn[KMAX + 1][kPRows];
+    auto load_sub = [&](u64 s2) {
+        const u64 ss2 = s2 * kSub;
+        const u64 cnt2 = g.nview - ss2 < (u64)kSub ? g.nview - ss2 : (u64)kSub;
 #pragma unroll
         for (int c = 0; c <= KMAX; ++c) {
             if (c < A) {
-                const u32* src = Wsrc + (u64)c * stride + ss;
+                const u32* src = Wsrc + (u64)c * stride + ss2 + lane;
+                if (cnt2 == (u64)kSub) {
 #pragma unroll
-                for (int i = 0; i < kPRows; ++i) {
-                    const u32 r = (u32)(i * 32 + lane);
-                    v[c][i] = r < cnt ? src[r] : 0u;
+                    for (int i = 0; i < kPRows; ++i) vn[c][i] = src[i * 32];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kPRows; ++i) vn[c][i] = (u32)(i * 32 + lane) < cnt2 ? src[i * 32] : 0u;
                 }
             }
         }
+    };
+    u64 s = (u64)blockIdx.x * (kPThreads / 32) + (threadIdx.x >> 5);
+    if (s < nsub) load_sub(s);
+    for (; s < nsub; s += sstep) {
+        const u64 ss = s * kSub;
+        const u64 cnt = g.nview - ss < (u64)kSub ? g.nview - ss : (u64)kSub;
+        const bool full = cnt == (u64)kSub;
+        u32 v[KMAX + 1][kPRows];
+#pragma unroll
+        for (int c = 0; c <= KMAX; ++c)
+#pragma unroll
+            for (int i = 0; i < kPRows; ++i) v[c][i] = vn[c][i];
+        if (s + sstep < nsub) load_sub(s + sstep);
         // geometry (warp-uniform)
         const TileParts tp = tile_parts(g, ss, cnt);
         const u64 t = ss / (u64)T;
@@ -685,6 +721,29 @@ __global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 3 : 1) sel_part_kernel(
             else { bL1 = l; bR1 = rr; d01 = d; y01 = y; }
         }
         const u32 r0a = tp.r0a, r0b = tp.r0b, r1a = tp.r1a, r1b = tp.r1b;
+        if (D0 >= 0 && full && !tp.has1 && r0a == 0 && r0b == (u32)kSub) {
+            // lean path: one segment part covers the whole subtile
+            const float yf = __uint_as_float(a.piv[tp.j0 * A + (D0 >= 0 ? D0 : 0)]);
+            u32 bl = (u32)bL0, br = (u32)bR0;
+            u32* dbase = Wdst + lane * 0;
+#pragma unroll
+            for (int i = 0; i < kPRows; ++i) {
+                const float xf = __uint_as_float(v[D0 >= 0 ? D0 : 0][i]);
+                int side = xf < yf ? 0 : (xf > yf ? 1 : 2);  // -0.0 == +0.0 like numpy
+                if (side == 2) side = part_tie_side(a, tp.j0, ss + (u64)(i * 32 + lane));
+                const u32 ml = __ballot_sync(kFullMask, side == 0);
+                const u32 mr = __ballot_sync(kFullMask, side == 1);
+                const u32 dst = side == 0 ? bl + __popc(ml & lt) : br + __popc(mr & lt);
+                bl += __popc(ml);
+                br += __popc(mr);
+                if (side < 2) {
+#pragma unroll
+                    for (int c = 0; c <= KMAX; ++c)
+                        if (c < A) dbase[(u64)c * stride + dst] = v[c][i];
+                }
+            }
+            continue;
+        }
 #pragma unroll
         for (int i = 0; i < kPRows; ++i) {
             const u32 r = (u32)(i * 32 + lane);
@@ -823,16 +882,26 @@ void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
     const u64 cap = 148ull * 8;
     if (grid > cap) grid = cap;
     // register-resident subtile: (KMAX + 1) x 8 words per lane
+    const int d0 = a.mode == kRoundRobin ? a.g.l % a.k : -1;  // RR: every segment splits dim l mod k
+#define LBKD_PART(KM)                                                                          \
+    switch (d0) {                                                                              \
+        case 0: sel_part_kernel<KM, 0><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;     \
+        case 1: sel_part_kernel<KM, (KM > 1 ? 1 : 0)><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break; \
+        case 2: sel_part_kernel<KM, (KM > 2 ? 2 : 0)><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break; \
+        case 3: sel_part_kernel<KM, (KM > 3 ? 3 : 0)><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break; \
+        default: sel_part_kernel<KM, -1><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;   \
+    }
     switch (a.k) {
-        case 1: sel_part_kernel<1><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
-        case 2: sel_part_kernel<2><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
-        case 3: sel_part_kernel<3><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
-        case 4: sel_part_kernel<4><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;
+        case 1: LBKD_PART(1); break;
+        case 2: LBKD_PART(2); break;
+        case 3: LBKD_PART(3); break;
+        case 4: LBKD_PART(4); break;
         default:
-            if (a.k <= 8) sel_part_kernel<8><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
-            else sel_part_kernel<16><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
+            if (a.k <= 8) sel_part_kernel<8, -1><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
+            else sel_part_kernel<16, -1><<<(unsigned)grid, kPThreads, 0, st>>>(a, T);
             break;
     }
+#undef LBKD_PART
 }
 
 }  // namespace lbkd
