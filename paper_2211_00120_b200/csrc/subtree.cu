@@ -444,7 +444,7 @@ size_t subtree_rr_smem_bytes(int b, int k) {
     bytes += sizeof(unsigned short) * Mp;             // packed state of each point
     size_t nloc = ((size_t)1 << (b - 2));             // segments at the deepest block level
     // level tables + node table (after the chain sorts) alias the sort scratch
-    size_t tables = sizeof(unsigned short) * 3 * (nloc + 8) + sizeof(unsigned short) * Mp;
+    size_t tables = sizeof(u32) * 2 * (nloc + 8) + sizeof(unsigned short) * Mp;
     size_t sortscr = sizeof(unsigned short) * kRRWarps * 256 + sizeof(u32) * 4 * 256;
     bytes += tables > sortscr ? tables : sortscr;
     bytes += sizeof(u64) * 64;
@@ -473,13 +473,15 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
     sp = smem_raw + (((size_t)(sp - smem_raw) + 15) & ~(size_t)15);  // keep the shared base (no uintptr_t round trip)
     // per-level tables alias the radix-sort scratch (chain sorts)
     const int nmax = (M + 1) / 4;  // 2^(b-2) segments at the deepest block level
-    u16* lbt = reinterpret_cast<u16*>(sp);   // segment begin in the lists
-    u16* pot = lbt + nmax + 8;               // pivot offset
-    u16* rtb = pot + nmax + 8;               // right elements of the earlier segments
-    u16* ntab = rtb + nmax + 8;              // local id of the point of every node, heap order
+    // per segment t: lp[t] = begin in the lists | pivot offset << 16;
+    //               rp[t] = right elements of the earlier segments | begin of
+    //               its right child in the next lists minus those << 16
+    u32* lp = reinterpret_cast<u32*>(sp);
+    u32* rp = lp + nmax + 8;
+    u16* ntab = reinterpret_cast<u16*>(rp + nmax + 8);  // local id of the point of every node, heap order
     unsigned short(*cnt)[256] = reinterpret_cast<unsigned short(*)[256]>(sp);
     u32(*gsum)[256] = reinterpret_cast<u32(*)[256]>(sp + sizeof(unsigned short) * kRRWarps * 256);
-    size_t tables = sizeof(u16) * 3 * ((size_t)nmax + 8) + sizeof(u16) * Mp;
+    size_t tables = sizeof(u32) * 2 * ((size_t)nmax + 8) + sizeof(u16) * Mp;
     size_t sortscr = sizeof(unsigned short) * kRRWarps * 256 + sizeof(u32) * 4 * 256;
     u32* scratch = reinterpret_cast<u32*>(sp + (tables > sortscr ? tables : sortscr));
     u64* scratch64 = reinterpret_cast<u64*>(scratch);
@@ -600,25 +602,29 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
         {
             u32 v = 0;
             const int per = (nloc + kRRThreads - 1) / kRRThreads;  // <= 2
-            u32 rs[2] = {0u, 0u};
-            for (int i = 0; i < per; ++i) {
+            u32 rs[2] = {0u, 0u}, lb2[2] = {0u, 0u}, po2[2] = {0u, 0u};
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
                 const int t = tid * per + i;
-                if (t < nloc) {
+                if (i < per && t < nloc) {
                     const u32 sz = seg_size_l(sh, J0 + t);
-                    const u32 po = pivot_off_l(sh, J0 + t);
-                    lbt[t] = (u16)(seg_begin_l(sh, J0 + t) - lb0);
-                    pot[t] = (u16)po;
-                    rs[i] = sz - po - 1u;
+                    po2[i] = pivot_off_l(sh, J0 + t);
+                    lb2[i] = (u32)(seg_begin_l(sh, J0 + t) - lb0);
+                    lp[t] = lb2[i] | (po2[i] << 16);
+                    rs[i] = sz - po2[i] - 1u;
                     v += rs[i];
                 }
             }
             const u32 ex = block_exclusive_scan<u32>(v, scratch, nullptr);
             u32 run = ex;
-            for (int i = 0; i < per; ++i) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
                 const int t = tid * per + i;
-                if (t < nloc) { rtb[t] = (u16)run; run += rs[i]; }
+                if (i < per && t < nloc) {
+                    rp[t] = run | ((lb2[i] - (u32)t + po2[i] - run) << 16);
+                    run += rs[i];
+                }
             }
-            if (tid == 0) lbt[nloc] = (u16)mc;
         }
         __syncthreads();
 
@@ -628,9 +634,10 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
         for (int p = tid; p < mc; p += kRRThreads) {
             const u32 lid = A[p];
             const u32 t = state[lid] >> 2;
-            const u32 lb = lbt[t];
+            const u32 lpt = lp[t];
+            const u32 lb = lpt & 0xffffu;
             const u32 o = (u32)p - lb;
-            const u32 po = pot[t];
+            const u32 po = lpt >> 16;
             if (o == po) {
                 state[lid] = (u16)(((2u * t) << 2) | 2u);
                 ntab[nloc - 1 + t] = (u16)lid;
@@ -706,18 +713,18 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                     const int p = p0 + i;
                     const u32 ca = sa[i] & 3u;
                     if (ca < 2u) {
-                        const u32 t = sa[i] >> 3;
+                        const u32 rpt = rp[sa[i] >> 3];
                         const u32 Rex = (u32)(ex & 0xffffu), Pex = (u32)((ex >> 16) & 0xffffu);
-                        const u32 dst = ca ? (u32)lbt[t] - t + pot[t] + Rex - rtb[t] : (u32)p - Rex - Pex + rtb[t];
+                        const u32 dst = ca ? (rpt >> 16) + Rex : (u32)p - Rex - Pex + (rpt & 0xffffu);
                         YA[dst] = (u16)la[i];
                     }
                     ex += (u64)(ca == 1u) | ((u64)(ca == 2u) << 16);
                     if (hasB) {
                         const u32 cb = sb[i] & 3u;
                         if (cb < 2u) {
-                            const u32 t = sb[i] >> 3;
+                            const u32 rpt = rp[sb[i] >> 3];
                             const u32 Rex = (u32)((ex >> 32) & 0xffffu), Pex = (u32)(ex >> 48);
-                            const u32 dst = cb ? (u32)lbt[t] - t + pot[t] + Rex - rtb[t] : (u32)p - Rex - Pex + rtb[t];
+                            const u32 dst = cb ? (rpt >> 16) + Rex : (u32)p - Rex - Pex + (rpt & 0xffffu);
                             YB[dst] = (u16)lb8[i];
                         }
                         ex += ((u64)(cb == 1u) << 32) | ((u64)(cb == 2u) << 48);
@@ -782,8 +789,8 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                 // rank inside the node from bit-sliced ballots: lanes of the
                 // same node (5 node bits), then those with a smaller key
                 u32 eq = __ballot_sync(kFullMask, act);
-#pragma unroll
-                for (int b = 0; b < kWarpSegBits; ++b) {
+                // node ids at depth dd are < 2^(dd+1): only those bits vary
+                for (int b = 0; b <= dd; ++b) {
                     const u32 bit = (nd >> b) & 1u;
                     const u32 bal = __ballot_sync(kFullMask, bit);
                     eq &= bit ? bal : ~bal;
@@ -804,7 +811,13 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                 if (act) {
                     const u32 off = nd + 1u - (1u << dd);  // node's index among depth dd
                     const u64 J = (Jt << dd) + off;
-                    const u32 po = pivot_off_l(sh2, J);
+                    // 32-bit: J << sh2 <= 2^(L-1) and B < 2^31 for n < 2^31
+                    u32 po = 0;
+                    if (sh2 > 0) {
+                        const u32 cw = 1u << (sh2 - 1), lo = (u32)J << sh2;
+                        u32 on = (u32)Bn > lo ? (u32)Bn - lo : 0u;
+                        po = cw - 1u + (on < cw ? on : cw);
+                    }
                     if (rank == po) {
                         ntab[(1u << (dl + dd)) - 1u + ((u32)t << dd) + off] = (u16)lid;
                         act = false;
