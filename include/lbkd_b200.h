@@ -143,6 +143,11 @@ int lbkd_profile_kernel(lbkd_ctx *ctx, int cls, int *n_launches, double *ms, dou
  * digit pass (1) kernel. */
 int lbkd_set_algorithm(lbkd_ctx *ctx, int algo);
 int lbkd_get_algorithm(const lbkd_ctx *ctx);
+/* In-CTA phase (the last levels, one CTA per subtree): -1 = default per
+ * split rule (round-robin: presorted chain lists; widest: per-level
+ * selection), 0 = presorted lists, 1 = selection.  Env LBKD_SUBTREE=lists|sel
+ * at context creation.  Both are bit-exact. */
+int lbkd_set_subtree_kernel(lbkd_ctx *ctx, int which);
 const char *lbkd_strerror(int code);
 const char *lbkd_last_cuda_error(void);
 

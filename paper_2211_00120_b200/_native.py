@@ -34,6 +34,7 @@ EXPORTED = (
     "lbkd_build_rr_top", "lbkd_build_rr_sub",
     "lbkd_profile_kernel", "lbkd_set_algorithm", "lbkd_get_algorithm",
     "lbkd_build_rr_host", "lbkd_build_widest_host", "lbkd_host_join",
+    "lbkd_set_subtree_kernel",
 )
 
 # kernel classes of lbkd_profile_kernel
@@ -115,6 +116,8 @@ def load():
         lib.lbkd_build_widest_host.restype = i32
         lib.lbkd_host_join.argtypes = [vp, vp, i32]
         lib.lbkd_host_join.restype = i32
+        lib.lbkd_set_subtree_kernel.argtypes = [vp, i32]
+        lib.lbkd_set_subtree_kernel.restype = i32
         lib.lbkd_strerror.argtypes = [i32]
         lib.lbkd_strerror.restype = ctypes.c_char_p
         lib.lbkd_last_cuda_error.argtypes = []
@@ -174,6 +177,12 @@ def set_algorithm(algo: str, device: int = 0) -> None:
     """Global-level algorithm of this thread's context: "select" (pivot
     selection + stable partition, default) or "sort" (per-level radix sort)."""
     check(load().lbkd_set_algorithm(context(device), ALGORITHMS.index(algo)), "lbkd_set_algorithm")
+
+
+def set_subtree_kernel(which: str, device: int = 0) -> None:
+    """In-CTA phase of this thread's context: "default", "lists" or "selection"."""
+    code = {"default": -1, "lists": 0, "selection": 1}[which]
+    check(load().lbkd_set_subtree_kernel(context(device), code), "lbkd_set_subtree_kernel")
 
 
 def get_algorithm(device: int = 0) -> str:

@@ -852,6 +852,12 @@ int lbkd_set_algorithm(lbkd_ctx* c, int algo) {
 
 int lbkd_get_algorithm(const lbkd_ctx* c) { return c ? c->algo : -1; }
 
+int lbkd_set_subtree_kernel(lbkd_ctx* c, int which) {
+    if (!c || which < -1 || which > 1) return LBKD_EINVAL_SHAPE;
+    c->subtree_sel = which;
+    return LBKD_OK;
+}
+
 const char* lbkd_strerror(int code) {
     switch (code) {
         case LBKD_OK: return "ok";

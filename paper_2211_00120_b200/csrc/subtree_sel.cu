@@ -458,17 +458,38 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             u32 tiemask = 0;  // widest: dims with equal coordinates in the segment
             for (int d = 0; d < k; ++d) {
                 const u32 key = act ? flip_key(P[d * Mp + lid]) : 0u;
-                u32 rank = 0;
-                bool tie = false;
-                for (int i = 0; i < 32; ++i) {
-                    const u32 ok = __shfl_sync(kFullMask, key, i);
-                    if (((actm >> i) & 1u) && i != lane) {
-                        rank += ok < key ? 1u : 0u;
-                        tie |= ok == key;
+                // bitonic sort of (key, lane) over the warp: lane p ends with
+                // the p-th smallest point, i.e. the rank of point bid is p
+                u32 bk = act ? key : 0xffffffffu, bid = (u32)lane;
+#pragma unroll
+                for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+                    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                        const u32 ok = __shfl_xor_sync(kFullMask, bk, stride);
+                        const u32 oi = __shfl_xor_sync(kFullMask, bid, stride);
+                        const bool asc = (lane & size) == 0;
+                        const bool lower = (lane & stride) == 0;
+                        const bool psmall = ok < bk || (ok == bk && oi < bid);
+                        if ((lower == asc) == psmall) { bk = ok; bid = oi; }
                     }
                 }
-                const u32 tiem = __ballot_sync(kFullMask, act && tie);
-                if (tiem) {
+                const u32 nk = __shfl_down_sync(kFullMask, bk, 1);
+                const u32 tiem = __ballot_sync(kFullMask, lane + 1 < (int)sz && nk == bk);
+                u32 rank = 0;
+                if (!tiem) {
+                    wrk[d * 32 + bid] = (uint8_t)lane;
+                    __syncwarp();
+                    rank = wrk[d * 32 + lane];
+                } else {
+                    // equal coordinates: exact ranks by comparison (chain on ties)
+                    bool tie = false;
+                    for (int i = 0; i < 32; ++i) {
+                        const u32 ok = __shfl_sync(kFullMask, key, i);
+                        if (((actm >> i) & 1u) && i != lane) {
+                            rank += ok < key ? 1u : 0u;
+                            tie |= ok == key;
+                        }
+                    }
                     tiemask |= 1u << d;
                     Chain ch;
                     if (rr_exact) rr_chain(d + ((lam - d + k - 1) / k) * k, k, ch);  // a level with dim d
@@ -482,6 +503,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                         }
                     }
                 }
+                __syncwarp();
                 wrk[d * 32 + lane] = (uint8_t)rank;
             }
             __syncwarp();

@@ -307,3 +307,19 @@ def test_pipelined_host_builds():
         host_join()
     build_round_robin_host(hin[1], hout[1], hperm[1])  # the flag was cleared
     host_join()
+
+
+@pytest.mark.parametrize("n", [5000, 70001, 1 << 20])
+def test_selection_subtree_kernel_for_round_robin(n):
+    """The in-CTA selection kernel (default for widest) is bit-exact for
+    round-robin too, including tie-heavy input and small trees."""
+    from paper_2211_00120_b200 import _native
+
+    _native.set_subtree_kernel("selection")
+    try:
+        for kind, k in (("uniform", 3), ("ties", 2), ("clustered", 4), ("signed_zero", 3)):
+            pts = datagen.make(kind, n, k, seed=n + 3 * k)
+            _, perm = gpu_rr(pts)
+            assert np.array_equal(perm, oracle.build_rr(pts)), (kind, n, k)
+    finally:
+        _native.set_subtree_kernel("default")
