@@ -102,7 +102,21 @@ static void prof_end(lbkd_ctx* c, cudaStream_t st, int cls, double bytes) {
     c->n_ev_used += 2;
 }
 
+static int choose_bits_default(int k, int mode);
+
+// subtree capacity bits: M = 2^b - 1 points per CTA (lam0 = L - b); env
+// LBKD_SUBTREE_BITS lowers it (tuning experiments)
 static int choose_bits(int k, int mode) {
+    int b = choose_bits_default(k, mode);
+    const char* e = getenv("LBKD_SUBTREE_BITS");
+    if (e && b > 0) {
+        const int want = atoi(e);
+        if (want >= 9 && want < b) b = want;
+    }
+    return b;
+}
+
+static int choose_bits_default(int k, int mode) {
     const size_t limit = 227 * 1024 - 256;  // one CTA per SM (general / trace kernel)
     const size_t two = 113 * 1024;           // two CTAs per SM
     const size_t four = 56 * 1024;           // four CTAs per SM
