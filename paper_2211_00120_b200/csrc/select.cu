@@ -463,7 +463,8 @@ __device__ __forceinline__ u32 rec_field(const u32* rec, const Chain& ch, int f,
     return f < (int)ch.m ? flip_key(__uint_as_float(rec[ch.d[f]])) : rec[k];
 }
 
-__global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T) {
+template <int NT>
+__global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
     __shared__ u32 hist[256];
     __shared__ u32 red[2][32];
     __shared__ u32 s_misc[4];
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
         while (n > 1) {
             // live range of field f
             u32 mn = 0xffffffffu, mx = 0u;
-            for (u32 i = tid; i < n; i += kSThreads) {
+            for (u32 i = tid; i < n; i += NT) {
                 const u32 v = rec_field(src + (u64)i * R, ch, f, k);
                 mn = min(mn, v);
                 mx = max(mx, v);
@@ -511,11 +512,11 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
             mn = __reduce_min_sync(kFullMask, mn);
             mx = __reduce_max_sync(kFullMask, mx);
             if (lane == 0) { red[0][warp] = mn; red[1][warp] = mx; }
-            hist[tid] = 0u;
+            for (int i = tid; i < 256; i += NT) hist[i] = 0u;
             __syncthreads();
             if (tid == 0) {
                 u32 a0 = 0xffffffffu, b0 = 0u;
-                for (int w = 0; w < kSThreads / 32; ++w) { a0 = min(a0, red[0][w]); b0 = max(b0, red[1][w]); }
+                for (int w = 0; w < NT / 32; ++w) { a0 = min(a0, red[0][w]); b0 = max(b0, red[1][w]); }
                 s_misc[0] = a0;
                 s_misc[1] = b0;
             }
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
             mx = s_misc[1];
             if (mn == mx) break;  // field constant over the candidates
             const u32 sh = bucket_shift(mn, mx, 8);
-            for (u32 i = tid; i < n; i += kSThreads)
+            for (u32 i = tid; i < n; i += NT)
                 atomicAdd(&hist[(rec_field(src + (u64)i * R, ch, f, k) - mn) >> sh], 1u);
             __syncthreads();
             if (tid == 0) {
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
             r -= s_misc[3];
             const u32 cnt = hist[bsel];
             u32* dst = bufs[nb_flip];
-            for (u32 i0 = 0; i0 < n; i0 += kSThreads) {
+            for (u32 i0 = 0; i0 < n; i0 += NT) {
                 const u32 i = i0 + tid;
                 bool hit = false;
                 if (i < n) {
@@ -601,14 +602,14 @@ __global__ void __launch_bounds__(kSThreads) sel_select_kernel(SelArgs a, int T)
     // per-tile counts below the pivot -> exclusive prefixes in tile order
     __syncthreads();
     u32 carry = 0;
-    for (u64 t0 = tfirst; t0 <= tlast; t0 += kSThreads) {
+    for (u64 t0 = tfirst; t0 <= tlast; t0 += NT) {
         const u64 t = t0 + tid;
         u32* slot = t <= tlast ? &a.tile_lt[t * 2 + (t == tfirst ? pfirst : 0u)] : nullptr;
         const u32 v = slot ? *slot : 0u;
         const u32 ex = block_exclusive_scan<u32>(v, wtot, nullptr);
         if (slot) *slot = carry + ex;
         // chunk total: last thread's inclusive value
-        if (tid == kSThreads - 1) s_misc[1] = ex + v;
+        if (tid == NT - 1) s_misc[1] = ex + v;
         __syncthreads();
         carry += s_misc[1];
         __syncthreads();
@@ -871,7 +872,12 @@ void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
 }
 
 void launch_sel_select(const SelArgs& a, int b, cudaStream_t st) {
-    sel_select_kernel<<<(unsigned)a.g.nseg, kSThreads, 0, st>>>(a, sel_tile(b));
+    // few segments with many candidates (top levels): wide CTAs; many
+    // segments with a few candidates (deep levels): narrow CTAs
+    const unsigned g = (unsigned)a.g.nseg;
+    if (a.g.nseg <= 16) sel_select_kernel<1024><<<g, 1024, 0, st>>>(a, sel_tile(b));
+    else if (a.g.nseg >= 2048) sel_select_kernel<64><<<g, 64, 0, st>>>(a, sel_tile(b));
+    else sel_select_kernel<256><<<g, 256, 0, st>>>(a, sel_tile(b));
 }
 
 void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
