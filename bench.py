@@ -79,6 +79,16 @@ def ncu_traffic():
         return {}
 
 
+def ncu_issue(name):
+    """Issue-rate roofline of an SM-bound kernel from its committed ncu capture
+    (profiles/ncu_issue_<name>.json, tools/ncu_issue.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_issue_{name}.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 KERNEL_NAMES = {
     "partition": "sel_part_kernel (stable 3-way partition, global levels)",
     "subtree": "subtree_rr_kernel / subtree_kernel (in-CTA levels)",
@@ -412,6 +422,7 @@ def main():
                          "by shared-memory instruction issue, not HBM -- see 'kernels' and DESIGN.md"),
             },
             "kernels": kern,
+            "issue_roofline": None,
             "model": {
                 "note": "SURVEY.md 8(d) fixed byte model of the 64-bit-key tag-and-sort algorithm",
                 "bytes": model_B,
@@ -423,6 +434,20 @@ def main():
             "output_is_permutation": ok,
         }
         line["e2e"]["value"] = round(total_pts / (e2e_ms / 1000.0) / 1e6, 2)
+        iss = ncu_issue(dom)
+        if iss is not None:
+            # the in-CTA kernel is bound by instruction issue, not HBM: its
+            # warp instructions (ncu) over the B200 issue peak (148 SMs x 4
+            # schedulers x 1 warp-instruction / cycle) vs its live device time
+            line["issue_roofline"] = {
+                "kernel": iss["kernel"],
+                "warp_instructions": iss["warp_instructions"],
+                "issue_peak_warp_inst_per_s": iss["issue_peak_warp_inst_per_s"],
+                "issue_bound_ms": round(iss["issue_bound_ms"], 3),
+                "live_ms": round(kms, 3),
+                "frac": round(iss["issue_bound_ms"] / kms, 4) if kms > 0 else None,
+                "source": "profiles/ncu_issue_%s.json (ncu --set full of the same build)" % dom,
+            }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(k, args.dist)
         print(json.dumps(line), flush=True)

@@ -9,6 +9,7 @@ python tools/ncu_traffic.py gpurun_out/launches_100m.csv gpurun_out/ncu_traffic.
 cp gpurun_out/ncu_traffic.json profiles/ncu_traffic.json
 ncu --set full --clock-control none --import-source on -k regex:sel_part -s 4 -c 1 -o gpurun_out/part python tools/one_build.py 100000000 3 rr uniform 1 > gpurun_out/prof2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:subtree -c 1 -o gpurun_out/subrr python tools/one_build.py 100000000 3 rr uniform 1 > gpurun_out/prof3.log 2>&1
+python tools/ncu_issue.py gpurun_out/subrr.ncu-rep gpurun_out/ncu_issue_subtree.json > /dev/null && cp gpurun_out/ncu_issue_subtree.json profiles/
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log > gpurun_out/bench.json; cat gpurun_out/bench.json | cut -c1-400
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -1 gpurun_out/bench_ref.json | cut -c1-300
 cat gpurun_out/launches_100m.txt
