@@ -808,6 +808,177 @@ __global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 2 : 1) sel_part_kernel(
     }
 }
 
+// Bulk-copy variant (k <= 4): every warp streams its subtiles through a
+// private 3-stage shared-memory ring filled by cp.async.bulk (the TMA engine)
+// with one mbarrier per stage -- two subtiles in flight per warp without
+// holding them in registers.
+constexpr int kPStages = 3;
+
+template <int KMAX, int D0>
+__global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, int T) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int k = a.k, A = k + 1;
+    const LevelGeom& g = a.g;
+    const u32* Wsrc = a.bf.w[a.par];
+    u32* Wdst = a.bf.w[a.par ^ 1u];
+    const u64 stride = a.bf.stride;
+    const u64 nsub = (g.nview + kSub - 1) / kSub;
+    const int nsub_tile = T / kSub;
+    const u32 lt = lanemask_lt();
+    const u64 sstep = (u64)gridDim.x * (kPThreads / 32);
+    const int warp = threadIdx.x >> 5;
+    u64* bars = reinterpret_cast<u64*>(smem_raw) + warp * kPStages;
+    u32* ring = reinterpret_cast<u32*>(smem_raw + 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1)) +
+                (size_t)warp * kPStages * (KMAX + 1) * kSub;
+    if (lane == 0) {
+        for (int st = 0; st < kPStages; ++st) mbar_init(&bars[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](u64 s2, int st) {  // lane 0
+        const u64 ss2 = s2 * kSub;
+        const u64 cnt2 = g.nview - ss2 < (u64)kSub ? g.nview - ss2 : (u64)kSub;
+        const u32 bytes = (u32)(((cnt2 + 3) & ~3ull) * 4);  // arrays padded to 4 words
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of the stage
+        mbar_expect_tx(&bars[st], bytes * (u32)A);
+        for (int c = 0; c < A; ++c)
+            bulk_g2s(ring + ((size_t)st * (KMAX + 1) + c) * kSub, Wsrc + (u64)c * stride + ss2, bytes, &bars[st]);
+    };
+    u64 s = (u64)blockIdx.x * (kPThreads / 32) + warp;
+    if (lane == 0) {
+        for (int q = 0; q < kPStages - 1; ++q)
+            if (s + q * sstep < nsub) issue(s + q * sstep, q);
+    }
+    u32 phases = 0u;
+    int stage = 0;
+    for (; s < nsub; s += sstep) {
+        const u64 ss = s * kSub;
+        const u64 cnt = g.nview - ss < (u64)kSub ? g.nview - ss : (u64)kSub;
+        const bool full = cnt == (u64)kSub;
+        if (lane == 0 && s + (kPStages - 1) * sstep < nsub)
+            issue(s + (kPStages - 1) * sstep, (stage + kPStages - 1) % kPStages);
+        mbar_wait(&bars[stage], (phases >> stage) & 1u);
+        phases ^= 1u << stage;
+        const u32* sv = ring + (size_t)stage * (KMAX + 1) * kSub + lane;
+#define V(c, i) (sv[(c) * kSub + (i) * 32])
+        // geometry (warp-uniform)
+        const TileParts tp = tile_parts(g, ss, cnt);
+        const u64 t = ss / (u64)T;
+        const u64 j0t = v_seg_of(g, t * (u64)T);  // the tile's first segment
+        const int sin = (int)(s - t * (u64)nsub_tile);  // subtile inside the tile
+        long long bL0 = 0, bR0 = 0, bL1 = 0, bR1 = 0;
+        int d00 = 0, d01 = 0;
+        u32 y00 = 0, y01 = 0;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            if (p == 1 && !tp.has1) continue;
+            const u64 j = tp.j0 + p;
+            const u32 pt = j == j0t ? 0u : 1u;
+            // below-pivot elements of segment j before this subtile
+            u32 below = lane < sin ? a.sub_lt[(t * (u64)nsub_tile + lane) * 2 + pt] : 0u;
+            below = __reduce_add_sync(kFullMask, below) + a.tile_lt[t * 2 + pt];
+            const u64 ib = p ? tp.ib1 : tp.ib0;
+            const u64 before = ss > ib ? ss - ib : 0ull;
+            const u64 pb = (before > 0 && a.ppos[j] < ss) ? 1ull : 0ull;
+            const long long l = (long long)(ib + below);
+            const long long rr = (long long)(ib + v_pivot(g, j) + 1 + (before - below - pb));
+            const int d = a.chains[j].d[0];
+            const u32 y = flip_key(__uint_as_float(a.piv[j * A + d]));
+            if (p == 0) { bL0 = l; bR0 = rr; d00 = d; y00 = y; }
+            else { bL1 = l; bR1 = rr; d01 = d; y01 = y; }
+        }
+        const u32 r0a = tp.r0a, r0b = tp.r0b, r1a = tp.r1a, r1b = tp.r1b;
+        if (D0 >= 0 && full && !tp.has1 && r0a == 0 && r0b == (u32)kSub) {
+            // lean path: one segment part covers the whole subtile
+            const float yf = __uint_as_float(a.piv[tp.j0 * A + (D0 >= 0 ? D0 : 0)]);
+            u32 bl = (u32)bL0, br = (u32)bR0;
+            u32* dbase = Wdst + lane * 0;
+#pragma unroll
+            for (int i = 0; i < kPRows; ++i) {
+                const float xf = __uint_as_float(V(D0 >= 0 ? D0 : 0, i));
+                int side = xf < yf ? 0 : (xf > yf ? 1 : 2);  // -0.0 == +0.0 like numpy
+                if (side == 2) side = part_tie_side(a, tp.j0, ss + (u64)(i * 32 + lane));
+                const u32 ml = __ballot_sync(kFullMask, side == 0);
+                const u32 mr = __ballot_sync(kFullMask, side == 1);
+                const u32 dst = side == 0 ? bl + __popc(ml & lt) : br + __popc(mr & lt);
+                bl += __popc(ml);
+                br += __popc(mr);
+                if (side < 2) {
+#pragma unroll
+                    for (int c = 0; c <= KMAX; ++c)
+                        if (c < A) dbase[(u64)c * stride + dst] = V(c, i);
+                }
+            }
+        } else {
+#pragma unroll
+        for (int i = 0; i < kPRows; ++i) {
+            const u32 r = (u32)(i * 32 + lane);
+            const bool in0 = r >= r0a && r < r0b, in1 = r >= r1a && r < r1b;
+            int side = 2;  // 2: pivot or outside the parts
+            if (in0 || in1) {
+                const int dd = in1 ? d01 : d00;
+                u32 x = 0;
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c)
+                    if (c == dd) x = V(c, i);
+                x = flip_key(__uint_as_float(x));
+                const u32 y = in1 ? y01 : y00;
+                if (x != y) {
+                    side = x < y ? 0 : 1;
+                } else {  // tie in the leading field: the rest of the chain, then the index
+                    const u64 j = tp.j0 + (in1 ? 1 : 0);
+                    const Chain* ch = a.chains + j;
+                    const u32* pv = a.piv + j * A;
+                    const u32 mm = ch->m;
+                    for (u32 f = 1; f < mm && side == 2; ++f) {
+                        const int d = ch->d[f];
+                        u32 xx = 0;
+#pragma unroll
+                        for (int c = 0; c < KMAX; ++c)
+                            if (c == d) xx = V(c, i);
+                        xx = flip_key(__uint_as_float(xx));
+                        const u32 yy = flip_key(__uint_as_float(pv[d]));
+                        if (xx != yy) side = xx < yy ? 0 : 1;
+                    }
+                    if (side == 2) {
+                        u32 xx = 0;
+#pragma unroll
+                        for (int c = 0; c <= KMAX; ++c)
+                            if (c == k) xx = V(c, i);
+                        const u32 yy = pv[k];
+                        side = xx < yy ? 0 : (xx > yy ? 1 : 2);
+                    }
+                }
+            }
+            const u32 ml = __ballot_sync(kFullMask, side == 0);
+            const u32 mr = __ballot_sync(kFullMask, side == 1);
+            const u32 pm = __ballot_sync(kFullMask, in1);
+            long long dst = -1;
+            if (side < 2) {
+                const u32 m = (side == 0 ? ml : mr) & (in1 ? pm : ~pm);
+                const long long base = side == 0 ? (in1 ? bL1 : bL0) : (in1 ? bR1 : bR0);
+                dst = base + __popc(m & lt);
+            }
+            // advance the four run bases by this row's counts
+            bL0 += __popc(ml & ~pm);
+            bR0 += __popc(mr & ~pm);
+            bL1 += __popc(ml & pm);
+            bR1 += __popc(mr & pm);
+            if (dst >= 0) {
+#pragma unroll
+                for (int c = 0; c <= KMAX; ++c)
+                    if (c < A) Wdst[(u64)c * stride + (u64)dst] = V(c, i);
+            }
+        }
+        }
+#undef V
+        __syncwarp();  // every lane is done with this stage before it is refilled
+        stage = stage + 1 == kPStages ? 0 : stage + 1;
+    }
+}
+
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -889,12 +1060,20 @@ void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
     if (grid > cap) grid = cap;
     // register-resident subtile: (KMAX + 1) x 8 words per lane
     const int d0 = a.mode == kRoundRobin ? a.g.l % a.k : -1;  // RR: every segment splits dim l mod k
+    auto bulk_go = [&](auto kern, int KM) {
+        const size_t sm = 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1) +
+                          sizeof(u32) * (size_t)(kPThreads / 32) * kPStages * (KM + 1) * kSub;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        u64 g2 = (nsub + per_cta - 1) / per_cta;
+        if (g2 > 148ull * 2) g2 = 148ull * 2;  // two CTAs per SM, persistent
+        kern<<<(unsigned)g2, kPThreads, sm, st>>>(a, T);
+    };
 #define LBKD_PART(KM)                                                                          \
     switch (d0) {                                                                              \
-        case 0: sel_part_kernel<KM, 0><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;     \
-        case 1: sel_part_kernel<KM, (KM > 1 ? 1 : 0)><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break; \
-        case 2: sel_part_kernel<KM, (KM > 2 ? 2 : 0)><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break; \
-        case 3: sel_part_kernel<KM, (KM > 3 ? 3 : 0)><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break; \
+        case 0: bulk_go(sel_part_bulk_kernel<KM, 0>, KM); break;                               \
+        case 1: bulk_go(sel_part_bulk_kernel<KM, (KM > 1 ? 1 : 0)>, KM); break;                \
+        case 2: bulk_go(sel_part_bulk_kernel<KM, (KM > 2 ? 2 : 0)>, KM); break;                \
+        case 3: bulk_go(sel_part_bulk_kernel<KM, (KM > 3 ? 3 : 0)>, KM); break;                \
         default: sel_part_kernel<KM, -1><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;   \
     }
     switch (a.k) {
