@@ -41,6 +41,26 @@ struct lbkd_ctx {
     int64_t launches = 0;
     int algo = 0;      // 0: select + partition (default), 1: per-level sort
     int subtree_sel = -1;  // in-CTA phase: -1 default per mode, 1 selection (subtree_sel.cu), 0 lists
+    // CUDA graph of the last build (select path, no profiling / trace):
+    // replayed when the same build is requested again (no launch gaps)
+    int use_graph = 1;
+    cudaStream_t cap_stream = nullptr;
+    cudaEvent_t cap_fork = nullptr, cap_join = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    struct GraphKey {
+        const void* pts;
+        const void* out;
+        const void* perm;
+        const void* dims;
+        int64_t n;
+        int k, mode, algo, sub, check, profile;
+        bool operator==(const GraphKey& o) const {
+            return pts == o.pts && out == o.out && perm == o.perm && dims == o.dims && n == o.n && k == o.k &&
+                   mode == o.mode && algo == o.algo && sub == o.sub && check == o.check && profile == o.profile;
+        }
+    } gkey{};
+    int64_t glaunches = 0;
+    int gn_ev = 0;  // profiling events recorded by the captured build
     int err_sticky = 0;  // pipelined host builds: the non-finite flag accumulates until lbkd_host_join
     // pipelined host-buffer builds (lbkd_build_*_host): two device buffer
     // sets alternate, H2D / build / D2H run on three streams
@@ -142,9 +162,13 @@ static int choose_bits_default(int k, int mode) {
         }                                      \
     } while (0)
 
+static void drop_graph(lbkd_ctx* c);
+static thread_local lbkd_ctx* g_grow_ctx = nullptr;  // the context whose buffers grow() reallocates
+
 template <typename T>
 static int grow(T*& p, size_t& cap_unused, size_t count) {
     (void)cap_unused;
+    if (g_grow_ctx) drop_graph(g_grow_ctx);  // captured graphs point at the old buffers
     if (p) cudaFree(p);
     p = nullptr;
     cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 256);
@@ -156,7 +180,16 @@ static int grow(T*& p, size_t& cap_unused, size_t count) {
     return LBKD_OK;
 }
 
+static void drop_graph(lbkd_ctx* c) {
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    c->gkey = lbkd_ctx::GraphKey{};
+}
+
 static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
+    g_grow_ctx = c;
     size_t dummy = 0;
     int rc;
     // W[2] holds k+1 SoA arrays of n words each (only when global levels run)
@@ -458,6 +491,52 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.split_dims = d_dims ? d_dims : c->dims_scratch;
     bp.dbg = d_trace;
     bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : (mode == kWidest ? 1 : 0);
+    // the select path is a fixed, host-sync-free sequence for given buffers:
+    // capture it once into a CUDA graph and replay it (the sort path carries
+    // per-launch lookback epochs and is always launched directly)
+    // (profiled builds launch directly: event timing of graph-recorded events
+    // is not available)
+    const bool graphable = c->use_graph && c->algo == 0 && !c->profile && !d_trace && bp.pts == d_points;
+    lbkd_ctx::GraphKey key{d_points, d_out, d_perm, d_dims, n_in, k, mode, c->algo, bp.subtree_sel, c->check,
+                           c->profile};
+    if (graphable && c->gexec && c->gkey == key) {
+        CK(cudaGraphLaunch(c->gexec, st));
+        c->launches = c->glaunches;
+        c->n_ev_used = c->gn_ev;
+        c->k_last = k;
+        return end_build(c, st);
+    }
+    if (graphable) {
+        if (!c->cap_stream) {
+            CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->cap_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->cap_join, cudaEventDisableTiming));
+        }
+        if (c->gexec) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+        int r2 = begin_build(c, k, c->cap_stream);
+        if (!r2) r2 = prologue(c, bp, lam0, c->cap_stream);
+        if (!r2) r2 = run_levels(c, bp, 0, lam0, c->cap_stream);
+        if (!r2) r2 = run_subtrees(c, bp, lam0, c->cap_stream);
+        const cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &graph);
+        if (r2) {
+            if (graph) cudaGraphDestroy(graph);
+            return r2;
+        }
+        CK(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&c->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(ie);
+        c->gkey = key;
+        c->glaunches = c->launches;
+        c->gn_ev = c->n_ev_used;
+        CK(cudaGraphLaunch(c->gexec, st));
+        return end_build(c, st);
+    }
     if ((rc = begin_build(c, k, st))) return rc;
     if ((rc = prologue(c, bp, lam0, st))) return rc;
     if ((rc = run_levels(c, bp, 0, lam0, st))) return rc;
@@ -678,6 +757,8 @@ int lbkd_create(lbkd_ctx** out, int device) {
     c->device = device;
     const char* algo = getenv("LBKD_ALGO");
     if (algo && strcmp(algo, "sort") == 0) c->algo = 1;
+    const char* gr = getenv("LBKD_GRAPH");
+    if (gr && strcmp(gr, "0") == 0) c->use_graph = 0;
     const char* sub = getenv("LBKD_SUBTREE");
     if (sub && strcmp(sub, "lists") == 0) c->subtree_sel = 0;
     if (sub && strcmp(sub, "sel") == 0) c->subtree_sel = 1;
@@ -688,6 +769,12 @@ int lbkd_create(lbkd_ctx** out, int device) {
 void lbkd_destroy(lbkd_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->cap_stream) {
+        cudaStreamDestroy(c->cap_stream);
+        cudaEventDestroy(c->cap_fork);
+        cudaEventDestroy(c->cap_join);
+    }
     if (c->hp.s_h2d) {
         cudaDeviceSynchronize();
         for (int i = 0; i < 2; ++i) {
