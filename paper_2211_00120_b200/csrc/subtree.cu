@@ -795,19 +795,14 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                     const u32 bal = __ballot_sync(kFullMask, bit);
                     eq &= bit ? bal : ~bal;
                 }
-                u32 lt = 0u;
-#pragma unroll
-                for (int b = kWarpSegBits - 1; b >= 0; --b) {
-                    const u32 bit = (key >> b) & 1u;
-                    const u32 bal = __ballot_sync(kFullMask, bit);
-                    if (bit) {
-                        lt |= eq & ~bal;
-                        eq &= bal;
-                    } else {
-                        eq &= ~bal;
-                    }
+                // the keys (segment-local ranks < 31) present in my node as
+                // a bit set: one segmented OR over each node's lanes (every
+                // active lane of a node passes the same mask)
+                u32 rank = 0;
+                if (act) {
+                    const u32 keys = __reduce_or_sync(eq, 1u << key);
+                    rank = (u32)__popc(keys & ((1u << key) - 1u));
                 }
-                const u32 rank = (u32)__popc(lt);
                 if (act) {
                     const u32 off = nd + 1u - (1u << dd);  // node's index among depth dd
                     const u64 J = (Jt << dd) + off;

@@ -538,22 +538,19 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                     // bit-sliced ballots: lanes of my node (5 node bits), then
                     // those with a smaller precomputed rank (5 rank bits)
                     const u32 key = act ? (u32)wrk[d * 32 + lane] : 0u;
-                    u32 eq = actm & __ballot_sync(kFullMask, act);
-#pragma unroll
-                    for (int bb = 0; bb < 5; ++bb) {
+                    u32 eq = __ballot_sync(kFullMask, act);
+                    for (int bb = 0; bb <= dd; ++bb) {  // node ids at depth dd use dd + 1 bits
                         const u32 bit = (nd >> bb) & 1u;
                         const u32 bal = __ballot_sync(kFullMask, bit);
                         eq &= bit ? bal : ~bal;
                     }
-                    u32 lt = 0u;
-#pragma unroll
-                    for (int bb = 4; bb >= 0; --bb) {
-                        const u32 bit = (key >> bb) & 1u;
-                        const u32 bal = __ballot_sync(kFullMask, bit);
-                        if (bit) { lt |= eq & ~bal; eq &= bal; }
-                        else eq &= ~bal;
+                    // ranks (< 31) present in my node as a bit set: one
+                    // segmented OR over each node's lanes
+                    rank = 0;
+                    if (act) {
+                        const u32 keys = __reduce_or_sync(eq, 1u << key);
+                        rank = (u32)__popc(keys & ((1u << key) - 1u));
                     }
-                    rank = (u32)__popc(lt);
                 } else {
                     // widest with equal coordinates in this dim: full chain comparisons
                     const u32 key = act ? flip_key(P[d * Mp + lid]) : 0u;
