@@ -310,13 +310,19 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
     Buffers& bf = c->bf;
     const int k = bp.k;
     const double A = 4.0 * (k + 1);
+    // from level kFuseFrom on (round-robin, k <= 4) each level's histogram
+    // (D = 8) is accumulated by the previous level's partition kernel
+    const int kFuseFrom = 6;
+    const bool fusable = bp.mode == kRoundRobin && k <= 4;
     for (int l = lfrom; l < lto; ++l) {
         const LevelGeom g = view_of(bp, l);
         const u64 nseg = g.nseg;
-        const int D = sel_digit_bits(nseg);
+        const bool fused_in = fusable && l > lfrom && l >= kFuseFrom;
+        const bool fuse_next = fusable && l + 1 < lto && l + 1 >= kFuseFrom;
+        const int D = fused_in ? 8 : sel_digit_bits(nseg);
         const u32 par = (u32)((l - bp.lroot) & 1);
         const double pts = (double)level_points(bp, l);
-        CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
+        if (!fused_in) CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
         CK(cudaMemsetAsync(bf.cand_ctr, 0, sizeof(u32), st));
         {  // per-tile below-pivot counts accumulate atomically in the filter
             const u64 T = (u64)sel_tile(bp.b);
@@ -345,9 +351,11 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.tile_lt = bf.tile_lt;
         a.sub_lt = bf.sub_lt;
         a.ppos = bf.ppos;
-        if (prof_begin(c, st)) return LBKD_ECUDA;
-        launch_sel_hist(a, bp.b, st);
-        prof_end(c, st, kPHist, 4.0 * pts);
+        if (!fused_in) {
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            launch_sel_hist(a, bp.b, st);
+            prof_end(c, st, kPHist, 4.0 * pts);
+        }
         if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_sel_pick(a, st);
         prof_end(c, st, kPPick, 4.0 * (double)(nseg << D));
@@ -357,6 +365,11 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_sel_select(a, bp.b, st);
         prof_end(c, st, kPSelect, 0.0);
+        a.hist_next = nullptr;
+        if (fuse_next) {  // this level's histogram has been read by pick
+            CK(cudaMemsetAsync(bf.hist, 0, (2 * nseg * 256) * sizeof(u32), st));
+            a.hist_next = bf.hist;
+        }
         if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_sel_part(a, bp.b, st);
         // reads every point of the level, writes all but the nodes

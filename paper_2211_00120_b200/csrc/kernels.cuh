@@ -118,6 +118,7 @@ struct SelArgs {
     u32* tile_lt;          // [tiles][2] below-pivot counts -> exclusive prefixes
     u32* sub_lt;           // [subtiles][2] below-pivot counts per 256-position warp subtile
     u32* ppos;             // [nseg] in-order position of each segment's pivot
+    u32* hist_next;        // partition (RR): the next level's histogram (D = 8), or null
     int tiles_per_cta;
     u64 ntiles;
 };

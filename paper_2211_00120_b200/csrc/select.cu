@@ -813,6 +813,9 @@ __global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 2 : 1) sel_part_kernel(
 // with one mbarrier per stage -- two subtiles in flight per warp without
 // holding them in registers.
 constexpr int kPStages = 3;
+// bulk partition smem: [mbarriers][per-warp fused histograms][per-warp rings]
+constexpr size_t kPHistOff = 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1);
+constexpr size_t kPRingOff = kPHistOff + sizeof(u32) * (kPThreads / 32) * 512;
 
 template <int KMAX, int D0>
 __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, int T) {
@@ -829,8 +832,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
     const u64 sstep = (u64)gridDim.x * (kPThreads / 32);
     const int warp = threadIdx.x >> 5;
     u64* bars = reinterpret_cast<u64*>(smem_raw) + warp * kPStages;
-    u32* ring = reinterpret_cast<u32*>(smem_raw + 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1)) +
-                (size_t)warp * kPStages * (KMAX + 1) * kSub;
+    u32* ring = reinterpret_cast<u32*>(smem_raw + kPRingOff) + (size_t)warp * kPStages * (KMAX + 1) * kSub;
     if (lane == 0) {
         for (int st = 0; st < kPStages; ++st) mbar_init(&bars[st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -845,19 +847,47 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
         for (int c = 0; c < A; ++c)
             bulk_g2s(ring + ((size_t)st * (KMAX + 1) + c) * kSub, Wsrc + (u64)c * stride + ss2, bytes, &bars[st]);
     };
-    u64 s = (u64)blockIdx.x * (kPThreads / 32) + warp;
+    // each warp owns a contiguous run of subtiles (the fused histogram of the
+    // next level then changes segment rarely)
+    const u64 nw = (u64)gridDim.x * (kPThreads / 32);
+    const u64 chunk = (nsub + nw - 1) / nw;
+    u64 s = ((u64)blockIdx.x * (kPThreads / 32) + warp) * chunk;
+    const u64 s_end = s + chunk < nsub ? s + chunk : nsub;
     if (lane == 0) {
         for (int q = 0; q < kPStages - 1; ++q)
-            if (s + q * sstep < nsub) issue(s + q * sstep, q);
+            if (s + q < s_end) issue(s + q, q);
+    }
+    // fused histogram of the next level (its two children of one segment,
+    // warp-private 2 x 256 bins), flushed when the segment changes
+    u32* wh = reinterpret_cast<u32*>(smem_raw + kPHistOff) + warp * 512;
+    const bool fuse = a.hist_next != nullptr;
+    u64 hseg = ~0ull;
+    Bucketer hb0{}, hb1{};
+    const int dn = (g.l + 1) % k;
+    auto hflush = [&]() {
+        if (hseg != ~0ull) {
+            for (int i = lane; i < 512; i += 32) {
+                const u32 v = wh[i];
+                if (v) {
+                    atomicAdd(&a.hist_next[(2 * hseg + (i >> 8)) * 256ull + (i & 255)], v);
+                    wh[i] = 0u;
+                }
+            }
+        }
+        __syncwarp();
+    };
+    if (fuse) {
+        for (int i = lane; i < 512; i += 32) wh[i] = 0u;
+        __syncwarp();
     }
     u32 phases = 0u;
     int stage = 0;
-    for (; s < nsub; s += sstep) {
+    for (; s < s_end; ++s) {
         const u64 ss = s * kSub;
         const u64 cnt = g.nview - ss < (u64)kSub ? g.nview - ss : (u64)kSub;
         const bool full = cnt == (u64)kSub;
-        if (lane == 0 && s + (kPStages - 1) * sstep < nsub)
-            issue(s + (kPStages - 1) * sstep, (stage + kPStages - 1) % kPStages);
+        if (lane == 0 && s + (kPStages - 1) < s_end)
+            issue(s + (kPStages - 1), (stage + kPStages - 1) % kPStages);
         mbar_wait(&bars[stage], (phases >> stage) & 1u);
         phases ^= 1u << stage;
         const u32* sv = ring + (size_t)stage * (KMAX + 1) * kSub + lane;
@@ -894,6 +924,14 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
             const float yf = __uint_as_float(a.piv[tp.j0 * A + (D0 >= 0 ? D0 : 0)]);
             u32 bl = (u32)bL0, br = (u32)bR0;
             u32* dbase = Wdst + lane * 0;
+            if (fuse && tp.j0 != hseg) {
+                hflush();
+                hseg = tp.j0;
+                const float* c0 = a.boxes_out + (2 * hseg) * 2ull * k;
+                const float* c1 = c0 + 2 * k;
+                hb0 = make_bucketer(c0[dn], c0[k + dn], 8);
+                hb1 = make_bucketer(c1[dn], c1[k + dn], 8);
+            }
 #pragma unroll
             for (int i = 0; i < kPRows; ++i) {
                 const float xf = __uint_as_float(V(D0 >= 0 ? D0 : 0, i));
@@ -904,6 +942,10 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                 const u32 dst = side == 0 ? bl + __popc(ml & lt) : br + __popc(mr & lt);
                 bl += __popc(ml);
                 br += __popc(mr);
+                if (fuse && side < 2) {
+                    const u32 kn = V(dn, i);
+                    atomicAdd(&wh[side * 256 + bucket_of(side ? hb1 : hb0, kn)], 1u);
+                }
                 if (side < 2) {
 #pragma unroll
                     for (int c = 0; c <= KMAX; ++c)
@@ -951,6 +993,12 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                     }
                 }
             }
+            if (fuse && side < 2) {
+                const u64 j = tp.j0 + (in1 ? 1 : 0);
+                const float* cb = a.boxes_out + (2 * j + side) * 2ull * k;
+                const Bucketer hb = make_bucketer(cb[dn], cb[k + dn], 8);
+                atomicAdd(&a.hist_next[(2 * j + side) * 256ull + bucket_of(hb, V(dn, i))], 1u);
+            }
             const u32 ml = __ballot_sync(kFullMask, side == 0);
             const u32 mr = __ballot_sync(kFullMask, side == 1);
             const u32 pm = __ballot_sync(kFullMask, in1);
@@ -976,6 +1024,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
         __syncwarp();  // every lane is done with this stage before it is refilled
         stage = stage + 1 == kPStages ? 0 : stage + 1;
     }
+    if (fuse) hflush();
 }
 
 
@@ -1061,8 +1110,7 @@ void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
     // register-resident subtile: (KMAX + 1) x 8 words per lane
     const int d0 = a.mode == kRoundRobin ? a.g.l % a.k : -1;  // RR: every segment splits dim l mod k
     auto bulk_go = [&](auto kern, int KM) {
-        const size_t sm = 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1) +
-                          sizeof(u32) * (size_t)(kPThreads / 32) * kPStages * (KM + 1) * kSub;
+        const size_t sm = kPRingOff + sizeof(u32) * (size_t)(kPThreads / 32) * kPStages * (KM + 1) * kSub;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         u64 g2 = (nsub + per_cta - 1) / per_cta;
         if (g2 > 148ull * 2) g2 = 148ull * 2;  // two CTAs per SM, persistent
