@@ -817,6 +817,10 @@ constexpr int kPStages = 3;
 constexpr size_t kPHistOff = 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1);
 constexpr size_t kPRingOff = kPHistOff + sizeof(u32) * (kPThreads / 32) * 512;
 
+struct PHdr {
+    u32 sl[2], tl[2], pp[2], y[2];
+};
+
 template <int KMAX, int D0>
 __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, int T) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -848,14 +852,16 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
             bulk_g2s(ring + ((size_t)st * (KMAX + 1) + c) * kSub, Wsrc + (u64)c * stride + ss2, bytes, &bars[st]);
     };
     // each warp owns a contiguous run of subtiles (the fused histogram of the
-    // next level then changes segment rarely)
+    // next level then changes segment rarely; interleaving the warps of a CTA
+    // over one run measured 10% slower)
     const u64 nw = (u64)gridDim.x * (kPThreads / 32);
     const u64 chunk = (nsub + nw - 1) / nw;
     u64 s = ((u64)blockIdx.x * (kPThreads / 32) + warp) * chunk;
     const u64 s_end = s + chunk < nsub ? s + chunk : nsub;
+    constexpr u64 sd = 1;
     if (lane == 0) {
         for (int q = 0; q < kPStages - 1; ++q)
-            if (s + q < s_end) issue(s + q, q);
+            if (s + q * sd < s_end) issue(s + q * sd, q);
     }
     // fused histogram of the next level (its two children of one segment,
     // warp-private 2 x 256 bins), flushed when the segment changes
@@ -880,50 +886,75 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
         for (int i = lane; i < 512; i += 32) wh[i] = 0u;
         __syncwarp();
     }
+    // per-subtile header: per segment part the lane's sub_lt word, the
+    // tile_lt prefix, the pivot position and the pivot's key
+    const int tsh = 31 - __clz(T);  // T is a power of two
+    auto hdr_load = [&](u64 s2, PHdr& h2) {
+        const u64 ss2 = s2 * kSub;
+        const u64 cnt2 = g.nview - ss2 < (u64)kSub ? g.nview - ss2 : (u64)kSub;
+        const TileParts tp2 = tile_parts(g, ss2, cnt2);
+        const u64 t2 = ss2 >> tsh;
+        const u64 j0t = v_seg_of(g, t2 << tsh);  // the tile's first segment
+        const int sin = (int)(s2 - t2 * (u64)nsub_tile);  // subtile inside the tile
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            h2.sl[p] = 0u; h2.tl[p] = 0u; h2.pp[p] = 0u; h2.y[p] = 0u;
+            if (p == 1 && !tp2.has1) continue;
+            const u64 j = tp2.j0 + p;
+            const u32 pt = j == j0t ? 0u : 1u;
+            h2.sl[p] = lane < sin ? a.sub_lt[(t2 * (u64)nsub_tile + lane) * 2 + pt] : 0u;
+            h2.tl[p] = a.tile_lt[t2 * 2 + pt];
+            h2.pp[p] = a.ppos[j];
+            h2.y[p] = a.piv[j * A + D0];
+        }
+    };
+    PHdr hn;
+    if (s < s_end) hdr_load(s, hn);
+    // per-column destination bases (the stores then need one 32-bit-offset
+    // address add each instead of a 64-bit column*stride product per row)
+    u32* dcol[KMAX + 1];
+#pragma unroll
+    for (int c = 0; c <= KMAX; ++c) dcol[c] = Wdst + (u64)(c < A ? c : 0) * stride;
     u32 phases = 0u;
     int stage = 0;
-    for (; s < s_end; ++s) {
+    for (; s < s_end; s += sd) {
         const u64 ss = s * kSub;
         const u64 cnt = g.nview - ss < (u64)kSub ? g.nview - ss : (u64)kSub;
         const bool full = cnt == (u64)kSub;
-        if (lane == 0 && s + (kPStages - 1) < s_end)
-            issue(s + (kPStages - 1), (stage + kPStages - 1) % kPStages);
+        if (lane == 0 && s + (kPStages - 1) * sd < s_end)
+            issue(s + (kPStages - 1) * sd, (stage + kPStages - 1) % kPStages);
         mbar_wait(&bars[stage], (phases >> stage) & 1u);
         phases ^= 1u << stage;
         const u32* sv = ring + (size_t)stage * (KMAX + 1) * kSub + lane;
 #define V(c, i) (sv[(c) * kSub + (i) * 32])
-        // geometry (warp-uniform)
+        // geometry (warp-uniform); the header words were loaded one subtile
+        // ahead (hdr_load) so their L2 latency overlaps the previous subtile
         const TileParts tp = tile_parts(g, ss, cnt);
-        const u64 t = ss / (u64)T;
-        const u64 j0t = v_seg_of(g, t * (u64)T);  // the tile's first segment
-        const int sin = (int)(s - t * (u64)nsub_tile);  // subtile inside the tile
+        const PHdr h = hn;
+        if (s + sd < s_end) hdr_load(s + sd, hn);
         long long bL0 = 0, bR0 = 0, bL1 = 0, bR1 = 0;
-        int d00 = 0, d01 = 0;
+        const int d00 = D0, d01 = D0;  // round robin: every segment splits dim l mod k
         u32 y00 = 0, y01 = 0;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
             if (p == 1 && !tp.has1) continue;
             const u64 j = tp.j0 + p;
-            const u32 pt = j == j0t ? 0u : 1u;
             // below-pivot elements of segment j before this subtile
-            u32 below = lane < sin ? a.sub_lt[(t * (u64)nsub_tile + lane) * 2 + pt] : 0u;
-            below = __reduce_add_sync(kFullMask, below) + a.tile_lt[t * 2 + pt];
+            const u32 below = __reduce_add_sync(kFullMask, h.sl[p]) + h.tl[p];
             const u64 ib = p ? tp.ib1 : tp.ib0;
             const u64 before = ss > ib ? ss - ib : 0ull;
-            const u64 pb = (before > 0 && a.ppos[j] < ss) ? 1ull : 0ull;
+            const u64 pb = (before > 0 && h.pp[p] < ss) ? 1ull : 0ull;
             const long long l = (long long)(ib + below);
             const long long rr = (long long)(ib + v_pivot(g, j) + 1 + (before - below - pb));
-            const int d = a.chains[j].d[0];
-            const u32 y = flip_key(__uint_as_float(a.piv[j * A + d]));
-            if (p == 0) { bL0 = l; bR0 = rr; d00 = d; y00 = y; }
-            else { bL1 = l; bR1 = rr; d01 = d; y01 = y; }
+            const u32 y = flip_key(__uint_as_float(h.y[p]));
+            if (p == 0) { bL0 = l; bR0 = rr; y00 = y; }
+            else { bL1 = l; bR1 = rr; y01 = y; }
         }
         const u32 r0a = tp.r0a, r0b = tp.r0b, r1a = tp.r1a, r1b = tp.r1b;
         if (D0 >= 0 && full && !tp.has1 && r0a == 0 && r0b == (u32)kSub) {
             // lean path: one segment part covers the whole subtile
             const float yf = __uint_as_float(a.piv[tp.j0 * A + (D0 >= 0 ? D0 : 0)]);
             u32 bl = (u32)bL0, br = (u32)bR0;
-            u32* dbase = Wdst + lane * 0;
             if (fuse && tp.j0 != hseg) {
                 hflush();
                 hseg = tp.j0;
@@ -949,7 +980,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                 if (side < 2) {
 #pragma unroll
                     for (int c = 0; c <= KMAX; ++c)
-                        if (c < A) dbase[(u64)c * stride + dst] = V(c, i);
+                        if (c < A) dcol[c][dst] = V(c, i);
                 }
             }
         } else {
@@ -1016,7 +1047,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
             if (dst >= 0) {
 #pragma unroll
                 for (int c = 0; c <= KMAX; ++c)
-                    if (c < A) Wdst[(u64)c * stride + (u64)dst] = V(c, i);
+                    if (c < A) dcol[c][dst] = V(c, i);
             }
         }
         }
