@@ -148,6 +148,35 @@ int lbkd_get_algorithm(const lbkd_ctx *ctx);
  * selection), 0 = presorted lists, 1 = selection.  Env LBKD_SUBTREE=lists|sel
  * at context creation.  Both are bit-exact. */
 int lbkd_set_subtree_kernel(lbkd_ctx *ctx, int which);
+/* ---- Queries over a built tree -------------------
+ * Replace lbkd.kernels_numpy.knn_search / radius_search
+ * (/root/reference/pkg/src/lbkd/kernels_numpy.py:114-196 and :199-245; the
+ * plugin seam accel.get_kernels(), accel.py:48-58) for a BATCH of queries;
+ * the reference answers one query per call.  All pointers are device
+ * pointers.  d_tree: the build's level-order output, n x k float32 rows;
+ * d_split_dims: u8[n] of a widest tree, or NULL for round-robin (dim =
+ * level(s) mod k).  d_queries: nq x k float64.  Distances are float64 squared
+ * euclidean, bit-identical to the reference's (same accumulation order, no
+ * FMA contraction).
+ *
+ * lbkd_knn: for every query the min(m, n) = m nearest nodes (1 <= m <= n)
+ * ordered by (dist2, node index), into row q of d_out_idx / d_out_d2 (nq x m,
+ * int64 / float64) -- queries.knn (queries.py:41-62) per row. */
+int lbkd_knn(const float *d_tree, int64_t n, int k, const uint8_t *d_split_dims, const double *d_queries,
+             int64_t nq, int m, int64_t *d_out_idx, double *d_out_d2, void *stream);
+/* Radius search in two calls (queries.radius_query, queries.py:65-77):
+ * lbkd_radius_count writes per-query hit counts (dist2 <= r2, boundary
+ * included) to d_counts[nq] and their exclusive prefix sums to
+ * d_offsets[nq + 1] (d_offsets[nq] = total hits); d_scratch holds
+ * lbkd_radius_scratch_len(nq) int64.  After sizing d_out_idx to the total,
+ * lbkd_radius_fill writes every query's hits to d_out_idx[d_offsets[q] ..
+ * d_offsets[q + 1]) sorted ascending. */
+int lbkd_radius_count(const float *d_tree, int64_t n, int k, const uint8_t *d_split_dims, const double *d_queries,
+                      int64_t nq, double r2, int64_t *d_counts, int64_t *d_offsets, int64_t *d_scratch,
+                      void *stream);
+int64_t lbkd_radius_scratch_len(int64_t nq);
+int lbkd_radius_fill(const float *d_tree, int64_t n, int k, const uint8_t *d_split_dims, const double *d_queries,
+                     int64_t nq, double r2, const int64_t *d_offsets, int64_t *d_out_idx, void *stream);
 const char *lbkd_strerror(int code);
 const char *lbkd_last_cuda_error(void);
 

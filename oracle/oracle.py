@@ -14,6 +14,9 @@ Contents
 - ``brute_subtree_boxes``: restatement of verify.brute_subtree_boxes
   (verify.py:347-374).
 - ``treemath`` scalar helpers restated from treemath.py:46-140.
+- ``brute_knn`` / ``brute_radius``: restatements of verify.brute_knn /
+  brute_radius (verify.py:305-320) with the distance accumulation of
+  verify._squared_distances (:295-302) -- the checker of the GPU queries.
 
 Parity pin: tests/test_oracle.py checks these against tests/golden/*, which
 tests/golden/make_golden.py produced by running the reference itself.
@@ -216,3 +219,34 @@ def brute_subtree_boxes(coords, split_dims=None):
             hi[lc + 1] = hi[s]
             lo[lc + 1, d] = max(lo[lc + 1, d], plane)
     return lo, hi
+
+
+# ---------------------------------------------------------------------------
+# query checkers (verify.py:295-320)
+
+def squared_distances(coords, query) -> np.ndarray:
+    """verify._squared_distances (verify.py:295-302): float64, accumulated
+    dim by dim in the traversal kernels' order."""
+    coords = np.asarray(coords, dtype=np.float64)
+    query = np.asarray(query, dtype=np.float64).reshape(-1)
+    d2 = np.zeros(coords.shape[0], dtype=np.float64)
+    for j in range(coords.shape[1]):
+        t = query[j] - coords[:, j]
+        d2 += t * t
+    return d2
+
+
+def brute_knn(coords, query, m: int):
+    """verify.brute_knn (verify.py:305-312): the m nearest rows by full scan
+    as (index, dist2) pairs ordered by (dist2, index)."""
+    d2 = squared_distances(coords, query)
+    order = np.lexsort((np.arange(d2.shape[0]), d2))
+    take = min(m, d2.shape[0])
+    return [(int(i), float(d2[i])) for i in order[:take]]
+
+
+def brute_radius(coords, query, radius: float) -> np.ndarray:
+    """verify.brute_radius (verify.py:315-320): every index with
+    dist2 <= radius**2, ascending int64."""
+    d2 = squared_distances(coords, query)
+    return np.nonzero(d2 <= float(radius) ** 2)[0].astype(np.int64)

@@ -10,6 +10,7 @@ CUDA behind the C-ABI library in ``_lib/`` (include/lbkd_b200.h).
 
 from .builder import BuildRecorder, KdTree, build_round_robin, build_round_robin_cuda
 from .widest import build_widest, build_widest_cuda
+from .queries import Neighbor, knn, knn_cuda, radius_cuda, radius_query
 
 __all__ = [
     "BuildRecorder",
@@ -18,6 +19,11 @@ __all__ = [
     "build_round_robin_cuda",
     "build_widest",
     "build_widest_cuda",
+    "Neighbor",
+    "knn",
+    "knn_cuda",
+    "radius_cuda",
+    "radius_query",
 ]
 
 __version__ = "0.1.0"

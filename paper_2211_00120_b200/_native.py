@@ -35,6 +35,7 @@ EXPORTED = (
     "lbkd_profile_kernel", "lbkd_set_algorithm", "lbkd_get_algorithm",
     "lbkd_build_rr_host", "lbkd_build_widest_host", "lbkd_host_join",
     "lbkd_set_subtree_kernel",
+    "lbkd_knn", "lbkd_radius_count", "lbkd_radius_scratch_len", "lbkd_radius_fill",
 )
 
 # kernel classes of lbkd_profile_kernel
@@ -118,6 +119,15 @@ def load():
         lib.lbkd_host_join.restype = i32
         lib.lbkd_set_subtree_kernel.argtypes = [vp, i32]
         lib.lbkd_set_subtree_kernel.restype = i32
+        f64 = ctypes.c_double
+        lib.lbkd_knn.argtypes = [vp, i64, i32, vp, vp, i64, i32, vp, vp, vp]
+        lib.lbkd_knn.restype = i32
+        lib.lbkd_radius_count.argtypes = [vp, i64, i32, vp, vp, i64, f64, vp, vp, vp, vp]
+        lib.lbkd_radius_count.restype = i32
+        lib.lbkd_radius_scratch_len.argtypes = [i64]
+        lib.lbkd_radius_scratch_len.restype = i64
+        lib.lbkd_radius_fill.argtypes = [vp, i64, i32, vp, vp, i64, f64, vp, vp, vp]
+        lib.lbkd_radius_fill.restype = i32
         lib.lbkd_strerror.argtypes = [i32]
         lib.lbkd_strerror.restype = ctypes.c_char_p
         lib.lbkd_last_cuda_error.argtypes = []

@@ -28,6 +28,7 @@ void note_cuda(cudaError_t e) {
 }  // namespace
 
 namespace lbkd {
+void note_cuda_error(cudaError_t e) { note_cuda(e); }
 void launch_update_tags_rr(u32* tags, long long n, int levels, int l, cudaStream_t st);
 void launch_update_tags_widest(u32* tags, const double* coords, int k, uint8_t* split_dims, const double* wlo,
                                const double* whi, long long n, int levels, int l, int dim_bits, cudaStream_t st);

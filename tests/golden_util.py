@@ -38,3 +38,43 @@ def small_cases():
             doff += n
         out.append(case)
     return out
+
+
+def query_cases():
+    """The reference's answers in golden/queries.npz (make_golden_queries.py),
+    one dict per tree: generator parameters, reference payload, queries and
+    per query the knn answers for every m in ``ms`` and the radius hits for
+    every radius in ``radii``."""
+    g = np.load(os.path.join(GOLDEN, "queries.npz"))
+    ms = [int(m) for m in g["ms"]]
+    nq = int(g["nq"])
+    out = []
+    po = qo = ko = kc = ro = rc = 0
+    for i in range(len(g["n"])):
+        n, k = int(g["n"][i]), int(g["k"][i])
+        case = {"kind": str(g["kind"][i]), "n": n, "k": k, "seed": int(g["seed"][i]), "mode": str(g["mode"][i])}
+        case["name"] = f"{case['mode']}-{case['kind']}-n{n}-k{k}-s{case['seed']}"
+        case["payload"] = g["payload"][po:po + n]
+        po += n
+        case["queries"] = g["queries"][qo:qo + nq * k].reshape(nq, k)
+        qo += nq * k
+        case["radii"] = [float(r) for r in g["radii"][i]]
+        knn, rad = [], []
+        for _ in range(nq):
+            per_m = {}
+            for m in ms:
+                c = int(g["knn_cnt"][kc])
+                kc += 1
+                per_m[m] = [(int(a), float(b)) for a, b in zip(g["knn_idx"][ko:ko + c], g["knn_d2"][ko:ko + c])]
+                ko += c
+            knn.append(per_m)
+            per_r = []
+            for _r in case["radii"]:
+                c = int(g["rad_cnt"][rc])
+                rc += 1
+                per_r.append(g["rad_idx"][ro:ro + c])
+                ro += c
+            rad.append(per_r)
+        case["knn"], case["radius"] = knn, rad
+        out.append(case)
+    return out

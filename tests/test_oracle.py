@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle
-from tests.golden_util import GOLDEN, gen_case, small_cases
+from tests.golden_util import GOLDEN, gen_case, query_cases, small_cases
 
 
 def sha(a):
@@ -85,3 +85,16 @@ def test_check_valid_catches_planted_violation():
     tree = pts[perm].copy()
     tree[40, 0] = tree[0, 0] + 100.0
     assert not oracle.check_valid(tree)
+
+
+def test_query_checkers_match_reference_answers():
+    """oracle.brute_knn / brute_radius against the reference's own
+    queries.knn / radius_query answers (golden/queries.npz)."""
+    for case in query_cases():
+        pts = gen_case(case)
+        coords = pts[case["payload"]].astype(np.float64)  # the reference tree
+        for qi, q in enumerate(case["queries"]):
+            for m, want in case["knn"][qi].items():
+                assert oracle.brute_knn(coords, q, m) == want, (case["name"], qi, m)
+            for r, want in zip(case["radii"], case["radius"][qi]):
+                assert np.array_equal(oracle.brute_radius(coords, q, r), want), (case["name"], qi, r)
