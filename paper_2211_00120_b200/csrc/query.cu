@@ -45,8 +45,11 @@ __device__ __forceinline__ double dist2(const float* row, const double* q, int k
 }
 
 // Keep-list in local memory (MCAP > 0) or in the caller's output row
-// (MCAP == 0, any m).
-template <int MCAP>
+// (MCAP == 0, any m).  HEAP = false: the reference's sorted insertion (cheap
+// for small m); HEAP = true: a max-heap on (dist2, node), O(log m) per take,
+// heap-sorted at the end.  Both keep exactly the m smallest (dist2, node)
+// pairs, so the answer is the same.
+template <int MCAP, bool HEAP>
 __global__ void __launch_bounds__(128) knn_kernel(const float* __restrict__ tree, u32 n, int k,
                                                   const uint8_t* __restrict__ split_dims,
                                                   const double* __restrict__ queries, u64 nq, int m,
@@ -65,6 +68,19 @@ __global__ void __launch_bounds__(128) knn_kernel(const float* __restrict__ tree
         if (MCAP > 0) { lidx[p] = i; ld2[p] = d; }
         else { oi[p] = i; od[p] = d; }
     };
+    // (d, i) after (pd, pi) in the (dist2, node) order
+    auto after = [](double d, u32 i, double pd, u32 pi) { return d > pd || (d == pd && i > pi); };
+    auto sift_down = [&](int p, int len, u32 i, double d) {  // place (d, i) from slot p down
+        while (true) {
+            int c = 2 * p + 1;
+            if (c >= len) break;
+            if (c + 1 < len && after(D2(c + 1), IDX(c + 1), D2(c), IDX(c))) ++c;
+            if (!after(D2(c), IDX(c), d, i)) break;
+            SET(p, IDX(c), D2(c));
+            p = c;
+        }
+        SET(p, i, d);
+    };
     u32 st_node[kStack];
     double st_d2[kStack];
     int top = 0, count = 0;
@@ -74,23 +90,40 @@ __global__ void __launch_bounds__(128) knn_kernel(const float* __restrict__ tree
         if (node < n) {
             const float* row = tree + (u64)node * k;
             const double d2 = dist2(row, q, k);
-            bool take;
-            if (count < m) take = true;
-            else if (d2 < worst) take = true;
-            else take = d2 == worst && node < IDX(count - 1);
-            if (take) {
-                int pos;
-                if (count < m) pos = count++;
-                else pos = m - 1;
-                while (pos > 0) {
-                    const double pd = D2(pos - 1);
-                    const u32 pi = IDX(pos - 1);
-                    if (!(pd > d2 || (pd == d2 && pi > node))) break;
-                    SET(pos, pi, pd);
-                    --pos;
+            if (HEAP) {
+                if (count < m) {
+                    int p = count++;
+                    while (p > 0) {  // sift up
+                        const int par = (p - 1) >> 1;
+                        if (!after(d2, node, D2(par), IDX(par))) break;
+                        SET(p, IDX(par), D2(par));
+                        p = par;
+                    }
+                    SET(p, node, d2);
+                    if (count == m) worst = D2(0);
+                } else if (!after(d2, node, D2(0), IDX(0))) {  // beats the worst kept
+                    sift_down(0, m, node, d2);
+                    worst = D2(0);
                 }
-                SET(pos, node, d2);
-                if (count == m) worst = D2(m - 1);
+            } else {
+                bool take;
+                if (count < m) take = true;
+                else if (d2 < worst) take = true;
+                else take = d2 == worst && node < IDX(count - 1);
+                if (take) {
+                    int pos;
+                    if (count < m) pos = count++;
+                    else pos = m - 1;
+                    while (pos > 0) {
+                        const double pd = D2(pos - 1);
+                        const u32 pi = IDX(pos - 1);
+                        if (!after(pd, pi, d2, node)) break;
+                        SET(pos, pi, pd);
+                        --pos;
+                    }
+                    SET(pos, node, d2);
+                    if (count == m) worst = D2(m - 1);
+                }
             }
             const int dim = node_dim(split_dims, node, k);
             const double delta = __dsub_rn(q[dim], (double)row[dim]);
@@ -113,6 +146,14 @@ __global__ void __launch_bounds__(128) knn_kernel(const float* __restrict__ tree
                 }
             }
             if (!found) break;
+        }
+    }
+    if (HEAP) {  // heap sort: the max goes to the end, ascending result
+        for (int e = count - 1; e > 0; --e) {
+            const u32 i = IDX(e);
+            const double d = D2(e);
+            SET(e, IDX(0), D2(0));
+            sift_down(0, e, i, d);
         }
     }
     if (MCAP > 0)
@@ -305,13 +346,16 @@ int lbkd_knn(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims,
     const unsigned grid = (unsigned)((nq + 127) / 128);
     const u32 un = (u32)n;
     const u64 unq = (u64)nq;
-#define LBKD_KNN(C) knn_kernel<C><<<grid, 128, 0, st>>>(d_tree, un, k, d_split_dims, d_queries, unq, m, d_out_idx, d_out_d2)
-    if (m <= 1) LBKD_KNN(1);
-    else if (m <= 4) LBKD_KNN(4);
-    else if (m <= 8) LBKD_KNN(8);
-    else if (m <= 16) LBKD_KNN(16);
-    else if (m <= 32) LBKD_KNN(32);
-    else LBKD_KNN(0);
+#define LBKD_KNN(C, H) \
+    knn_kernel<C, H><<<grid, 128, 0, st>>>(d_tree, un, k, d_split_dims, d_queries, unq, m, d_out_idx, d_out_d2)
+    if (m <= 1) LBKD_KNN(1, false);
+    else if (m <= 4) LBKD_KNN(4, false);
+    else if (m <= 8) LBKD_KNN(8, false);
+    else if (m <= 16) LBKD_KNN(16, true);
+    else if (m <= 32) LBKD_KNN(32, true);
+    else if (m <= 64) LBKD_KNN(64, true);
+    else if (m <= 128) LBKD_KNN(128, true);
+    else LBKD_KNN(0, true);
 #undef LBKD_KNN
     return rc_of(finish());
 }
