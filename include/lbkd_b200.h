@@ -177,6 +177,19 @@ int lbkd_radius_count(const float *d_tree, int64_t n, int k, const uint8_t *d_sp
 int64_t lbkd_radius_scratch_len(int64_t nq);
 int lbkd_radius_fill(const float *d_tree, int64_t n, int k, const uint8_t *d_split_dims, const double *d_queries,
                      int64_t nq, double r2, const int64_t *d_offsets, int64_t *d_out_idx, void *stream);
+/* ---- Validation over a built tree ---------------
+ * lbkd_check_valid replaces verify.check_valid (verify.py:195-245): every node
+ * against every ancestor's split plane, closed on both sides.  Writes
+ * d_witness[3] = {descendant, ancestor, dim} of the first violation (lowest
+ * descendant, then nearest ancestor) or {-1, -1, -1} for a valid tree;
+ * d_scratch: one uint64.  lbkd_subtree_boxes replaces
+ * verify.brute_subtree_boxes (verify.py:347-374): d_lo / d_hi (n x k
+ * float64) = world bounds clipped by every ancestor plane (a zero extreme of
+ * the world bounds is reported as +0.0). */
+int lbkd_check_valid(const float *d_tree, int64_t n, int k, const uint8_t *d_split_dims, int64_t *d_witness,
+                     uint64_t *d_scratch, void *stream);
+int lbkd_subtree_boxes(const float *d_tree, int64_t n, int k, const uint8_t *d_split_dims, double *d_lo,
+                       double *d_hi, void *stream);
 const char *lbkd_strerror(int code);
 const char *lbkd_last_cuda_error(void);
 

@@ -9,8 +9,9 @@ Contents
 - ``build_rr`` / ``build_widest``: ctypes front of ``lbkd_oracle.c``, a C
   restatement of the reference's tag-and-sort loop
   (/root/reference/pkg/src/lbkd/builder.py:200-236, widest.py:134-191).
-- ``check_valid``: numpy restatement of verify.check_valid
-  (/root/reference/pkg/src/lbkd/verify.py:195-245).
+- ``check_valid`` / ``validity_witness``: numpy restatement of
+  verify.check_valid (/root/reference/pkg/src/lbkd/verify.py:195-245) and of
+  its witness rescan (:226-243).
 - ``brute_subtree_boxes``: restatement of verify.brute_subtree_boxes
   (verify.py:347-374).
 - ``treemath`` scalar helpers restated from treemath.py:46-140.
@@ -193,6 +194,27 @@ def check_valid(coords, split_dims=None) -> bool:
             return False
         cur = par
     return True
+
+
+def validity_witness(coords, split_dims=None):
+    """The witness of verify.check_valid's deterministic rescan
+    (verify.py:226-243): (descendant, ancestor, dim) of the lowest violating
+    node and its nearest violated ancestor, or None for a valid tree."""
+    coords = np.asarray(coords)
+    n, k = coords.shape
+    if check_valid(coords, split_dims):
+        return None
+    dims = node_split_dims(n, k, split_dims)
+    for d in range(1, n):
+        a = d
+        while a > 0:
+            p = (a - 1) >> 1
+            dp = int(dims[p])
+            own, plane = coords[d, dp], coords[p, dp]
+            if (a & 1 == 1 and own > plane) or (a & 1 == 0 and own < plane):
+                return d, p, dp
+            a = p
+    return None
 
 
 def brute_subtree_boxes(coords, split_dims=None):

@@ -36,6 +36,7 @@ EXPORTED = (
     "lbkd_build_rr_host", "lbkd_build_widest_host", "lbkd_host_join",
     "lbkd_set_subtree_kernel",
     "lbkd_knn", "lbkd_radius_count", "lbkd_radius_scratch_len", "lbkd_radius_fill",
+    "lbkd_check_valid", "lbkd_subtree_boxes",
 )
 
 # kernel classes of lbkd_profile_kernel
@@ -128,6 +129,10 @@ def load():
         lib.lbkd_radius_scratch_len.restype = i64
         lib.lbkd_radius_fill.argtypes = [vp, i64, i32, vp, vp, i64, f64, vp, vp, vp]
         lib.lbkd_radius_fill.restype = i32
+        lib.lbkd_check_valid.argtypes = [vp, i64, i32, vp, vp, vp, vp]
+        lib.lbkd_check_valid.restype = i32
+        lib.lbkd_subtree_boxes.argtypes = [vp, i64, i32, vp, vp, vp, vp]
+        lib.lbkd_subtree_boxes.restype = i32
         lib.lbkd_strerror.argtypes = [i32]
         lib.lbkd_strerror.restype = ctypes.c_char_p
         lib.lbkd_last_cuda_error.argtypes = []
