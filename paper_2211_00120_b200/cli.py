@@ -1,0 +1,257 @@
+"""Command-line interface -- drop-in for ``lbkd.cli`` (build / query / bench).
+
+Mirrors /root/reference/pkg/src/lbkd/cli.py: the same subcommands and flags,
+the same file formats and the same output lines::
+
+    python -m paper_2211_00120_b200 build --input points.csv --dims 2 --mode widest --output tree.csv
+    python -m paper_2211_00120_b200 query --tree tree.csv --point 45,40 --knn 3
+    python -m paper_2211_00120_b200 query --tree tree.csv --point 45,40 --radius 10
+    python -m paper_2211_00120_b200 bench --n 1000000 --dims 4 --mode round-robin --seed 0 --reps 3
+
+Point files: headerless CSV, one point per row (``--payload`` adds a trailing
+integer column) -- read_points (cli.py:41-67).  Tree files: CSV with header
+``coord_0..coord_{k-1}[,split_dim][,payload]``, data row i = node i; an empty
+tree is a zero-byte file -- write_tree / read_tree (cli.py:70-141).  Query
+results print ``index,dist2`` per hit (cli.py:152-170).  Data errors exit 1
+with the message on stderr.
+
+The build and the queries run on the GPU.  Differences, both from the GPU
+path's input scope: coordinates must be float32-representable
+(the reference accepts any float64), and ``bench`` draws float32 points
+(``rng.random((n, dims), dtype=float32)``; the reference draws float64) and
+adds device-side fields to its JSON record (cli.py:173-194): ``dtype``,
+``device_millis`` (build with the points already in HBM, CUDA events) and
+``mpts_per_s``.  ``selftest`` (cli.py:197-300) is the reference's
+self-check against its own recursive oracle and is not mirrored here; the
+test-suite (tests/) and ``__graft_entry__.smoke()`` play that role.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+
+import numpy as np
+
+from . import builder, queries, widest
+
+
+def format_scalar(value: float) -> str:
+    """Shortest faithful text for a finite float; integral values print bare
+    (cli.py:30-33)."""
+    f = float(value)
+    return str(int(f)) if f == int(f) else repr(f)
+
+
+def _build_fn(mode: str):
+    return widest.build_widest if mode == "widest" else builder.build_round_robin
+
+
+def _rows(path: str):
+    """(physical line number, comma-split fields) of every non-blank line."""
+    with open(path) as fh:
+        for ln, raw in enumerate(fh, 1):
+            text = raw.strip()
+            if text:
+                yield ln, text.split(",")
+
+
+def read_points(path: str, dims: int, with_payload: bool = False):
+    """Headerless CSV of points -> (coords float64 (n, dims), payload int64 or
+    None); errors name the file and line like cli.py:41-67."""
+    width = dims + int(with_payload)
+    coords: list[list[float]] = []
+    tails: list[int] = []
+    for ln, fields in _rows(path):
+        if len(fields) != width:
+            raise ValueError(f"{path}:{ln}: expected {width} comma-separated fields, got {len(fields)}")
+        try:
+            coords.append(list(map(float, fields[:dims])))
+        except ValueError:
+            raise ValueError(f"{path}:{ln}: unparseable coordinate") from None
+        if with_payload:
+            try:
+                tails.append(int(fields[-1]))
+            except ValueError:
+                raise ValueError(f"{path}:{ln}: unparseable payload") from None
+    pts = np.array(coords, dtype=np.float64).reshape(len(coords), dims)
+    return pts, (np.array(tails, dtype=np.int64) if with_payload else None)
+
+
+def write_tree(path: str, tree: builder.KdTree, with_payload: bool = False) -> None:
+    """Tree CSV (cli.py:70-87): header coord_0..coord_{k-1}[,split_dim]
+    [,payload], data row i = node i; an empty tree is a zero-byte file."""
+    if tree.n == 0:
+        with open(path, "w"):
+            pass
+        return
+    columns = [[format_scalar(v) for v in tree.coords[:, j]] for j in range(tree.k)]
+    names = [f"coord_{j}" for j in range(tree.k)]
+    if tree.split_dims is not None:
+        names.append("split_dim")
+        columns.append([str(int(v)) for v in tree.split_dims])
+    if with_payload:
+        names.append("payload")
+        columns.append([str(int(v)) for v in tree.payload])
+    body = "\n".join(",".join(row) for row in zip(*columns))
+    with open(path, "w") as fh:
+        fh.write(",".join(names) + "\n" + body + "\n")
+
+
+def _tree_layout(path: str, names: list[str]):
+    """(k, has split_dim column, has payload column) from a tree CSV header."""
+    k = next((j for j, name in enumerate(names) if name != f"coord_{j}"), len(names))
+    if k == 0:
+        raise ValueError(f"{path}: header must start with coord_0")
+    extra = names[k:]
+    has_dims = extra[:1] == ["split_dim"]
+    extra = extra[int(has_dims):]
+    has_payload = extra[:1] == ["payload"]
+    extra = extra[int(has_payload):]
+    if extra:
+        raise ValueError(f"{path}: unrecognized columns {extra}")
+    return k, has_dims, has_payload
+
+
+def read_tree(path: str) -> builder.KdTree:
+    """Parse a tree CSV written by :func:`write_tree` (cli.py:90-141)."""
+    rows = [fields for _, fields in _rows(path)]
+    if not rows:
+        return builder.KdTree(np.empty((0, 1), dtype=np.float64), np.empty(0, dtype=np.int64))
+    k, has_dims, has_payload = _tree_layout(path, rows[0])
+    n = len(rows) - 1
+    width = k + int(has_dims) + int(has_payload)
+    coords = np.empty((n, k), dtype=np.float64)
+    dims = np.zeros(n, dtype=np.min_scalar_type(max(k - 1, 0))) if has_dims else None
+    payload = np.arange(n, dtype=np.int64)
+    for i, fields in enumerate(rows[1:]):
+        line_no = i + 2  # data row i sits on line i + 2 (after the header)
+        if len(fields) != width:
+            raise ValueError(f"{path}:{line_no}: expected {width} fields, got {len(fields)}")
+        try:
+            coords[i] = list(map(float, fields[:k]))
+            if has_dims:
+                d = int(fields[k])
+                if d < 0 or d >= k:
+                    raise ValueError
+                dims[i] = d
+            if has_payload:
+                payload[i] = int(fields[width - 1])
+        except ValueError:
+            raise ValueError(f"{path}:{line_no}: unparseable field") from None
+    if not np.isfinite(coords).all():
+        raise ValueError(f"{path}: tree coordinates must be finite")
+    return builder.KdTree(coords, payload, dims)
+
+
+def cmd_build(args) -> int:
+    coords, payload = read_points(args.input, args.dims, args.payload)
+    tree = _build_fn(args.mode)(coords, args.dims, payload=payload)
+    write_tree(args.output, tree, with_payload=args.payload)
+    print(f"{tree.n} nodes, {args.dims} dims, {args.mode} -> {args.output}")
+    return 0
+
+
+def cmd_query(args) -> int:
+    tree = read_tree(args.tree)
+    try:
+        point = [float(p) for p in args.point.split(",")]
+    except ValueError:
+        raise ValueError(f"unparseable query point {args.point!r}") from None
+    if args.knn is not None:
+        for nb in queries.knn(tree, point, args.knn):
+            print(f"{nb.index},{format_scalar(nb.dist2)}")
+    else:
+        indices = queries.radius_query(tree, point, args.radius)
+        q = np.asarray(point, dtype=np.float64)
+        for i in indices:
+            d2 = 0.0
+            for j in range(tree.k):
+                t = q[j] - tree.coords[i, j]
+                d2 += t * t
+            print(f"{int(i)},{format_scalar(d2)}")
+    return 0
+
+
+def cmd_bench(args) -> int:
+    if args.n < 1 or args.dims < 1 or args.reps < 1:
+        raise ValueError("--n, --dims, and --reps must all be at least 1")
+    import torch
+
+    rng = np.random.default_rng(args.seed)
+    coords = rng.random((args.n, args.dims), dtype=np.float32)
+    build = _build_fn(args.mode)
+    build(coords, args.dims)  # warmup: library load, context, scratch
+    total = 0.0
+    for _ in range(args.reps):
+        t0 = time.perf_counter()
+        build(coords, args.dims)
+        total += time.perf_counter() - t0
+    # device-resident build time (points already in HBM)
+    d = torch.from_numpy(coords).cuda()
+    dev_build = builder.build_round_robin_cuda if args.mode != "widest" else widest.build_widest_cuda
+    dev_build(d)
+    dev_ms = 0.0
+    for _ in range(args.reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dev_build(d, check_finite=False)
+        b.record()
+        torch.cuda.synchronize()
+        dev_ms += a.elapsed_time(b)
+    record = {
+        "n": args.n,
+        "k": args.dims,
+        "mode": args.mode,
+        "seed": args.seed,
+        "reps": args.reps,
+        "millis": total / args.reps * 1000.0,
+        "dtype": "float32",
+        "device_millis": dev_ms / args.reps,
+        "mpts_per_s": args.n / (dev_ms / args.reps) / 1e3,
+    }
+    print(json.dumps(record))
+    return 0
+
+
+def make_parser() -> argparse.ArgumentParser:
+    p = argparse.ArgumentParser(prog="paper_2211_00120_b200", description="B200 left-balanced k-d trees")
+    sub = p.add_subparsers(dest="cmd", required=True)
+    b = sub.add_parser("build", help="build a tree from a CSV of points")
+    b.add_argument("--input", required=True)
+    b.add_argument("--dims", type=int, required=True)
+    b.add_argument("--mode", choices=["round-robin", "widest"], default="round-robin")
+    b.add_argument("--output", required=True)
+    b.add_argument("--payload", action="store_true", help="input rows end with an integer payload column")
+    b.set_defaults(fn=cmd_build)
+    q = sub.add_parser("query", help="nearest-neighbor or radius query against a tree CSV")
+    q.add_argument("--tree", required=True)
+    q.add_argument("--point", required=True)
+    g = q.add_mutually_exclusive_group(required=True)
+    g.add_argument("--knn", type=int)
+    g.add_argument("--radius", type=float)
+    q.set_defaults(fn=cmd_query)
+    be = sub.add_parser("bench", help="time builds of uniform random points")
+    be.add_argument("--n", type=int, required=True)
+    be.add_argument("--dims", type=int, default=3)
+    be.add_argument("--mode", choices=["round-robin", "widest"], default="round-robin")
+    be.add_argument("--seed", type=int, default=0)
+    be.add_argument("--reps", type=int, default=3)
+    be.set_defaults(fn=cmd_bench)
+    return p
+
+
+def main(argv: list[str] | None = None) -> int:
+    args = make_parser().parse_args(argv)
+    try:
+        return args.fn(args)
+    except (ValueError, OSError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
