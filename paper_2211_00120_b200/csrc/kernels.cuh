@@ -164,6 +164,7 @@ struct SubtreeArgs {
     int entry_sorted;  // sort path: each subtree arrives in the reference's
                        // order T(parent); select path: in input order
     int src_par;       // select path: W[src_par] holds the subtree (else prev_state)
+    int bucket_lists;  // RR list kernel: chain orders by one bucket pass each (env LBKD_BUCKET=0: radix passes)
 };
 
 size_t subtree_smem_bytes(int b, int k, int mode);

@@ -20,6 +20,8 @@
 //         in-CTA ancestors' (dim, plane) pairs up to the subtree root box
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace lbkd {
 
 constexpr int kSubThreads = 1024;  // general kernel (widest, small trees)
@@ -158,6 +160,116 @@ __device__ __forceinline__ int list_sort_dim(ET* buf0, ET* buf1, int cur, int m,
         cur ^= 1;
     }
     return cur;
+}
+
+// One round-robin chain order T_d = (c[d], c[d-1], ..., c[d-k+1], local id)
+// of the m points of P, written to out as local ids, by ONE value-linear
+// bucket pass instead of 3-4 radix passes: NB equal-width buckets over the
+// points' [min, max] in dim d (monotone in the key, so buckets are ordered),
+// shared-atomic counts, a block scan, an atomic scatter, then every bucket
+// is put in T_d order by insertion sort under the full chain comparator (the
+// scatter's order inside a bucket does not matter).  Local ids compare like
+// the input order (ids follow input order, or T_e order -- which agrees with
+// the input order on points that tie in all k coordinates).  Returns false,
+// leaving out undefined, if some bucket holds more than kBucketRun points
+// (tie-heavy data): the caller then runs the radix passes.
+constexpr int kBucketRun = 24;
+
+template <int NT, int KT>
+__device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m, const float* __restrict__ P, int Mp,
+                                         int d, int kk, int NB, u32* __restrict__ hist, u32* __restrict__ scratch) {
+    const int k = KT ? KT : kk;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* Pd = P + d * Mp;
+    u32 kmin = 0xffffffffu, kmax = 0u;
+    for (int p = tid; p < m; p += NT) {
+        const u32 key = flip_key(Pd[p]);
+        kmin = min(kmin, key);
+        kmax = max(kmax, key);
+    }
+    for (int b = tid; b < NB; b += NT) hist[b] = 0u;
+    kmin = __reduce_min_sync(kFullMask, kmin);
+    kmax = __reduce_max_sync(kFullMask, kmax);
+    scratch[warp] = kmin;  // every lane stores the warp-uniform value (NVVM 12.9, list_sort_dim)
+    scratch[32 + warp] = kmax;
+    __syncthreads();
+    kmin = 0xffffffffu;
+    kmax = 0u;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        kmin = min(kmin, scratch[w]);
+        kmax = max(kmax, scratch[32 + w]);
+    }
+    const float lo = unflip_key(kmin);
+    const float range = __fsub_rn(unflip_key(kmax), lo);
+    float scale = range > 0.f ? __fdiv_rn((float)NB, range) : 0.f;
+    if (!(scale <= 3.0e38f)) scale = 0.f;  // overflowing range / denormal width: one bucket -> radix
+    auto bucket = [&](float x) -> u32 {
+        const u32 b = (u32)__fmul_rn(__fsub_rn(x, lo), scale);  // NaN-free: x >= lo, finite
+        return b < (u32)NB ? b : (u32)NB - 1u;
+    };
+    for (int p = tid; p < m; p += NT) atomicAdd(&hist[bucket(Pd[p])], 1u);
+    __syncthreads();
+    // exclusive scan over NB counts, NB / NT consecutive per thread, and the
+    // largest bucket
+    const int per = NB / NT;
+    u32 s = 0, big = 0;
+    for (int i = 0; i < per; ++i) {
+        const u32 c = hist[tid * per + i];
+        s += c;
+        big = max(big, c);
+    }
+    big = __reduce_max_sync(kFullMask, big);
+    const u32 ex = block_exclusive_scan<u32>(s, scratch, nullptr);
+    scratch[32 + warp] = big;
+    u32 run = ex;
+    for (int i = 0; i < per; ++i) {
+        const u32 c = hist[tid * per + i];
+        hist[tid * per + i] = run;
+        run += c;
+    }
+    __syncthreads();
+    big = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) big = max(big, scratch[32 + w]);
+    if (big > (u32)kBucketRun) {
+        __syncthreads();
+        return false;
+    }
+    for (int p = tid; p < m; p += NT) out[atomicAdd(&hist[bucket(Pd[p])], 1u)] = (unsigned short)p;
+    __syncthreads();
+    // hist[b] = end of bucket b; order each bucket under T_d
+    for (int b = tid; b < NB; b += NT) {
+        const int e = (int)hist[b];
+        const int st = b ? (int)hist[b - 1] : 0;
+        for (int i = st + 1; i < e; ++i) {
+            const u32 v = out[i];
+            const u32 kv = flip_key(Pd[v]);
+            int t = i - 1;
+            while (t >= st) {
+                const u32 w = out[t];
+                const u32 kw = flip_key(Pd[w]);
+                bool less = kv < kw;
+                if (kv == kw) {
+                    less = v < w;
+                    for (int f = 1; f < k; ++f) {
+                        const int dd = (d - f + k) % k;
+                        const u32 x = flip_key(P[dd * Mp + v]), y = flip_key(P[dd * Mp + w]);
+                        if (x != y) {
+                            less = x < y;
+                            break;
+                        }
+                    }
+                }
+                if (!less) break;
+                out[t + 1] = (unsigned short)w;
+                --t;
+            }
+            out[t + 1] = (unsigned short)v;
+        }
+    }
+    __syncthreads();
+    return true;
 }
 
 // Entry order of a subtree that arrives in INPUT order (select path): the
@@ -507,7 +619,21 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
         state[lid] = 0;
     }
     __syncthreads();
-    if (!a.entry_sorted) {
+    // the k chain orders by one bucket pass each (tie-heavy subtrees fall
+    // back to the radix passes below)
+    bool listed = a.bucket_lists && (Mp % kRRThreads) == 0;
+    if (listed) {
+        u32* hist = reinterpret_cast<u32*>(sp);  // the tables / sort-scratch region holds >= 4 Mp bytes
+        for (int d = 0; d < k && listed; ++d) {
+            if (a.entry_sorted && d == e) continue;
+            listed = bucket_list<kRRThreads, KT>(LB + Lo[d], m, P, Mp, d, k, Mp, hist, scratch);
+        }
+        if (!listed) {
+            for (int lid = tid; lid < m; lid += kRRThreads) ident[lid] = (u16)lid;
+            __syncthreads();
+        }
+    }
+    if (!listed && !a.entry_sorted) {
         // input order -> T_e (full chain: lam0 >= k), then hand the other
         // buffers out as the remaining lists and the spares
         Chain ch;
@@ -523,7 +649,7 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
     }
 
     // ---- chain sorts: T_d = stable_sort(T_{d-1}, c[d]) for the k-1 other dims
-    for (int q = 1; q < k; ++q) {
+    for (int q = 1; q < k && !listed; ++q) {
         const int d = (e + q) % k;
         const int dprev = (e + q - 1) % k;
         const float* Pd = P + d * Mp;
@@ -870,6 +996,10 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entr
     a.from_pts = lam0 == 0 ? 1 : 0;
     a.entry_sorted = entry_sorted;
     a.src_par = src_par;
+    {
+        const char* e = getenv("LBKD_BUCKET");
+        a.bucket_lists = !(e && e[0] == '0');
+    }
     unsigned grid = (unsigned)(1ull << (lam0 - bp.lroot));
     const bool sel_ok = !bp.dbg && (bp.mode == kRoundRobin || bp.k <= 4);
     if (sel_ok && (bp.subtree_sel || (bp.mode == kRoundRobin && lam0 < bp.k))) {

@@ -26,3 +26,4 @@ if __name__ == "__main__":
         t(n, 3)
     t(10**8, 2); t(10**7, 4)
     t(10**8, 3, "widest", "clustered")
+    t(10**8, 3, "rr", "clustered")
