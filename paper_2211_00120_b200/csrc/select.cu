@@ -400,13 +400,29 @@ __global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
             const u32 bs = sel[kSelB];
             const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
             u32 hits = 0, nlt = 0;
+            const u32 r0 = (u32)threadIdx.x * ITEMS;
+            if (r0 >= ra && r0 + ITEMS <= rb) {
+                // the thread's 8 keys lie in this part: two 16-byte loads (the
+                // SoA columns are 16-byte aligned and tiles start at multiples
+                // of T words)
+                const uint4 q0 = *reinterpret_cast<const uint4*>(kp + r0);
+                const uint4 q1 = *reinterpret_cast<const uint4*>(kp + r0 + 4);
+                const u32 key[ITEMS] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const u32 r = (u32)(threadIdx.x * ITEMS + i);
-                if (r >= ra && r < rb) {
-                    const u32 b = bucket_of(bk, kp[r]);
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 b = bucket_of(bk, key[i]);
                     if (b == bs) hits |= 1u << i;
                     nlt += b < bs ? 1u : 0u;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 r = r0 + (u32)i;
+                    if (r >= ra && r < rb) {
+                        const u32 b = bucket_of(bk, kp[r]);
+                        if (b == bs) hits |= 1u << i;
+                        nlt += b < bs ? 1u : 0u;
+                    }
                 }
             }
             nlt = __reduce_add_sync(kFullMask, nlt);
