@@ -906,29 +906,23 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
             bool act = (u32)lane < sz;
             const u32 lid = act ? member[sb + lane] : 0u;
             u32 nd = 0;  // heap index of the point's node inside segment t's subtree (< 31)
+            // lanes of my node (every active lane of a node holds the same
+            // mask): the segment's lanes, then per level narrowed to my side
+            u32 eq = __ballot_sync(kFullMask, act);
             for (int l2 = lam; l2 <= L - 1; ++l2) {
                 const int dd = l2 - lam;
                 const int sh2 = L - l2 - 1;
                 // local rank under T_d inside the segment (< 31): the segment
                 // begins at sb in every list
                 const u32 key = (act && l2 <= L - 2) ? (u32)LB[rko[l2 % k] + lid] - sb : 0u;
-                // rank inside the node from bit-sliced ballots: lanes of the
-                // same node (5 node bits), then those with a smaller key
-                u32 eq = __ballot_sync(kFullMask, act);
-                // node ids at depth dd are < 2^(dd+1): only those bits vary
-                for (int b = 0; b <= dd; ++b) {
-                    const u32 bit = (nd >> b) & 1u;
-                    const u32 bal = __ballot_sync(kFullMask, bit);
-                    eq &= bit ? bal : ~bal;
-                }
                 // the keys (segment-local ranks < 31) present in my node as
-                // a bit set: one segmented OR over each node's lanes (every
-                // active lane of a node passes the same mask)
+                // a bit set: one segmented OR over the node's lanes
                 u32 rank = 0;
                 if (act) {
                     const u32 keys = __reduce_or_sync(eq, 1u << key);
                     rank = (u32)__popc(keys & ((1u << key) - 1u));
                 }
+                bool right = false;
                 if (act) {
                     const u32 off = nd + 1u - (1u << dd);  // node's index among depth dd
                     const u64 J = (Jt << dd) + off;
@@ -943,10 +937,14 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                         ntab[(1u << (dl + dd)) - 1u + ((u32)t << dd) + off] = (u16)lid;
                         act = false;
                     } else {
-                        nd = 2u * nd + 1u + (rank > po ? 1u : 0u);
+                        right = rank > po;
+                        nd = 2u * nd + 1u + (right ? 1u : 0u);
                     }
                 }
-                if (!__any_sync(kFullMask, act)) break;
+                const u32 live = __ballot_sync(kFullMask, act);
+                if (!live) break;
+                const u32 rb = __ballot_sync(kFullMask, right);
+                eq &= live & (right ? rb : ~rb);
             }
         }
     }
@@ -955,6 +953,10 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
     // each level's nodes of this subtree are one contiguous range of the
     // level-order arrays: coalesced stores of points and input rows
     __syncthreads();
+    // the input rows, staged once (coalesced) in the dead list buffers
+    u32* const vs = reinterpret_cast<u32*>(LB);
+    for (int lid = tid; lid < m; lid += kRRThreads) vs[lid] = vin[lid];
+    __syncthreads();
     for (int dl = 0; a.lam0 + dl <= L - 1; ++dl) {
         const int l2 = a.lam0 + dl;
         const u64 first = ((1ull << l2) - 1ull) + (j << dl);
@@ -962,7 +964,7 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
         u64 cntn = 1ull << dl;
         if (first + cntn > a.n) cntn = a.n - first;
         const u32 h0 = (1u << dl) - 1u;
-        for (u32 i = tid; i < (u32)cntn; i += kRRThreads) a.perm[first + i] = vin[ntab[h0 + i]];
+        for (u32 i = tid; i < (u32)cntn; i += kRRThreads) a.perm[first + i] = vs[ntab[h0 + i]];
         float* dst = a.out_pts + first * (u64)k;
         for (u32 i = tid; i < (u32)cntn * (u32)k; i += kRRThreads) {
             const u32 t = i / (u32)k, c = i - t * (u32)k;

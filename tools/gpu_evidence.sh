@@ -1,0 +1,16 @@
+# Round evidence (v5): bench line, reference arm, launch list + per-class DRAM traffic,
+# ncu full captures (partition, subtree, filter) with source lines, clocks
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+python __graft_entry__.py build > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log > gpurun_out/bench.json; cut -c1-300 gpurun_out/bench.json
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log > gpurun_out/bench_ref.json; cut -c1-300 gpurun_out/bench_ref.json
+L=$(python tools/one_build.py 100000000 3 rr uniform 1 | awk '/launches per build/{print $4}')
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s $L -c $L --csv --log-file gpurun_out/launches_100m.csv python tools/one_build.py 100000000 3 rr uniform 2 > gpurun_out/prof1.log 2>&1
+python tools/launches.py gpurun_out/launches_100m.csv > gpurun_out/launches_100m.txt
+python tools/ncu_traffic.py gpurun_out/launches_100m.csv gpurun_out/ncu_traffic.json > /dev/null
+ncu --set full --clock-control none --import-source on -k regex:sel_part -s 4 -c 1 -o gpurun_out/part python tools/one_build.py 100000000 3 rr uniform 1 > gpurun_out/prof2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:subtree -c 1 -o gpurun_out/subrr python tools/one_build.py 100000000 3 rr uniform 1 > gpurun_out/prof3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sel_filter -s 6 -c 1 -o gpurun_out/filter python tools/one_build.py 100000000 3 rr uniform 1 > gpurun_out/prof4.log 2>&1
+python tools/ncu_issue.py gpurun_out/subrr.ncu-rep gpurun_out/ncu_issue_subtree.json > /dev/null
+cat gpurun_out/launches_100m.txt
