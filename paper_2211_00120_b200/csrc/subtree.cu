@@ -181,12 +181,13 @@ __device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m
     const int k = KT ? KT : kk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float* Pd = P + d * Mp;
-    u32 kmin = 0xffffffffu, kmax = 0u;
+    float fmn = __int_as_float(0x7f800000), fmx = -__int_as_float(0x7f800000);
     for (int p = tid; p < m; p += NT) {
-        const u32 key = flip_key(Pd[p]);
-        kmin = min(kmin, key);
-        kmax = max(kmax, key);
+        const float x = Pd[p];
+        fmn = fminf(fmn, x);
+        fmx = fmaxf(fmx, x);
     }
+    u32 kmin = flip_key(fmn), kmax = flip_key(fmx);
     for (int b = tid; b < NB; b += NT) hist[b] = 0u;
     kmin = __reduce_min_sync(kFullMask, kmin);
     kmax = __reduce_max_sync(kFullMask, kmax);
@@ -212,21 +213,27 @@ __device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m
     __syncthreads();
     // exclusive scan over NB counts, NB / NT consecutive per thread, and the
     // largest bucket
-    const int per = NB / NT;
+    const int per = NB / NT;  // a multiple of 4 (NB = Mp >= 4 NT): 16-byte shared loads / stores
+    uint4* const h4 = reinterpret_cast<uint4*>(hist) + tid * (per / 4);
     u32 s = 0, big = 0;
-    for (int i = 0; i < per; ++i) {
-        const u32 c = hist[tid * per + i];
-        s += c;
-        big = max(big, c);
+    for (int i = 0; i < per / 4; ++i) {
+        const uint4 c = h4[i];
+        s += c.x + c.y + c.z + c.w;
+        big = max(big, max(max(c.x, c.y), max(c.z, c.w)));
     }
     big = __reduce_max_sync(kFullMask, big);
     const u32 ex = block_exclusive_scan<u32>(s, scratch, nullptr);
     scratch[32 + warp] = big;
     u32 run = ex;
-    for (int i = 0; i < per; ++i) {
-        const u32 c = hist[tid * per + i];
-        hist[tid * per + i] = run;
-        run += c;
+    for (int i = 0; i < per / 4; ++i) {
+        const uint4 c = h4[i];
+        uint4 o;
+        o.x = run;
+        o.y = run + c.x;
+        o.z = o.y + c.y;
+        o.w = o.z + c.z;
+        run = o.w + c.w;
+        h4[i] = o;
     }
     __syncthreads();
     big = 0;
@@ -243,18 +250,19 @@ __device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m
         const int e = (int)hist[b];
         const int st = b ? (int)hist[b - 1] : 0;
         for (int i = st + 1; i < e; ++i) {
+            // finite coordinates: float order == flipped-key order (-0 == +0)
             const u32 v = out[i];
-            const u32 kv = flip_key(Pd[v]);
+            const float kv = Pd[v];
             int t = i - 1;
             while (t >= st) {
                 const u32 w = out[t];
-                const u32 kw = flip_key(Pd[w]);
+                const float kw = Pd[w];
                 bool less = kv < kw;
                 if (kv == kw) {
                     less = v < w;
                     for (int f = 1; f < k; ++f) {
                         const int dd = (d - f + k) % k;
-                        const u32 x = flip_key(P[dd * Mp + v]), y = flip_key(P[dd * Mp + w]);
+                        const float x = P[dd * Mp + v], y = P[dd * Mp + w];
                         if (x != y) {
                             less = x < y;
                             break;
@@ -621,7 +629,7 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
     __syncthreads();
     // the k chain orders by one bucket pass each (tie-heavy subtrees fall
     // back to the radix passes below)
-    bool listed = a.bucket_lists && (Mp % kRRThreads) == 0;
+    bool listed = a.bucket_lists && (Mp % (4 * kRRThreads)) == 0;
     if (listed) {
         u32* hist = reinterpret_cast<u32*>(sp);  // the tables / sort-scratch region holds >= 4 Mp bytes
         for (int d = 0; d < k && listed; ++d) {
