@@ -809,10 +809,12 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
             const u16* XB = LB + (hasB ? Lo[dB] : Lo[dA]);
             u16* YA = LB + Lo[k];
             u16* YB = LB + Lo[k + 1];
-            // 8 consecutive positions per thread, one 16-byte load per list
+            // 8 consecutive positions per thread, one 16-byte load per list;
+            // per list the counts (right | pivot << 16) of the thread's
+            // positions, both lists scanned in one 64-bit block scan
             const int p0 = tid * 8;
             u32 la[8], lb8[8], sa[8], sb[8];
-            u64 v = 0;
+            u32 va = 0, vb = 0;
             if (p0 < mc) {
                 const uint4 qa = *reinterpret_cast<const uint4*>(XA + p0);
                 const u32 wa[4] = {qa.x, qa.y, qa.z, qa.w};
@@ -830,38 +832,40 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                         sb[i] = p0 + i < mc ? (u32)state[lb8[i]] : 3u;
                     }
                 }
+                // state & 3: 0 left, 1 right, 2 node, 3 past the end
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const u32 ca = sa[i] & 3u;
-                    v += (u64)(ca == 1u) | ((u64)(ca == 2u) << 16);
+                    va += ca == 1u ? 1u : (ca == 2u ? 0x10000u : 0u);
                     if (hasB) {
                         const u32 cb = sb[i] & 3u;
-                        v += ((u64)(cb == 1u) << 32) | ((u64)(cb == 2u) << 48);
+                        vb += cb == 1u ? 1u : (cb == 2u ? 0x10000u : 0u);
                     }
                 }
             }
-            u64 ex = block_exclusive_scan<u64>(v, scratch64, nullptr);
+            const u64 ex64 = block_exclusive_scan<u64>((u64)va | ((u64)vb << 32), scratch64, nullptr);
             if (p0 < mc) {
+                u32 exa = (u32)ex64, exb = (u32)(ex64 >> 32);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int p = p0 + i;
                     const u32 ca = sa[i] & 3u;
                     if (ca < 2u) {
                         const u32 rpt = rp[sa[i] >> 3];
-                        const u32 Rex = (u32)(ex & 0xffffu), Pex = (u32)((ex >> 16) & 0xffffu);
+                        const u32 Rex = exa & 0xffffu, Pex = exa >> 16;
                         const u32 dst = ca ? (rpt >> 16) + Rex : (u32)p - Rex - Pex + (rpt & 0xffffu);
                         YA[dst] = (u16)la[i];
                     }
-                    ex += (u64)(ca == 1u) | ((u64)(ca == 2u) << 16);
+                    exa += ca == 1u ? 1u : (ca == 2u ? 0x10000u : 0u);
                     if (hasB) {
                         const u32 cb = sb[i] & 3u;
                         if (cb < 2u) {
                             const u32 rpt = rp[sb[i] >> 3];
-                            const u32 Rex = (u32)((ex >> 32) & 0xffffu), Pex = (u32)(ex >> 48);
+                            const u32 Rex = exb & 0xffffu, Pex = exb >> 16;
                             const u32 dst = cb ? (rpt >> 16) + Rex : (u32)p - Rex - Pex + (rpt & 0xffffu);
                             YB[dst] = (u16)lb8[i];
                         }
-                        ex += ((u64)(cb == 1u) << 32) | ((u64)(cb == 2u) << 48);
+                        exb += cb == 1u ? 1u : (cb == 2u ? 0x10000u : 0u);
                     }
                 }
             }
