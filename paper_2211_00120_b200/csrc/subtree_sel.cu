@@ -514,6 +514,9 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 for (int c = 0; c < kBoxK; ++c)
                     if (c < k) { blo[c] = boxA[t * 2 * k + c]; bhi[c] = boxA[t * 2 * k + k + c]; }
             }
+            // lanes of my node (the same mask on every active lane of a node):
+            // the segment's lanes, narrowed to my side after every level
+            u32 eqn = __ballot_sync(kFullMask, act);
             for (int l2 = lam; l2 <= L - 1; ++l2) {
                 const int dd = l2 - lam;
                 const int sh2 = L - l2 - 1;
@@ -535,15 +538,10 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 u32 rank;
                 const bool exact = rr_exact || !__any_sync(kFullMask, act && ((tiemask >> d) & 1u));
                 if (exact) {
-                    // bit-sliced ballots: lanes of my node (5 node bits), then
-                    // those with a smaller precomputed rank (5 rank bits)
+                    // lanes of my node, then those with a smaller precomputed
+                    // rank (5 rank bits)
                     const u32 key = act ? (u32)wrk[d * 32 + lane] : 0u;
-                    u32 eq = __ballot_sync(kFullMask, act);
-                    for (int bb = 0; bb <= dd; ++bb) {  // node ids at depth dd use dd + 1 bits
-                        const u32 bit = (nd >> bb) & 1u;
-                        const u32 bal = __ballot_sync(kFullMask, bit);
-                        eq &= bit ? bal : ~bal;
-                    }
+                    const u32 eq = eqn;
                     // ranks (< 31) present in my node as a bit set: one
                     // segmented OR over each node's lanes
                     rank = 0;
@@ -586,8 +584,9 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                     }
                 }
                 __syncwarp();
+                bool right = false;
                 if (act && !is_piv) {
-                    const bool right = rank > po;
+                    right = rank > po;
                     if (a.mode == kWidest) {
                         const float pl = wplane[nd];
                         const int pd = (int)wpdim[nd];
@@ -602,7 +601,10 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 }
                 act = act && !is_piv;
                 __syncwarp();
-                if (!__any_sync(kFullMask, act)) break;
+                const u32 live = __ballot_sync(kFullMask, act);
+                if (!live) break;
+                const u32 rb = __ballot_sync(kFullMask, right);
+                eqn &= live & (right ? rb : ~rb);
             }
             __syncwarp();
         }
