@@ -13,10 +13,14 @@ JSON line.
 - e2e: the same build through the C-ABI with HOST buffers: pinned host points
   -> H2D -> lbkd_build_rr -> D2H of the level-order points and permutation,
   all inside the timed region.
-- roofline: the dominant kernel (the onesweep digit pass) -- its algorithmic
-  bytes (each reordered point reads and writes its k coordinates + index)
-  over its device time, both measured inside the library with CUDA events
-  on the build stream during the timed region (lbkd_set_profile).
+- roofline: the dominant kernel class by device time per build (today the
+  in-CTA subtree kernel; the HBM-bound partition is second) -- its
+  algorithmic bytes over its device time, both measured inside the library
+  with CUDA events on the build stream during the timed region
+  (lbkd_set_profile); `traffic` from the committed ncu launch list.  The
+  in-CTA kernel moves each point once and is bound by instruction issue, so
+  `issue_roofline` states that bound (ncu warp instructions / 148 x 4 issue
+  slots per clock) and `kernels` lists every class with its HBM rate.
 - cpu_baseline: the CPU oracle port (oracle/, a C restatement of the
   reference's tag-and-sort loop) on a bounded sample of the same workload.
 - --impl reference: the reference path on the host cores: the oracle port
