@@ -72,10 +72,10 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
+def ncu_traffic(mode: str = "rr"):
     """Per-kernel DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum per
     launch) from the committed ncu summary of this build (profiles/)."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json" if mode == "rr" else f"ncu_traffic_{mode}.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -83,11 +83,12 @@ def ncu_traffic():
         return {}
 
 
-def ncu_issue(name):
+def ncu_issue(name, mode: str = "rr"):
     """Issue-rate roofline of an SM-bound kernel from its committed ncu capture
-    (profiles/ncu_issue_<name>.json, tools/ncu_issue.py)."""
+    (profiles/ncu_issue_<name>[_<mode>].json, tools/ncu_issue.py)."""
+    fn = f"ncu_issue_{name}.json" if mode == "rr" else f"ncu_issue_{name}_{mode}.json"
     try:
-        with open(os.path.join(ROOT, "profiles", f"ncu_issue_{name}.json")) as f:
+        with open(os.path.join(ROOT, "profiles", fn)) as f:
             return json.load(f)
     except Exception:
         return None
@@ -103,6 +104,12 @@ KERNEL_NAMES = {
     "init": "init_stats_kernel (AoS -> SoA, world box)",
     "sort_pass": "pass_kernel (onesweep digit pass, LBKD_ALGO=sort)",
     "other": "root / extract / small kernels",
+}
+
+
+KERNEL_NAMES_WIDEST = {
+    "partition": "sel_part_kernel (stable 3-way partition, global levels)",
+    "subtree": "subtree_sel_kernel (in-CTA levels, per-level selection)",
 }
 
 
@@ -312,6 +319,7 @@ def main():
     h_out = torch.empty((n, k), dtype=torch.float32).pin_memory() if have_input else None
     h_perm = torch.empty(n, dtype=torch.int32).pin_memory() if have_input else None
     d_in = torch.empty_like(d_pts) if have_input else None
+    h_dims = torch.empty(n, dtype=torch.uint8).pin_memory() if (have_input and args.mode == "widest") else None
 
     def e2e_step():
         if sharded:
@@ -324,13 +332,10 @@ def main():
         elif args.mode == "rr":
             kd.builder.build_round_robin_host(h_pts, h_out, h_perm, device=local)
         else:
-            d_in.copy_(h_pts, non_blocking=True)
-            build(d_in, out, perm)
-            h_out.copy_(out, non_blocking=True)
-            h_perm.copy_(perm, non_blocking=True)
+            kd.widest.build_widest_host(h_pts, h_out, h_perm, h_dims, device=local)
 
     def e2e_join():
-        if not sharded and args.mode == "rr":
+        if not sharded:
             kd.builder.host_join(device=local, sync=False)
 
     for _ in range(args.warmup):
@@ -365,7 +370,7 @@ def main():
         total_pts = n * args.steps
         value = total_pts / (ms / 1000.0) / 1e6
         peak, peak_src = measured_peak()
-        traffic = ncu_traffic()
+        traffic = ncu_traffic(args.mode)
         model_B = survey_model_bytes(n, k, args.mode == "widest")
         step_s = ms / 1000.0 / args.steps
         kern = {}
@@ -406,11 +411,11 @@ def main():
                 "value": None,
                 "unit": "Mpoints/s",
                 "h2d_bytes_per_step": n * k * 4,
-                "d2h_bytes_per_step": n * k * 4 + n * 4,
+                "d2h_bytes_per_step": n * k * 4 + n * 4 + (n if args.mode == "widest" else 0),
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": KERNEL_NAMES.get(dom, dom),
+                "kernel": (KERNEL_NAMES_WIDEST.get(dom) if args.mode == "widest" else None) or KERNEL_NAMES.get(dom, dom),
                 "achieved": round(achieved, 1),
                 "peak": peak,
                 "unit": "GB/s",
@@ -438,7 +443,7 @@ def main():
             "output_is_permutation": ok,
         }
         line["e2e"]["value"] = round(total_pts / (e2e_ms / 1000.0) / 1e6, 2)
-        iss = ncu_issue(dom)
+        iss = ncu_issue(dom, args.mode)
         if iss is not None:
             # the in-CTA kernel is bound by instruction issue, not HBM: its
             # warp instructions (ncu) over the B200 issue peak (148 SMs x 4

@@ -9,7 +9,7 @@ CUDA behind the C-ABI library in ``_lib/`` (include/lbkd_b200.h).
 """
 
 from .builder import BuildRecorder, KdTree, build_round_robin, build_round_robin_cuda
-from .widest import build_widest, build_widest_cuda
+from .widest import build_widest, build_widest_cuda, build_widest_host
 from .queries import Neighbor, knn, knn_cuda, radius_cuda, radius_query
 
 __all__ = [
@@ -19,6 +19,7 @@ __all__ = [
     "build_round_robin_cuda",
     "build_widest",
     "build_widest_cuda",
+    "build_widest_host",
     "Neighbor",
     "knn",
     "knn_cuda",

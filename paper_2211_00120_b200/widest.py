@@ -132,6 +132,27 @@ def build_widest_cuda(points, *, out=None, perm=None, split_dims=None, stream=No
     return out, perm, split_dims
 
 
+def build_widest_host(points, out, perm, split_dims, *, device: int = 0, stream=None) -> None:
+    """Pipelined widest build from HOST memory through lbkd_build_widest_host.
+
+    ``points`` / ``out``: (n, k) float32, ``perm``: (n,) int32, ``split_dims``:
+    (n,) uint8 CPU tensors, all pinned for overlap.  The call only enqueues
+    H2D -> build -> D2H; consecutive calls overlap their copies with the
+    neighbouring builds.  The buffers are valid after ``builder.host_join``.
+    """
+    torch = _torch()
+    for t in (points, out, perm, split_dims):
+        if t.device.type != "cpu" or not t.is_contiguous():
+            raise ValueError("host buffers must be contiguous CPU tensors")
+    n, k = points.shape
+    lib = _native.load()
+    ctx = _native.context(device)
+    with torch.cuda.device(device):
+        rc = lib.lbkd_build_widest_host(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(),
+                                        split_dims.data_ptr(), _stream_ptr(torch, stream))
+    _raise_for(rc, "lbkd_build_widest_host", n, k, widest=True)
+
+
 def build_widest(points, k: int | None = None, payload=None, *, skip_prefix: bool = False,
                  recorder: BuildRecorder | None = None) -> KdTree:
     """Drop-in for lbkd.build_widest (widest.py:134-191)."""

@@ -309,6 +309,28 @@ def test_pipelined_host_builds():
     host_join()
 
 
+def test_pipelined_host_builds_widest():
+    """lbkd_build_widest_host: pipelined host-buffer widest builds, each exact
+    (permutation and split dims) against the oracle."""
+    from paper_2211_00120_b200.builder import host_join
+    from paper_2211_00120_b200.widest import build_widest_host
+
+    n, k = 200003, 3
+    inputs = [datagen.make(kind, n, k, seed=s) for s, kind in enumerate(("clustered", "uniform", "ties"))]
+    hin = [torch.from_numpy(p).pin_memory() for p in inputs]
+    hout = [torch.empty((n, k), dtype=torch.float32).pin_memory() for _ in inputs]
+    hperm = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in inputs]
+    hdims = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in inputs]
+    for i in range(len(inputs)):
+        build_widest_host(hin[i], hout[i], hperm[i], hdims[i])
+    host_join()
+    for i, p in enumerate(inputs):
+        wp, wd = oracle.build_widest(p)
+        assert np.array_equal(hperm[i].numpy().view(np.uint32), wp), i
+        assert np.array_equal(hdims[i].numpy(), wd), i
+        assert np.array_equal(hout[i].numpy(), p[wp.astype(np.int64)]), i
+
+
 @pytest.mark.parametrize("n", [5000, 70001, 1 << 20])
 def test_selection_subtree_kernel_for_round_robin(n):
     """The in-CTA selection kernel (default for widest) is bit-exact for

@@ -3,6 +3,8 @@
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 python __graft_entry__.py build > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+timeout 300 python __graft_entry__.py 2>&1 | tail -2
+timeout 1200 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -4
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log > gpurun_out/bench.json; cut -c1-300 gpurun_out/bench.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log > gpurun_out/bench_ref.json; cut -c1-300 gpurun_out/bench_ref.json
 L=$(python tools/one_build.py 100000000 3 rr uniform 1 | awk '/launches per build/{print $4}')
@@ -14,3 +16,5 @@ ncu --set full --clock-control none --import-source on -k regex:subtree -c 1 -o 
 ncu --set full --clock-control none --import-source on -k regex:sel_filter -s 6 -c 1 -o gpurun_out/filter python tools/one_build.py 100000000 3 rr uniform 1 > gpurun_out/prof4.log 2>&1
 python tools/ncu_issue.py gpurun_out/subrr.ncu-rep gpurun_out/ncu_issue_subtree.json > /dev/null
 cat gpurun_out/launches_100m.txt
+timeout 900 python bench.py --steps 5 --warmup 3 --mode widest --dist clustered > gpurun_out/bench_widest.log 2>&1; tail -1 gpurun_out/bench_widest.log > gpurun_out/bench_widest.json; cut -c1-300 gpurun_out/bench_widest.json
+timeout 900 python tools/big_build.py 1000000000 clustered 3 > gpurun_out/big_1b.log 2>&1; tail -1 gpurun_out/big_1b.log | cut -c1-400
