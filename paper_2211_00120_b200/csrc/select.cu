@@ -382,6 +382,9 @@ __global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
     if (t0 >= t1) return;
     SegCursor sc;
     sc.init(g, t0 * T);
+    u64 cj = ~0ull;
+    Bucketer cbk{};
+    u32 cbs = 0;
     for (u64 t = t0; t < t1; ++t) {
         const u64 ts = t * T;
         const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
@@ -396,8 +399,13 @@ __global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
             const u32 ra = part ? r1a : r0a, rb = part ? r1b : r0b;
             if (!((part == 0 || has1) && ra < rb)) continue;
             u32* sel = a.sel + j * kSelW;
-            const Bucketer bk = make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D);
-            const u32 bs = sel[kSelB];
+            if (j != cj) {  // the segment's bucketer, kept while tiles stay in it
+                cj = j;
+                cbk = make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D);
+                cbs = sel[kSelB];
+            }
+            const Bucketer bk = cbk;
+            const u32 bs = cbs;
             const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
             u32 hits = 0, nlt = 0;
             const u32 r0 = (u32)threadIdx.x * ITEMS;
@@ -430,14 +438,14 @@ __global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
             if (lane == 0 && nlt) atomicAdd(&a.tile_lt[t * 2 + part], nlt);
             // candidates: warp-aggregated slot reservation
             const u32 nh = (u32)__popc(hits);
-            u32 x = nh;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 y = __shfl_up_sync(kFullMask, x, o);
-                if (lane >= o) x += y;
-            }
-            const u32 wtot = __shfl_sync(kFullMask, x, 31);
+            const u32 wtot = __reduce_add_sync(kFullMask, nh);  // usually 0: skip the scan
             if (wtot) {
+                u32 x = nh;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 y = __shfl_up_sync(kFullMask, x, o);
+                    if (lane >= o) x += y;
+                }
                 u32 base = 0;
                 if (lane == 31) base = atomicAdd(&sel[kSelFill], wtot);
                 base = __shfl_sync(kFullMask, base, 31);
