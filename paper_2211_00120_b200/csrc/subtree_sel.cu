@@ -338,31 +338,46 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             if (bk == s[kSgB]) cand[s[kSgOff] + atomicAdd(&s[kSgFill], 1u)] = (u16)p;
         }
         __syncthreads();
-        // ---- resolve: warp per segment, rank of each candidate by comparison
-        for (int t = warp; t < nloc; t += kSelWarps) {
-            u32* s = sv + t * kSegWords;
-            const u32 C = s[kSgCnt], r = s[kSgR], off = s[kSgOff];
-            const int d = (int)s[kSgDim];
-            Chain wch;
-            if (a.mode == kWidest) widest_chain_of(hbase + t, dl, wch);
-            else rr_chain(lam, k, wch);
-            auto chain_at = [&](int f) -> int { return wch.d[f]; };
-            for (u32 i0 = 0; i0 < C; i0 += 32) {
-                const u32 i = i0 + lane;
-                bool mine = false;
-                u32 ci = 0;
-                if (i < C) {
-                    ci = cand[off + i];
-                    const u32 ki = flip_key(P[d * Mp + ci]);
-                    u32 rank = 0;
-                    for (u32 jj = 0; jj < C; ++jj) {
-                        const u32 cj = cand[off + jj];
-                        const u32 kj = flip_key(P[d * Mp + cj]);
-                        rank += (kj < ki || (kj == ki && cj != ci && less_tie(cj, ci, (int)wch.m, chain_at))) ? 1u : 0u;
-                    }
-                    mine = rank == r;
+        // ---- resolve: rank of each candidate inside its segment by
+        // comparison, one thread per candidate over the whole CTA (a warp per
+        // segment left most warps idle at the top levels, where one or two
+        // segments hold all candidates); the chain is built only on a tie
+        {
+            const u32* sl = sv + (nloc - 1) * kSegWords;
+            const u32 total = sl[kSgOff] + sl[kSgCnt];
+            for (u32 q = tid; q < total; q += kSelThreads) {
+                // segment of candidate q: offsets strictly increase (every
+                // segment's pivot bucket holds its pivot)
+                int lo = 0, hi = nloc - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sv[mid * kSegWords + kSgOff] <= q) lo = mid;
+                    else hi = mid - 1;
                 }
-                if (mine) s[kSgPiv] = ci;
+                const int t = lo;
+                u32* s = sv + t * kSegWords;
+                const u32 C = s[kSgCnt], off = s[kSgOff];
+                const int d = (int)s[kSgDim];
+                const u32 ci = cand[q];
+                const float ki = P[d * Mp + ci];  // finite: float order == flipped-key order
+                Chain wch;
+                bool have = false;
+                u32 rank = 0;
+                for (u32 jj = 0; jj < C; ++jj) {
+                    const u32 cj = cand[off + jj];
+                    const float kj = P[d * Mp + cj];
+                    bool lt = kj < ki;
+                    if (kj == ki && cj != ci) {
+                        if (!have) {
+                            if (a.mode == kWidest) widest_chain_of(hbase + t, dl, wch);
+                            else rr_chain(lam, k, wch);
+                            have = true;
+                        }
+                        lt = less_tie(cj, ci, (int)wch.m, [&](int f) -> int { return wch.d[f]; });
+                    }
+                    rank += lt ? 1u : 0u;
+                }
+                if (rank == s[kSgR]) s[kSgPiv] = ci;
             }
         }
         __syncthreads();
@@ -391,7 +406,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 continue;
             }
             const int d = (int)s[kSgDim];
-            const u32 kp = flip_key(P[d * Mp + p]), kv = flip_key(P[d * Mp + piv]);
+            const float kp = P[d * Mp + p], kv = P[d * Mp + piv];  // finite: float order == flipped-key order
             bool lt;
             if (kp != kv) {
                 lt = kp < kv;
