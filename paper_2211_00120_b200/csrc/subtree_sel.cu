@@ -80,7 +80,14 @@ __host__ __device__ inline SelLayout sel_layout(int b, int k) {
 
 size_t subtree_sel_smem_bytes(int b, int k) { return sel_layout(b, k).total; }
 
-enum { kSgSize = 0, kSgPo, kSgDim, kSgB, kSgR, kSgOff, kSgCnt, kSgFill, kSgPiv, kSgLo, kSgHi };
+enum { kSgSize = 0, kSgPo, kSgDim, kSgB, kSgR, kSgOff, kSgCnt, kSgFill, kSgPiv, kSgLo, kSgHi };  // kSgLo / kSgHi: bucketer (half lo, scale)
+
+// block-phase bucket of coordinate v in a segment (fp32, round-to-nearest
+// each step: monotone in v; NaN -> the top bucket)
+__device__ __forceinline__ u32 seg_bucket(const u32* s, float v) {
+    const float x = __fmul_rn(__fsub_rn(0.5f * v, __uint_as_float(s[kSgLo])), __uint_as_float(s[kSgHi]));
+    return x < (float)(kNB - 1) ? (u32)x : (u32)(kNB - 1);
+}
 
 template <int KT>
 __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(SubtreeArgs a, int b) {
@@ -269,8 +276,13 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             s[kSgSize] = seg_size_l(sh, J0 + t);
             s[kSgPo] = pivot_off_l(sh, J0 + t);
             s[kSgDim] = (u32)d;
-            s[kSgLo] = __float_as_uint(box[d]);
-            s[kSgHi] = __float_as_uint(box[k + d]);
+            // value-linear buckets of the node box in fp32 (halves: no
+            // overflow of hi - lo for any finite box); the same function in
+            // hist and gather, monotone in the coordinate
+            const float hlo = 0.5f * box[d];
+            const float w = 0.5f * box[k + d] - hlo;
+            s[kSgLo] = __float_as_uint(hlo);
+            s[kSgHi] = __float_as_uint(w > 0.0f ? __fdiv_rn((float)kNB, w) : 0.0f);
             s[kSgFill] = 0u;
         }
         for (int i = tid; i < nloc * (kNB / 2); i += kSelThreads) hist[i] = 0u;
@@ -280,11 +292,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             const u32 t = seg[p];
             if (t == kFin) continue;
             const u32* s = sv + t * kSegWords;
-            const float lo = __uint_as_float(s[kSgLo]), hi = __uint_as_float(s[kSgHi]);
-            const int d = (int)s[kSgDim];
-            const double w = (double)hi - (double)lo;
-            const double x = w > 0.0 ? ((double)P[d * Mp + p] - (double)lo) * ((double)kNB / w) : 0.0;
-            const u32 bk = x < (double)(kNB - 1) ? (u32)x : (u32)(kNB - 1);
+            const u32 bk = seg_bucket(s, P[(int)s[kSgDim] * Mp + p]);
             atomicAdd(&hist[t * (kNB / 2) + (bk >> 1)], (bk & 1u) ? 0x10000u : 1u);
         }
         __syncthreads();
@@ -330,11 +338,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             const u32 t = seg[p];
             if (t == kFin) continue;
             u32* s = sv + t * kSegWords;
-            const float lo = __uint_as_float(s[kSgLo]), hi = __uint_as_float(s[kSgHi]);
-            const int d = (int)s[kSgDim];
-            const double w = (double)hi - (double)lo;
-            const double x = w > 0.0 ? ((double)P[d * Mp + p] - (double)lo) * ((double)kNB / w) : 0.0;
-            const u32 bk = x < (double)(kNB - 1) ? (u32)x : (u32)(kNB - 1);
+            const u32 bk = seg_bucket(s, P[(int)s[kSgDim] * Mp + p]);
             if (bk == s[kSgB]) cand[s[kSgOff] + atomicAdd(&s[kSgFill], 1u)] = (u16)p;
         }
         __syncthreads();
