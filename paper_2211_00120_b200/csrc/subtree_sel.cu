@@ -84,9 +84,9 @@ enum { kSgSize = 0, kSgPo, kSgDim, kSgB, kSgR, kSgOff, kSgCnt, kSgFill, kSgPiv, 
 
 // block-phase bucket of coordinate v in a segment (fp32, round-to-nearest
 // each step: monotone in v; NaN -> the top bucket)
-__device__ __forceinline__ u32 seg_bucket(const u32* s, float v) {
+__device__ __forceinline__ u32 seg_bucket(const u32* s, float v, u32 top) {
     const float x = __fmul_rn(__fsub_rn(0.5f * v, __uint_as_float(s[kSgLo])), __uint_as_float(s[kSgHi]));
-    return x < (float)(kNB - 1) ? (u32)x : (u32)(kNB - 1);
+    return x < (float)top ? (u32)x : top;
 }
 
 template <int KT>
@@ -263,6 +263,11 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
         const int nloc = 1 << dl;
         const u64 J0 = j << dl;
         const u32 hbase = (1u << dl) - 1u;  // heap index of segment 0
+        // buckets per segment: the whole histogram (nsb * kNB bins) split
+        // over this level's nloc <= nsb segments -- 2048 at the in-CTA root
+        // for b = 11, so the pivot's bucket holds a handful of candidates
+        const int nbw = max(kNB / 2, (Ly.nsb * (kNB / 2)) >> dl);  // 32-bit words (2 bins) per segment
+        const u32 nbtop = 2u * (u32)nbw - 1u;
         // ---- setup
         for (int t = tid; t < nloc; t += kSelThreads) {
             u32* s = sv + t * kSegWords;
@@ -282,41 +287,50 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             const float hlo = 0.5f * box[d];
             const float w = 0.5f * box[k + d] - hlo;
             s[kSgLo] = __float_as_uint(hlo);
-            s[kSgHi] = __float_as_uint(w > 0.0f ? __fdiv_rn((float)kNB, w) : 0.0f);
+            s[kSgHi] = __float_as_uint(w > 0.0f ? __fdiv_rn((float)(2 * nbw), w) : 0.0f);
             s[kSgFill] = 0u;
         }
-        for (int i = tid; i < nloc * (kNB / 2); i += kSelThreads) hist[i] = 0u;
+        for (int i = tid; i < nloc * nbw; i += kSelThreads) hist[i] = 0u;
         __syncthreads();
         // ---- hist (two 16-bit bins per word)
         for (int p = tid; p < m; p += kSelThreads) {
             const u32 t = seg[p];
             if (t == kFin) continue;
             const u32* s = sv + t * kSegWords;
-            const u32 bk = seg_bucket(s, P[(int)s[kSgDim] * Mp + p]);
-            atomicAdd(&hist[t * (kNB / 2) + (bk >> 1)], (bk & 1u) ? 0x10000u : 1u);
+            const u32 bk = seg_bucket(s, P[(int)s[kSgDim] * Mp + p], nbtop);
+            atomicAdd(&hist[t * nbw + (bk >> 1)], (bk & 1u) ? 0x10000u : 1u);
         }
         __syncthreads();
         // ---- pick: warp per segment
         for (int t = warp; t < nloc; t += kSelWarps) {
             u32* s = sv + t * kSegWords;
-            const u32 hw = hist[t * (kNB / 2) + lane];  // kNB == 64: one word per lane
-            const u32 c0 = hw & 0xffffu, c1 = hw >> 16;
-            u32 x = c0 + c1;
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 y = __shfl_up_sync(kFullMask, x, o);
-                if (lane >= o) x += y;
-            }
-            const u32 ex = x - c0 - c1;  // elements before bucket 2*lane
             const u32 po = s[kSgPo];
-            int bsel = -1;
+            u32 base = 0;  // elements in the buckets before this 64-bucket chunk
+            int bs = 0;
             u32 cum = 0, cnt = 0;
-            if (po >= ex && po < ex + c0) { bsel = 2 * lane; cum = ex; cnt = c0; }
-            else if (po >= ex + c0 && po < ex + c0 + c1) { bsel = 2 * lane + 1; cum = ex + c0; cnt = c1; }
-            const u32 who = __ballot_sync(kFullMask, bsel >= 0);
-            const int src_l = __ffs(who) - 1;
-            const int bs = __shfl_sync(kFullMask, bsel, src_l);
-            cum = __shfl_sync(kFullMask, cum, src_l);
-            cnt = __shfl_sync(kFullMask, cnt, src_l);
+            for (int w0 = 0; w0 < nbw; w0 += 32) {
+                const u32 hw = hist[t * nbw + w0 + lane];  // one word (two bins) per lane
+                const u32 c0 = hw & 0xffffu, c1 = hw >> 16;
+                u32 x = c0 + c1;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 y = __shfl_up_sync(kFullMask, x, o);
+                    if (lane >= o) x += y;
+                }
+                const u32 ex = base + x - c0 - c1;  // elements before bucket 2*(w0+lane)
+                int bsel = -1;
+                u32 cu = 0, cn = 0;
+                if (po >= ex && po < ex + c0) { bsel = 2 * (w0 + lane); cu = ex; cn = c0; }
+                else if (po >= ex + c0 && po < ex + c0 + c1) { bsel = 2 * (w0 + lane) + 1; cu = ex + c0; cn = c1; }
+                const u32 who = __ballot_sync(kFullMask, bsel >= 0);
+                if (who) {
+                    const int src_l = __ffs(who) - 1;
+                    bs = __shfl_sync(kFullMask, bsel, src_l);
+                    cum = __shfl_sync(kFullMask, cu, src_l);
+                    cnt = __shfl_sync(kFullMask, cn, src_l);
+                    break;
+                }
+                base += __shfl_sync(kFullMask, x, 31);
+            }
             if (lane == 0) {
                 s[kSgB] = (u32)bs;
                 s[kSgR] = po - cum;
@@ -338,7 +352,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             const u32 t = seg[p];
             if (t == kFin) continue;
             u32* s = sv + t * kSegWords;
-            const u32 bk = seg_bucket(s, P[(int)s[kSgDim] * Mp + p]);
+            const u32 bk = seg_bucket(s, P[(int)s[kSgDim] * Mp + p], nbtop);
             if (bk == s[kSgB]) cand[s[kSgOff] + atomicAdd(&s[kSgFill], 1u)] = (u16)p;
         }
         __syncthreads();
