@@ -311,10 +311,12 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
     Buffers& bf = c->bf;
     const int k = bp.k;
     const double A = 4.0 * (k + 1);
-    // from level kFuseFrom on (round-robin, k <= 4) each level's histogram
-    // (D = 8) is accumulated by the previous level's partition kernel
+    // from level kFuseFrom on (k <= 4) each level's histogram (D = 8) is
+    // accumulated by the previous level's partition kernel (widest: binned
+    // in each child's own split dim, written by the select kernel)
     const int kFuseFrom = 6;
-    const bool fusable = bp.mode == kRoundRobin && k <= 4;
+    const bool fusable = k <= 4 && (bp.mode == kRoundRobin || getenv("LBKD_FUSE_WIDEST") == nullptr ||
+                                    getenv("LBKD_FUSE_WIDEST")[0] != '0');
     for (int l = lfrom; l < lto; ++l) {
         const LevelGeom g = view_of(bp, l);
         const u64 nseg = g.nseg;

@@ -842,7 +842,7 @@ constexpr size_t kPHistOff = 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1);
 constexpr size_t kPRingOff = kPHistOff + sizeof(u32) * (kPThreads / 32) * 512;
 
 struct PHdr {
-    u32 sl[2], tl[2], pp[2], y[2];
+    u32 sl[2], tl[2], pp[2], y[2], d[2];  // d: the part's split dim (widest)
 };
 
 template <int KMAX, int D0>
@@ -894,6 +894,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
     u64 hseg = ~0ull;
     Bucketer hb0{}, hb1{};
     const int dn = (g.l + 1) % k;
+    int hdn0 = dn, hdn1 = dn;  // the children's dims (widest: per segment)
     auto hflush = [&]() {
         if (hseg != ~0ull) {
             for (int i = lane; i < 512; i += 32) {
@@ -922,14 +923,15 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
         const int sin = (int)(s2 - t2 * (u64)nsub_tile);  // subtile inside the tile
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-            h2.sl[p] = 0u; h2.tl[p] = 0u; h2.pp[p] = 0u; h2.y[p] = 0u;
+            h2.sl[p] = 0u; h2.tl[p] = 0u; h2.pp[p] = 0u; h2.y[p] = 0u; h2.d[p] = D0 >= 0 ? (u32)D0 : 0u;
             if (p == 1 && !tp2.has1) continue;
             const u64 j = tp2.j0 + p;
             const u32 pt = j == j0t ? 0u : 1u;
             h2.sl[p] = lane < sin ? a.sub_lt[(t2 * (u64)nsub_tile + lane) * 2 + pt] : 0u;
             h2.tl[p] = a.tile_lt[t2 * 2 + pt];
             h2.pp[p] = a.ppos[j];
-            h2.y[p] = a.piv[j * A + D0];
+            if (D0 < 0) h2.d[p] = (u32)a.split_dims[g.Fl + g.sbase + j];  // widest: the segment's dim
+            h2.y[p] = a.piv[j * A + h2.d[p]];
         }
     };
     PHdr hn;
@@ -957,7 +959,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
         const PHdr h = hn;
         if (s + sd < s_end) hdr_load(s + sd, hn);
         long long bL0 = 0, bR0 = 0, bL1 = 0, bR1 = 0;
-        const int d00 = D0, d01 = D0;  // round robin: every segment splits dim l mod k
+        const int d00 = (int)h.d[0], d01 = (int)h.d[1];  // round robin: D0 for every segment
         u32 y00 = 0, y01 = 0;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
@@ -975,21 +977,27 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
             else { bL1 = l; bR1 = rr; y01 = y; }
         }
         const u32 r0a = tp.r0a, r0b = tp.r0b, r1a = tp.r1a, r1b = tp.r1b;
-        if (D0 >= 0 && full && !tp.has1 && r0a == 0 && r0b == (u32)kSub) {
+        if (full && !tp.has1 && r0a == 0 && r0b == (u32)kSub) {
             // lean path: one segment part covers the whole subtile
-            const float yf = __uint_as_float(a.piv[tp.j0 * A + (D0 >= 0 ? D0 : 0)]);
+            const int dl0 = D0 >= 0 ? D0 : d00;
+            const float yf = __uint_as_float(a.piv[tp.j0 * A + dl0]);
             u32 bl = (u32)bL0, br = (u32)bR0;
             if (fuse && tp.j0 != hseg) {
                 hflush();
                 hseg = tp.j0;
                 const float* c0 = a.boxes_out + (2 * hseg) * 2ull * k;
                 const float* c1 = c0 + 2 * k;
-                hb0 = make_bucketer(c0[dn], c0[k + dn], 8);
-                hb1 = make_bucketer(c1[dn], c1[k + dn], 8);
+                if (D0 < 0) {  // widest: the children's own split dims (written by select)
+                    const u64 cn = 2 * (g.Fl + g.sbase + hseg) + 1;
+                    hdn0 = cn < g.n ? (int)a.split_dims[cn] : 0;
+                    hdn1 = cn + 1 < g.n ? (int)a.split_dims[cn + 1] : 0;
+                }
+                hb0 = make_bucketer(c0[hdn0], c0[k + hdn0], 8);
+                hb1 = make_bucketer(c1[hdn1], c1[k + hdn1], 8);
             }
 #pragma unroll
             for (int i = 0; i < kPRows; ++i) {
-                const float xf = __uint_as_float(V(D0 >= 0 ? D0 : 0, i));
+                const float xf = __uint_as_float(V(dl0, i));
                 int side = xf < yf ? 0 : (xf > yf ? 1 : 2);  // -0.0 == +0.0 like numpy
                 if (side == 2) side = part_tie_side(a, tp.j0, ss + (u64)(i * 32 + lane));
                 const u32 ml = __ballot_sync(kFullMask, side == 0);
@@ -998,7 +1006,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                 bl += __popc(ml);
                 br += __popc(mr);
                 if (fuse && side < 2) {
-                    const u32 kn = V(dn, i);
+                    const u32 kn = V(side ? hdn1 : hdn0, i);
                     atomicAdd(&wh[side * 256 + bucket_of(side ? hb1 : hb0, kn)], 1u);
                 }
                 if (side < 2) {
@@ -1051,8 +1059,10 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
             if (fuse && side < 2) {
                 const u64 j = tp.j0 + (in1 ? 1 : 0);
                 const float* cb = a.boxes_out + (2 * j + side) * 2ull * k;
-                const Bucketer hb = make_bucketer(cb[dn], cb[k + dn], 8);
-                atomicAdd(&a.hist_next[(2 * j + side) * 256ull + bucket_of(hb, V(dn, i))], 1u);
+                const u64 cn = 2 * (g.Fl + g.sbase + j) + 1 + side;
+                const int dnc = D0 >= 0 ? dn : (cn < g.n ? (int)a.split_dims[cn] : 0);
+                const Bucketer hb = make_bucketer(cb[dnc], cb[k + dnc], 8);
+                atomicAdd(&a.hist_next[(2 * j + side) * 256ull + bucket_of(hb, V(dnc, i))], 1u);
             }
             const u32 ml = __ballot_sync(kFullMask, side == 0);
             const u32 mr = __ballot_sync(kFullMask, side == 1);
@@ -1177,7 +1187,7 @@ void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
         case 1: bulk_go(sel_part_bulk_kernel<KM, (KM > 1 ? 1 : 0)>, KM); break;                \
         case 2: bulk_go(sel_part_bulk_kernel<KM, (KM > 2 ? 2 : 0)>, KM); break;                \
         case 3: bulk_go(sel_part_bulk_kernel<KM, (KM > 3 ? 3 : 0)>, KM); break;                \
-        default: sel_part_kernel<KM, -1><<<(unsigned)grid, kPThreads, 0, st>>>(a, T); break;   \
+        default: bulk_go(sel_part_bulk_kernel<KM, -1>, KM); break; /* widest: per-segment dims */ \
     }
     switch (a.k) {
         case 1: LBKD_PART(1); break;
