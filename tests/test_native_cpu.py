@@ -103,3 +103,29 @@ def test_flip_key_restatement_orders_like_numpy():
     key = np.where(u >> 31, ~u, u | 0x80000000).astype(np.uint32)
     assert np.all(np.diff(key.astype(np.int64)) >= 0)
     assert key[3] == key[4]
+
+
+def test_entry_points_fail_loudly_without_cuda():
+    """No CPU fallback: every build entry point raises when no CUDA device is
+    present (here), before any work -- including the pipelined host-buffer
+    variants."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    import paper_2211_00120_b200 as kd
+    from paper_2211_00120_b200.builder import build_round_robin_host
+
+    pts = np.random.default_rng(0).random((100, 3), dtype=np.float32)
+    t = torch.from_numpy(pts)
+    out = torch.empty_like(t)
+    perm = torch.empty(100, dtype=torch.int32)
+    dims = torch.empty(100, dtype=torch.uint8)
+    calls = [
+        lambda: kd.build_round_robin(pts),
+        lambda: kd.build_widest(pts),
+        lambda: build_round_robin_host(t, out, perm),
+        lambda: kd.build_widest_host(t, out, perm, dims),
+    ]
+    for call in calls:
+        with pytest.raises(RuntimeError, match="no CPU fallback"):
+            call()
