@@ -311,7 +311,7 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
     Buffers& bf = c->bf;
     const int k = bp.k;
     const double A = 4.0 * (k + 1);
-    // from level kFuseFrom on (k <= 4) each level's histogram (D = 8) is
+    // from level kFuseFrom on (k <= 4) each level's histogram (D = 9) is
     // accumulated by the previous level's partition kernel (widest: binned
     // in each child's own split dim, written by the select kernel)
     const int kFuseFrom = 6;
@@ -322,7 +322,7 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         const u64 nseg = g.nseg;
         const bool fused_in = fusable && l > lfrom && l >= kFuseFrom;
         const bool fuse_next = fusable && l + 1 < lto && l + 1 >= kFuseFrom;
-        const int D = fused_in ? 8 : sel_digit_bits(nseg);
+        const int D = fused_in ? 9 : sel_digit_bits(nseg);  // 9 = kFuseD (select.cu)
         const u32 par = (u32)((l - bp.lroot) & 1);
         const double pts = (double)level_points(bp, l);
         if (!fused_in) CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
@@ -370,7 +370,7 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         prof_end(c, st, kPSelect, 0.0);
         a.hist_next = nullptr;
         if (fuse_next) {  // this level's histogram has been read by pick
-            CK(cudaMemsetAsync(bf.hist, 0, (2 * nseg * 256) * sizeof(u32), st));
+            CK(cudaMemsetAsync(bf.hist, 0, (2 * nseg * 512) * sizeof(u32), st));  // 2 children x 2^kFuseD
             a.hist_next = bf.hist;
         }
         if (prof_begin(c, st)) return LBKD_ECUDA;

@@ -839,6 +839,11 @@ __global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 2 : 1) sel_part_kernel(
 constexpr int kPStages = 3;
 // bulk partition smem: [mbarriers][per-warp fused histograms][per-warp rings]
 constexpr size_t kPHistOff = 128 * ((kPThreads / 32) * kPStages * 8 / 128 + 1);
+// fused next-level histogram: 2^kFuseD bins per child; warp-private copies
+// hold two 16-bit bins per word (flushed at least every 255 subtiles, so a
+// bin never exceeds 255 x 256 < 2^16 between flushes)
+constexpr int kFuseD = 9;
+constexpr int kFuseBins = 1 << kFuseD;
 constexpr size_t kPRingOff = kPHistOff + sizeof(u32) * (kPThreads / 32) * 512;
 
 struct PHdr {
@@ -895,16 +900,20 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
     Bucketer hb0{}, hb1{};
     const int dn = (g.l + 1) % k;
     int hdn0 = dn, hdn1 = dn;  // the children's dims (widest: per segment)
+    int hcnt = 0;  // subtiles binned since the last flush
     auto hflush = [&]() {
         if (hseg != ~0ull) {
             for (int i = lane; i < 512; i += 32) {
                 const u32 v = wh[i];
                 if (v) {
-                    atomicAdd(&a.hist_next[(2 * hseg + (i >> 8)) * 256ull + (i & 255)], v);
+                    u32* gh = a.hist_next + (2 * hseg + (i >> 8)) * (u64)kFuseBins + 2 * (i & 255);
+                    if (v & 0xffffu) atomicAdd(gh, v & 0xffffu);
+                    if (v >> 16) atomicAdd(gh + 1, v >> 16);
                     wh[i] = 0u;
                 }
             }
         }
+        hcnt = 0;
         __syncwarp();
     };
     if (fuse) {
@@ -992,8 +1001,12 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                     hdn0 = cn < g.n ? (int)a.split_dims[cn] : 0;
                     hdn1 = cn + 1 < g.n ? (int)a.split_dims[cn + 1] : 0;
                 }
-                hb0 = make_bucketer(c0[hdn0], c0[k + hdn0], 8);
-                hb1 = make_bucketer(c1[hdn1], c1[k + hdn1], 8);
+                hb0 = make_bucketer(c0[hdn0], c0[k + hdn0], kFuseD);
+                hb1 = make_bucketer(c1[hdn1], c1[k + hdn1], kFuseD);
+            }
+            if (fuse) {
+                if (hcnt == 255) hflush();  // 16-bit bins: flush before they could overflow
+                ++hcnt;
             }
 #pragma unroll
             for (int i = 0; i < kPRows; ++i) {
@@ -1007,7 +1020,8 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                 br += __popc(mr);
                 if (fuse && side < 2) {
                     const u32 kn = V(side ? hdn1 : hdn0, i);
-                    atomicAdd(&wh[side * 256 + bucket_of(side ? hb1 : hb0, kn)], 1u);
+                    const u32 hbk = bucket_of(side ? hb1 : hb0, kn);
+                    atomicAdd(&wh[side * 256 + (hbk >> 1)], (hbk & 1u) ? 0x10000u : 1u);
                 }
                 if (side < 2) {
 #pragma unroll
@@ -1061,8 +1075,8 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                 const float* cb = a.boxes_out + (2 * j + side) * 2ull * k;
                 const u64 cn = 2 * (g.Fl + g.sbase + j) + 1 + side;
                 const int dnc = D0 >= 0 ? dn : (cn < g.n ? (int)a.split_dims[cn] : 0);
-                const Bucketer hb = make_bucketer(cb[dnc], cb[k + dnc], 8);
-                atomicAdd(&a.hist_next[(2 * j + side) * 256ull + bucket_of(hb, V(dnc, i))], 1u);
+                const Bucketer hb = make_bucketer(cb[dnc], cb[k + dnc], kFuseD);
+                atomicAdd(&a.hist_next[(2 * j + side) * (u64)kFuseBins + bucket_of(hb, V(dnc, i))], 1u);
             }
             const u32 ml = __ballot_sync(kFullMask, side == 0);
             const u32 mr = __ballot_sync(kFullMask, side == 1);
