@@ -118,7 +118,8 @@ struct SelArgs {
     u32* tile_lt;          // [tiles][2] below-pivot counts -> exclusive prefixes
     u32* sub_lt;           // [subtiles][2] below-pivot counts per 256-position warp subtile
     u32* ppos;             // [nseg] in-order position of each segment's pivot
-    u32* hist_next;        // partition (RR): the next level's histogram (D = 8), or null
+    u32* hist_next;        // partition: the next level's histogram (D = kFuseD), or null
+    int hflush_every;      // partition: flush the warp-private 16-bit bins every this many subtiles (<= 255)
     int tiles_per_cta;
     u64 ntiles;
 };

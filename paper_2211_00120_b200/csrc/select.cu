@@ -28,6 +28,8 @@
 // [ib(j), ib(j) + ss(j)) of W[(l - lfirst) & 1]; finished nodes leave a hole.
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace lbkd {
 
 __device__ __forceinline__ int seg_key_dim(const SelArgs& a, u64 t) {
@@ -1005,7 +1007,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, 
                 hb1 = make_bucketer(c1[hdn1], c1[k + hdn1], kFuseD);
             }
             if (fuse) {
-                if (hcnt == 255) hflush();  // 16-bit bins: flush before they could overflow
+                if (hcnt >= a.hflush_every) hflush();  // 16-bit bins: flush before they could overflow
                 ++hcnt;
             }
 #pragma unroll
@@ -1179,7 +1181,16 @@ void launch_sel_select(const SelArgs& a, int b, cudaStream_t st) {
     else sel_select_kernel<256><<<g, 256, 0, st>>>(a, sel_tile(b));
 }
 
-void launch_sel_part(const SelArgs& a, int b, cudaStream_t st) {
+void launch_sel_part(const SelArgs& a0, int b, cudaStream_t st) {
+    SelArgs a = a0;
+    // the fused histogram's 16-bit warp bins take <= 255 subtiles x 256
+    // points between flushes; LBKD_HFLUSH_EVERY lowers it (tests of the
+    // flush path at small sizes)
+    a.hflush_every = 255;
+    if (const char* e = getenv("LBKD_HFLUSH_EVERY")) {
+        const int v = atoi(e);
+        if (v >= 1 && v < 255) a.hflush_every = v;
+    }
     const int T = sel_tile(b);
     const u64 nsub = (a.g.nview + kSub - 1) / kSub;
     const u64 per_cta = kPThreads / 32;

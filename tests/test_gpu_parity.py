@@ -345,3 +345,34 @@ def test_selection_subtree_kernel_for_round_robin(n):
             assert np.array_equal(perm, oracle.build_rr(pts)), (kind, n, k)
     finally:
         _native.set_subtree_kernel("default")
+
+
+def test_fused_histogram_flush_path():
+    """The partition's fused next-level histogram keeps two 16-bit bins per
+    warp-private word and flushes them at least every 255 subtiles; at test
+    sizes a warp never reaches 255, so LBKD_HFLUSH_EVERY=1 forces the flush
+    path on every subtile -- the builds must stay bit-exact."""
+    import subprocess
+    import sys
+
+    code = r'''
+import numpy as np, torch
+import paper_2211_00120_b200 as kd
+from paper_2211_00120_b200 import datagen
+from oracle import oracle
+for kind in ("uniform", "ties", "clustered"):
+    pts = datagen.make(kind, 1_500_003, 3, seed=11)
+    d = torch.from_numpy(pts).cuda()
+    _, perm = kd.build_round_robin_cuda(d)
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), oracle.build_rr(pts)), ("rr", kind)
+    _, perm, dims = kd.build_widest_cuda(d)
+    wp, wd = oracle.build_widest(pts)
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), wp), ("widest", kind)
+    assert np.array_equal(dims.cpu().numpy(), wd), ("widest dims", kind)
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LBKD_HFLUSH_EVERY="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
