@@ -164,7 +164,7 @@ __device__ __forceinline__ int list_sort_dim(ET* buf0, ET* buf1, int cur, int m,
 
 // One round-robin chain order T_d = (c[d], c[d-1], ..., c[d-k+1], local id)
 // of the m points of P, written to out as local ids, by ONE value-linear
-// bucket pass instead of 3-4 radix passes: NB equal-width buckets over the
+// bucket pass instead of 3-4 radix passes: 2 NB equal-width buckets over the
 // points' [min, max] in dim d (monotone in the key, so buckets are ordered),
 // shared-atomic counts, a block scan, an atomic scatter, then every bucket
 // is put in T_d order by insertion sort under the full chain comparator (the
@@ -201,38 +201,56 @@ __device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m
         kmin = min(kmin, scratch[w]);
         kmax = max(kmax, scratch[32 + w]);
     }
+    // 2 NB buckets as 16-bit halves of the NB shared words (counts, then
+    // starts, then ends; every value <= m < 2^16, so no half carries)
+    const u32 NBK = 2u * (u32)NB;
     const float lo = unflip_key(kmin);
     const float range = __fsub_rn(unflip_key(kmax), lo);
-    float scale = range > 0.f ? __fdiv_rn((float)NB, range) : 0.f;
+    float scale = range > 0.f ? __fdiv_rn((float)NBK, range) : 0.f;
     if (!(scale <= 3.0e38f)) scale = 0.f;  // overflowing range / denormal width: one bucket -> radix
     auto bucket = [&](float x) -> u32 {
         const u32 b = (u32)__fmul_rn(__fsub_rn(x, lo), scale);  // NaN-free: x >= lo, finite
-        return b < (u32)NB ? b : (u32)NB - 1u;
+        return b < NBK ? b : NBK - 1u;
     };
-    for (int p = tid; p < m; p += NT) atomicAdd(&hist[bucket(Pd[p])], 1u);
+    for (int p = tid; p < m; p += NT) {
+        const u32 b = bucket(Pd[p]);
+        atomicAdd(&hist[b >> 1], (b & 1u) ? 0x10000u : 1u);
+    }
     __syncthreads();
-    // exclusive scan over NB counts, NB / NT consecutive per thread, and the
-    // largest bucket
+    // exclusive scan over the 2 NB counts, NB / NT consecutive words per
+    // thread, and the largest bucket
     const int per = NB / NT;  // a multiple of 4 (NB = Mp >= 4 NT): 16-byte shared loads / stores
     uint4* const h4 = reinterpret_cast<uint4*>(hist) + tid * (per / 4);
     u32 s = 0, big = 0;
+    auto acc = [&](u32 c) {
+        s += (c & 0xffffu) + (c >> 16);
+        big = max(big, max(c & 0xffffu, c >> 16));
+    };
     for (int i = 0; i < per / 4; ++i) {
         const uint4 c = h4[i];
-        s += c.x + c.y + c.z + c.w;
-        big = max(big, max(max(c.x, c.y), max(c.z, c.w)));
+        acc(c.x);
+        acc(c.y);
+        acc(c.z);
+        acc(c.w);
     }
     big = __reduce_max_sync(kFullMask, big);
     const u32 ex = block_exclusive_scan<u32>(s, scratch, nullptr);
     scratch[32 + warp] = big;
     u32 run = ex;
+    auto starts = [&](u32 c) -> u32 {
+        const u32 s0 = run;
+        run += c & 0xffffu;
+        const u32 s1 = run;
+        run += c >> 16;
+        return s0 | (s1 << 16);
+    };
     for (int i = 0; i < per / 4; ++i) {
         const uint4 c = h4[i];
         uint4 o;
-        o.x = run;
-        o.y = run + c.x;
-        o.z = o.y + c.y;
-        o.w = o.z + c.z;
-        run = o.w + c.w;
+        o.x = starts(c.x);
+        o.y = starts(c.y);
+        o.z = starts(c.z);
+        o.w = starts(c.w);
         h4[i] = o;
     }
     __syncthreads();
@@ -243,12 +261,14 @@ __device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m
         __syncthreads();
         return false;
     }
-    for (int p = tid; p < m; p += NT) out[atomicAdd(&hist[bucket(Pd[p])], 1u)] = (unsigned short)p;
+    for (int p = tid; p < m; p += NT) {
+        const u32 b = bucket(Pd[p]);
+        const u32 old = atomicAdd(&hist[b >> 1], (b & 1u) ? 0x10000u : 1u);
+        out[(b & 1u) ? old >> 16 : old & 0xffffu] = (unsigned short)p;
+    }
     __syncthreads();
-    // hist[b] = end of bucket b; order each bucket under T_d
-    for (int b = tid; b < NB; b += NT) {
-        const int e = (int)hist[b];
-        const int st = b ? (int)hist[b - 1] : 0;
+    // the halves now hold the buckets' ends; order each bucket under T_d
+    auto isort = [&](int st, int e) {
         for (int i = st + 1; i < e; ++i) {
             // finite coordinates: float order == flipped-key order (-0 == +0)
             const u32 v = out[i];
@@ -275,6 +295,13 @@ __device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m
             }
             out[t + 1] = (unsigned short)v;
         }
+    };
+    for (int w = tid; w < NB; w += NT) {
+        const u32 c = hist[w];
+        const int e0 = (int)(c & 0xffffu), e1 = (int)(c >> 16);
+        const int st0 = w ? (int)(hist[w - 1] >> 16) : 0;
+        if (e0 - st0 > 1) isort(st0, e0);
+        if (e1 - e0 > 1) isort(e0, e1);
     }
     __syncthreads();
     return true;
