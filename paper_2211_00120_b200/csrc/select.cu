@@ -540,11 +540,13 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
             if (lane == 0) { red[0][warp] = mn; red[1][warp] = mx; }
             for (int i = tid; i < 256; i += NT) hist[i] = 0u;
             __syncthreads();
-            if (tid == 0) {
-                u32 a0 = 0xffffffffu, b0 = 0u;
-                for (int w = 0; w < NT / 32; ++w) { a0 = min(a0, red[0][w]); b0 = max(b0, red[1][w]); }
-                s_misc[0] = a0;
-                s_misc[1] = b0;
+            if (warp == 0) {  // the block's range: one reduction over the warps' values
+                const u32 a0 = __reduce_min_sync(kFullMask, lane < NT / 32 ? red[0][lane] : 0xffffffffu);
+                const u32 b0 = __reduce_max_sync(kFullMask, lane < NT / 32 ? red[1][lane] : 0u);
+                if (lane == 0) {
+                    s_misc[0] = a0;
+                    s_misc[1] = b0;
+                }
             }
             __syncthreads();
             mn = s_misc[0];
@@ -554,13 +556,36 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
             for (u32 i = tid; i < n; i += NT)
                 atomicAdd(&hist[(rec_field(src + (u64)i * R, ch, f, k) - mn) >> sh], 1u);
             __syncthreads();
-            if (tid == 0) {
-                u32 cum = 0;
-                int b = 0;
-                while (cum + hist[b] <= r) { cum += hist[b]; ++b; }
-                s_misc[2] = (u32)b;
-                s_misc[3] = cum;
-                s_misc[0] = 0u;  // compaction counter
+            if (warp == 0) {
+                // bucket holding rank r: 8 bins per lane, a warp scan of the
+                // lane sums, then the one lane whose range holds r walks its bins
+                u32 c[8];
+                u32 sum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    c[q] = hist[lane * 8 + q];
+                    sum += c[q];
+                }
+                u32 x = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 y = __shfl_up_sync(kFullMask, x, o);
+                    if (lane >= o) x += y;
+                }
+                u32 cum = x - sum;
+                if (r >= cum && r < x) {
+                    int bsel = -1;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (bsel < 0) {
+                            if (cum + c[q] > r) bsel = lane * 8 + q;
+                            else cum += c[q];
+                        }
+                    }
+                    s_misc[2] = (u32)bsel;
+                    s_misc[3] = cum;
+                    s_misc[0] = 0u;  // compaction counter
+                }
             }
             __syncthreads();
             const u32 bsel = s_misc[2];
