@@ -467,11 +467,18 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             if (t != kFin) atomicAdd(&sv[t * kSegWords + kSgCnt], 1u);
         }
         __syncthreads();
-        if (tid == 0) {
-            u32 o = 0;
-            for (int t = 0; t < nloc; ++t) {
-                sv[t * kSegWords + kSgOff] = o;
-                o += sv[t * kSegWords + kSgCnt];
+        if (warp == 0) {  // segment offsets: warp scan, 32 segments per step
+            u32 base = 0;
+            for (int t0 = 0; t0 < nloc; t0 += 32) {
+                const int t = t0 + lane;
+                const u32 c = t < nloc ? sv[t * kSegWords + kSgCnt] : 0u;
+                u32 x = c;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 y = __shfl_up_sync(kFullMask, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (t < nloc) sv[t * kSegWords + kSgOff] = base + x - c;
+                base += __shfl_sync(kFullMask, x, 31);
             }
         }
         __syncthreads();
