@@ -1190,8 +1190,16 @@ void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
     const int T = sel_tile(b);
     a.ntiles = (a.g.nview + T - 1) / T;
     const u64 grid = a.ntiles < 148 * 8 ? a.ntiles : 148 * 8;
-    // contiguous runs of tiles per CTA (the segment cursor advances locally)
-    const u64 target = 148 * 16;
+    // contiguous runs of tiles per CTA (the segment cursor advances locally);
+    // CTAs per SM (LBKD_FILTER_CTAS_PER_SM): measured at 100M, 2048-point
+    // tiles (RR) best at 32 (2.30 ms vs 2.38 at 16), 1024-point tiles
+    // (widest) at 64 (2.87 vs 3.10)
+    u64 per_sm = T >= 2048 ? 32 : 64;
+    if (const char* e = getenv("LBKD_FILTER_CTAS_PER_SM")) {
+        const int v = atoi(e);
+        if (v >= 1 && v <= 64) per_sm = (u64)v;
+    }
+    const u64 target = 148 * per_sm;
     u64 tpc = (a.ntiles + target - 1) / target;
     if (tpc < 1) tpc = 1;
     a.tiles_per_cta = (int)tpc;
