@@ -68,6 +68,23 @@ int lbkd_build_rr(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int
 int lbkd_build_widest(lbkd_ctx *ctx, const float *d_points, float *d_points_out, int64_t n, int k,
                       uint32_t *d_perm, uint8_t *d_split_dims, void *stream);
 
+/* float64 input -- the reference's own coordinate dtype (ingest promotes
+ * every input to float64, builder.py:131-133).  Same contract as
+ * lbkd_build_rr / lbkd_build_widest with n x k float64 rows in and out; the
+ * permutation and split dims are bit-identical to the reference's on the
+ * same float64 input.  The device computes each dimension's dense ranks
+ * (-0.0 == +0.0), builds on the rank codes and gathers the float64 rows;
+ * widest widths are float64 differences of the original values.  Ends with
+ * k + 1 stream synchronisations (distinct-value counts, non-finite flag). */
+int lbkd_build_rr_f64(lbkd_ctx *ctx, const double *d_points, double *d_points_out, int64_t n, int k,
+                      uint32_t *d_perm, void *stream);
+int lbkd_build_widest_f64(lbkd_ctx *ctx, const double *d_points, double *d_points_out, int64_t n, int k,
+                          uint32_t *d_perm, uint8_t *d_split_dims, void *stream);
+int lbkd_build_rr_f64_trace(lbkd_ctx *ctx, const double *d_points, double *d_points_out, int64_t n, int k,
+                            uint32_t *d_perm, uint32_t *d_trace, void *stream);
+int lbkd_build_widest_f64_trace(lbkd_ctx *ctx, const double *d_points, double *d_points_out, int64_t n, int k,
+                                uint32_t *d_perm, uint8_t *d_split_dims, uint32_t *d_trace, void *stream);
+
 /* Round-robin build that also records, for every sort level l, the order of
  * the not-yet-final points after the sort: d_trace[l*n + p] = index (into
  * d_points) of the point at working position p (the reference's array with
@@ -190,6 +207,20 @@ int lbkd_check_valid(const float *d_tree, int64_t n, int k, const uint8_t *d_spl
                      uint64_t *d_scratch, void *stream);
 int lbkd_subtree_boxes(const float *d_tree, int64_t n, int k, const uint8_t *d_split_dims, double *d_lo,
                        double *d_hi, void *stream);
+/* The same four calls on float64 level-order rows (trees built from float64
+ * input by lbkd_build_*_f64). */
+int lbkd_knn_f64(const double *d_tree, int64_t n, int k, const uint8_t *d_split_dims, const double *d_queries,
+                 int64_t nq, int m, int64_t *d_out_idx, double *d_out_d2, void *stream);
+int lbkd_radius_count_f64(const double *d_tree, int64_t n, int k, const uint8_t *d_split_dims,
+                          const double *d_queries, int64_t nq, double r2, int64_t *d_counts, int64_t *d_offsets,
+                          int64_t *d_scratch, void *stream);
+int lbkd_radius_fill_f64(const double *d_tree, int64_t n, int k, const uint8_t *d_split_dims,
+                         const double *d_queries, int64_t nq, double r2, const int64_t *d_offsets,
+                         int64_t *d_out_idx, void *stream);
+int lbkd_check_valid_f64(const double *d_tree, int64_t n, int k, const uint8_t *d_split_dims, int64_t *d_witness,
+                         uint64_t *d_scratch, void *stream);
+int lbkd_subtree_boxes_f64(const double *d_tree, int64_t n, int k, const uint8_t *d_split_dims, double *d_lo,
+                           double *d_hi, void *stream);
 const char *lbkd_strerror(int code);
 const char *lbkd_last_cuda_error(void);
 

@@ -46,9 +46,9 @@ def build_lib() -> str:
 def _load():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(
-            os.path.join(_HERE, "lbkd_oracle.c")
-        ):
+        srcs = [os.path.join(_HERE, f) for f in ("lbkd_oracle.c", "lbkd_recursive.cpp", "Makefile")]
+        if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
+                os.path.getmtime(f) for f in srcs if os.path.exists(f)):
             build_lib()
         lib = ctypes.CDLL(_LIB_PATH)
         p = ctypes.c_void_p
@@ -56,6 +56,10 @@ def _load():
         lib.oracle_build_rr.restype = ctypes.c_int
         lib.oracle_build_widest.argtypes = [p, ctypes.c_int64, ctypes.c_int, p, p]
         lib.oracle_build_widest.restype = ctypes.c_int
+        lib.oracle_rec_build_f32.argtypes = [p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, p, p, ctypes.c_int]
+        lib.oracle_rec_build_f32.restype = ctypes.c_int
+        lib.oracle_rec_build_f64.argtypes = [p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, p, p, ctypes.c_int]
+        lib.oracle_rec_build_f64.restype = ctypes.c_int
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         lib.oracle_threads.restype = ctypes.c_int
         lib.oracle_set_threads(0)
@@ -119,6 +123,33 @@ def build_widest(points):
     rc = _load().oracle_build_widest(pts.ctypes.data, n, k, perm.ctypes.data, dims.ctypes.data)
     assert rc == 0
     return perm, dims
+
+
+def rec_build(points, widest: bool = False, threads: int = 0):
+    """Recursive median-placement oracle (lbkd_recursive.cpp, restating
+    verify.reference_build, verify.py:121-168), threaded over subtrees.
+
+    float32 input is used as is; anything else is promoted to float64 like the
+    reference's ingest (builder.py:131-133).  Returns perm (uint32), and for
+    ``widest`` also split_dims (uint8)."""
+    pts = np.asarray(points)
+    if pts.ndim == 1:
+        pts = pts.reshape(-1, 1)
+    n, k = pts.shape
+    perm = np.empty(n, dtype=np.uint32)
+    dims = np.zeros(n, dtype=np.uint8)
+    if n:
+        lib = _load()
+        if pts.dtype == np.float32:
+            pts = np.ascontiguousarray(pts)
+            rc = lib.oracle_rec_build_f32(pts.ctypes.data, n, k, int(widest), perm.ctypes.data,
+                                          dims.ctypes.data if widest else None, int(threads))
+        else:
+            pts = np.ascontiguousarray(pts, dtype=np.float64)
+            rc = lib.oracle_rec_build_f64(pts.ctypes.data, n, k, int(widest), perm.ctypes.data,
+                                          dims.ctypes.data if widest else None, int(threads))
+        assert rc == 0, rc
+    return (perm, dims) if widest else perm
 
 
 def timed_build(points, mode: str = "rr") -> float:

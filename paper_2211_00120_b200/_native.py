@@ -27,6 +27,7 @@ EXPORTED = (
     "lbkd_create", "lbkd_destroy", "lbkd_set_check",
     "lbkd_build_rr", "lbkd_build_widest",
     "lbkd_build_rr_trace", "lbkd_build_widest_trace",
+    "lbkd_build_rr_f64", "lbkd_build_widest_f64", "lbkd_build_rr_f64_trace", "lbkd_build_widest_f64_trace",
     "lbkd_update_tags_rr", "lbkd_update_tags_widest",
     "lbkd_num_levels", "lbkd_single_cta_capacity", "lbkd_plan_info",
     "lbkd_last_launch_count", "lbkd_strerror", "lbkd_last_cuda_error",
@@ -37,6 +38,8 @@ EXPORTED = (
     "lbkd_set_subtree_kernel",
     "lbkd_knn", "lbkd_radius_count", "lbkd_radius_scratch_len", "lbkd_radius_fill",
     "lbkd_check_valid", "lbkd_subtree_boxes",
+    "lbkd_knn_f64", "lbkd_radius_count_f64", "lbkd_radius_fill_f64", "lbkd_check_valid_f64",
+    "lbkd_subtree_boxes_f64",
 )
 
 # kernel classes of lbkd_profile_kernel
@@ -85,6 +88,14 @@ def load():
         lib.lbkd_build_rr_trace.restype = i32
         lib.lbkd_build_widest_trace.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp, vp]
         lib.lbkd_build_widest_trace.restype = i32
+        lib.lbkd_build_rr_f64.argtypes = [vp, vp, vp, i64, i32, vp, vp]
+        lib.lbkd_build_rr_f64.restype = i32
+        lib.lbkd_build_widest_f64.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp]
+        lib.lbkd_build_widest_f64.restype = i32
+        lib.lbkd_build_rr_f64_trace.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp]
+        lib.lbkd_build_rr_f64_trace.restype = i32
+        lib.lbkd_build_widest_f64_trace.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp, vp]
+        lib.lbkd_build_widest_f64_trace.restype = i32
         lib.lbkd_build_rr_top.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, i64, vp]
         lib.lbkd_build_rr_top.restype = i32
         lib.lbkd_build_rr_sub.argtypes = [vp, vp, i64, i64, i32, i32, i64, vp, vp, vp]
@@ -133,6 +144,17 @@ def load():
         lib.lbkd_check_valid.restype = i32
         lib.lbkd_subtree_boxes.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         lib.lbkd_subtree_boxes.restype = i32
+        for suffix in ("", "_f64"):
+            getattr(lib, "lbkd_knn" + suffix).argtypes = [vp, i64, i32, vp, vp, i64, i32, vp, vp, vp]
+            getattr(lib, "lbkd_knn" + suffix).restype = i32
+            getattr(lib, "lbkd_radius_count" + suffix).argtypes = [vp, i64, i32, vp, vp, i64, f64, vp, vp, vp, vp]
+            getattr(lib, "lbkd_radius_count" + suffix).restype = i32
+            getattr(lib, "lbkd_radius_fill" + suffix).argtypes = [vp, i64, i32, vp, vp, i64, f64, vp, vp, vp]
+            getattr(lib, "lbkd_radius_fill" + suffix).restype = i32
+            getattr(lib, "lbkd_check_valid" + suffix).argtypes = [vp, i64, i32, vp, vp, vp, vp]
+            getattr(lib, "lbkd_check_valid" + suffix).restype = i32
+            getattr(lib, "lbkd_subtree_boxes" + suffix).argtypes = [vp, i64, i32, vp, vp, vp, vp]
+            getattr(lib, "lbkd_subtree_boxes" + suffix).restype = i32
         lib.lbkd_strerror.argtypes = [i32]
         lib.lbkd_strerror.restype = ctypes.c_char_p
         lib.lbkd_last_cuda_error.argtypes = []

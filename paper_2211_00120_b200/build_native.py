@@ -32,19 +32,47 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
-    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-shared", "-o", LIB + ".tmp", *sources(), "-cudart", "static"]
+def _compile(nvcc, src, obj):
+    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-c", "-o", obj + ".tmp", src]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stderr[-8000:])
+        raise RuntimeError(f"nvcc failed on {os.path.basename(src)}:\n" + r.stderr[-8000:])
+    os.replace(obj + ".tmp", obj)
+    return r.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """One object per translation unit (compiled in parallel, each rebuilt
+    when it or any header is newer), linked into one shared library with a
+    static CUDA runtime."""
+    if not force and not _stale():
+        return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    obj_dir = os.path.join(LIB_DIR, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
+    newest_header = max((os.path.getmtime(h) for h in headers), default=0.0)
+    jobs = []
+    objs = []
+    for src in sources():
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), newest_header):
+            jobs.append((src, obj))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        logs = list(ex.map(lambda j: _compile(nvcc, *j), jobs))
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs,
+           "-cudart", "static"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc link failed:\n" + r.stderr[-8000:])
     if verbose:
-        print(r.stderr)
-    with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as f:
-        f.write(r.stderr)
+        print("".join(logs))
+    if logs:
+        with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as f:
+            f.write("".join(logs))
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -96,11 +96,14 @@ class BuildRecorder:
 
 
 def ingest(points, k: int | None = None, payload=None):
-    """Validate like the reference (builder.py:108-142); return float32
-    (n, k) C-contiguous coordinates and an int64 payload.
+    """Validate like the reference (builder.py:108-142); return C-contiguous
+    (n, k) coordinates and an int64 payload.
 
-    The B200 path computes in float32: float64 inputs must be exactly
-    float32-representable (the benchmark configurations are float32)."""
+    The reference promotes every input to float64.  Inputs that are exactly
+    float32-representable (float32 data, small integers, ...) come back as
+    float32 -- the fast device path, whose results are identical because the
+    promotion is exact; anything else comes back as float64 and is built by
+    the float64 device path (lbkd_build_*_f64: per-dimension ranks)."""
     raw = np.asarray(points)
     if raw.ndim not in (1, 2):
         raise ValueError(f"points must be a 2-d array, got shape {raw.shape}")
@@ -118,16 +121,13 @@ def ingest(points, k: int | None = None, payload=None):
     if raw.dtype == np.float32:
         coords = np.ascontiguousarray(raw)
     else:
-        wide = np.asarray(raw, dtype=np.float64)
-        coords = np.ascontiguousarray(wide, dtype=np.float32)
-        finite = np.isfinite(wide)
-        if not np.all(finite):
+        wide = np.ascontiguousarray(raw, dtype=np.float64)
+        if not np.all(np.isfinite(wide)):
             raise ValueError("coordinates must be finite (no NaN or infinity)")
-        if not np.array_equal(coords.astype(np.float64), wide):
-            raise ValueError(
-                "coordinates must be exactly representable in float32 "
-                "(the B200 build computes in float32)"
-            )
+        with np.errstate(over="ignore"):
+            narrow = wide.astype(np.float32)
+        # -0.0 and +0.0 compare equal here and are both exact in float32
+        coords = narrow if np.array_equal(narrow, wide) else wide
     if not np.all(np.isfinite(coords)):
         raise ValueError("coordinates must be finite (no NaN or infinity)")
     if payload is None:
@@ -153,22 +153,61 @@ def _stream_ptr(torch, stream):
 
 
 def _check_points_tensor(torch, points):
-    if points.device.type != "cuda" or points.dtype != torch.float32 or points.dim() != 2:
-        raise ValueError("points must be a 2-d float32 CUDA tensor")
+    if points.device.type != "cuda" or points.dtype not in (torch.float32, torch.float64) or points.dim() != 2:
+        raise ValueError("points must be a 2-d float32 or float64 CUDA tensor")
     if not points.is_contiguous():
         raise ValueError("points must be C-contiguous (n, k)")
 
 
+def _check_out_buffers(torch, points, out=None, perm=None, split_dims=None):
+    """Caller-supplied outputs must match the points exactly: the C ABI takes
+    raw pointers and writes n rows / entries into each of them."""
+    n, k = points.shape
+    if out is not None and (out.device != points.device or out.dtype != points.dtype
+                            or tuple(out.shape) != (n, k) or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous ({n}, {k}) {points.dtype} tensor on {points.device}")
+    if perm is not None and (perm.device != points.device or perm.dtype not in (torch.int32, torch.uint32)
+                             or tuple(perm.shape) != (n,) or not perm.is_contiguous()):
+        raise ValueError(f"perm must be a contiguous ({n},) int32 tensor on {points.device}")
+    if split_dims is not None and (split_dims.device != points.device or split_dims.dtype != torch.uint8
+                                   or tuple(split_dims.shape) != (n,) or not split_dims.is_contiguous()):
+        raise ValueError(f"split_dims must be a contiguous ({n},) uint8 tensor on {points.device}")
+
+
+def _check_host_buffers(torch, points, out, perm, split_dims=None):
+    """Host-pipeline buffers: contiguous CPU tensors of the right dtype and
+    shape (the native side copies n rows into / out of each)."""
+    for t in (points, out, perm) + ((split_dims,) if split_dims is not None else ()):
+        if t.device.type != "cpu" or not t.is_contiguous():
+            raise ValueError("host buffers must be contiguous CPU tensors")
+    if points.dtype != torch.float32 or points.dim() != 2:
+        raise ValueError("points must be a 2-d float32 CPU tensor")
+    n, k = points.shape
+    if out.dtype != torch.float32 or tuple(out.shape) != (n, k):
+        raise ValueError(f"out must be a ({n}, {k}) float32 CPU tensor")
+    if perm.dtype not in (torch.int32, torch.uint32) or tuple(perm.shape) != (n,):
+        raise ValueError(f"perm must be a ({n},) int32 CPU tensor")
+    if split_dims is not None and (split_dims.dtype != torch.uint8 or tuple(split_dims.shape) != (n,)):
+        raise ValueError(f"split_dims must be a ({n},) uint8 CPU tensor")
+
+
 def build_round_robin_cuda(points, *, out=None, perm=None, stream=None, check_finite: bool = True,
                            trace=None):
-    """Device-resident build. ``points``: (n, k) float32 CUDA tensor.
+    """Device-resident build. ``points``: (n, k) float32 or float64 CUDA
+    tensor (float64: lbkd_build_rr_f64, the reference's own dtype).
 
-    Returns (out, perm): level-order points (n, k) float32 and the input row
-    of each node (uint32 stored in an int32 tensor).  ``out`` may be
+    Returns (out, perm): level-order points (n, k) of the input dtype and the
+    input row of each node (uint32 stored in an int32 tensor).  ``out`` may be
     ``points`` itself (in-place reordering).
     """
     torch = _torch()
     _check_points_tensor(torch, points)
+    _check_out_buffers(torch, points, out, perm)
+    if trace is not None:
+        L = treemath.num_levels(points.shape[0])
+        if (trace.device != points.device or trace.dtype != torch.int32 or not trace.is_contiguous()
+                or trace.numel() < max(L, 1) * points.shape[0]):
+            raise ValueError("trace must be a contiguous int32 tensor of num_levels(n) * n entries")
     n, k = points.shape
     dev = points.device.index if points.device.index is not None else torch.cuda.current_device()
     if out is None:
@@ -180,11 +219,13 @@ def build_round_robin_cuda(points, *, out=None, perm=None, stream=None, check_fi
     lib.lbkd_set_check(ctx, 1 if check_finite else 0)
     with torch.cuda.device(dev):
         sp = _stream_ptr(torch, stream)
+        f64 = points.dtype == torch.float64
         if trace is None:
-            rc = lib.lbkd_build_rr(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(), sp)
+            fn = lib.lbkd_build_rr_f64 if f64 else lib.lbkd_build_rr
+            rc = fn(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(), sp)
         else:
-            rc = lib.lbkd_build_rr_trace(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(),
-                                         trace.data_ptr(), sp)
+            fn = lib.lbkd_build_rr_f64_trace if f64 else lib.lbkd_build_rr_trace
+            rc = fn(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(), trace.data_ptr(), sp)
     _raise_for(rc, "lbkd_build_rr", n, k)
     return out, perm
 
@@ -198,9 +239,7 @@ def build_round_robin_host(points, out, perm, *, device: int = 0, stream=None) -
     buffers are valid after :func:`host_join`.
     """
     torch = _torch()
-    for t in (points, out, perm):
-        if t.device.type != "cpu" or not t.is_contiguous():
-            raise ValueError("host buffers must be contiguous CPU tensors")
+    _check_host_buffers(torch, points, out, perm)
     n, k = points.shape
     lib = _native.load()
     ctx = _native.context(device)

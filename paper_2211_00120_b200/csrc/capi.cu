@@ -47,22 +47,37 @@ struct lbkd_ctx {
     int use_graph = 1;
     cudaStream_t cap_stream = nullptr;
     cudaEvent_t cap_fork = nullptr, cap_join = nullptr;
-    cudaGraphExec_t gexec = nullptr;
     struct GraphKey {
         const void* pts;
         const void* out;
         const void* perm;
         const void* dims;
+        const void* err;
         int64_t n;
         int k, mode, algo, sub, check, profile;
         bool operator==(const GraphKey& o) const {
-            return pts == o.pts && out == o.out && perm == o.perm && dims == o.dims && n == o.n && k == o.k &&
+            return pts == o.pts && out == o.out && perm == o.perm && dims == o.dims && err == o.err && n == o.n && k == o.k &&
                    mode == o.mode && algo == o.algo && sub == o.sub && check == o.check && profile == o.profile;
         }
-    } gkey{};
-    int64_t glaunches = 0;
-    int gn_ev = 0;  // profiling events recorded by the captured build
-    int err_sticky = 0;  // pipelined host builds: the non-finite flag accumulates until lbkd_host_join
+    };
+    // a few instantiated graphs (the pipelined host builds alternate two
+    // buffer slots, so two keys are live at once); least recently used evicted
+    struct GraphEntry {
+        GraphKey key{};
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        int n_ev = 0;  // profiling events recorded by the captured build
+        u64 used = 0;
+    };
+    static constexpr int kGraphSlots = 4;
+    GraphEntry graphs[kGraphSlots];
+    u64 graph_tick = 0;
+    int err_sticky = 0;  // set while a pipelined host build is enqueued: its flag accumulates until lbkd_host_join
+    u32* err_host = nullptr;  // the pipelined host builds' own non-finite flag (device builds use bf.err)
+    // every build on this context (device or host, any stream) uses the same
+    // scratch buffers: each build's stream first waits for the previous
+    // build's completion event, so builds on one context never overlap
+    cudaEvent_t done_ev = nullptr;
     // pipelined host-buffer builds (lbkd_build_*_host): two device buffer
     // sets alternate, H2D / build / D2H run on three streams
     struct HostPipe {
@@ -70,7 +85,8 @@ struct lbkd_ctx {
         float* d_out[2] = {nullptr, nullptr};
         u32* d_perm[2] = {nullptr, nullptr};
         uint8_t* d_dims[2] = {nullptr, nullptr};
-        size_t cap = 0;
+        size_t cap = 0;    // capacity of d_in / d_out in floats (n * k)
+        size_t cap_n = 0;  // capacity of d_perm / d_dims in points
         cudaStream_t s_h2d = nullptr, s_build = nullptr, s_d2h = nullptr;
         cudaEvent_t start = nullptr, h2d_done[2], build_done[2], d2h_done[2];
         int slot = 0, pending = 0;
@@ -93,6 +109,19 @@ struct lbkd_ctx {
     int n_ev_used = 0;
     u64* d_moved = nullptr;
     int k_last = 0;
+    // float64 builds (rank64.cu): rank scratch, rank-coded points, the float32
+    // build's output, the widest value table; cur_wt is handed to build()
+    u32* rank_scratch = nullptr;
+    size_t cap_rank = 0;
+    float* codes = nullptr;
+    float* out32 = nullptr;
+    size_t cap_codes = 0;
+    double* vtab = nullptr;
+    size_t cap_vtab = 0;
+    double* out64_tmp = nullptr;
+    size_t cap_out64 = 0;
+    u32* f64_err = nullptr;
+    WidthTab cur_wt{};
 };
 
 // kernel classes of the profile (lbkd_profile_kernel)
@@ -182,11 +211,10 @@ static int grow(T*& p, size_t& cap_unused, size_t count) {
 }
 
 static void drop_graph(lbkd_ctx* c) {
-    if (c->gexec) {
-        cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
+    for (auto& e : c->graphs) {
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+        e = lbkd_ctx::GraphEntry{};
     }
-    c->gkey = lbkd_ctx::GraphKey{};
 }
 
 static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
@@ -252,9 +280,11 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
         if ((rc = grow(c->bf.tile_ctr, dummy, 4 * 64))) return rc;
         if ((rc = grow(c->d_moved, dummy, 256))) return rc;
         if ((rc = grow(c->bf.err, dummy, 4))) return rc;
+        if ((rc = grow(c->err_host, dummy, 4))) return rc;
+        CK(cudaMemset(c->err_host, 0, 4 * sizeof(u32)));
         if ((rc = grow(c->bf.cand_ctr, dummy, 4))) return rc;
         if ((rc = grow(c->minmax, dummy, 2 * LBKD_MAX_K))) return rc;
-        CK(cudaMallocHost(&c->h_err, sizeof(u32) * 4));
+        if (!c->h_err) CK(cudaMallocHost(&c->h_err, sizeof(u32) * 4));
     }
     return LBKD_OK;
 }
@@ -336,6 +366,7 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.g = g;
         a.k = k;
         a.mode = bp.mode;
+        a.wt = bp.wt;
         a.D = D;
         a.bf = bf;
         a.par = par;
@@ -413,8 +444,16 @@ static int begin_build(lbkd_ctx* c, int k, cudaStream_t st) {
     return LBKD_OK;
 }
 
+// order this build after the previous one on the context (shared scratch)
+static int begin_order(lbkd_ctx* c, cudaStream_t st) {
+    if (!c->done_ev) CK(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
+    else CK(cudaStreamWaitEvent(st, c->done_ev, 0));
+    return LBKD_OK;
+}
+
 static int end_build(lbkd_ctx* c, cudaStream_t st) {
     CK(cudaGetLastError());
+    CK(cudaEventRecord(c->done_ev, st));
     if (c->check) {
         CK(cudaMemcpyAsync(c->h_err, c->bf.err, sizeof(u32), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -448,6 +487,11 @@ static int prologue(lbkd_ctx* c, const BuildParams& bp, int lam0, cudaStream_t s
         launch_root(bp, c->bf, c->minmax, st);
         prof_end(c, st, kPOther, 0.0);
         return LBKD_OK;
+    }
+    if (lam0 == 0) {  // no init pass: check the caller's array directly
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_check_finite(bp.pts, bp.n * (u64)k, c->bf.err, st);
+        prof_end(c, st, kPOther, pts * 4.0 * k);
     }
     if (bp.mode == kWidest) {
         CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
@@ -484,6 +528,7 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     const bool inplace = (const void*)d_points == (const void*)d_out;
     rc = ensure(c, n, k, b, lam0);
     if (rc) return rc;
+    if ((rc = begin_order(c, st))) return rc;
 
     BuildParams bp;
     bp.n = n;
@@ -506,19 +551,29 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.perm = d_perm ? d_perm : c->perm_scratch;
     bp.split_dims = d_dims ? d_dims : c->dims_scratch;
     bp.dbg = d_trace;
+    bp.wt = c->cur_wt;
     bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : (mode == kWidest ? 1 : 0);
     // the select path is a fixed, host-sync-free sequence for given buffers:
     // capture it once into a CUDA graph and replay it (the sort path carries
     // per-launch lookback epochs and is always launched directly)
     // (profiled builds launch directly: event timing of graph-recorded events
     // is not available)
-    const bool graphable = c->use_graph && c->algo == 0 && !c->profile && !d_trace && bp.pts == d_points;
-    lbkd_ctx::GraphKey key{d_points, d_out, d_perm, d_dims, n_in, k, mode, c->algo, bp.subtree_sel, c->check,
+    // (value-table builds carry their table in the kernel arguments: never graphed)
+    const bool graphable =
+        c->use_graph && c->algo == 0 && !c->profile && !d_trace && bp.pts == d_points && !bp.wt.v;
+    lbkd_ctx::GraphKey key{d_points, d_out, d_perm, d_dims, c->bf.err, n_in, k, mode, c->algo, bp.subtree_sel, c->check,
                            c->profile};
-    if (graphable && c->gexec && c->gkey == key) {
-        CK(cudaGraphLaunch(c->gexec, st));
-        c->launches = c->glaunches;
-        c->n_ev_used = c->gn_ev;
+    lbkd_ctx::GraphEntry* hit = nullptr;
+    lbkd_ctx::GraphEntry* victim = &c->graphs[0];
+    for (auto& e : c->graphs) {
+        if (e.exec && e.key == key) hit = &e;
+        if (!e.exec || (victim->exec && e.used < victim->used)) victim = &e;
+    }
+    if (graphable && hit) {
+        hit->used = ++c->graph_tick;
+        CK(cudaGraphLaunch(hit->exec, st));
+        c->launches = hit->launches;
+        c->n_ev_used = hit->n_ev;
         c->k_last = k;
         return end_build(c, st);
     }
@@ -528,9 +583,9 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
             CK(cudaEventCreateWithFlags(&c->cap_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->cap_join, cudaEventDisableTiming));
         }
-        if (c->gexec) {
-            cudaGraphExecDestroy(c->gexec);
-            c->gexec = nullptr;
+        if (victim->exec) {
+            cudaGraphExecDestroy(victim->exec);
+            *victim = lbkd_ctx::GraphEntry{};
         }
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -544,13 +599,14 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
             return r2;
         }
         CK(ce);
-        const cudaError_t ie = cudaGraphInstantiate(&c->gexec, graph, 0);
+        const cudaError_t ie = cudaGraphInstantiate(&victim->exec, graph, 0);
         cudaGraphDestroy(graph);
         CK(ie);
-        c->gkey = key;
-        c->glaunches = c->launches;
-        c->gn_ev = c->n_ev_used;
-        CK(cudaGraphLaunch(c->gexec, st));
+        victim->key = key;
+        victim->launches = c->launches;
+        victim->n_ev = c->n_ev_used;
+        victim->used = ++c->graph_tick;
+        CK(cudaGraphLaunch(victim->exec, st));
         return end_build(c, st);
     }
     if ((rc = begin_build(c, k, st))) return rc;
@@ -558,6 +614,76 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     if ((rc = run_levels(c, bp, 0, lam0, st))) return rc;
     if ((rc = run_subtrees(c, bp, lam0, st))) return rc;
     return end_build(c, st);
+}
+
+// float64 input (rank64.cu): per-dimension dense ranks coded as float32,
+// the float32 build, then the float64 rows gathered by the permutation
+static int build_f64(lbkd_ctx* c, const double* d_points, double* d_out, int64_t n_in, int k, u32* d_perm,
+                     uint8_t* d_dims, u32* d_trace, int mode, cudaStream_t st) {
+    int rc = check_args(c, n_in, k, mode);
+    if (rc) return rc;
+    c->launches = 0;
+    if (n_in == 0) return LBKD_OK;
+    if (!d_points || !d_out) return LBKD_EINVAL_SHAPE;
+    CK(cudaSetDevice(c->device));
+    const u64 n = (u64)n_in;
+    g_grow_ctx = c;
+    size_t dummy = 0;
+    const size_t rw = rank_scratch_words(n);
+    if (rw > c->cap_rank) {
+        if ((rc = grow(c->rank_scratch, dummy, rw))) return rc;
+        c->cap_rank = rw;
+    }
+    if (n * (u64)k > c->cap_codes) {
+        if ((rc = grow(c->codes, dummy, n * (size_t)k))) return rc;
+        if ((rc = grow(c->out32, dummy, n * (size_t)k))) return rc;
+        c->cap_codes = n * (size_t)k;
+    }
+    if (mode == kWidest && n * (u64)k > c->cap_vtab) {
+        if ((rc = grow(c->vtab, dummy, n * (size_t)k))) return rc;
+        c->cap_vtab = n * (size_t)k;
+    }
+    if (!c->f64_err && (rc = grow(c->f64_err, dummy, 4))) return rc;
+    if (!c->h_err) CK(cudaMallocHost(&c->h_err, sizeof(u32) * 4));
+    if ((rc = begin_order(c, st))) return rc;
+    CK(cudaMemsetAsync(c->f64_err, 0, 4 * sizeof(u32), st));
+    WidthTab wt{};
+    wt.stride = n;
+    wt.v = mode == kWidest ? c->vtab : nullptr;
+    for (int d = 0; d < k; ++d) {
+        if ((rc = rank_sort_dim(d_points, n, k, d, c->rank_scratch, c->f64_err, st))) return rc;
+        u32* hc = c->h_err + 1;  // pinned
+        CK(cudaMemcpyAsync(hc, rank_count_word(c->rank_scratch, n), sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const u64 distinct = (u64)*hc + 1;
+        const int wide = distinct > 2ull * kRankSide - 1;
+        wt.wide |= (u32)wide << d;
+        wt.center[d] = wide ? 0u : (u32)(distinct / 2);
+        if ((rc = rank_assign_dim(n, k, d, wt.center[d], wide, c->codes, wt.v ? c->vtab + (u64)d * n : nullptr,
+                                  c->rank_scratch, st)))
+            return rc;
+    }
+    CK(cudaMemcpyAsync(c->h_err, c->f64_err, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c->h_err[0]) return LBKD_ENONFINITE;
+    c->cur_wt = wt;
+    rc = build(c, c->codes, c->out32, n_in, k, d_perm, d_dims, d_trace, mode, st);
+    c->cur_wt = WidthTab{};
+    if (rc) return rc;
+    const u32* perm = d_perm ? d_perm : c->perm_scratch;
+    if ((const void*)d_out == (const void*)d_points) {
+        if (n * (u64)k > c->cap_out64) {
+            if ((rc = grow(c->out64_tmp, dummy, n * (size_t)k))) return rc;
+            c->cap_out64 = n * (size_t)k;
+        }
+        launch_gather_rows_f64(d_points, perm, n, k, c->out64_tmp, st);
+        CK(cudaMemcpyAsync(d_out, c->out64_tmp, n * (size_t)k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    } else {
+        launch_gather_rows_f64(d_points, perm, n, k, d_out, st);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->done_ev, st));
+    return LBKD_OK;
 }
 
 // multi-device, rank 0: the top `top` levels of the whole tree, then the
@@ -588,6 +714,7 @@ static int build_top(lbkd_ctx* c, const float* d_points, int64_t n_in, int k, in
     bp.perm = d_perm;
     bp.split_dims = c->dims_scratch;
     bp.dbg = nullptr;
+    if ((rc = begin_order(c, st))) return rc;
     if ((rc = begin_build(c, k, st))) return rc;
     if ((rc = prologue(c, bp, lam0, st))) return rc;
     if ((rc = run_levels(c, bp, 0, top, st))) return rc;
@@ -631,6 +758,7 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     bp.lroot = root_level;
     bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : 0;
     bp.jroot = (u64)root_index;
+    if ((rc = begin_order(c, st))) return rc;
     if ((rc = begin_build(c, k, st))) return rc;
     CK(cudaMemcpy2DAsync(c->bf.w[0], c->bf.stride * sizeof(u32), d_sub, (size_t)sub_stride * sizeof(u32),
                          nview * sizeof(u32), (size_t)k + 1, cudaMemcpyDeviceToDevice, st));
@@ -656,6 +784,7 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
 // ---------------------------------------------------------------------------
 static int host_pipe_ensure(lbkd_ctx* c, size_t n, int k) {
     auto& h = c->hp;
+    g_grow_ctx = c;
     if (!h.s_h2d) {
         CK(cudaStreamCreateWithFlags(&h.s_h2d, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&h.s_build, cudaStreamNonBlocking));
@@ -669,18 +798,25 @@ static int host_pipe_ensure(lbkd_ctx* c, size_t n, int k) {
             CK(cudaEventRecord(h.d2h_done[i], h.s_d2h));
         }
     }
+    // point buffers grow on n * k, perm / split-dim buffers on n (a later
+    // call may have more points and fewer dimensions)
     const size_t need = n * (size_t)k;
-    if (need > h.cap) {
+    if (need > h.cap || n > h.cap_n) {
         CK(cudaDeviceSynchronize());
         size_t dummy = 0;
         int rc;
         for (int i = 0; i < 2; ++i) {
-            if ((rc = grow(h.d_in[i], dummy, need))) return rc;
-            if ((rc = grow(h.d_out[i], dummy, need))) return rc;
-            if ((rc = grow(h.d_perm[i], dummy, n))) return rc;
-            if ((rc = grow(h.d_dims[i], dummy, n))) return rc;
+            if (need > h.cap) {
+                if ((rc = grow(h.d_in[i], dummy, need))) return rc;
+                if ((rc = grow(h.d_out[i], dummy, need))) return rc;
+            }
+            if (n > h.cap_n) {
+                if ((rc = grow(h.d_perm[i], dummy, n))) return rc;
+                if ((rc = grow(h.d_dims[i], dummy, n))) return rc;
+            }
         }
-        h.cap = need;
+        if (need > h.cap) h.cap = need;
+        if (n > h.cap_n) h.cap_n = n;
     }
     return LBKD_OK;
 }
@@ -709,10 +845,21 @@ static int build_host(lbkd_ctx* c, const float* h_points, float* h_out, int64_t 
     CK(cudaEventRecord(h.h2d_done[s], h.s_h2d));
     CK(cudaStreamWaitEvent(h.s_build, h.h2d_done[s], 0));
     CK(cudaStreamWaitEvent(h.s_build, h.d2h_done[s], 0));  // d_out[s] drained
+    // the build writes the pipeline's own non-finite flag, which accumulates
+    // until lbkd_host_join (device builds keep theirs in bf.err)
+    if (!c->err_host) {
+        size_t dummy = 0;
+        if ((rc = grow(c->err_host, dummy, 4))) return rc;
+        CK(cudaMemset(c->err_host, 0, 4 * sizeof(u32)));
+    }
     const int check = c->check;
+    u32* const dev_err = c->bf.err;
     c->check = 0;
     c->err_sticky = 1;
+    c->bf.err = c->err_host;
     rc = build(c, h.d_in[s], h.d_out[s], n_in, k, h.d_perm[s], h.d_dims[s], nullptr, mode, h.s_build);
+    c->bf.err = dev_err;
+    c->err_sticky = 0;
     c->check = check;
     if (rc) return rc;
     CK(cudaEventRecord(h.build_done[s], h.s_build));
@@ -734,12 +881,11 @@ static int host_join(lbkd_ctx* c, cudaStream_t st, int sync) {
     CK(cudaSetDevice(c->device));
     for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(st, h.d2h_done[i], 0));
     if (!sync) return LBKD_OK;
-    CK(cudaMemcpyAsync(c->h_err, c->bf.err, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_err, c->err_host, sizeof(u32), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const u32 e = c->h_err[0];
-    CK(cudaMemsetAsync(c->bf.err, 0, sizeof(u32) * 4, st));
+    CK(cudaMemsetAsync(c->err_host, 0, sizeof(u32) * 4, st));
     CK(cudaStreamSynchronize(st));
-    c->err_sticky = 0;
     h.pending = 0;
     return e ? LBKD_ENONFINITE : LBKD_OK;
 }
@@ -785,7 +931,8 @@ int lbkd_create(lbkd_ctx** out, int device) {
 void lbkd_destroy(lbkd_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (auto& e : c->graphs)
+        if (e.exec) cudaGraphExecDestroy(e.exec);
     if (c->cap_stream) {
         cudaStreamDestroy(c->cap_stream);
         cudaEventDestroy(c->cap_fork);
@@ -827,11 +974,19 @@ void lbkd_destroy(lbkd_ctx* c) {
     cudaFree(c->bf.status);
     cudaFree(c->bf.tile_ctr);
     cudaFree(c->bf.err);
+    cudaFree(c->err_host);
+    if (c->done_ev) cudaEventDestroy(c->done_ev);
     cudaFree(c->pts_copy);
     cudaFree(c->perm_scratch);
     cudaFree(c->dims_scratch);
     cudaFree(c->minmax);
     cudaFree(c->d_moved);
+    cudaFree(c->rank_scratch);
+    cudaFree(c->codes);
+    cudaFree(c->out32);
+    cudaFree(c->vtab);
+    cudaFree(c->out64_tmp);
+    cudaFree(c->f64_err);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->h_err) cudaFreeHost(c->h_err);
     delete c;
@@ -849,6 +1004,28 @@ int lbkd_build_rr(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n, i
 int lbkd_build_widest(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n, int k, uint32_t* d_perm,
                       uint8_t* d_dims, void* stream) {
     return build(c, d_points, d_out, n, k, d_perm, d_dims, nullptr, kWidest, (cudaStream_t)stream);
+}
+
+int lbkd_build_rr_f64(lbkd_ctx* c, const double* d_points, double* d_out, int64_t n, int k, uint32_t* d_perm,
+                      void* stream) {
+    return build_f64(c, d_points, d_out, n, k, d_perm, nullptr, nullptr, kRoundRobin, (cudaStream_t)stream);
+}
+
+int lbkd_build_widest_f64(lbkd_ctx* c, const double* d_points, double* d_out, int64_t n, int k, uint32_t* d_perm,
+                          uint8_t* d_dims, void* stream) {
+    return build_f64(c, d_points, d_out, n, k, d_perm, d_dims, nullptr, kWidest, (cudaStream_t)stream);
+}
+
+int lbkd_build_rr_f64_trace(lbkd_ctx* c, const double* d_points, double* d_out, int64_t n, int k,
+                            uint32_t* d_perm, uint32_t* d_trace, void* stream) {
+    if (!d_trace) return LBKD_EINVAL_SHAPE;
+    return build_f64(c, d_points, d_out, n, k, d_perm, nullptr, d_trace, kRoundRobin, (cudaStream_t)stream);
+}
+
+int lbkd_build_widest_f64_trace(lbkd_ctx* c, const double* d_points, double* d_out, int64_t n, int k,
+                                uint32_t* d_perm, uint8_t* d_dims, uint32_t* d_trace, void* stream) {
+    if (!d_trace) return LBKD_EINVAL_SHAPE;
+    return build_f64(c, d_points, d_out, n, k, d_perm, d_dims, d_trace, kWidest, (cudaStream_t)stream);
 }
 
 int lbkd_build_rr_trace(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n, int k, uint32_t* d_perm,

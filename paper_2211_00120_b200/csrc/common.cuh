@@ -57,6 +57,62 @@ __host__ __device__ __forceinline__ float unflip_key(u32 k) {
     return bits_float(u);
 }
 
+// ---- rank-coded coordinates (float64 inputs) ---------------------------------
+// A float64 build (lbkd_build_*_f64, rank64.cu) replaces every coordinate by
+// its dense rank among the distinct values of its dimension (-0.0 == +0.0,
+// exactly numpy's ordering of the values) and codes the rank as a float32,
+// strictly increasing in the rank.  Every comparison of the build then gives
+// the float64 answer; the only arithmetic on coordinate VALUES -- the widest
+// variant's float64 widths (widest.py:91-93) -- looks the values up again in
+// a per-dimension table of the distinct values (WidthTab).
+//
+// Code: v = rank - center[d]; |v| < 2^24 -> (float)v exactly; beyond that
+// the float32 bit pattern keeps counting (0x4B800000 = 2^24 plus |v| - 2^24
+// ulps), so values stay nearly linear in the rank (the selection's value-
+// linear buckets stay balanced) and each side holds 889M ranks.  The wide
+// code (a dimension with more distinct values than that, only possible above
+// 1.7G points) counts through the whole order-flipped float range instead.
+constexpr u32 kRankLin = 1u << 24;
+constexpr u32 kRankSide = 0x7F7FFFFFu - 0x4B800000u + (1u << 24);  // ranks per side in the linear code
+
+struct WidthTab {
+    const double* v;      // [k][stride] distinct values of each dim in rank order; null: plain float32 input
+    u64 stride;
+    u32 wide;             // bit d: dimension d uses the wide code
+    u32 center[16];
+};
+
+__host__ __device__ __forceinline__ float rank_code(u32 r, u32 center, int wide) {
+    if (wide) {
+        u32 key = 0x00800000u + r;
+        if (key >= 0x7FFFFFFFu) key += 1u;  // skip the -0.0 key
+        return unflip_key(key);
+    }
+    const bool neg = r < center;
+    const u32 m = neg ? center - r : r - center;
+    const u32 bits = m < kRankLin ? float_bits((float)m) : 0x4B800000u + (m - kRankLin);
+    return bits_float(bits | (neg ? 0x80000000u : 0u));
+}
+
+__host__ __device__ __forceinline__ u32 rank_decode(float f, u32 center, int wide) {
+    if (wide) {
+        const u32 key = flip_key(f);
+        return key - 0x00800000u - (key > 0x7FFFFFFFu ? 1u : 0u);
+    }
+    const u32 b = float_bits(f);
+    const u32 mb = b & 0x7FFFFFFFu;
+    const u32 m = mb < 0x4B800000u ? (u32)bits_float(mb) : mb - 0x4B800000u + kRankLin;
+    return (b >> 31) ? center - m : center + m;
+}
+
+// float64 width hi - lo of dimension d (the widest variant's argmax key)
+__host__ __device__ __forceinline__ double coord_width(const WidthTab& t, int d, float lo, float hi) {
+    if (!t.v) return (double)hi - (double)lo;
+    const double* v = t.v + (u64)d * t.stride;
+    const int wide = (int)((t.wide >> d) & 1u);
+    return v[rank_decode(hi, t.center[d], wide)] - v[rank_decode(lo, t.center[d], wide)];
+}
+
 // Geometry of one level of the implicit left-balanced tree.
 struct LevelGeom {
     int l;        // level being split

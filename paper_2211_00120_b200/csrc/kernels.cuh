@@ -89,6 +89,7 @@ struct BuildParams {
     int subtree_sel = 1;   // in-CTA levels by selection (subtree_sel.cu) or by presorted lists
     int lroot = 0;         // sub-build: root node (level, index) of the view;
     u64 jroot = 0;         // the whole tree is (0, 0)
+    WidthTab wt{};         // float64 builds: rank-coded coordinates' value table (else wt.v == null)
 };
 
 inline LevelGeom view_of(const BuildParams& bp, int l) { return make_view(bp.n, l, bp.lroot, bp.jroot); }
@@ -122,9 +123,11 @@ struct SelArgs {
     int hflush_every;      // partition: flush the warp-private 16-bit bins every this many subtiles (<= 255)
     int tiles_per_cta;
     u64 ntiles;
+    WidthTab wt;           // widths of rank-coded (float64) builds
 };
 int sel_digit_bits(u64 nseg);
 void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cudaStream_t st);
+void launch_check_finite(const float* pts, u64 total, u32* err, cudaStream_t st);
 void launch_view_minmax(const BuildParams& bp, const Buffers& bf, u32* minmax, u64 m, cudaStream_t st);
 void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cudaStream_t st);
 void launch_sel_hist(const SelArgs& a, int b, cudaStream_t st);
@@ -166,6 +169,7 @@ struct SubtreeArgs {
                        // order T(parent); select path: in input order
     int src_par;       // select path: W[src_par] holds the subtree (else prev_state)
     int bucket_lists;  // RR list kernel: chain orders by one bucket pass each (env LBKD_BUCKET=0: radix passes)
+    WidthTab wt;       // widths of rank-coded (float64) builds
 };
 
 size_t subtree_smem_bytes(int b, int k, int mode);
@@ -174,6 +178,15 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entr
                     cudaStream_t st);
 size_t subtree_sel_smem_bytes(int b, int k);
 void launch_subtree_sel(const SubtreeArgs& a, unsigned grid, int b, cudaStream_t st);
+
+// rank64.cu (float64 input: per-dimension dense ranks, see the file header)
+void note_cuda_error(cudaError_t e);
+size_t rank_scratch_words(u64 n);
+int rank_sort_dim(const double* pts, u64 n, int k, int d, u32* scratch, u32* err, cudaStream_t st);
+const u32* rank_count_word(const u32* scratch, u64 n);
+int rank_assign_dim(u64 n, int k, int d, u32 center, int wide, float* codes, double* table, u32* scratch,
+                    cudaStream_t st);
+void launch_gather_rows_f64(const double* pts, const u32* perm, u64 n, int k, double* out, cudaStream_t st);
 
 // widest.cu
 void launch_world_bounds(const BuildParams& bp, u32* d_minmax, cudaStream_t st);

@@ -6,11 +6,11 @@
 // lbkd.queries.knn / radius_query (queries.py:41-77).  The reference answers
 // one query per call on the host; here one thread answers one query of a
 // batch, reading the tree straight from the build's output (level-order
-// float32 AoS rows; node s has children 2s+1 and 2s+2, its split plane is its
+// float32 or float64 AoS rows; node s has children 2s+1 and 2s+2, its split plane is its
 // own coordinate in dim level(s) mod k, or split_dims[s] for widest trees).
 //
-// Exactness: the reference computes in float64 on float64 copies of the
-// float32 points.  Every float32 widens exactly, and the distance is
+// Exactness: the reference computes in float64 (on float64 copies of
+// float32 points, which widen exactly; float64 trees are read as they are), and the distance is
 // accumulated in the same order with separately rounded multiply and add
 // (__dmul_rn / __dadd_rn: no FMA contraction), so squared distances are
 // bit-identical.  The kNN answer is the unique m smallest (dist2, node) pairs
@@ -35,7 +35,8 @@ __device__ __forceinline__ int node_dim(const uint8_t* split_dims, u32 node, int
     return lvl % k;
 }
 
-__device__ __forceinline__ double dist2(const float* row, const double* q, int k) {
+template <typename T>
+__device__ __forceinline__ double dist2(const T* row, const double* q, int k) {
     double d2 = 0.0;
     for (int j = 0; j < k; ++j) {
         const double t = __dsub_rn(q[j], (double)row[j]);
@@ -49,8 +50,8 @@ __device__ __forceinline__ double dist2(const float* row, const double* q, int k
 // for small m); HEAP = true: a max-heap on (dist2, node), O(log m) per take,
 // heap-sorted at the end.  Both keep exactly the m smallest (dist2, node)
 // pairs, so the answer is the same.
-template <int MCAP, bool HEAP>
-__global__ void __launch_bounds__(128) knn_kernel(const float* __restrict__ tree, u32 n, int k,
+template <typename T, int MCAP, bool HEAP>
+__global__ void __launch_bounds__(128) knn_kernel(const T* __restrict__ tree, u32 n, int k,
                                                   const uint8_t* __restrict__ split_dims,
                                                   const double* __restrict__ queries, u64 nq, int m,
                                                   int64_t* __restrict__ out_idx, double* __restrict__ out_d2) {
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(128) knn_kernel(const float* __restrict__ tree
     u32 node = 0;
     while (true) {
         if (node < n) {
-            const float* row = tree + (u64)node * k;
+            const T* row = tree + (u64)node * k;
             const double d2 = dist2(row, q, k);
             if (HEAP) {
                 if (count < m) {
@@ -162,8 +163,8 @@ __global__ void __launch_bounds__(128) knn_kernel(const float* __restrict__ tree
 
 // Radius traversal.  FILL = false: count the hits; FILL = true: write them
 // from out_idx[offsets[qi]] in traversal order.
-template <bool FILL>
-__global__ void __launch_bounds__(128) radius_kernel(const float* __restrict__ tree, u32 n, int k,
+template <typename T, bool FILL>
+__global__ void __launch_bounds__(128) radius_kernel(const T* __restrict__ tree, u32 n, int k,
                                                      const uint8_t* __restrict__ split_dims,
                                                      const double* __restrict__ queries, u64 nq, double r2,
                                                      int64_t* __restrict__ counts,
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(128) radius_kernel(const float* __restrict__ t
     u32 node = 0;
     while (true) {
         if (node < n) {
-            const float* row = tree + (u64)node * k;
+            const T* row = tree + (u64)node * k;
             if (dist2(row, q, k) <= r2) {
                 if (FILL) dst[count] = node;
                 ++count;
@@ -323,7 +324,7 @@ cudaError_t finish(void) { return cudaGetLastError(); }
 using namespace lbkd;
 
 namespace {
-int query_args_ok(const float* tree, int64_t n, int k, const double* q, int64_t nq) {
+int query_args_ok(const void* tree, int64_t n, int k, const double* q, int64_t nq) {
     if (n < 0 || n > (int64_t)0x7fffffff || k < 1 || k > LBKD_MAX_K || nq < 0) return 0;
     if ((n > 0 && !tree) || (nq > 0 && !q)) return 0;
     return 1;
@@ -335,9 +336,10 @@ int rc_of(cudaError_t e) {
 }
 }  // namespace
 
-extern "C" {
+namespace {
 
-int lbkd_knn(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
+template <typename T>
+int knn_impl(const T* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
              int64_t nq, int m, int64_t* d_out_idx, double* d_out_d2, void* stream) {
     if (!query_args_ok(d_tree, n, k, d_queries, nq) || m < 1 || m > n || (nq > 0 && (!d_out_idx || !d_out_d2)))
         return LBKD_EINVAL_SHAPE;
@@ -347,7 +349,7 @@ int lbkd_knn(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims,
     const u32 un = (u32)n;
     const u64 unq = (u64)nq;
 #define LBKD_KNN(C, H) \
-    knn_kernel<C, H><<<grid, 128, 0, st>>>(d_tree, un, k, d_split_dims, d_queries, unq, m, d_out_idx, d_out_d2)
+    knn_kernel<T, C, H><<<grid, 128, 0, st>>>(d_tree, un, k, d_split_dims, d_queries, unq, m, d_out_idx, d_out_d2)
     if (m <= 1) LBKD_KNN(1, false);
     else if (m <= 4) LBKD_KNN(4, false);
     else if (m <= 8) LBKD_KNN(8, false);
@@ -360,7 +362,8 @@ int lbkd_knn(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims,
     return rc_of(finish());
 }
 
-int lbkd_radius_count(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
+template <typename T>
+int radius_count_impl(const T* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
                       int64_t nq, double r2, int64_t* d_counts, int64_t* d_offsets, int64_t* d_scratch,
                       void* stream) {
     if (!query_args_ok(d_tree, n, k, d_queries, nq) || !(r2 >= 0.0) || !d_offsets || (nq > 0 && !d_counts))
@@ -373,7 +376,7 @@ int lbkd_radius_count(const float* d_tree, int64_t n, int k, const uint8_t* d_sp
     }
     if (!d_scratch) return LBKD_EINVAL_SHAPE;
     const unsigned grid = (unsigned)((nq + 127) / 128);
-    radius_kernel<false><<<grid, 128, 0, st>>>(d_tree, (u32)n, k, d_split_dims, d_queries, (u64)nq, r2, d_counts,
+    radius_kernel<T, false><<<grid, 128, 0, st>>>(d_tree, (u32)n, k, d_split_dims, d_queries, (u64)nq, r2, d_counts,
                                                 nullptr, nullptr);
     const u64 nb = ((u64)nq + kScanT - 1) / kScanT;
     scan_sums_kernel<<<(unsigned)nb, kScanT, 0, st>>>(d_counts, (u64)nq, d_scratch);
@@ -382,19 +385,57 @@ int lbkd_radius_count(const float* d_tree, int64_t n, int k, const uint8_t* d_sp
     return rc_of(finish());
 }
 
-int64_t lbkd_radius_scratch_len(int64_t nq) { return nq <= 0 ? 1 : (nq + kScanT - 1) / kScanT + 1; }
-
-int lbkd_radius_fill(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
+template <typename T>
+int radius_fill_impl(const T* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
                      int64_t nq, double r2, const int64_t* d_offsets, int64_t* d_out_idx, void* stream) {
     if (!query_args_ok(d_tree, n, k, d_queries, nq) || !(r2 >= 0.0) || (nq > 0 && !d_offsets))
         return LBKD_EINVAL_SHAPE;
     if (nq == 0 || n == 0) return LBKD_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned grid = (unsigned)((nq + 127) / 128);
-    radius_kernel<true><<<grid, 128, 0, st>>>(d_tree, (u32)n, k, d_split_dims, d_queries, (u64)nq, r2, nullptr,
+    radius_kernel<T, true><<<grid, 128, 0, st>>>(d_tree, (u32)n, k, d_split_dims, d_queries, (u64)nq, r2, nullptr,
                                                d_offsets, d_out_idx);
     radius_sort_kernel<<<(unsigned)nq, kSortT, 0, st>>>(d_offsets, d_out_idx);
     return rc_of(finish());
+}
+
+}  // namespace
+
+extern "C" {
+
+int lbkd_knn(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
+             int64_t nq, int m, int64_t* d_out_idx, double* d_out_d2, void* stream) {
+    return knn_impl(d_tree, n, k, d_split_dims, d_queries, nq, m, d_out_idx, d_out_d2, stream);
+}
+
+int lbkd_knn_f64(const double* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
+                 int64_t nq, int m, int64_t* d_out_idx, double* d_out_d2, void* stream) {
+    return knn_impl(d_tree, n, k, d_split_dims, d_queries, nq, m, d_out_idx, d_out_d2, stream);
+}
+
+int lbkd_radius_count(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
+                      int64_t nq, double r2, int64_t* d_counts, int64_t* d_offsets, int64_t* d_scratch,
+                      void* stream) {
+    return radius_count_impl(d_tree, n, k, d_split_dims, d_queries, nq, r2, d_counts, d_offsets, d_scratch, stream);
+}
+
+int lbkd_radius_count_f64(const double* d_tree, int64_t n, int k, const uint8_t* d_split_dims,
+                          const double* d_queries, int64_t nq, double r2, int64_t* d_counts, int64_t* d_offsets,
+                          int64_t* d_scratch, void* stream) {
+    return radius_count_impl(d_tree, n, k, d_split_dims, d_queries, nq, r2, d_counts, d_offsets, d_scratch, stream);
+}
+
+int64_t lbkd_radius_scratch_len(int64_t nq) { return nq <= 0 ? 1 : (nq + kScanT - 1) / kScanT + 1; }
+
+int lbkd_radius_fill(const float* d_tree, int64_t n, int k, const uint8_t* d_split_dims, const double* d_queries,
+                     int64_t nq, double r2, const int64_t* d_offsets, int64_t* d_out_idx, void* stream) {
+    return radius_fill_impl(d_tree, n, k, d_split_dims, d_queries, nq, r2, d_offsets, d_out_idx, stream);
+}
+
+int lbkd_radius_fill_f64(const double* d_tree, int64_t n, int k, const uint8_t* d_split_dims,
+                         const double* d_queries, int64_t nq, double r2, const int64_t* d_offsets,
+                         int64_t* d_out_idx, void* stream) {
+    return radius_fill_impl(d_tree, n, k, d_split_dims, d_queries, nq, r2, d_offsets, d_out_idx, stream);
 }
 
 }  // extern "C"

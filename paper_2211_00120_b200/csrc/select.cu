@@ -187,6 +187,22 @@ void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cu
     init_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(bp.pts, bp.n, bp.k, bf.w[0], bf.stride, bf.err, minmax);
 }
 
+// non-finite check of builder.py:134-135 for builds without global levels
+// (single-CTA trees read the input straight from the caller's array)
+__global__ void check_finite_kernel(const float* __restrict__ pts, u64 total, u32* err) {
+    bool bad = false;
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < total; e += (u64)gridDim.x * blockDim.x)
+        bad |= !isfinite(__ldg(pts + e));
+    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+void launch_check_finite(const float* pts, u64 total, u32* err, cudaStream_t st) {
+    u64 blocks = (total + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    if (blocks < 1) blocks = 1;
+    check_finite_kernel<<<(unsigned)blocks, 256, 0, st>>>(pts, total, err);
+}
+
 // bounding box of a sub-build's points (W[0], blockIdx.y = dimension): the
 // view root's box (any valid bound of its points works)
 __global__ void view_minmax_kernel(const u32* __restrict__ w0, u64 stride, u64 m, int k, u32* minmax) {
@@ -212,7 +228,7 @@ void launch_view_minmax(const BuildParams& bp, const Buffers& bf, u32* minmax, u
 
 // root box = world box (widest.py:84-88); widest: root dim = first argmax
 // of the float64 widths (widest.py:91-93, :164-166)
-__global__ void root_kernel(const u32* minmax, int k, int mode, float* box0, uint8_t* split_dims) {
+__global__ void root_kernel(const u32* minmax, int k, int mode, float* box0, uint8_t* split_dims, WidthTab wt) {
     if (threadIdx.x != 0) return;
     int d0 = 0;
     double bw = 0.0;
@@ -220,14 +236,14 @@ __global__ void root_kernel(const u32* minmax, int k, int mode, float* box0, uin
         const float lo = unflip_key(minmax[d]), hi = unflip_key(minmax[k + d]);
         box0[d] = lo;
         box0[k + d] = hi;
-        const double w = (double)hi - (double)lo;
+        const double w = coord_width(wt, d, lo, hi);
         if (d == 0 || w > bw) { bw = w; d0 = d; }
     }
     if (mode == kWidest) split_dims[0] = (uint8_t)d0;
 }
 
 void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cudaStream_t st) {
-    root_kernel<<<1, 32, 0, st>>>(minmax, bp.k, bp.mode, bf.boxes[0], bp.split_dims);
+    root_kernel<<<1, 32, 0, st>>>(minmax, bp.k, bp.mode, bf.boxes[0], bp.split_dims, bp.wt);
 }
 
 __device__ __forceinline__ Bucketer seg_bucketer(const SelArgs& a, u64 t, int d) {
@@ -288,8 +304,11 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
         u32 key[ITEMS];
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
+            // only the tile's segment parts (the finished nodes between
+            // segments hold no data in this buffer)
             const u32 r = (u32)(i * kHThreads + threadIdx.x);
-            key[i] = (r < (u32)cnt) ? kp[ts + r] : 0u;
+            const bool use = (r >= r0a && r < r0b) || (has1 && r >= r1a && r < r1b);
+            key[i] = use ? kp[ts + r] : 0u;
         }
         if (has1 && seg_key_dim(a, cur + 1) != dk) {  // widest: the next segment splits another dim
             const u32* k1 = W + (u64)seg_key_dim(a, cur + 1) * a.bf.stride;
@@ -644,7 +663,7 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
         for (int q = 0; q < k; ++q) {
             bout[q] = lo[q];
             bout[k + q] = hi[q];
-            const double w = (double)hi[q] - (double)lo[q];
+            const double w = coord_width(a.wt, q, lo[q], hi[q]);
             if (q == 0 || w > bw) { bw = w; best = q; }
         }
         const u64 cnode = 2 * node + 1 + tid;

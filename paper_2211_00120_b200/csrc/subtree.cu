@@ -538,9 +538,9 @@ __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) 
                     u = par;
                 }
                 int best = 0;
-                double bw = (double)hi[0] - (double)lo[0];
+                double bw = coord_width(a.wt, 0, lo[0], hi[0]);
                 for (int d = 1; d < k; ++d) {
-                    double w = (double)hi[d] - (double)lo[d];
+                    double w = coord_width(a.wt, d, lo[d], hi[d]);
                     if (w > bw) { bw = w; best = d; }
                 }
                 ndim[cb + c] = (unsigned char)best;
@@ -1020,6 +1020,7 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entr
     a.lam0 = lam0;
     a.k = bp.k;
     a.mode = bp.mode;
+    a.wt = bp.wt;
     a.M = (1 << bp.b) - 1;
     a.w[0] = bf.w[0];
     a.w[1] = bf.w[1];

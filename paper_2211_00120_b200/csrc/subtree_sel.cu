@@ -216,13 +216,14 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
     // widest: chain of a node = its dim, then its ancestors' dims (repeats
     // dropped).  Ancestors inside the subtree come from ndim (heap order),
     // above it from the global split dims.
-    auto widest_chain_of = [&](u32 heap, int depth, Chain& ch) {
+    // own_dim >= 0: the node's own dim (not yet stored in ndim)
+    auto widest_chain_of = [&](u32 heap, int depth, Chain& ch, int own_dim = -1) {
         ch.m = 0;
         u32 seen = 0;
         u32 h = heap;
         int dd = depth;
         while (true) {
-            const int d = ndim[h];
+            const int d = (h == heap && own_dim >= 0) ? own_dim : ndim[h];
             if (!((seen >> d) & 1u)) {
                 seen |= 1u << d;
                 ch.d[ch.m++] = (uint8_t)d;
@@ -247,9 +248,9 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
     };
     auto first_argmax = [&](const float* box) -> int {
         int best = 0;
-        double bw = (double)box[k] - (double)box[0];
+        double bw = coord_width(a.wt, 0, box[0], box[k]);
         for (int d = 1; d < k; ++d) {
-            const double w = (double)box[k + d] - (double)box[d];
+            const double w = coord_width(a.wt, d, box[d], box[k + d]);
             if (w > bw) { bw = w; best = d; }
         }
         return best;
@@ -574,10 +575,10 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 int d = l2 % k;
                 if (a.mode == kWidest && act) {
                     int best = 0;
-                    double bw = (double)bhi[0] - (double)blo[0];
+                    double bw = coord_width(a.wt, 0, blo[0], bhi[0]);
                     for (int c = 1; c < kBoxK; ++c) {
                         if (c < k) {
-                            const double w = (double)bhi[c] - (double)blo[c];
+                            const double w = coord_width(a.wt, c, blo[c], bhi[c]);
                             if (w > bw) { bw = w; best = c; }
                         }
                     }
@@ -604,8 +605,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                     if (a.mode == kRoundRobin) {
                         rr_chain(l2, k, ch);  // (tiny trees: truncated chains near the root)
                     } else if (act) {
-                        ndim[heap] = (uint8_t)d;  // the node's own dim heads its chain
-                        widest_chain_of(heap, dl + dd, ch);
+                        widest_chain_of(heap, dl + dd, ch, d);  // the node's own dim heads its chain
                     }
                     rank = 0;
                     for (int i = 0; i < 32; ++i) {

@@ -50,18 +50,18 @@ void launch_world_bounds(const BuildParams& bp, u32* d_minmax, cudaStream_t st) 
     world_bounds_kernel<<<(unsigned)blocks, 256, 0, st>>>(bp.pts, bp.n, bp.k, d_minmax);
 }
 
-__device__ __forceinline__ int first_argmax_width(const float* lo, const float* hi, int k) {
+__device__ __forceinline__ int first_argmax_width(const float* lo, const float* hi, int k, const WidthTab& wt) {
     int best = 0;
-    double bw = (double)hi[0] - (double)lo[0];
+    double bw = coord_width(wt, 0, lo[0], hi[0]);
     for (int d = 1; d < k; ++d) {
-        double w = (double)hi[d] - (double)lo[d];
+        double w = coord_width(wt, d, lo[d], hi[d]);
         if (w > bw) { bw = w; best = d; }
     }
     return best;
 }
 
 // root: box = world, dim = widest_dim(world) (widest.py:91-93, :164-166)
-__global__ void widest_root_kernel(const u32* d_minmax, int k, float* box0, uint8_t* split_dims) {
+__global__ void widest_root_kernel(const u32* d_minmax, int k, float* box0, uint8_t* split_dims, WidthTab wt) {
     if (threadIdx.x != 0) return;
     float lo[kMaxKW], hi[kMaxKW];
     for (int d = 0; d < k; ++d) {
@@ -70,17 +70,17 @@ __global__ void widest_root_kernel(const u32* d_minmax, int k, float* box0, uint
         box0[d] = lo[d];
         box0[k + d] = hi[d];
     }
-    split_dims[0] = (uint8_t)first_argmax_width(lo, hi, k);
+    split_dims[0] = (uint8_t)first_argmax_width(lo, hi, k, wt);
 }
 
 void launch_widest_root(const BuildParams& bp, const u32* d_minmax, float* box0, cudaStream_t st) {
-    widest_root_kernel<<<1, 32, 0, st>>>(d_minmax, bp.k, box0, bp.split_dims);
+    widest_root_kernel<<<1, 32, 0, st>>>(d_minmax, bp.k, box0, bp.split_dims, bp.wt);
 }
 
 // children of level-lp nodes: box_c = box_parent clipped by the parent's
 // plane (left: hi, right: lo), dim_c = first argmax of f64 widths
 __global__ void widest_nodes_kernel(u64 n, int lp, const float* __restrict__ boxes_in, float* boxes_out,
-                                    uint8_t* split_dims, const float* __restrict__ out_pts, int k) {
+                                    uint8_t* split_dims, const float* __restrict__ out_pts, int k, WidthTab wt) {
     u64 nchild = 2ull << lp;
     u64 c = blockIdx.x * (u64)blockDim.x + threadIdx.x;
     if (c >= nchild) return;
@@ -96,7 +96,7 @@ __global__ void widest_nodes_kernel(u64 n, int lp, const float* __restrict__ box
     if ((c & 1ull) == 0) { if (plane < hi[d]) hi[d] = plane; }   // left child
     else { if (plane > lo[d]) lo[d] = plane; }                     // right child
     for (int q = 0; q < k; ++q) { boxes_out[c * 2 * k + q] = lo[q]; boxes_out[c * 2 * k + k + q] = hi[q]; }
-    split_dims[node] = (uint8_t)first_argmax_width(lo, hi, k);
+    split_dims[node] = (uint8_t)first_argmax_width(lo, hi, k, wt);
 }
 
 void launch_widest_nodes(const BuildParams& bp, int parent_level, const float* boxes_in, float* boxes_out,
@@ -104,7 +104,7 @@ void launch_widest_nodes(const BuildParams& bp, int parent_level, const float* b
     u64 nchild = 2ull << parent_level;
     unsigned blocks = (unsigned)((nchild + 255) / 256);
     widest_nodes_kernel<<<blocks, 256, 0, st>>>(bp.n, parent_level, boxes_in, boxes_out, bp.split_dims,
-                                                bp.out_pts, bp.k);
+                                                bp.out_pts, bp.k, bp.wt);
 }
 
 }  // namespace lbkd

@@ -32,23 +32,33 @@ class Neighbor(NamedTuple):
 
 def _device_tree(torch, tree: KdTree):
     """float32 level-order rows (+ split dims) of ``tree`` on the current
-    device, cached on the tree object while its arrays are unchanged."""
+    device.  The device copy is cached on the tree object together with a
+    host snapshot of the arrays it was made from; every call compares the
+    tree's current contents with the snapshot (a memory compare, far cheaper
+    than the upload), so in-place edits of ``coords`` / ``split_dims`` are
+    always seen."""
     dev = torch.cuda.current_device()
-    key = (id(tree.coords), tree.coords.__array_interface__['data'][0], tree.coords.shape, id(tree.split_dims), dev)
     cached = getattr(tree, "_lbkd_device", None)
-    if cached is not None and cached[0] == key:
-        return cached[1], cached[2]
+    if cached is not None:
+        cdev, c_coords, c_dims, pts, dims = cached
+        same_dims = (c_dims is None and tree.split_dims is None) or (
+            c_dims is not None and tree.split_dims is not None and np.array_equal(c_dims, tree.split_dims))
+        if cdev == dev and same_dims and np.shape(tree.coords) == c_coords.shape and np.array_equal(
+                tree.coords, c_coords):
+            return pts, dims
     c64 = np.ascontiguousarray(tree.coords, dtype=np.float64)
-    c32 = c64.astype(np.float32)
-    if not np.array_equal(c32.astype(np.float64), c64):
-        # the builder only accepts float32-representable inputs (ingest), so
-        # any tree it produced passes; a foreign tree must too
-        raise ValueError("tree coordinates must be exactly representable as float32")
-    pts = torch.from_numpy(c32).to(f"cuda:{dev}")
+    with np.errstate(over="ignore"):
+        c32 = c64.astype(np.float32)
+    # float32 rows when they are exact (half the bytes), else the float64 rows
+    # (trees built from float64 input); the kernels widen to float64 either way
+    rows = c32 if np.array_equal(c32, c64) else c64
+    pts = torch.from_numpy(rows).to(f"cuda:{dev}")
     dims = None
+    snap_dims = None
     if tree.split_dims is not None:
+        snap_dims = np.array(tree.split_dims, copy=True)
         dims = torch.from_numpy(np.ascontiguousarray(tree.split_dims, dtype=np.uint8)).to(f"cuda:{dev}")
-    tree._lbkd_device = (key, pts, dims)
+    tree._lbkd_device = (dev, c64.copy(), snap_dims, pts, dims)
     return pts, dims
 
 
@@ -64,8 +74,9 @@ def _prep_queries(tree_k: int, queries) -> np.ndarray:
 
 
 def _check_tree_tensor(torch, pts, split_dims):
-    if pts.device.type != "cuda" or pts.dtype != torch.float32 or pts.dim() != 2 or not pts.is_contiguous():
-        raise ValueError("tree points must be a contiguous (n, k) float32 CUDA tensor")
+    if (pts.device.type != "cuda" or pts.dtype not in (torch.float32, torch.float64) or pts.dim() != 2
+            or not pts.is_contiguous()):
+        raise ValueError("tree points must be a contiguous (n, k) float32 or float64 CUDA tensor")
     if split_dims is not None:
         if split_dims.dtype != torch.uint8 or split_dims.numel() != pts.shape[0] or not split_dims.is_contiguous():
             raise ValueError("split_dims must be a contiguous uint8 CUDA tensor with one entry per node")
@@ -74,7 +85,7 @@ def _check_tree_tensor(torch, pts, split_dims):
 def knn_cuda(tree_points, queries, m: int, *, split_dims=None, stream=None):
     """Batched kNN on device tensors.
 
-    ``tree_points``: (n, k) float32 level-order rows; ``split_dims``: uint8
+    ``tree_points``: (n, k) float32 or float64 level-order rows; ``split_dims``: uint8
     (n,) for widest trees, None for round-robin; ``queries``: (nq, k) float64.
     Returns (idx int64 (nq, m'), dist2 float64 (nq, m')) with m' = min(m, n),
     each row ordered by (dist2, node index).
@@ -94,9 +105,9 @@ def knn_cuda(tree_points, queries, m: int, *, split_dims=None, stream=None):
     d2 = torch.empty((nq, want), dtype=torch.float64, device=tree_points.device)
     lib = _native.load()
     with torch.cuda.device(tree_points.device):
-        rc = lib.lbkd_knn(tree_points.data_ptr(), n, k, split_dims.data_ptr() if split_dims is not None else None,
-                          queries.data_ptr(), nq, want, idx.data_ptr(), d2.data_ptr(),
-                          _stream_ptr(torch, stream))
+        fn = lib.lbkd_knn_f64 if tree_points.dtype == torch.float64 else lib.lbkd_knn
+        rc = fn(tree_points.data_ptr(), n, k, split_dims.data_ptr() if split_dims is not None else None,
+                queries.data_ptr(), nq, want, idx.data_ptr(), d2.data_ptr(), _stream_ptr(torch, stream))
     _native.check(rc, "lbkd_knn")
     return idx, d2
 
@@ -124,15 +135,18 @@ def radius_cuda(tree_points, queries, radius: float, *, split_dims=None, stream=
     scratch = torch.empty(int(lib.lbkd_radius_scratch_len(nq)), dtype=torch.int64, device=dev)
     dp = split_dims.data_ptr() if split_dims is not None else None
     tp = tree_points.data_ptr() if n else None
+    f64 = tree_points.dtype == torch.float64
+    count_fn = lib.lbkd_radius_count_f64 if f64 else lib.lbkd_radius_count
+    fill_fn = lib.lbkd_radius_fill_f64 if f64 else lib.lbkd_radius_fill
     with torch.cuda.device(dev):
         sp = _stream_ptr(torch, stream)
-        _native.check(lib.lbkd_radius_count(tp, n, k, dp, queries.data_ptr() if nq else None, nq, r2,
+        _native.check(count_fn(tp, n, k, dp, queries.data_ptr() if nq else None, nq, r2,
                                             counts.data_ptr(), offsets.data_ptr(), scratch.data_ptr(), sp),
                       "lbkd_radius_count")
         (stream if stream is not None else torch.cuda.current_stream()).synchronize()
         total = int(offsets[nq].cpu())
         idx = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
-        _native.check(lib.lbkd_radius_fill(tp, n, k, dp, queries.data_ptr() if nq else None, nq, r2,
+        _native.check(fill_fn(tp, n, k, dp, queries.data_ptr() if nq else None, nq, r2,
                                            offsets.data_ptr(), idx.data_ptr(), sp), "lbkd_radius_fill")
     return offsets, idx[:total]
 

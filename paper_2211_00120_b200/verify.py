@@ -32,8 +32,9 @@ class ValidityReport:
 
 
 def _check(torch, pts, split_dims):
-    if pts.device.type != "cuda" or pts.dtype != torch.float32 or pts.dim() != 2 or not pts.is_contiguous():
-        raise ValueError("tree points must be a contiguous (n, k) float32 CUDA tensor")
+    if (pts.device.type != "cuda" or pts.dtype not in (torch.float32, torch.float64) or pts.dim() != 2
+            or not pts.is_contiguous()):
+        raise ValueError("tree points must be a contiguous (n, k) float32 or float64 CUDA tensor")
     if split_dims is not None and (split_dims.dtype != torch.uint8 or split_dims.numel() != pts.shape[0]):
         raise ValueError("split_dims must be a uint8 CUDA tensor with one entry per node")
 
@@ -46,7 +47,9 @@ def check_valid_cuda(tree_points, *, split_dims=None, stream=None):
     wit = torch.empty(3, dtype=torch.int64, device=tree_points.device)
     scratch = torch.empty(1, dtype=torch.int64, device=tree_points.device)
     with torch.cuda.device(tree_points.device):
-        rc = _native.load().lbkd_check_valid(tree_points.data_ptr() if n else None, n, k,
+        lib = _native.load()
+        fn = lib.lbkd_check_valid_f64 if tree_points.dtype == torch.float64 else lib.lbkd_check_valid
+        rc = fn(tree_points.data_ptr() if n else None, n, k,
                                              split_dims.data_ptr() if split_dims is not None else None,
                                              wit.data_ptr(), scratch.data_ptr(), _stream_ptr(torch, stream))
     _native.check(rc, "lbkd_check_valid")
@@ -62,7 +65,9 @@ def subtree_boxes_cuda(tree_points, *, split_dims=None, stream=None):
     lo = torch.empty((n, k), dtype=torch.float64, device=tree_points.device)
     hi = torch.empty((n, k), dtype=torch.float64, device=tree_points.device)
     with torch.cuda.device(tree_points.device):
-        rc = _native.load().lbkd_subtree_boxes(tree_points.data_ptr() if n else None, n, k,
+        lib = _native.load()
+        fn = lib.lbkd_subtree_boxes_f64 if tree_points.dtype == torch.float64 else lib.lbkd_subtree_boxes
+        rc = fn(tree_points.data_ptr() if n else None, n, k,
                                                split_dims.data_ptr() if split_dims is not None else None,
                                                lo.data_ptr(), hi.data_ptr(), _stream_ptr(torch, stream))
     _native.check(rc, "lbkd_subtree_boxes")

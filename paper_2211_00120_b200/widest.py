@@ -19,6 +19,8 @@ from .builder import (
     MAX_POINTS,
     BuildRecorder,
     KdTree,
+    _check_host_buffers,
+    _check_out_buffers,
     _check_points_tensor,
     _raise_for,
     _record_trace,
@@ -104,11 +106,18 @@ def subtree_bounds(tree_coords, split_dims, node: int, world: Aabb) -> Aabb:
 
 def build_widest_cuda(points, *, out=None, perm=None, split_dims=None, stream=None, check_finite: bool = True,
                       trace=None):
-    """Device-resident widest build on a (n, k) float32 CUDA tensor.
+    """Device-resident widest build on a (n, k) float32 or float64 CUDA
+    tensor (float64: lbkd_build_widest_f64).
 
     Returns (out, perm, split_dims)."""
     torch = _torch()
     _check_points_tensor(torch, points)
+    _check_out_buffers(torch, points, out, perm, split_dims)
+    if trace is not None:
+        L = treemath.num_levels(points.shape[0])
+        if (trace.device != points.device or trace.dtype != torch.int32 or not trace.is_contiguous()
+                or trace.numel() < max(L, 1) * points.shape[0]):
+            raise ValueError("trace must be a contiguous int32 tensor of num_levels(n) * n entries")
     n, k = points.shape
     dev = points.device.index if points.device.index is not None else torch.cuda.current_device()
     if out is None:
@@ -122,12 +131,14 @@ def build_widest_cuda(points, *, out=None, perm=None, split_dims=None, stream=No
     lib.lbkd_set_check(ctx, 1 if check_finite else 0)
     with torch.cuda.device(dev):
         sp = _stream_ptr(torch, stream)
+        f64 = points.dtype == torch.float64
         if trace is None:
-            rc = lib.lbkd_build_widest(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(),
-                                       split_dims.data_ptr(), sp)
+            fn = lib.lbkd_build_widest_f64 if f64 else lib.lbkd_build_widest
+            rc = fn(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(), split_dims.data_ptr(), sp)
         else:
-            rc = lib.lbkd_build_widest_trace(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(),
-                                             split_dims.data_ptr(), trace.data_ptr(), sp)
+            fn = lib.lbkd_build_widest_f64_trace if f64 else lib.lbkd_build_widest_trace
+            rc = fn(ctx, points.data_ptr(), out.data_ptr(), n, k, perm.data_ptr(), split_dims.data_ptr(),
+                    trace.data_ptr(), sp)
     _raise_for(rc, "lbkd_build_widest", n, k, widest=True)
     return out, perm, split_dims
 
@@ -141,9 +152,7 @@ def build_widest_host(points, out, perm, split_dims, *, device: int = 0, stream=
     neighbouring builds.  The buffers are valid after ``builder.host_join``.
     """
     torch = _torch()
-    for t in (points, out, perm, split_dims):
-        if t.device.type != "cpu" or not t.is_contiguous():
-            raise ValueError("host buffers must be contiguous CPU tensors")
+    _check_host_buffers(torch, points, out, perm, split_dims)
     n, k = points.shape
     lib = _native.load()
     ctx = _native.context(device)

@@ -78,3 +78,38 @@ def query_cases():
         case["knn"], case["radius"] = knn, rad
         out.append(case)
     return out
+
+
+# --- float64 inputs (the reference's own dtype; make_golden_f64.py) ---------
+
+def gen_f64(kind: str, n: int, k: int, seed: int) -> np.ndarray:
+    """float64 point sets that are NOT float32-representable (so the drop-in
+    takes its float64 device path); the reference's CLI bench draws exactly
+    ``default_rng(seed).random((n, k))`` (cli.py:176-177)."""
+    rng = np.random.default_rng(seed)
+    if kind == "uniform64":  # the reference bench's distribution
+        return rng.random((n, k))
+    if kind == "ties64":  # multiples of 1/1000: duplicates, none float32-exact
+        return np.floor(rng.random((n, k)) * 1000) / 1000
+    if kind == "signed_zero64":
+        vals = np.array([0.0, -0.0, 0.1, -0.1, 0.3])
+        return vals[rng.integers(0, len(vals), size=(n, k))]
+    if kind == "clustered64":
+        cen = rng.random((256, k))
+        return cen[rng.integers(0, 256, size=n)] + rng.normal(0.0, 0.01, size=(n, k))
+    if kind == "near64":  # distinct values closer than a float32 ulp
+        return 1.0 + rng.integers(0, 1 << 12, size=(n, k)) * 2.0 ** -40
+    if kind == "range64":  # far outside the float32 range, both signs
+        return 10.0 ** rng.uniform(-300, 300, size=(n, k)) * np.where(rng.random((n, k)) < 0.5, -1.0, 1.0)
+    if kind == "mixed64":  # one float32-exact dim next to float64 dims
+        p = rng.random((n, k))
+        p[:, 0] = np.float32(rng.random(n, dtype=np.float32))
+        return p
+    raise ValueError(kind)
+
+
+def f64_cases():
+    import json
+
+    with open(os.path.join(GOLDEN, "hashes_f64.json")) as f:
+        return list(json.load(f).values())

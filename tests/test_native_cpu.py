@@ -78,8 +78,14 @@ def test_ingest_contract():
         ingest(np.zeros((4, 1)), 1, payload=np.arange(3))
     with pytest.raises(ValueError):
         ingest(np.broadcast_to(np.zeros((1, 1)), (2**31, 1)))
-    with pytest.raises(ValueError, match="float32"):
-        ingest(np.array([[0.1]], dtype=np.float64))
+    # float64 input is accepted like the reference's: float32-exact values take
+    # the float32 device path, anything else the float64 one
+    c, _ = ingest(np.array([[0.1]], dtype=np.float64))
+    assert c.dtype == np.float64 and c[0, 0] == 0.1
+    c, _ = ingest(np.array([[1e300], [-0.0]]))
+    assert c.dtype == np.float64
+    c, _ = ingest(np.array([[0.5, -0.0], [3.0, 1e-3]]).astype(np.float32).astype(np.float64))
+    assert c.dtype == np.float32 and np.signbit(c[0, 1])
     c, p = ingest([5.0, 1.0, 9.0])
     assert c.dtype == np.float32 and c.shape == (3, 1) and p.tolist() == [0, 1, 2]
 

@@ -1,0 +1,62 @@
+#!/usr/bin/env bash
+# One entry point for the GPU-box steps (run through gpurun from the repo root):
+#   bash tools/gpu.sh <step> [<step> ...]
+# steps:
+#   build      compile the CUDA library + oracle (__graft_entry__.build)
+#   smoke      __graft_entry__.smoke()
+#   test       pytest -m gpu (without the slow 1B tests)
+#   testall    pytest -m gpu (everything, incl. the 1B config-4 pin)
+#   sanitize   compute-sanitizer memcheck / racecheck / synccheck / initcheck
+#              of tools/sanitize.py  -> gpurun_out/sanitize_<tool>.log
+#   bench      bench.py headline (100M float3 RR) + widest config 5 + reference arm
+#   launches   ncu launch lists (time + DRAM bytes per launch) of one 100M RR and
+#              one 100M clustered widest build -> gpurun_out/launches_*.{csv,txt}
+#   full       ncu --set full captures of the partition / in-CTA / filter kernels
+#   robust     tools/robust_time.py + tools/quick_time.py
+#   big        tools/big_build.py (1B clustered, sharded decomposition on one GPU)
+# Env: TEST_ARGS (extra pytest args), KSEL (ncu kernel regex for `full`, default all three)
+set -u
+mkdir -p gpurun_out
+step_build() { python __graft_entry__.py build > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }; }
+step_smoke() { timeout 300 python __graft_entry__.py 2>&1 | tail -2; }
+step_test() { timeout 2400 python -m pytest tests/ -q -m "gpu and not slow" ${TEST_ARGS:-} 2>&1 | tail -25; }
+step_testall() { timeout 3000 python -m pytest tests/ -q -m gpu ${TEST_ARGS:-} 2>&1 | tail -25; }
+step_sanitize() {
+  for tool in memcheck racecheck synccheck initcheck; do
+    LBKD_GRAPH=0 timeout 1500 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize.py 200000 \
+      > gpurun_out/sanitize_$tool.log 2>&1
+    echo "== $tool rc=$?"; tail -4 gpurun_out/sanitize_$tool.log
+  done
+}
+step_bench() {
+  timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log > gpurun_out/bench.json; cut -c1-400 gpurun_out/bench.json
+  timeout 900 python bench.py --steps 10 --warmup 3 --mode widest --dist clustered --no-cpu-baseline > gpurun_out/bench_widest.log 2>&1; tail -1 gpurun_out/bench_widest.log > gpurun_out/bench_widest.json; cut -c1-400 gpurun_out/bench_widest.json
+  timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log > gpurun_out/bench_ref.json; cut -c1-400 gpurun_out/bench_ref.json
+}
+step_launches() {
+  L=$(python tools/one_build.py 100000000 3 rr uniform 1 | awk '/launches per build/{print $4}')
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s $L -c $L --csv --log-file gpurun_out/launches_100m.csv python tools/one_build.py 100000000 3 rr uniform 2 > gpurun_out/prof1.log 2>&1
+  python tools/launches.py gpurun_out/launches_100m.csv > gpurun_out/launches_100m.txt
+  python tools/ncu_traffic.py gpurun_out/launches_100m.csv gpurun_out/ncu_traffic.json > /dev/null
+  L=$(python tools/one_build.py 100000000 3 widest clustered 1 | awk '/launches per build/{print $4}')
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s $L -c $L --csv --log-file gpurun_out/launches_widest.csv python tools/one_build.py 100000000 3 widest clustered 2 > gpurun_out/profw1.log 2>&1
+  python tools/launches.py gpurun_out/launches_widest.csv > gpurun_out/launches_widest.txt
+  python tools/ncu_traffic.py gpurun_out/launches_widest.csv gpurun_out/ncu_traffic_widest.json > /dev/null
+  cat gpurun_out/launches_100m.txt gpurun_out/launches_widest.txt | head -80
+}
+step_full() {
+  for ks in ${KSEL:-sel_part subtree sel_filter}; do
+    skip=0; [ "$ks" = sel_part ] && skip=4; [ "$ks" = sel_filter ] && skip=6
+    ncu --set full --clock-control none --import-source on -k regex:$ks -s $skip -c 1 -o gpurun_out/full_$ks python tools/one_build.py 100000000 3 rr uniform 1 > gpurun_out/full_$ks.log 2>&1
+    python tools/ncu_lines.py gpurun_out/full_$ks.ncu-rep 60 > gpurun_out/full_${ks}_lines.txt 2>&1
+    python tools/ncu_issue.py gpurun_out/full_$ks.ncu-rep gpurun_out/ncu_issue_$ks.json > /dev/null 2>&1
+    ncu -i gpurun_out/full_$ks.ncu-rep --page details --csv > gpurun_out/full_${ks}_details.csv 2>/dev/null
+  done
+}
+step_robust() {
+  timeout 600 python tools/robust_time.py > gpurun_out/robust_time.txt 2>&1; cat gpurun_out/robust_time.txt
+  timeout 300 python tools/quick_time.py > gpurun_out/quick_time.txt 2>&1; cat gpurun_out/quick_time.txt
+}
+step_big() { timeout 900 python tools/big_build.py 1000000000 clustered 3 > gpurun_out/big_1b.log 2>&1; tail -1 gpurun_out/big_1b.log | cut -c1-600; }
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv,noheader
+for s in "$@"; do echo "=== $s"; step_$s; done
