@@ -21,10 +21,12 @@ JSON line.
   in-CTA kernel moves each point once and is bound by instruction issue, so
   `issue_roofline` states that bound (ncu warp instructions / 148 x 4 issue
   slots per clock) and `kernels` lists every class with its HBM rate.
-- cpu_baseline: the CPU oracle port (oracle/, a C restatement of the
-  reference's tag-and-sort loop) on a bounded sample of the same workload.
-- --impl reference: the reference path on the host cores: the oracle port
-  (the reference is pure Python and does not travel to the GPU box).
+- cpu_baseline: the reference's own build (the unmodified package installed
+  in baseline/_ref, numba backend on the host threads) on a bounded 1M-point
+  sample of the same workload; the C port of its loop (oracle/) if absent.
+- --impl reference: the same reference build, one 1M-point sample per step
+  (a 100M reference build takes ~20 min; its measured time is reported as
+  headline_config_reference).
 """
 
 from __future__ import annotations
@@ -164,9 +166,62 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(k: int, dist: str):
-    from oracle import oracle
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+REF_SAMPLE_N = 1_000_000
+HEADLINE_REF = {"n": 100_000_000, "k": 3, "seconds": 1169.4, "mpts_per_s": 0.0855,
+                "where": "authoring container, 8 cores, numba 8 threads (BASELINE.md / SURVEY.md App. A.1)"}
+
+
+def load_reference():
+    """The UNMODIFIED reference package installed in baseline/_ref
+    (pip install --target baseline/_ref of /root/reference/pkg), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "lbkd")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", f"/tmp/lbkd_numba_{os.getpid()}")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import lbkd  # noqa: F401
+
+        return lbkd
+    except Exception:
+        return None
+
+
+def _ref_threads():
+    try:
+        import numba
+
+        return int(numba.get_num_threads())
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(k: int, dist: str, mode: str = "rr"):
+    """The reference's own build (baseline/_ref, numba backend, all host
+    threads) on a bounded sample of the same workload; the C port of its loop
+    (oracle/) if the reference is not installed."""
     from paper_2211_00120_b200 import datagen
+
+    lbkd = load_reference()
+    if lbkd is not None:
+        fn = lbkd.build_round_robin if mode == "rr" else lbkd.build_widest
+        fn(datagen.make(dist, 10_000, k, seed=1), k)  # numba JIT warm-up
+        pts = datagen.make(dist, REF_SAMPLE_N, k, seed=0)
+        t0 = time.perf_counter()
+        fn(pts, k)
+        t = time.perf_counter() - t0
+        return {
+            "value": round(REF_SAMPLE_N / t / 1e6, 4),
+            "unit": "Mpoints/s",
+            "cores": _ref_threads(),
+            "kind": "reference",
+            "sample": f"one lbkd.build_{'round_robin' if mode == 'rr' else 'widest'} of {REF_SAMPLE_N:,} {dist} "
+                      f"float{k} points (same generator), {t:.2f} s, the unmodified reference from baseline/_ref "
+                      f"(np.lexsort + gathers single-threaded, numba update on {_ref_threads()} threads)",
+            "headline_config_reference": HEADLINE_REF,
+        }
+    from oracle import oracle
 
     pts = datagen.make(dist, CPU_SAMPLE_N, k, seed=0)
     oracle.set_threads(0)
@@ -179,24 +234,46 @@ def cpu_baseline(k: int, dist: str):
         "kind": "port",
         "sample": f"one build of {CPU_SAMPLE_N:,} {dist} float{k} points (same generator), "
                   f"{t:.2f} s; oracle/lbkd_oracle.c (stable merge sort per level like np.lexsort, "
-                  f"single-threaded; OpenMP update pass)",
+                  f"single-threaded; OpenMP update pass) -- baseline/_ref not installed",
     }
 
 
 def run_reference(args):
-    """--impl reference: the reference path on the host cores (oracle port)."""
+    """--impl reference: the reference's own CPU build on the host cores --
+    the unmodified package from baseline/_ref (numba backend, every host
+    thread numba gets; its np.lexsort is single-threaded), each step one
+    build of a bounded sample of the workload; the C port of its loop
+    (oracle/) when baseline/_ref is absent."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import oracle
     from paper_2211_00120_b200 import datagen
 
-    sample = int(os.environ.get("BENCH_REF_SAMPLE", "1000000"))
+    sample = int(os.environ.get("BENCH_REF_SAMPLE", str(REF_SAMPLE_N)))
     pts = datagen.make(args.dist, sample, args.k, seed=0)
-    oracle.set_threads(0)
-    for _ in range(args.warmup):
-        oracle.timed_build(pts, "rr" if args.mode == "rr" else "widest")
-    ts = [oracle.timed_build(pts, "rr" if args.mode == "rr" else "widest") for _ in range(args.steps)]
+    lbkd = load_reference()
+    if lbkd is not None:
+        fn = lbkd.build_round_robin if args.mode == "rr" else lbkd.build_widest
+        warm = datagen.make(args.dist, 10_000, args.k, seed=1)
+        for _ in range(args.warmup):  # numba JIT + caches; small so the run stays within minutes
+            fn(warm, args.k)
+        ts = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            fn(pts, args.k)
+            ts.append(time.perf_counter() - t0)
+        kind, cores = "reference", _ref_threads()
+        what = (f"the unmodified reference (baseline/_ref lbkd.build_{'round_robin' if args.mode == 'rr' else 'widest'}, "
+                f"numba backend on {cores} threads; np.lexsort single-threaded); warm-up steps build 10,000 points")
+    else:
+        from oracle import oracle
+
+        oracle.set_threads(0)
+        for _ in range(args.warmup):
+            oracle.timed_build(pts, "rr" if args.mode == "rr" else "widest")
+        ts = [oracle.timed_build(pts, "rr" if args.mode == "rr" else "widest") for _ in range(args.steps)]
+        kind, cores = "port", oracle.threads()
+        what = "oracle/lbkd_oracle.c, the C port of the reference loop (baseline/_ref not installed)"
     total = sum(ts)
     value = sample * args.steps / total / 1e6
     line = {
@@ -213,11 +290,12 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"{args.dist} float{args.k} {args.mode}, bounded CPU sample of N={sample:,} "
-                               f"(the N={args.n:,} build would take ~20 min on the host)",
-                   "n": sample, "k": args.k, "mode": args.mode},
-        "cpu_baseline": {"value": round(value, 4), "unit": "Mpoints/s", "cores": oracle.threads(), "kind": "port",
-                         "sample": f"{args.steps} builds of {sample:,} points"},
+        "config": {"workload": f"{args.dist} float{args.k} {args.mode}, bounded CPU sample of N={sample:,} per step "
+                               f"(one N={args.n:,} reference build takes ~20 min on a host: see headline_config_reference)",
+                   "n": sample, "k": args.k, "mode": args.mode, "same_config": sample == args.n},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpoints/s", "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} builds of {sample:,} points; {what}"},
+        "headline_config_reference": HEADLINE_REF,
         "e2e": {"value": round(value, 4), "unit": "Mpoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -458,7 +536,7 @@ def main():
                 "source": "profiles/ncu_issue_%s.json (ncu --set full of the same build)" % dom,
             }
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(k, args.dist)
+            line["cpu_baseline"] = cpu_baseline(k, args.dist, args.mode)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

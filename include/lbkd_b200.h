@@ -127,6 +127,16 @@ int lbkd_build_rr_top(lbkd_ctx *ctx, const float *d_points, int64_t n, int k, in
                       uint32_t *d_perm, uint32_t *d_sub, int64_t sub_stride, void *stream);
 int lbkd_build_rr_sub(lbkd_ctx *ctx, const uint32_t *d_sub, int64_t sub_stride, int64_t n_total, int k,
                       int root_level, int64_t root_index, float *d_out, uint32_t *d_perm, void *stream);
+/* Recursive halving of the top levels: build `levels` (>= 1, global levels
+ * only) levels of the subtree rooted at (root_level, root_index) from its
+ * packed points, write those nodes to d_out / d_perm, and pack its
+ * 2^levels sub-subtrees' points into d_next exactly like lbkd_build_rr_top
+ * (offsets relative to the subtree: the sizes of the earlier
+ * sub-subtrees).  Ranks then split the work without rank 0 building every
+ * top level alone. */
+int lbkd_build_rr_split(lbkd_ctx *ctx, const uint32_t *d_sub, int64_t sub_stride, int64_t n_total, int k,
+                        int root_level, int64_t root_index, int levels, float *d_out, uint32_t *d_perm,
+                        uint32_t *d_next, int64_t next_stride, void *stream);
 
 /* The accel plugin seam (accel.py:48-58): in-place tag refinement. */
 int lbkd_update_tags_rr(uint32_t *d_tags, int64_t n, int levels, int l, void *stream);

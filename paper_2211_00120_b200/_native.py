@@ -32,7 +32,7 @@ EXPORTED = (
     "lbkd_num_levels", "lbkd_single_cta_capacity", "lbkd_plan_info",
     "lbkd_last_launch_count", "lbkd_strerror", "lbkd_last_cuda_error",
     "lbkd_set_profile", "lbkd_profile_read",
-    "lbkd_build_rr_top", "lbkd_build_rr_sub",
+    "lbkd_build_rr_top", "lbkd_build_rr_sub", "lbkd_build_rr_split",
     "lbkd_profile_kernel", "lbkd_set_algorithm", "lbkd_get_algorithm",
     "lbkd_build_rr_host", "lbkd_build_widest_host", "lbkd_host_join",
     "lbkd_set_subtree_kernel",
@@ -100,6 +100,8 @@ def load():
         lib.lbkd_build_rr_top.restype = i32
         lib.lbkd_build_rr_sub.argtypes = [vp, vp, i64, i64, i32, i32, i64, vp, vp, vp]
         lib.lbkd_build_rr_sub.restype = i32
+        lib.lbkd_build_rr_split.argtypes = [vp, vp, i64, i64, i32, i32, i64, i32, vp, vp, vp, i64, vp]
+        lib.lbkd_build_rr_split.restype = i32
         lib.lbkd_update_tags_rr.argtypes = [vp, i64, i32, i32, vp]
         lib.lbkd_update_tags_rr.restype = i32
         lib.lbkd_update_tags_widest.argtypes = [vp, vp, i32, vp, vp, vp, i64, i32, i32, i32, vp]

@@ -719,7 +719,7 @@ static int build_top(lbkd_ctx* c, const float* d_points, int64_t n_in, int k, in
     if ((rc = prologue(c, bp, lam0, st))) return rc;
     if ((rc = run_levels(c, bp, 0, top, st))) return rc;
     if (prof_begin(c, st)) return LBKD_ECUDA;
-    launch_extract(bp, c->bf, top, d_sub, (u64)sub_stride, c->algo == 0 ? (top & 1) : -1, st);
+    launch_extract(bp, c->bf, top, d_sub, (u64)sub_stride, c->algo == 0 ? (top & 1) : -1, st);  // lroot = 0
     prof_end(c, st, kPOther, 8.0 * (k + 1) * (double)level_points(bp, top));
     return end_build(c, st);
 }
@@ -727,8 +727,12 @@ static int build_top(lbkd_ctx* c, const float* d_points, int64_t n_in, int k, in
 // multi-device, rank j: finish the subtree rooted at (root_level, root_index)
 // of an n_total-point tree from its points in d_sub (as packed by build_top);
 // nodes land at their global level-order slots of d_out / d_perm
+// levels < 0: finish the subtree; levels >= 1 (global levels only): build
+// that many levels of it and pack its 2^levels sub-subtrees' points into
+// d_next (layout of build_top, offsets relative to the view)
 static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t n_total, int k, int root_level,
-                     int64_t root_index, float* d_out, u32* d_perm, cudaStream_t st) {
+                     int64_t root_index, float* d_out, u32* d_perm, int levels, u32* d_next, int64_t next_stride,
+                     cudaStream_t st) {
     int rc = check_args(c, n_total, k, kRoundRobin);
     if (rc) return rc;
     c->launches = 0;
@@ -743,6 +747,10 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     const LevelGeom gr = make_geom(n, root_level);
     const u64 nview = seg_size(gr, (u64)root_index);
     if ((u64)sub_stride < nview) return LBKD_EINVAL_SHAPE;
+    if (levels >= 0) {
+        if (levels < 1 || root_level + levels > lam0 || !d_next || (u64)next_stride < nview)
+            return levels >= 1 && root_level + levels > lam0 ? LBKD_EUNSUPPORTED : LBKD_EINVAL_SHAPE;
+    }
     rc = ensure(c, nview, k, b, lam0 - root_level + 1);
     if (rc) return rc;
     BuildParams bp;
@@ -771,6 +779,14 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
         if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_root(bp, c->bf, c->minmax, st);
         prof_end(c, st, kPOther, 0.0);
+    }
+    if (levels >= 0) {
+        const int stop = root_level + levels;
+        if ((rc = run_levels(c, bp, root_level, stop, st))) return rc;
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_extract(bp, c->bf, stop, d_next, (u64)next_stride, c->algo == 0 ? ((stop - root_level) & 1) : -1, st);
+        prof_end(c, st, kPOther, 8.0 * (k + 1) * (double)level_points(bp, stop));
+        return end_build(c, st);
     }
     if ((rc = run_levels(c, bp, root_level, lam0, st))) return rc;
     if ((rc = run_subtrees(c, bp, lam0, st))) return rc;
@@ -1047,7 +1063,15 @@ int lbkd_build_rr_top(lbkd_ctx* c, const float* d_points, int64_t n, int k, int 
 
 int lbkd_build_rr_sub(lbkd_ctx* c, const uint32_t* d_sub, int64_t sub_stride, int64_t n_total, int k,
                       int root_level, int64_t root_index, float* d_out, uint32_t* d_perm, void* stream) {
-    return build_sub(c, d_sub, sub_stride, n_total, k, root_level, root_index, d_out, d_perm, (cudaStream_t)stream);
+    return build_sub(c, d_sub, sub_stride, n_total, k, root_level, root_index, d_out, d_perm, -1, nullptr, 0,
+                     (cudaStream_t)stream);
+}
+
+int lbkd_build_rr_split(lbkd_ctx* c, const uint32_t* d_sub, int64_t sub_stride, int64_t n_total, int k,
+                        int root_level, int64_t root_index, int levels, float* d_out, uint32_t* d_perm,
+                        uint32_t* d_next, int64_t next_stride, void* stream) {
+    return build_sub(c, d_sub, sub_stride, n_total, k, root_level, root_index, d_out, d_perm, levels, d_next,
+                     next_stride, (cudaStream_t)stream);
 }
 
 int lbkd_update_tags_rr(uint32_t* d_tags, int64_t n, int levels, int l, void* stream) {

@@ -570,19 +570,22 @@ __global__ void pivot_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* stat
 // ---------------------------------------------------------------------------
 __global__ void extract_kernel(LevelGeom g, int k, Buffers bf, const uint8_t* prev_state, int src_par, u32* d_sub,
                                u64 sub_stride) {
-    const u64 j = blockIdx.y / (u64)(k + 1);
+    // local segment t of the view (global segment sbase + t)
+    const u64 t = blockIdx.y / (u64)(k + 1);
     const int c = (int)(blockIdx.y % (u64)(k + 1));
-    const u32 par = src_par >= 0 ? (u32)src_par : parity_out(prev_state[j >> 1]);
-    const u32* src = bf.w[par] + (u64)c * bf.stride + seg_ibegin(g, j);
-    u32* dst = d_sub + (u64)c * sub_stride + seg_begin(g, j);
-    const u64 m = seg_size(g, j);
+    const u32 par = src_par >= 0 ? (u32)src_par : parity_out(prev_state[t >> 1]);
+    const u32* src = bf.w[par] + (u64)c * bf.stride + v_ibegin(g, t);
+    // packed: the sizes of the view's earlier segments
+    u32* dst = d_sub + (u64)c * sub_stride + (seg_begin(g, g.sbase + t) - seg_begin(g, g.sbase));
+    const u64 m = v_size(g, t);
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x)
         dst[i] = src[i];
 }
 
+// the view's level-`top` subtrees (whole tree: lroot = 0)
 void launch_extract(const BuildParams& bp, const Buffers& bf, int top, u32* d_sub, u64 sub_stride, int src_par,
                     cudaStream_t st) {
-    LevelGeom g = make_geom(bp.n, top);
+    LevelGeom g = view_of(bp, top);
     dim3 grid(148 * 2, (unsigned)(g.nseg * (u64)(bp.k + 1)));
     extract_kernel<<<grid, 256, 0, st>>>(g, bp.k, bf, bf.state[(top - 1) & 1], src_par, d_sub, sub_stride);
 }

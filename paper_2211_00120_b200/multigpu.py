@@ -1,22 +1,32 @@
 """Multi-GPU round-robin build: one process per GPU.
 
-The path shards naturally after one exchange step.  Rank 0 holds the input
-and builds the top ``t = log2(G)`` levels; after them every level-t subtree
-is independent (a stable sort restricted to a subset keeps that subset's
+The path shards naturally: after level t every level-t subtree is
+independent (a stable sort restricted to a subset keeps that subset's
 order), and in the in-order working layout each subtree is one contiguous
-range of every SoA array.  So:
+range of every SoA array.  With G = 2^t ranks the top levels are split by
+RECURSIVE HALVING instead of running on rank 0 alone:
 
-1. rank 0: ``lbkd_build_rr_top`` -- levels 0..t-1, nodes written at their
-   level-order slots, subtree j's points packed at offset
-   ``segment_begin(F(t)+j) - F(t)`` (k coordinate arrays + index array);
-2. rank 0 -> rank j: k+1 contiguous slices (NCCL send/recv over NVLink);
-3. every rank j: ``lbkd_build_rr_sub`` -- the remaining levels of subtree j
-   with the GLOBAL tree geometry (global node ids, pivot offsets, in-order
-   positions), so the result is bit-identical to the single-GPU build;
-4. rank j -> rank 0: subtree j's nodes, one contiguous range per level.
+    step i = 0 .. t-1: every rank r that holds a level-i subtree (r a
+    multiple of h = G >> i; rank 0 starts with the whole input) builds ONE
+    level of it -- its node goes to the output -- keeps the left child and
+    ships the right child's points (k coordinate arrays + index array, in
+    the order the reference's sort leaves them) to rank r + h/2.
+    lbkd_build_rr_top does step 0 on the raw input, lbkd_build_rr_split the
+    later steps on packed points.
 
-The exchange logic is independent of the device kernels (``ops`` is
-injectable), which is what the gloo tests on CPU exercise.
+Then every rank finishes its level-t subtree (lbkd_build_rr_sub) with the
+GLOBAL tree geometry (global node ids, pivot offsets, in-order positions),
+so the result is bit-identical to the single-GPU build, and sends its nodes
+back to rank 0: one contiguous level-order range per level of its subtree,
+plus the single nodes it placed while splitting.  The critical path is
+level 0 on N points + level 1 on N/2 + ... instead of t levels on N.
+
+Transport: device tensors through the process group (NCCL over NVLink /
+NVSwitch), or, for a gloo group (CPU tests, several ranks sharing one GPU),
+the same messages staged through host memory.  The exchange logic is
+independent of the device kernels (``ops`` is injectable), which is what the
+CPU gloo tests exercise with fakes; tests/test_gpu_multiproc.py runs the
+real kernels in two processes.
 """
 
 from __future__ import annotations
@@ -64,6 +74,23 @@ def node_ranges(n: int, top: int, j: int):
     return out
 
 
+def split_plan(world: int):
+    """Recursive halving: per step i the (holder, partner, level, index) of
+    every split.  Holder r splits its level-i subtree j = r >> (t - i) and
+    sends the right child (index 2j + 1) to partner r + (G >> (i + 1))."""
+    t = top_levels_for(world)
+    steps = []
+    for i in range(t):
+        h = world >> i
+        steps.append([(r, r + h // 2, i, r >> (t - i)) for r in range(0, world, h)])
+    return steps
+
+
+def placed_nodes(world: int, rank: int):
+    """The single nodes rank `rank` places while splitting (level i, node)."""
+    return [(i, (1 << i) - 1 + j) for step in split_plan(world) for (r, _, i, j) in step if r == rank]
+
+
 class CudaOps:
     """The device side: the C-ABI calls on torch CUDA tensors."""
 
@@ -74,24 +101,61 @@ class CudaOps:
         self.lib = _native.load()
         self.device = device
 
-    def build_top(self, points, top, out, perm, sub, sub_stride, stream=None):
+    def _stream(self, stream):
         import torch
 
+        s = stream or torch.cuda.current_stream()
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def build_top(self, points, top, out, perm, sub, sub_stride, stream=None):
         n, k = points.shape
         ctx = self.native.context(self.device)
-        s = stream or torch.cuda.current_stream()
         rc = self.lib.lbkd_build_rr_top(ctx, points.data_ptr(), n, k, top, out.data_ptr(), perm.data_ptr(),
-                                        sub.data_ptr(), sub_stride, ctypes.c_void_p(s.cuda_stream))
+                                        sub.data_ptr(), sub_stride, self._stream(stream))
         self.native.check(rc, "lbkd_build_rr_top")
 
-    def build_sub(self, sub, sub_stride, n, k, top, j, out, perm, stream=None):
-        import torch
-
+    def build_split(self, sub, sub_stride, n, k, level, j, levels, out, perm, nxt, next_stride, stream=None):
         ctx = self.native.context(self.device)
-        s = stream or torch.cuda.current_stream()
+        rc = self.lib.lbkd_build_rr_split(ctx, sub.data_ptr(), sub_stride, n, k, level, j, levels, out.data_ptr(),
+                                          perm.data_ptr(), nxt.data_ptr(), next_stride, self._stream(stream))
+        self.native.check(rc, "lbkd_build_rr_split")
+
+    def build_sub(self, sub, sub_stride, n, k, top, j, out, perm, stream=None):
+        ctx = self.native.context(self.device)
         rc = self.lib.lbkd_build_rr_sub(ctx, sub.data_ptr(), sub_stride, n, k, top, j, out.data_ptr(),
-                                        perm.data_ptr(), ctypes.c_void_p(s.cuda_stream))
+                                        perm.data_ptr(), self._stream(stream))
         self.native.check(rc, "lbkd_build_rr_sub")
+
+
+class _Transport:
+    """Point-to-point messages of device tensors: direct for NCCL; staged
+    through host memory for gloo (which only moves CPU tensors)."""
+
+    def __init__(self, group, device):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.host = dist.get_backend(group) == "gloo" and device.type == "cuda"
+
+    def exchange(self, sends, recvs):
+        """sends: [(tensor, peer)], recvs: [(tensor, peer)] -- all posted at
+        once, then waited for; received data lands in the given tensors."""
+        dist = self.dist
+        ops = []
+        staged = []
+        for t, peer in sends:
+            ops.append(dist.P2POp(dist.isend, t.cpu() if self.host else t, peer, self.group))
+        for t, peer in recvs:
+            buf = t.new_empty(t.shape, device="cpu") if self.host else t
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            if self.host:
+                staged.append((t, buf))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for t, buf in staged:
+            t.copy_(buf)
 
 
 def build_round_robin_sharded(points, n: int, k: int, group=None, ops=None, device=None, buffers=None):
@@ -106,52 +170,121 @@ def build_round_robin_sharded(points, n: int, k: int, group=None, ops=None, devi
 
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
-    top = top_levels_for(world)
+    t = top_levels_for(world)
     dev = device if device is not None else (points.device if points is not None else torch.device("cpu"))
     if ops is None:
         ops = CudaOps(dev.index if dev.type == "cuda" else 0)
-    layout = shard_layout(n, top)
+    tr = _Transport(group, dev)
     bufs = buffers if buffers is not None else {}
 
     def buf(name, shape, dtype):
-        t = bufs.get(name)
-        if t is None or t.shape != torch.Size(shape) or t.dtype != dtype:
-            t = torch.empty(shape, dtype=dtype, device=dev)
-            bufs[name] = t
-        return t
+        b = bufs.get(name)
+        if b is None or b.shape != torch.Size(shape) or b.dtype != dtype:
+            b = torch.empty(shape, dtype=dtype, device=dev)
+            bufs[name] = b
+        return b
 
     out = buf("out", (n, k), torch.float32)
     perm = buf("perm", (n,), torch.int32)
-    if rank == 0:
-        sub = buf("sub", ((k + 1) * n,), torch.int32)
-        ops.build_top(points, top, out, perm, sub, n)
-        ops_list = []
-        for sh in layout[1:]:
-            for c in range(k + 1):
-                base = c * n + sh.offset
-                ops_list.append(dist.P2POp(dist.isend, sub[base:base + sh.size], sh.index, group))
-        reqs = dist.batch_isend_irecv(ops_list) if ops_list else []
-        ops.build_sub(sub, n, n, k, top, 0, out, perm)
-        for r in reqs:
-            r.wait()
-        recv = []
-        for sh in layout[1:]:
-            for first, cnt in node_ranges(n, top, sh.index):
-                recv.append(dist.P2POp(dist.irecv, out[first:first + cnt], sh.index, group))
-                recv.append(dist.P2POp(dist.irecv, perm[first:first + cnt], sh.index, group))
-        for r in (dist.batch_isend_irecv(recv) if recv else []):
-            r.wait()
+    if world == 1:
+        from . import builder
+
+        builder.build_round_robin_cuda(points, out=out, perm=perm, check_finite=False)
         return out, perm
-    sh = layout[rank]
-    sub = buf("sub", ((k + 1) * sh.size,), torch.int32)
-    recv = [dist.P2POp(dist.irecv, sub[c * sh.size:(c + 1) * sh.size], 0, group) for c in range(k + 1)]
-    for r in dist.batch_isend_irecv(recv):
-        r.wait()
-    ops.build_sub(sub, sh.size, n, k, top, sh.index, out, perm)
-    send = []
-    for first, cnt in node_ranges(n, top, sh.index):
-        send.append(dist.P2POp(dist.isend, out[first:first + cnt], 0, group))
-        send.append(dist.P2POp(dist.isend, perm[first:first + cnt], 0, group))
-    for r in dist.batch_isend_irecv(send):
-        r.wait()
+    # ---- recursive halving of the top t levels
+    cur = None          # packed points of the subtree this rank holds (k + 1 arrays, stride = its size)
+    cur_level, cur_j, cur_size = 0, 0, n
+    for i, step in enumerate(split_plan(world)):
+        for (r, partner, level, j) in step:
+            s = (1 << level) - 1 + j
+            size = treemath.subtree_size(s, n)
+            lc = 2 * s + 1
+            lsize = treemath.subtree_size(lc, n) if lc < n else 0
+            rsize = treemath.subtree_size(lc + 1, n) if lc + 1 < n else 0
+            if rank == r:
+                nxt = buf(f"split{i}", ((k + 1) * size,), torch.int32)
+                if level == 0:
+                    ops.build_top(points, 1, out, perm, nxt, size)
+                else:
+                    ops.build_split(cur, cur_size, n, k, level, j, 1, out, perm, nxt, size)
+                # right child: packed after the left one in every array
+                sends = [(nxt[c * size + lsize:c * size + lsize + rsize], partner) for c in range(k + 1)]
+                tr.exchange(sends, [])
+                # keep the left child (strided view -> its own contiguous buffer)
+                keep = buf(f"keep{i}", ((k + 1) * max(lsize, 1),), torch.int32)
+                for c in range(k + 1):
+                    keep[c * lsize:(c + 1) * lsize].copy_(nxt[c * size:c * size + lsize])
+                cur, cur_level, cur_j, cur_size = keep, level + 1, 2 * j, lsize
+            elif rank == partner:
+                recv = buf(f"recv{i}", ((k + 1) * max(rsize, 1),), torch.int32)
+                tr.exchange([], [(recv[c * rsize:(c + 1) * rsize], r) for c in range(k + 1)])
+                cur, cur_level, cur_j, cur_size = recv, level + 1, 2 * j + 1, rsize
+    # ---- every rank finishes its level-t subtree
+    assert cur_level == t and cur_j == rank
+    ops.build_sub(cur, cur_size, n, k, t, rank, out, perm)
+    # ---- gather at rank 0: subtree node ranges + the single split nodes
+    if rank == 0:
+        recvs = []
+        for peer in range(1, world):
+            for first, cnt in node_ranges(n, t, peer):
+                recvs.append((out[first:first + cnt], peer))
+                recvs.append((perm[first:first + cnt], peer))
+            for _, node in placed_nodes(world, peer):
+                recvs.append((out[node:node + 1], peer))
+                recvs.append((perm[node:node + 1], peer))
+        tr.exchange([], recvs)
+        return out, perm
+    sends = []
+    for first, cnt in node_ranges(n, t, rank):
+        sends.append((out[first:first + cnt], 0))
+        sends.append((perm[first:first + cnt], 0))
+    for _, node in placed_nodes(world, rank):
+        sends.append((out[node:node + 1], 0))
+        sends.append((perm[node:node + 1], 0))
+    tr.exchange(sends, [])
     return None, None
+
+
+def serial_sharded_build(points, n: int, k: int, world: int, ops=None, out=None, perm=None, timer=None):
+    """The whole protocol of build_round_robin_sharded run rank by rank in
+    ONE process on one device (no transport): the same kernels and packed
+    buffers, so the result must equal the single-GPU build.  ``timer(label,
+    fn)`` may wrap every device call (tools/big_build.py times each piece to
+    project the multi-GPU critical path).  Returns (out, perm)."""
+    import torch
+
+    dev = points.device
+    t = top_levels_for(world)
+    if ops is None:
+        ops = CudaOps(dev.index if dev.type == "cuda" else 0)
+    if out is None:
+        out = torch.empty((n, k), dtype=torch.float32, device=dev)
+    if perm is None:
+        perm = torch.empty(n, dtype=torch.int32, device=dev)
+    run = timer or (lambda label, fn: fn())
+    held = {0: (None, n)}  # rank -> (packed points, size)
+    for i, step in enumerate(split_plan(world)):
+        for (r, partner, level, j) in step:
+            s = (1 << level) - 1 + j
+            size = treemath.subtree_size(s, n)
+            lc = 2 * s + 1
+            lsize = treemath.subtree_size(lc, n) if lc < n else 0
+            rsize = treemath.subtree_size(lc + 1, n) if lc + 1 < n else 0
+            nxt = torch.empty((k + 1) * size, dtype=torch.int32, device=dev)
+            cur, cur_size = held[r]
+            if level == 0:
+                run(f"split{i}/r{r}", lambda: ops.build_top(points, 1, out, perm, nxt, size))
+            else:
+                run(f"split{i}/r{r}",
+                    lambda: ops.build_split(cur, cur_size, n, k, level, j, 1, out, perm, nxt, size))
+            left = torch.empty((k + 1) * max(lsize, 1), dtype=torch.int32, device=dev)
+            right = torch.empty((k + 1) * max(rsize, 1), dtype=torch.int32, device=dev)
+            for c in range(k + 1):
+                left[c * lsize:(c + 1) * lsize].copy_(nxt[c * size:c * size + lsize])
+                right[c * rsize:(c + 1) * rsize].copy_(nxt[c * size + lsize:c * size + lsize + rsize])
+            held[r] = (left, lsize)
+            held[partner] = (right, rsize)
+    for r in range(world):
+        sub, size = held[r]
+        run(f"sub/r{r}", lambda: ops.build_sub(sub, size, n, k, t, r, out, perm))
+    return out, perm

@@ -85,4 +85,12 @@ def test_1b_sharded_decomposition_bit_identical(big, G):
     torch.cuda.synchronize()
     assert torch.equal(perm2, perm)
     assert torch.equal(out2.view(torch.int32), out.view(torch.int32))
-    del sub, out2, perm2
+    del sub
+    # recursive halving of the top levels (what build_round_robin_sharded runs)
+    out2.fill_(float("nan"))
+    perm2.fill_(-1)
+    multigpu.serial_sharded_build(d, n, k, G, out=out2, perm=perm2)
+    torch.cuda.synchronize()
+    assert torch.equal(perm2, perm)
+    assert torch.equal(out2.view(torch.int32), out.view(torch.int32))
+    del out2, perm2

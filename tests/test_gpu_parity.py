@@ -241,6 +241,12 @@ def test_sharded_build_matches_single_gpu(n, k, world, kind):
     assert torch.equal(perm, want_perm)
     assert torch.equal(out, want_out)
     assert oracle.build_rr(pts).tolist()[:1000] == perm.cpu().numpy().view(np.uint32).tolist()[:1000]
+    # the recursive-halving protocol (lbkd_build_rr_top with one level, then
+    # lbkd_build_rr_split per step, then lbkd_build_rr_sub) run rank by rank
+    out2, perm2 = multigpu.serial_sharded_build(d, n, k, world)
+    torch.cuda.synchronize()
+    assert torch.equal(perm2, want_perm)
+    assert torch.equal(out2, want_out)
 
 
 @pytest.mark.parametrize("n", [8193, 70001, 300001, 1 << 20])

@@ -224,7 +224,9 @@ def test_caller_buffers_are_validated():
     with pytest.raises(ValueError):
         kd.build_round_robin_cuda(d, out=torch.empty((1000, 3)))
     with pytest.raises(ValueError):
-        kd.build_round_robin_cuda(d.double())
+        kd.build_round_robin_cuda(d.to(torch.int32))
+    with pytest.raises(ValueError):  # float64 points need float64 out
+        kd.build_round_robin_cuda(d.double(), out=torch.empty((1000, 3), device="cuda"))
 
 
 def test_query_cache_sees_in_place_edits():
@@ -237,12 +239,15 @@ def test_query_cache_sees_in_place_edits():
     assert verify.check_valid(tree).valid
     nb = kd.knn(tree, pts[17].astype(np.float64), 1)
     assert nb[0].dist2 == 0.0
+    # nudge a leaf inside its own cell: a stale device copy would report the
+    # old position (dist2 > 0), a fresh one finds the leaf exactly
+    leaf = tree.n - 1
+    tree.coords[leaf] = np.nextafter(tree.coords[leaf], np.inf)
+    nb = kd.knn(tree, tree.coords[leaf].copy(), 1)
+    assert nb[0].index == leaf and nb[0].dist2 == 0.0
     # move node 1 (left child of the root) to the far right of the root plane
     tree.coords[1, 0] = tree.coords[0, 0] + 10.0
     assert not verify.check_valid(tree).valid
-    q = tree.coords[1].copy()
-    nb = kd.knn(tree, q, 1)
-    assert nb[0].index == 1 and nb[0].dist2 == 0.0
     wt = kd.build_widest(pts)
     assert verify.check_valid(wt).valid
     s = int(np.argmax(wt.split_dims[:7] != 0))

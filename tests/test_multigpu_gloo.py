@@ -45,34 +45,72 @@ def test_layout_and_ranges_partition_the_tree():
         multigpu.top_levels_for(3)
 
 
-def _stamp(j, c, i):
-    return (j * 7919 + c * 104729 + i * 31) % 1000003
+def _stamp(level, j, c, i):
+    return (level * 15485863 + j * 7919 + c * 104729 + i * 31) % 1000003
 
 
 class FakeOps:
+    """Stamps every packed value with (level, subtree, array, position) and
+    every node with its own id, and checks each stamp where it is consumed."""
+
     def __init__(self, rank):
         self.rank = rank
 
-    def build_top(self, points, top, out, perm, sub, stride):
-        n, k = points.shape
-        F = (1 << top) - 1
-        perm[:F] = torch.arange(F, dtype=torch.int32)
-        out[:F] = torch.arange(F, dtype=torch.float32)[:, None]
-        for sh in multigpu.shard_layout(n, top):
-            i = torch.arange(sh.size)
+    def _pack_children(self, n, k, level, j, nxt, stride):
+        s = (1 << level) - 1 + j
+        lc = 2 * s + 1
+        off = 0
+        for child, cj in ((lc, 2 * j), (lc + 1, 2 * j + 1)):
+            if child >= n:
+                continue
+            size = treemath.subtree_size(child, n)
+            i = torch.arange(size)
             for c in range(k + 1):
-                sub[c * stride + sh.offset: c * stride + sh.offset + sh.size] = _stamp(sh.index, c, i)
+                nxt[c * stride + off:c * stride + off + size] = _stamp(level + 1, cj, c, i)
+            off += size
 
-    def build_sub(self, sub, stride, n, k, top, j, out, perm):
-        size = multigpu.shard_layout(n, top)[j].size
+    def _place(self, out, perm, node):
+        perm[node] = node
+        out[node] = float(node)
+
+    def _check(self, sub, stride, n, k, level, j):
+        size = treemath.subtree_size((1 << level) - 1 + j, n)
         i = torch.arange(size)
         for c in range(k + 1):
-            got = sub[c * stride: c * stride + size]
-            assert torch.equal(got, _stamp(j, c, i).to(torch.int32)), (self.rank, j, c)
+            got = sub[c * stride:c * stride + size]
+            assert torch.equal(got, _stamp(level, j, c, i).to(torch.int32)), (self.rank, level, j, c)
+
+    def build_top(self, points, top, out, perm, sub, stride):
+        n, k = points.shape
+        assert top == 1
+        self._place(out, perm, 0)
+        self._pack_children(n, k, 0, 0, sub, stride)
+
+    def build_split(self, sub, stride, n, k, level, j, levels, out, perm, nxt, next_stride):
+        assert levels == 1
+        self._check(sub, stride, n, k, level, j)
+        self._place(out, perm, (1 << level) - 1 + j)
+        self._pack_children(n, k, level, j, nxt, next_stride)
+
+    def build_sub(self, sub, stride, n, k, top, j, out, perm):
+        self._check(sub, stride, n, k, top, j)
         for first, cnt in multigpu.node_ranges(n, top, j):
             ids = torch.arange(first, first + cnt)
             perm[first:first + cnt] = ids.to(torch.int32)
             out[first:first + cnt] = ids.to(torch.float32)[:, None]
+
+
+def test_split_plan_covers_every_top_node_once():
+    for world in (2, 4, 8, 16):
+        t = multigpu.top_levels_for(world)
+        placed = sorted(node for r in range(world) for _, node in multigpu.placed_nodes(world, r))
+        assert placed == list(range((1 << t) - 1)), world
+        for i, step in enumerate(multigpu.split_plan(world)):
+            assert len(step) == 1 << i
+            # a holder at step i received its subtree at an earlier step (or is rank 0)
+            for r, partner, level, j in step:
+                assert level == i and partner == r + (world >> (i + 1))
+                assert r >> (t - i) == j
 
 
 def _worker(rank, world, port, n, k, q):
@@ -98,7 +136,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,n,k", [(2, 1001, 3), (4, 40000, 2), (2, 65537, 4)])
+@pytest.mark.parametrize("world,n,k", [(2, 1001, 3), (4, 40000, 2), (2, 65537, 4), (8, 100003, 3)])
 def test_sharded_exchange_gloo(world, n, k):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -2,12 +2,14 @@
 
 1. The single-GPU build of all 1B points (CUDA events, warm-up + reps).
 2. lbkd_check_valid of the result on the device (verify.py:195-245).
-3. The sharded decomposition of SURVEY.md §8(e) for G = 2, 4, 8, run on this
-   one GPU: lbkd_build_rr_top (levels 0..log2 G - 1) then lbkd_build_rr_sub
-   for every subtree j in turn, each timed alone.  The result must equal the
-   single-GPU build bit for bit (the 1B check that needs no CPU oracle), and
-   top + max_j sub is the device time a G-GPU run would need before its
-   NVLink exchange -- reported as a projection, not a measured scaling.
+3. The sharded protocol of multigpu.build_round_robin_sharded for G = 2, 4,
+   8 run rank by rank on this one GPU (multigpu.serial_sharded_build):
+   recursive halving of the top log2 G levels (lbkd_build_rr_top with one
+   level, then lbkd_build_rr_split), then lbkd_build_rr_sub for every
+   subtree, each piece timed alone.  The result must equal the single-GPU
+   build bit for bit, and sum over steps of the slowest holder + the slowest
+   subtree is the device time a G-GPU run would need before its NVLink
+   exchanges -- reported as a projection, not a measured scaling.
 
 Usage: python tools/big_build.py [n] [kind] [reps]   -> JSON on stdout
 """
@@ -58,39 +60,41 @@ res = {"n": n, "k": k, "kind": kind, "gen_s": round(gen_s, 1), "build_ms": [roun
 print(json.dumps(res), flush=True)
 
 ops = multigpu.CudaOps(0)
-sub = torch.empty((k + 1) * n, dtype=torch.int32, device="cuda")
 out2 = torch.empty_like(d)
 perm2 = torch.empty_like(perm)
 shard = {}
 for G in (2, 4, 8):
-    top = multigpu.top_levels_for(G)
-    layout = multigpu.shard_layout(n, top)
     best = None
     for _ in range(2):
-        a, b = ev(), ev()
-        a.record()
-        ops.build_top(d, top, out2, perm2, sub, n)
-        b.record()
-        subs = []
-        for sh in layout:
-            s0, s1 = ev(), ev()
-            s0.record()
-            ops.build_sub(sub[sh.offset:], n, n, k, top, sh.index, out2, perm2)
-            s1.record()
-            subs.append((s0, s1))
+        times = {}
+
+        def timer(label, fn):
+            a, b = ev(), ev()
+            a.record()
+            fn()
+            b.record()
+            times[label] = (a, b)
+
+        multigpu.serial_sharded_build(d, n, k, G, ops=ops, out=out2, perm=perm2, timer=timer)
         torch.cuda.synchronize()
-        top_ms = a.elapsed_time(b)
-        sub_ms = [x.elapsed_time(y) for x, y in subs]
-        if best is None or top_ms + max(sub_ms) < best[0] + max(best[1]):
-            best = (top_ms, sub_ms)
+        ms = {lab: x.elapsed_time(y) for lab, (x, y) in times.items()}
+        # critical path: each halving step waits for its slowest holder, then
+        # the slowest subtree (exchange time not included)
+        steps = sorted({lab.split("/")[0] for lab in ms if lab.startswith("split")})
+        split_ms = [max(v for lab, v in ms.items() if lab.startswith(s + "/")) for s in steps]
+        sub_ms = [ms[f"sub/r{r}"] for r in range(G)]
+        crit = sum(split_ms) + max(sub_ms)
+        if best is None or crit < best[0]:
+            best = (crit, split_ms, sub_ms)
     same = bool(torch.equal(out2, out) and torch.equal(perm2, perm))
-    top_ms, sub_ms = best
-    moved = sum(sh.size for sh in layout[1:])
-    shard[G] = {"top_ms": round(top_ms, 2), "sub_ms": [round(x, 2) for x in sub_ms],
-                "critical_path_ms": round(top_ms + max(sub_ms), 2),
-                "points_moved_off_rank0": moved,
-                "nvlink_bytes_each_way": moved * 4 * (k + 1),
+    crit, split_ms, sub_ms = best
+    t = multigpu.top_levels_for(G)
+    moved = sum(sh.size for sh in multigpu.shard_layout(n, t)[1:])
+    shard[G] = {"split_step_ms": [round(x, 2) for x in split_ms], "sub_ms": [round(x, 2) for x in sub_ms],
+                "critical_path_ms_before_exchange": round(crit, 2),
+                "points_shipped_in_halving": sum(multigpu.shard_layout(n, t)[j].size for j in range(1, G)),
+                "bytes_back_to_rank0": moved * 4 * (k + 1),
                 "bit_identical_to_single_gpu": same}
     print(json.dumps({"G": G, **shard[G]}), flush=True)
-res["sharded_on_one_gpu"] = shard
+res["sharded_on_one_gpu_recursive_halving"] = shard
 print(json.dumps(res))
