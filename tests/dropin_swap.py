@@ -16,6 +16,8 @@ brute-force scans, treemath) stay the reference's own:
 Used by tests/test_gpu_dropin.py:  pytest -p tests.dropin_swap <ref tests>
 """
 
+import os
+
 import lbkd
 import lbkd.builder
 import lbkd.queries
@@ -44,6 +46,10 @@ def pytest_configure(config):
     _swap(lbkd.queries, "radius_query", ours.radius_query)
     # create the CUDA context and load the library once, outside any test
     ours.build_round_robin([[1.0, 2.0], [3.0, 4.0], [0.5, 0.25]])
+    report = os.environ.get("LBKD_DROPIN_REPORT")
+    if report:
+        with open(report, "w") as f:
+            f.write("\n".join(SWAPPED) + "\n")
 
 
 def pytest_report_header(config):

@@ -27,8 +27,10 @@ FILES = ["test_builder.py", "test_widest.py", "test_acceptance.py", "test_querie
 
 
 @pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "tests")), reason="baseline/_ref/tests not installed")
-def test_reference_test_suite_passes_against_dropin():
-    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, ROOT]), NUMBA_CACHE_DIR="/tmp/lbkd_dropin_numba")
+def test_reference_test_suite_passes_against_dropin(tmp_path):
+    report = str(tmp_path / "swapped.txt")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, ROOT]), NUMBA_CACHE_DIR="/tmp/lbkd_dropin_numba",
+               LBKD_DROPIN_REPORT=report)
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "tests.dropin_swap", "-p", "no:cacheprovider",
            "--rootdir", os.path.join(REF, "tests"), "-o", "addopts="] + [os.path.join(REF, "tests", f) for f in FILES]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
@@ -36,5 +38,7 @@ def test_reference_test_suite_passes_against_dropin():
     with open(os.path.join(ROOT, "gpurun_out", "dropin_reference_tests.txt") if os.path.isdir(
             os.path.join(ROOT, "gpurun_out")) else os.devnull, "w") as f:
         f.write(out)
-    assert "drop-in swap: lbkd.build_round_robin" in out, out[-3000:]
+    swapped = open(report).read().split() if os.path.exists(report) else []
+    assert "lbkd.builder.build_round_robin" in swapped and "lbkd.widest.build_widest" in swapped, out[-3000:]
     assert r.returncode == 0, out[-6000:]
+    assert " passed" in out and " failed" not in out, out[-3000:]

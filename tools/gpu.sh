@@ -13,6 +13,8 @@
 #              one 100M clustered widest build -> gpurun_out/launches_*.{csv,txt}
 #   full       ncu --set full captures of the partition / in-CTA / filter kernels
 #   robust     tools/robust_time.py + tools/quick_time.py
+#   degen      ncu launch lists of adversarial 10M builds (identical, huge range, constant axis, ties)
+#   knobs      tools/knobs.py: per-kernel-class times under env variants ($KNOBS)
 #   big        tools/big_build.py (1B clustered, sharded decomposition on one GPU)
 # Env: TEST_ARGS (extra pytest args), KSEL (ncu kernel regex for `full`, default all three)
 set -u
@@ -56,6 +58,18 @@ step_full() {
 step_robust() {
   timeout 600 python tools/robust_time.py > gpurun_out/robust_time.txt 2>&1; cat gpurun_out/robust_time.txt
   timeout 300 python tools/quick_time.py > gpurun_out/quick_time.txt 2>&1; cat gpurun_out/quick_time.txt
+}
+step_degen() {  # ncu launch lists of adversarial 10M builds (where the time goes)
+  for kind in identical huge constaxis ties; do
+    for mode in rr widest; do
+      L=$(python tools/one_build.py 10000000 3 $mode $kind 1 | awk '/launches per build/{print $4}')
+      ncu --metrics gpu__time_duration.sum --clock-control none -s $L -c $L --csv --log-file gpurun_out/degen_${kind}_$mode.csv python tools/one_build.py 10000000 3 $mode $kind 2 > /dev/null 2>&1
+      echo "== $kind $mode"; python tools/launches.py gpurun_out/degen_${kind}_$mode.csv | head -14
+    done
+  done
+}
+step_knobs() {  # per-class times of 100M builds under tuning switches (KNOBS overrides the list)
+  python tools/knobs.py 100000000 3 rr uniform -- ${KNOBS:-"" LBKD_SUBTREE_BITS=11 LBKD_SUBTREE=sel}
 }
 step_big() { timeout 900 python tools/big_build.py 1000000000 clustered 3 > gpurun_out/big_1b.log 2>&1; tail -1 gpurun_out/big_1b.log | cut -c1-600; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv,noheader

@@ -11,7 +11,13 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 mode = sys.argv[3] if len(sys.argv) > 3 else "rr"
 kind = sys.argv[4] if len(sys.argv) > 4 else "uniform"
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 2
-pts = datagen.make(kind, n, k, seed=0)
+ADV = {  # adversarial inputs of tools/robust_time.py
+    "identical": lambda n, k: np.full((n, k), 0.25, np.float32),
+    "huge": lambda n, k: (10.0 ** np.random.default_rng(4).uniform(-30, 30, (n, k))).astype(np.float32),
+    "constaxis": lambda n, k: np.c_[datagen.uniform(n, k - 1, seed=3), np.zeros(n, np.float32)],
+    "sorted": lambda n, k: np.sort(datagen.uniform(n, k, seed=2), axis=0),
+}
+pts = ADV[kind](n, k) if kind in ADV else datagen.make(kind, n, k, seed=0)
 d = torch.from_numpy(pts).cuda()
 out = torch.empty_like(d); perm = torch.empty(n, dtype=torch.int32, device="cuda")
 for _ in range(reps):
