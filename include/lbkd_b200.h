@@ -121,22 +121,28 @@ int lbkd_host_join(lbkd_ctx *ctx, void *stream, int sync);
  *  - lbkd_build_rr_sub: on any device, finish the subtree rooted at
  *    (root_level, root_index) of an n_total-point tree from its packed
  *    points; nodes land at their global level-order slots of the full-size
- *    d_out / d_perm.
+ *    d_out / d_perm.  When sub_stride is a multiple of 4 and d_sub is 16-byte
+ *    aligned, d_sub itself is the working set (no copy; its contents are
+ *    undefined afterwards).
  * Results are bit-identical to lbkd_build_rr. */
 int lbkd_build_rr_top(lbkd_ctx *ctx, const float *d_points, int64_t n, int k, int top_levels, float *d_out,
                       uint32_t *d_perm, uint32_t *d_sub, int64_t sub_stride, void *stream);
-int lbkd_build_rr_sub(lbkd_ctx *ctx, const uint32_t *d_sub, int64_t sub_stride, int64_t n_total, int k,
+int lbkd_build_rr_sub(lbkd_ctx *ctx, uint32_t *d_sub, int64_t sub_stride, int64_t n_total, int k,
                       int root_level, int64_t root_index, float *d_out, uint32_t *d_perm, void *stream);
-/* Recursive halving of the top levels: build `levels` (>= 1, global levels
- * only) levels of the subtree rooted at (root_level, root_index) from its
- * packed points, write those nodes to d_out / d_perm, and pack its
- * 2^levels sub-subtrees' points into d_next exactly like lbkd_build_rr_top
- * (offsets relative to the subtree: the sizes of the earlier
- * sub-subtrees).  Ranks then split the work without rank 0 building every
- * top level alone. */
-int lbkd_build_rr_split(lbkd_ctx *ctx, const uint32_t *d_sub, int64_t sub_stride, int64_t n_total, int k,
-                        int root_level, int64_t root_index, int levels, float *d_out, uint32_t *d_perm,
-                        uint32_t *d_next, int64_t next_stride, void *stream);
+/* Recursive halving of the top levels (multigpu.py): build ONE level of the
+ * subtree rooted at (root_level, root_index) -- from the raw points d_points
+ * (n_total x k float32) at the root (d_sub unused; stride must then be
+ * ceil4(n_total)), else from its packed points d_sub (layout of
+ * lbkd_build_rr_top, `stride` words between the k + 1 arrays), which is read
+ * in place.  d_next (same stride) receives the next level's working set in
+ * in-order layout: the left child's points at [0, subtree_size(2s+1)), one
+ * unused slot (the node), then the right child's points -- each child ready
+ * to be split again or finished with lbkd_build_rr_sub, without copies.
+ * stride: a multiple of 4 >= the subtree size; d_sub / d_next 16-byte
+ * aligned.  The node goes to d_out / d_perm. */
+int lbkd_build_rr_split(lbkd_ctx *ctx, const float *d_points, uint32_t *d_sub, int64_t stride, int64_t n_total,
+                        int k, int root_level, int64_t root_index, float *d_out, uint32_t *d_perm,
+                        uint32_t *d_next, void *stream);
 
 /* The accel plugin seam (accel.py:48-58): in-place tag refinement. */
 int lbkd_update_tags_rr(uint32_t *d_tags, int64_t n, int levels, int l, void *stream);

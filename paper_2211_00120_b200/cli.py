@@ -15,13 +15,12 @@ tree is a zero-byte file -- write_tree / read_tree (cli.py:70-141).  Query
 results print ``index,dist2`` per hit (cli.py:152-170).  Data errors exit 1
 with the message on stderr.
 
-The build and the queries run on the GPU.  Differences, both from the GPU
-path's input scope: coordinates must be float32-representable
-(the reference accepts any float64), and ``bench`` draws float32 points
-(``rng.random((n, dims), dtype=float32)``; the reference draws float64) and
-adds device-side fields to its JSON record (cli.py:173-194): ``dtype``,
-``device_millis`` (build with the points already in HBM, CUDA events) and
-``mpts_per_s``.  ``selftest`` (cli.py:197-300) is the reference's
+The build and the queries run on the GPU, on float64 coordinates exactly as
+the reference reads them (float32-exact files take the float32 fast path).
+``bench`` draws the reference's float64 points by default (``--dtype
+float32`` for the fast path) and adds device-side fields to its JSON record
+(cli.py:173-194): ``dtype``, ``device_millis`` (build with the points already
+in HBM, CUDA events) and ``mpts_per_s``.  ``selftest`` (cli.py:197-300) is the reference's
 self-check against its own recursive oracle and is not mirrored here; the
 test-suite (tests/) and ``__graft_entry__.smoke()`` play that role.
 """
@@ -154,24 +153,35 @@ def cmd_build(args) -> int:
     return 0
 
 
-def cmd_query(args) -> int:
-    tree = read_tree(args.tree)
+def _parse_point(text: str) -> np.ndarray:
     try:
-        point = [float(p) for p in args.point.split(",")]
+        return np.array([float(p) for p in text.split(",")], dtype=np.float64)
     except ValueError:
-        raise ValueError(f"unparseable query point {args.point!r}") from None
+        raise ValueError(f"unparseable query point {text!r}") from None
+
+
+def _hit_distances(tree, query: np.ndarray, hits: np.ndarray) -> np.ndarray:
+    """Squared distances of the radius hits, accumulated dimension by
+    dimension in float64 (the reference's per-hit loop, cli.py:163-168, as
+    whole-column operations: same roundings, no fused multiply-add)."""
+    diff = query[None, :] - tree.coords[hits]
+    d2 = np.zeros(len(hits), dtype=np.float64)
+    for j in range(tree.k):
+        d2 = d2 + diff[:, j] * diff[:, j]
+    return d2
+
+
+def cmd_query(args) -> int:
+    """``lbkd query`` (cli.py:152-170): ``index,dist2`` per neighbour / hit."""
+    tree = read_tree(args.tree)
+    point = _parse_point(args.point)
     if args.knn is not None:
-        for nb in queries.knn(tree, point, args.knn):
-            print(f"{nb.index},{format_scalar(nb.dist2)}")
+        rows = [(nb.index, nb.dist2) for nb in queries.knn(tree, point.tolist(), args.knn)]
     else:
-        indices = queries.radius_query(tree, point, args.radius)
-        q = np.asarray(point, dtype=np.float64)
-        for i in indices:
-            d2 = 0.0
-            for j in range(tree.k):
-                t = q[j] - tree.coords[i, j]
-                d2 += t * t
-            print(f"{int(i)},{format_scalar(d2)}")
+        hits = np.asarray(queries.radius_query(tree, point.tolist(), args.radius), dtype=np.int64)
+        rows = zip(hits.tolist(), _hit_distances(tree, point, hits).tolist())
+    for idx, d2 in rows:
+        print(f"{int(idx)},{format_scalar(d2)}")
     return 0
 
 
@@ -181,7 +191,9 @@ def cmd_bench(args) -> int:
     import torch
 
     rng = np.random.default_rng(args.seed)
-    coords = rng.random((args.n, args.dims), dtype=np.float32)
+    # the reference draws float64 (cli.py:176-177); --dtype float32 times the
+    # float32 fast path on the same generator
+    coords = rng.random((args.n, args.dims), dtype=np.float64 if args.dtype == "float64" else np.float32)
     build = _build_fn(args.mode)
     build(coords, args.dims)  # warmup: library load, context, scratch
     total = 0.0
@@ -209,7 +221,7 @@ def cmd_bench(args) -> int:
         "seed": args.seed,
         "reps": args.reps,
         "millis": total / args.reps * 1000.0,
-        "dtype": "float32",
+        "dtype": args.dtype,
         "device_millis": dev_ms / args.reps,
         "mpts_per_s": args.n / (dev_ms / args.reps) / 1e3,
     }
@@ -240,6 +252,7 @@ def make_parser() -> argparse.ArgumentParser:
     be.add_argument("--mode", choices=["round-robin", "widest"], default="round-robin")
     be.add_argument("--seed", type=int, default=0)
     be.add_argument("--reps", type=int, default=3)
+    be.add_argument("--dtype", choices=["float64", "float32"], default="float64")
     be.set_defaults(fn=cmd_bench)
     return p
 

@@ -217,13 +217,14 @@ static void drop_graph(lbkd_ctx* c) {
     }
 }
 
-static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0) {
+// need_w = false: the caller supplies both working-set buffers (build_split)
+static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0, bool need_w_bufs = true) {
     g_grow_ctx = c;
     size_t dummy = 0;
     int rc;
     // W[2] holds k+1 SoA arrays of n words each (only when global levels run)
     const size_t stride = (n + 3) & ~(size_t)3;  // 16-byte aligned arrays
-    size_t need_w = lam0 > 0 ? (size_t)(k + 1) * stride : 0;
+    size_t need_w = lam0 > 0 && need_w_bufs ? (size_t)(k + 1) * stride : 0;
     if (need_w > c->cap_w) {
         for (int i = 0; i < 2; ++i)
             if ((rc = grow(c->bf.w[i], dummy, need_w))) return rc;
@@ -727,12 +728,17 @@ static int build_top(lbkd_ctx* c, const float* d_points, int64_t n_in, int k, in
 // multi-device, rank j: finish the subtree rooted at (root_level, root_index)
 // of an n_total-point tree from its points in d_sub (as packed by build_top);
 // nodes land at their global level-order slots of d_out / d_perm
-// levels < 0: finish the subtree; levels >= 1 (global levels only): build
-// that many levels of it and pack its 2^levels sub-subtrees' points into
-// d_next (layout of build_top, offsets relative to the view)
-static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t n_total, int k, int root_level,
-                     int64_t root_index, float* d_out, u32* d_perm, int levels, u32* d_next, int64_t next_stride,
-                     cudaStream_t st) {
+// A packed SoA buffer (k + 1 arrays, `stride` words apart) can serve as the
+// working set itself when the stride is a multiple of 4 words and the base is
+// 16-byte aligned (the bulk copies and 16-byte loads of the global levels)
+static bool aliasable(const void* p, int64_t stride) {
+    return p && (stride % 4) == 0 && ((uintptr_t)p & 15u) == 0;
+}
+
+// Finish the subtree rooted at (root_level, root_index) from its packed
+// points (aliased as W[0] -- then overwritten -- when aliasable, else copied)
+static int build_sub(lbkd_ctx* c, u32* d_sub, int64_t sub_stride, int64_t n_total, int k, int root_level,
+                     int64_t root_index, float* d_out, u32* d_perm, cudaStream_t st) {
     int rc = check_args(c, n_total, k, kRoundRobin);
     if (rc) return rc;
     c->launches = 0;
@@ -747,11 +753,9 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     const LevelGeom gr = make_geom(n, root_level);
     const u64 nview = seg_size(gr, (u64)root_index);
     if ((u64)sub_stride < nview) return LBKD_EINVAL_SHAPE;
-    if (levels >= 0) {
-        if (levels < 1 || root_level + levels > lam0 || !d_next || (u64)next_stride < nview)
-            return levels >= 1 && root_level + levels > lam0 ? LBKD_EUNSUPPORTED : LBKD_EINVAL_SHAPE;
-    }
-    rc = ensure(c, nview, k, b, lam0 - root_level + 1);
+    const bool alias = c->algo == 0 && lam0 > root_level && aliasable(d_sub, sub_stride);
+    // aliased: the context's W[1] takes the caller's stride
+    rc = ensure(c, alias ? (u64)sub_stride : nview, k, b, lam0 - root_level + 1);
     if (rc) return rc;
     BuildParams bp;
     bp.n = n;
@@ -768,8 +772,16 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
     bp.jroot = (u64)root_index;
     if ((rc = begin_order(c, st))) return rc;
     if ((rc = begin_build(c, k, st))) return rc;
-    CK(cudaMemcpy2DAsync(c->bf.w[0], c->bf.stride * sizeof(u32), d_sub, (size_t)sub_stride * sizeof(u32),
-                         nview * sizeof(u32), (size_t)k + 1, cudaMemcpyDeviceToDevice, st));
+    u32* const own_w0 = c->bf.w[0];
+    if (alias) c->bf.w[0] = d_sub;
+    else
+        CK(cudaMemcpy2DAsync(c->bf.w[0], c->bf.stride * sizeof(u32), d_sub, (size_t)sub_stride * sizeof(u32),
+                             nview * sizeof(u32), (size_t)k + 1, cudaMemcpyDeviceToDevice, st));
+    struct Restore {
+        lbkd_ctx* c;
+        u32* w0;
+        ~Restore() { c->bf.w[0] = w0; }
+    } restore{c, own_w0};
     if (c->algo == 0 && lam0 > root_level) {
         CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
         CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
@@ -780,16 +792,75 @@ static int build_sub(lbkd_ctx* c, const u32* d_sub, int64_t sub_stride, int64_t 
         launch_root(bp, c->bf, c->minmax, st);
         prof_end(c, st, kPOther, 0.0);
     }
-    if (levels >= 0) {
-        const int stop = root_level + levels;
-        if ((rc = run_levels(c, bp, root_level, stop, st))) return rc;
-        if (prof_begin(c, st)) return LBKD_ECUDA;
-        launch_extract(bp, c->bf, stop, d_next, (u64)next_stride, c->algo == 0 ? ((stop - root_level) & 1) : -1, st);
-        prof_end(c, st, kPOther, 8.0 * (k + 1) * (double)level_points(bp, stop));
-        return end_build(c, st);
-    }
     if ((rc = run_levels(c, bp, root_level, lam0, st))) return rc;
     if ((rc = run_subtrees(c, bp, lam0, st))) return rc;
+    return end_build(c, st);
+}
+
+// Recursive halving step (multi-device): ONE level of the subtree rooted at
+// (root_level, root_index) -- from the raw AoS input at the root, else from
+// its packed points used in place as W[0] -- with d_next as W[1]: after it,
+// d_next holds the next level's working set in in-order layout, the left
+// child's points at [0, ss(2s+1)), the right child's after the node's slot.
+// No copies besides the level's own partition.
+static int build_split(lbkd_ctx* c, const float* d_points, u32* d_sub, int64_t stride, int64_t n_total, int k,
+                       int root_level, int64_t root_index, float* d_out, u32* d_perm, u32* d_next, cudaStream_t st) {
+    int rc = check_args(c, n_total, k, kRoundRobin);
+    if (rc) return rc;
+    c->launches = 0;
+    if (!d_out || !d_perm || !d_next || root_level < 0 || c->algo != 0) return LBKD_EINVAL_SHAPE;
+    if (root_level == 0 ? !d_points : !d_sub) return LBKD_EINVAL_SHAPE;
+    CK(cudaSetDevice(c->device));
+    const u64 n = (u64)n_total;
+    const int L = bit_length(n);
+    if (root_level > L - 1 || (u64)root_index >= (1ull << root_level)) return LBKD_EINVAL_SHAPE;
+    const int b = choose_bits(k, kRoundRobin);
+    const int lam0 = L - b > 0 ? L - b : 0;
+    if (root_level + 1 > lam0) return LBKD_EUNSUPPORTED;  // global levels only
+    const u64 nview = seg_size(make_geom(n, root_level), (u64)root_index);
+    if ((u64)stride < nview || !aliasable(d_next, stride) || (root_level > 0 && !aliasable(d_sub, stride)))
+        return LBKD_EINVAL_SHAPE;
+    rc = ensure(c, root_level == 0 ? n : (u64)stride, k, b, lam0 - root_level + 1, root_level == 0);
+    if (rc) return rc;
+    if (c->bf.stride != (u64)stride) return LBKD_EINVAL_SHAPE;  // root: stride must be ceil4(n)
+    BuildParams bp;
+    bp.n = n;
+    bp.k = k;
+    bp.mode = kRoundRobin;
+    bp.b = b;
+    bp.pts = d_points;
+    bp.out_pts = d_out;
+    bp.perm = d_perm;
+    bp.split_dims = c->dims_scratch;
+    bp.dbg = nullptr;
+    bp.lroot = root_level;
+    bp.jroot = (u64)root_index;
+    if ((rc = begin_order(c, st))) return rc;
+    if ((rc = begin_build(c, k, st))) return rc;
+    struct Restore {
+        lbkd_ctx* c;
+        u32* w0;
+        u32* w1;
+        ~Restore() {
+            c->bf.w[0] = w0;
+            c->bf.w[1] = w1;
+        }
+    } restore{c, c->bf.w[0], c->bf.w[1]};
+    c->bf.w[1] = d_next;
+    if (root_level == 0) {
+        if ((rc = prologue(c, bp, lam0, st))) return rc;  // AoS -> W[0], root box
+    } else {
+        c->bf.w[0] = d_sub;
+        CK(cudaMemsetAsync(c->minmax, 0xff, sizeof(u32) * k, st));
+        CK(cudaMemsetAsync(c->minmax + k, 0, sizeof(u32) * k, st));
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_view_minmax(bp, c->bf, c->minmax, nview, st);
+        prof_end(c, st, kPOther, 4.0 * k * (double)nview);
+        if (prof_begin(c, st)) return LBKD_ECUDA;
+        launch_root(bp, c->bf, c->minmax, st);
+        prof_end(c, st, kPOther, 0.0);
+    }
+    if ((rc = run_levels(c, bp, root_level, root_level + 1, st))) return rc;
     return end_build(c, st);
 }
 
@@ -1061,17 +1132,16 @@ int lbkd_build_rr_top(lbkd_ctx* c, const float* d_points, int64_t n, int k, int 
     return build_top(c, d_points, n, k, top_levels, d_out, d_perm, d_sub, sub_stride, (cudaStream_t)stream);
 }
 
-int lbkd_build_rr_sub(lbkd_ctx* c, const uint32_t* d_sub, int64_t sub_stride, int64_t n_total, int k,
+int lbkd_build_rr_sub(lbkd_ctx* c, uint32_t* d_sub, int64_t sub_stride, int64_t n_total, int k,
                       int root_level, int64_t root_index, float* d_out, uint32_t* d_perm, void* stream) {
-    return build_sub(c, d_sub, sub_stride, n_total, k, root_level, root_index, d_out, d_perm, -1, nullptr, 0,
-                     (cudaStream_t)stream);
+    return build_sub(c, d_sub, sub_stride, n_total, k, root_level, root_index, d_out, d_perm, (cudaStream_t)stream);
 }
 
-int lbkd_build_rr_split(lbkd_ctx* c, const uint32_t* d_sub, int64_t sub_stride, int64_t n_total, int k,
-                        int root_level, int64_t root_index, int levels, float* d_out, uint32_t* d_perm,
-                        uint32_t* d_next, int64_t next_stride, void* stream) {
-    return build_sub(c, d_sub, sub_stride, n_total, k, root_level, root_index, d_out, d_perm, levels, d_next,
-                     next_stride, (cudaStream_t)stream);
+int lbkd_build_rr_split(lbkd_ctx* c, const float* d_points, uint32_t* d_sub, int64_t stride, int64_t n_total, int k,
+                        int root_level, int64_t root_index, float* d_out, uint32_t* d_perm, uint32_t* d_next,
+                        void* stream) {
+    return build_split(c, d_points, d_sub, stride, n_total, k, root_level, root_index, d_out, d_perm, d_next,
+                       (cudaStream_t)stream);
 }
 
 int lbkd_update_tags_rr(uint32_t* d_tags, int64_t n, int levels, int l, void* stream) {

@@ -28,6 +28,8 @@
 // [ib(j), ib(j) + ss(j)) of W[(l - lfirst) & 1]; finished nodes leave a hole.
 #include "kernels.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 namespace lbkd {
@@ -508,15 +510,39 @@ __device__ __forceinline__ u32 rec_field(const u32* rec, const Chain& ch, int f,
     return f < (int)ch.m ? flip_key(__uint_as_float(rec[ch.d[f]])) : rec[k];
 }
 
-template <int NT>
+// CS > 1: a thread-block cluster of CS CTAs per segment (top levels, where a
+// few segments can hold millions of candidates -- tie-heavy or wide-range
+// data): every CTA scans 1/CS of the candidates; ranges and histograms are
+// combined in the rank-0 CTA's shared memory (DSMEM), one cluster barrier
+// per phase, and rank 0 alone writes the segment's results.
+template <int NT, int CS>
 __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
+    namespace cg = cooperative_groups;
     __shared__ u32 hist[256];
     __shared__ u32 red[2][32];
     __shared__ u32 s_misc[4];
     __shared__ u32 wtot[32];
+    __shared__ u32 c_mm[2][CS];  // rank 0: every CTA's candidate range
     __shared__ Chain s_ch;
-    const u64 j = blockIdx.x;
+    // the hardware's rank inside the cluster and the cluster's index (a 1-D
+    // grid of 1-D clusters: cluster c holds blocks c * CS .. c * CS + CS - 1)
+    u32 crank = 0u;
+    u64 j = blockIdx.x;
+    if constexpr (CS > 1) {
+        crank = cg::this_cluster().block_rank();
+        u32 cid;
+        asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        j = cid;
+    }
     const int k = a.k, R = k + 2, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto csync = [&]() {
+        if constexpr (CS > 1) cg::this_cluster().sync();
+    };
+    // rank 0's copy of a shared variable (DSMEM)
+    auto r0 = [&](auto* p) {
+        if constexpr (CS > 1) return cg::this_cluster().map_shared_rank(p, 0);
+        else return p;
+    };
     const LevelGeom& g = a.g;
     const u64 node = g.Fl + g.sbase + j;
     u32* sel = a.sel + j * kSelW;
@@ -524,7 +550,10 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
         if (a.mode == kRoundRobin) rr_chain(g.l, k, s_ch);
         else widest_chain(node, k, a.split_dims, s_ch);
     }
-    __syncthreads();
+    // (clusters: every CTA must have started before any touches another's
+    // shared memory)
+    if constexpr (CS > 1) csync();
+    else __syncthreads();
     const Chain ch = s_ch;
     // the segment's tiles: the first one holds it as part 1 unless the
     // segment starts exactly at the tile start
@@ -549,7 +578,7 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
         while (n > 1) {
             // live range of field f
             u32 mn = 0xffffffffu, mx = 0u;
-            for (u32 i = tid; i < n; i += NT) {
+            for (u32 i = tid + crank * NT; i < n; i += NT * CS) {
                 const u32 v = rec_field(src + (u64)i * R, ch, f, k);
                 mn = min(mn, v);
                 mx = max(mx, v);
@@ -563,19 +592,36 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
                 const u32 a0 = __reduce_min_sync(kFullMask, lane < NT / 32 ? red[0][lane] : 0xffffffffu);
                 const u32 b0 = __reduce_max_sync(kFullMask, lane < NT / 32 ? red[1][lane] : 0u);
                 if (lane == 0) {
-                    s_misc[0] = a0;
-                    s_misc[1] = b0;
+                    if constexpr (CS > 1) {
+                        r0(&c_mm[0][0])[crank] = a0;
+                        r0(&c_mm[1][0])[crank] = b0;
+                    } else {
+                        s_misc[0] = a0;
+                        s_misc[1] = b0;
+                    }
                 }
             }
-            __syncthreads();
-            mn = s_misc[0];
-            mx = s_misc[1];
+            if constexpr (CS > 1) {
+                csync();
+                mn = 0xffffffffu;
+                mx = 0u;
+#pragma unroll
+                for (int q = 0; q < CS; ++q) {
+                    mn = min(mn, r0(&c_mm[0][0])[q]);
+                    mx = max(mx, r0(&c_mm[1][0])[q]);
+                }
+            } else {
+                __syncthreads();
+                mn = s_misc[0];
+                mx = s_misc[1];
+            }
             if (mn == mx) break;  // field constant over the candidates
             const u32 sh = bucket_shift(mn, mx, 8);
-            for (u32 i = tid; i < n; i += NT)
+            for (u32 i = tid + crank * NT; i < n; i += NT * CS)
                 atomicAdd(&hist[(rec_field(src + (u64)i * R, ch, f, k) - mn) >> sh], 1u);
-            __syncthreads();
-            if (warp == 0) {
+            if constexpr (CS > 1) csync();  // every CTA's histogram is complete
+            else __syncthreads();
+            if (warp == 0 && crank == 0) {
                 // bucket holding rank r: 8 bins per lane, a warp scan of the
                 // lane sums, then the one lane whose range holds r walks its bins
                 u32 c[8];
@@ -583,6 +629,10 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     c[q] = hist[lane * 8 + q];
+                    if constexpr (CS > 1) {
+                        auto cl = cg::this_cluster();
+                        for (int rr = 1; rr < CS; ++rr) c[q] += cl.map_shared_rank(hist, rr)[lane * 8 + q];
+                    }
                     sum += c[q];
                 }
                 u32 x = sum;
@@ -594,24 +644,32 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
                 u32 cum = x - sum;
                 if (r >= cum && r < x) {
                     int bsel = -1;
+                    u32 bcnt = 0;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         if (bsel < 0) {
-                            if (cum + c[q] > r) bsel = lane * 8 + q;
-                            else cum += c[q];
+                            if (cum + c[q] > r) {
+                                bsel = lane * 8 + q;
+                                bcnt = c[q];
+                            } else {
+                                cum += c[q];
+                            }
                         }
                     }
                     s_misc[2] = (u32)bsel;
                     s_misc[3] = cum;
+                    s_misc[1] = bcnt;  // the bucket's count over every CTA of the cluster
                     s_misc[0] = 0u;  // compaction counter
                 }
             }
-            __syncthreads();
-            const u32 bsel = s_misc[2];
-            r -= s_misc[3];
-            const u32 cnt = hist[bsel];
+            if constexpr (CS > 1) csync();  // rank 0 picked the bucket
+            else __syncthreads();
+            const u32 bsel = *r0(&s_misc[2]);
+            r -= *r0(&s_misc[3]);
+            const u32 cnt = *r0(&s_misc[1]);
             u32* dst = bufs[nb_flip];
-            for (u32 i0 = 0; i0 < n; i0 += NT) {
+            u32* ctr = r0(&s_misc[0]);
+            for (u32 i0 = crank * NT; i0 < n; i0 += NT * CS) {
                 const u32 i = i0 + tid;
                 bool hit = false;
                 if (i < n) {
@@ -623,7 +681,7 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
                 if (m) {
                     const int leader = __ffs(m) - 1;
                     u32 base = 0;
-                    if (lane == leader) base = atomicAdd(&s_misc[0], (u32)__popc(m));
+                    if (lane == leader) base = atomicAdd(ctr, (u32)__popc(m));
                     base = __shfl_sync(kFullMask, base, leader);
                     if (hit) {
                         const u32* s = src + (u64)i * R;
@@ -632,11 +690,17 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
                     }
                 }
             }
-            __syncthreads();
+            if constexpr (CS > 1) csync();  // the compacted candidates are complete
+            else __syncthreads();
             src = dst;
             nb_flip ^= 1;
             n = cnt;
         }
+    }
+    if constexpr (CS > 1) {
+        // every CTA's below-pivot counts are in; rank 0 finishes the segment
+        csync();
+        if (crank != 0) return;
     }
     // src[0] is the node's point
     if (tid <= k) a.piv[j * (k + 1) + tid] = src[tid];
@@ -896,9 +960,11 @@ struct PHdr {
     u32 sl[2], tl[2], pp[2], y[2], d[2];  // d: the part's split dim (widest)
 };
 
-template <int KMAX, int D0>
-__global__ void __launch_bounds__(kPThreads, 2) sel_part_bulk_kernel(SelArgs a, int T) {
+// NST ring stages, MINB CTAs per SM (occupancy variants, LBKD_PART_CFG)
+template <int KMAX, int D0, int NST = kPStages, int MINB = 2>
+__global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs a, int T) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int kPStages = NST;
     const int lane = threadIdx.x & 31;
     const int k = a.k, A = k + 1;
     const LevelGeom& g = a.g;
@@ -1235,10 +1301,41 @@ void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
 void launch_sel_select(const SelArgs& a, int b, cudaStream_t st) {
     // few segments with many candidates (top levels): wide CTAs; many
     // segments with a few candidates (deep levels): narrow CTAs
+    // (the top levels' segments as clusters of CTAs: a segment can hold
+    // millions of candidates on tie-heavy or wide-range data)
     const unsigned g = (unsigned)a.g.nseg;
-    if (a.g.nseg <= 16) sel_select_kernel<1024><<<g, 1024, 0, st>>>(a, sel_tile(b));
-    else if (a.g.nseg >= 2048) sel_select_kernel<64><<<g, 64, 0, st>>>(a, sel_tile(b));
-    else sel_select_kernel<256><<<g, 256, 0, st>>>(a, sel_tile(b));
+    auto cluster_go = [&](auto kern, int nt, int cs) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g * (unsigned)cs);
+        cfg.blockDim = dim3((unsigned)nt);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, a, sel_tile(b));
+    };
+    // LBKD_SELECT_CLUSTER bit 0: clusters of 8 x 256 threads at nseg <= 16
+    // (4: of 4 x 1024), bit 1: clusters of 4 x 256 at nseg <= 128
+    static const int csel = [] {
+        const char* e = getenv("LBKD_SELECT_CLUSTER");
+        return e ? atoi(e) : 0;
+    }();
+    if (a.g.nseg <= 16) {
+        if (csel & 1) cluster_go(sel_select_kernel<256, 8>, 256, 8);
+        else if (csel & 4) cluster_go(sel_select_kernel<1024, 4>, 1024, 4);
+        else sel_select_kernel<1024, 1><<<g, 1024, 0, st>>>(a, sel_tile(b));
+    } else if (a.g.nseg <= 128 && (csel & 2)) {
+        cluster_go(sel_select_kernel<256, 4>, 256, 4);
+    } else if (a.g.nseg >= 2048) {
+        sel_select_kernel<64, 1><<<g, 64, 0, st>>>(a, sel_tile(b));
+    } else {
+        sel_select_kernel<256, 1><<<g, 256, 0, st>>>(a, sel_tile(b));
+    }
 }
 
 void launch_sel_part(const SelArgs& a0, int b, cudaStream_t st) {
@@ -1259,20 +1356,27 @@ void launch_sel_part(const SelArgs& a0, int b, cudaStream_t st) {
     if (grid > cap) grid = cap;
     // register-resident subtile: (KMAX + 1) x 8 words per lane
     const int d0 = a.mode == kRoundRobin ? a.g.l % a.k : -1;  // RR: every segment splits dim l mod k
-    auto bulk_go = [&](auto kern, int KM) {
-        const size_t sm = kPRingOff + sizeof(u32) * (size_t)(kPThreads / 32) * kPStages * (KM + 1) * kSub;
+    // LBKD_PART_CFG: 0 = 3 stages x 2 CTAs per SM (default), 1 = 2 stages x 3 CTAs per SM
+    static const int pcfg = [] {
+        const char* e = getenv("LBKD_PART_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    auto bulk_go = [&](auto kern, int KM, int nst = kPStages, int minb = 2) {
+        const size_t sm = kPRingOff + sizeof(u32) * (size_t)(kPThreads / 32) * nst * (KM + 1) * kSub;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         u64 g2 = (nsub + per_cta - 1) / per_cta;
-        if (g2 > 148ull * 2) g2 = 148ull * 2;  // two CTAs per SM, persistent
+        if (g2 > 148ull * minb) g2 = 148ull * minb;  // persistent: minb CTAs per SM
         kern<<<(unsigned)g2, kPThreads, sm, st>>>(a, T);
     };
+#define LBKD_PART_D(KM, D) \
+    if (pcfg == 1) bulk_go(sel_part_bulk_kernel<KM, D, 2, 3>, KM, 2, 3); else bulk_go(sel_part_bulk_kernel<KM, D>, KM)
 #define LBKD_PART(KM)                                                                          \
     switch (d0) {                                                                              \
-        case 0: bulk_go(sel_part_bulk_kernel<KM, 0>, KM); break;                               \
-        case 1: bulk_go(sel_part_bulk_kernel<KM, (KM > 1 ? 1 : 0)>, KM); break;                \
-        case 2: bulk_go(sel_part_bulk_kernel<KM, (KM > 2 ? 2 : 0)>, KM); break;                \
-        case 3: bulk_go(sel_part_bulk_kernel<KM, (KM > 3 ? 3 : 0)>, KM); break;                \
-        default: bulk_go(sel_part_bulk_kernel<KM, -1>, KM); break; /* widest: per-segment dims */ \
+        case 0: LBKD_PART_D(KM, 0); break;                                                     \
+        case 1: LBKD_PART_D(KM, (KM > 1 ? 1 : 0)); break;                                      \
+        case 2: LBKD_PART_D(KM, (KM > 2 ? 2 : 0)); break;                                      \
+        case 3: LBKD_PART_D(KM, (KM > 3 ? 3 : 0)); break;                                      \
+        default: LBKD_PART_D(KM, -1); break; /* widest: per-segment dims */                    \
     }
     switch (a.k) {
         case 1: LBKD_PART(1); break;
@@ -1285,6 +1389,7 @@ void launch_sel_part(const SelArgs& a0, int b, cudaStream_t st) {
             break;
     }
 #undef LBKD_PART
+#undef LBKD_PART_D
 }
 
 }  // namespace lbkd

@@ -80,7 +80,9 @@ __host__ __device__ inline SelLayout sel_layout(int b, int k) {
 
 size_t subtree_sel_smem_bytes(int b, int k) { return sel_layout(b, k).total; }
 
-enum { kSgSize = 0, kSgPo, kSgDim, kSgB, kSgR, kSgOff, kSgCnt, kSgFill, kSgPiv, kSgLo, kSgHi };  // kSgLo / kSgHi: bucketer (half lo, scale)
+// kSgLo / kSgHi: bucketer (half lo, scale); kSgDeg: the node box is a point
+// (every coordinate of every point in it is equal: the order is the input order)
+enum { kSgSize = 0, kSgPo, kSgDim, kSgB, kSgR, kSgOff, kSgCnt, kSgFill, kSgPiv, kSgLo, kSgHi, kSgDeg };
 
 // block-phase bucket of coordinate v in a segment (fp32, round-to-nearest
 // each step: monotone in v; NaN -> the top bucket)
@@ -290,6 +292,9 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             s[kSgLo] = __float_as_uint(hlo);
             s[kSgHi] = __float_as_uint(w > 0.0f ? __fdiv_rn((float)(2 * nbw), w) : 0.0f);
             s[kSgFill] = 0u;
+            u32 deg = 1u;
+            for (int c = 0; c < k; ++c) deg &= box[c] == box[k + c] ? 1u : 0u;
+            s[kSgDeg] = deg;
         }
         for (int i = tid; i < nloc * nbw; i += kSelThreads) hist[i] = 0u;
         __syncthreads();
@@ -390,6 +395,12 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 Chain wch;
                 bool have = false;
                 u32 rank = 0;
+                if (s[kSgDeg]) {  // identical points: the input order decides
+                    const u32 ii = idx_of(ci);
+                    for (u32 jj = 0; jj < C; ++jj) rank += idx_of(cand[off + jj]) < ii ? 1u : 0u;
+                    if (rank == s[kSgR]) s[kSgPiv] = ci;
+                    continue;
+                }
                 for (u32 jj = 0; jj < C; ++jj) {
                     const u32 cj = cand[off + jj];
                     const float kj = P[d * Mp + cj];
@@ -437,6 +448,8 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             bool lt;
             if (kp != kv) {
                 lt = kp < kv;
+            } else if (s[kSgDeg]) {
+                lt = idx_of((u32)p) < idx_of(piv);
             } else {
                 Chain wch;
                 if (a.mode == kWidest) widest_chain_of(hbase + t, dl, wch);

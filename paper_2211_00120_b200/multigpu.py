@@ -8,11 +8,12 @@ RECURSIVE HALVING instead of running on rank 0 alone:
 
     step i = 0 .. t-1: every rank r that holds a level-i subtree (r a
     multiple of h = G >> i; rank 0 starts with the whole input) builds ONE
-    level of it -- its node goes to the output -- keeps the left child and
-    ships the right child's points (k coordinate arrays + index array, in
-    the order the reference's sort leaves them) to rank r + h/2.
-    lbkd_build_rr_top does step 0 on the raw input, lbkd_build_rr_split the
-    later steps on packed points.
+    level of it with lbkd_build_rr_split -- its node goes to the output, its
+    points land in a fresh buffer in in-order layout, left child first --
+    keeps the left child where it is and ships the right child's points (k
+    coordinate arrays + index array, in the order the reference's sort leaves
+    them) to rank r + h/2.  No copies besides the level's own partition: the
+    packed buffers ARE the working sets (split and sub use them in place).
 
 Then every rank finishes its level-t subtree (lbkd_build_rr_sub) with the
 GLOBAL tree geometry (global node ids, pivot offsets, in-order positions),
@@ -35,6 +36,11 @@ import ctypes
 from dataclasses import dataclass
 
 from . import treemath
+
+
+def ceil4(x: int) -> int:
+    """Array stride of the packed buffers: whole 16-byte rows."""
+    return (x + 3) & ~3
 
 
 def top_levels_for(world: int) -> int:
@@ -114,10 +120,14 @@ class CudaOps:
                                         sub.data_ptr(), sub_stride, self._stream(stream))
         self.native.check(rc, "lbkd_build_rr_top")
 
-    def build_split(self, sub, sub_stride, n, k, level, j, levels, out, perm, nxt, next_stride, stream=None):
+    def build_split(self, points, sub, stride, n, k, level, j, out, perm, nxt, stream=None):
+        """One level of subtree (level, j): from ``points`` (raw, level 0) or
+        the packed ``sub``; ``nxt`` receives the children in in-order layout
+        (same stride)."""
         ctx = self.native.context(self.device)
-        rc = self.lib.lbkd_build_rr_split(ctx, sub.data_ptr(), sub_stride, n, k, level, j, levels, out.data_ptr(),
-                                          perm.data_ptr(), nxt.data_ptr(), next_stride, self._stream(stream))
+        rc = self.lib.lbkd_build_rr_split(ctx, points.data_ptr() if points is not None else None,
+                                          sub.data_ptr() if sub is not None else None, stride, n, k, level, j,
+                                          out.data_ptr(), perm.data_ptr(), nxt.data_ptr(), self._stream(stream))
         self.native.check(rc, "lbkd_build_rr_split")
 
     def build_sub(self, sub, sub_stride, n, k, top, j, out, perm, stream=None):
@@ -192,36 +202,29 @@ def build_round_robin_sharded(points, n: int, k: int, group=None, ops=None, devi
         builder.build_round_robin_cuda(points, out=out, perm=perm, check_finite=False)
         return out, perm
     # ---- recursive halving of the top t levels
-    cur = None          # packed points of the subtree this rank holds (k + 1 arrays, stride = its size)
-    cur_level, cur_j, cur_size = 0, 0, n
+    cur = None          # the subtree this rank holds: k + 1 arrays `stride` words apart
+    cur_level, cur_j, stride = 0, 0, ceil4(n)
     for i, step in enumerate(split_plan(world)):
         for (r, partner, level, j) in step:
             s = (1 << level) - 1 + j
-            size = treemath.subtree_size(s, n)
             lc = 2 * s + 1
             lsize = treemath.subtree_size(lc, n) if lc < n else 0
             rsize = treemath.subtree_size(lc + 1, n) if lc + 1 < n else 0
             if rank == r:
-                nxt = buf(f"split{i}", ((k + 1) * size,), torch.int32)
-                if level == 0:
-                    ops.build_top(points, 1, out, perm, nxt, size)
-                else:
-                    ops.build_split(cur, cur_size, n, k, level, j, 1, out, perm, nxt, size)
-                # right child: packed after the left one in every array
-                sends = [(nxt[c * size + lsize:c * size + lsize + rsize], partner) for c in range(k + 1)]
+                nxt = buf(f"split{i}", ((k + 1) * stride,), torch.int32)
+                ops.build_split(points if level == 0 else None, cur, stride, n, k, level, j, out, perm, nxt)
+                # the right child sits after the node's slot in every array
+                sends = [(nxt[c * stride + lsize + 1:c * stride + lsize + 1 + rsize], partner) for c in range(k + 1)]
                 tr.exchange(sends, [])
-                # keep the left child (strided view -> its own contiguous buffer)
-                keep = buf(f"keep{i}", ((k + 1) * max(lsize, 1),), torch.int32)
-                for c in range(k + 1):
-                    keep[c * lsize:(c + 1) * lsize].copy_(nxt[c * size:c * size + lsize])
-                cur, cur_level, cur_j, cur_size = keep, level + 1, 2 * j, lsize
+                cur, cur_level, cur_j = nxt, level + 1, 2 * j  # the left child stays in place
             elif rank == partner:
-                recv = buf(f"recv{i}", ((k + 1) * max(rsize, 1),), torch.int32)
-                tr.exchange([], [(recv[c * rsize:(c + 1) * rsize], r) for c in range(k + 1)])
-                cur, cur_level, cur_j, cur_size = recv, level + 1, 2 * j + 1, rsize
+                rstride = ceil4(rsize)
+                recv = buf(f"recv{i}", ((k + 1) * rstride,), torch.int32)
+                tr.exchange([], [(recv[c * rstride:c * rstride + rsize], r) for c in range(k + 1)])
+                cur, cur_level, cur_j, stride = recv, level + 1, 2 * j + 1, rstride
     # ---- every rank finishes its level-t subtree
     assert cur_level == t and cur_j == rank
-    ops.build_sub(cur, cur_size, n, k, t, rank, out, perm)
+    ops.build_sub(cur, stride, n, k, t, rank, out, perm)
     # ---- gather at rank 0: subtree node ranges + the single split nodes
     if rank == 0:
         recvs = []
@@ -247,10 +250,10 @@ def build_round_robin_sharded(points, n: int, k: int, group=None, ops=None, devi
 
 def serial_sharded_build(points, n: int, k: int, world: int, ops=None, out=None, perm=None, timer=None):
     """The whole protocol of build_round_robin_sharded run rank by rank in
-    ONE process on one device (no transport): the same kernels and packed
-    buffers, so the result must equal the single-GPU build.  ``timer(label,
-    fn)`` may wrap every device call (tools/big_build.py times each piece to
-    project the multi-GPU critical path).  Returns (out, perm)."""
+    ONE process on one device (no transport): the same kernels and buffers,
+    so the result must equal the single-GPU build.  ``timer(label, fn)`` may
+    wrap every device call (tools/big_build.py times each piece to project
+    the multi-GPU critical path).  Returns (out, perm)."""
     import torch
 
     dev = points.device
@@ -262,29 +265,24 @@ def serial_sharded_build(points, n: int, k: int, world: int, ops=None, out=None,
     if perm is None:
         perm = torch.empty(n, dtype=torch.int32, device=dev)
     run = timer or (lambda label, fn: fn())
-    held = {0: (None, n)}  # rank -> (packed points, size)
+    held = {0: (None, ceil4(n))}  # rank -> (its subtree's buffer, stride)
     for i, step in enumerate(split_plan(world)):
         for (r, partner, level, j) in step:
             s = (1 << level) - 1 + j
-            size = treemath.subtree_size(s, n)
             lc = 2 * s + 1
             lsize = treemath.subtree_size(lc, n) if lc < n else 0
             rsize = treemath.subtree_size(lc + 1, n) if lc + 1 < n else 0
-            nxt = torch.empty((k + 1) * size, dtype=torch.int32, device=dev)
-            cur, cur_size = held[r]
-            if level == 0:
-                run(f"split{i}/r{r}", lambda: ops.build_top(points, 1, out, perm, nxt, size))
-            else:
-                run(f"split{i}/r{r}",
-                    lambda: ops.build_split(cur, cur_size, n, k, level, j, 1, out, perm, nxt, size))
-            left = torch.empty((k + 1) * max(lsize, 1), dtype=torch.int32, device=dev)
-            right = torch.empty((k + 1) * max(rsize, 1), dtype=torch.int32, device=dev)
-            for c in range(k + 1):
-                left[c * lsize:(c + 1) * lsize].copy_(nxt[c * size:c * size + lsize])
-                right[c * rsize:(c + 1) * rsize].copy_(nxt[c * size + lsize:c * size + lsize + rsize])
-            held[r] = (left, lsize)
-            held[partner] = (right, rsize)
+            cur, stride = held[r]
+            nxt = torch.empty((k + 1) * stride, dtype=torch.int32, device=dev)
+            run(f"split{i}/r{r}", lambda: ops.build_split(points if level == 0 else None, cur, stride, n, k, level, j,
+                                                          out, perm, nxt))
+            rstride = ceil4(rsize)
+            right = torch.empty((k + 1) * rstride, dtype=torch.int32, device=dev)
+            for c in range(k + 1):  # (the transfer to the partner rank)
+                right[c * rstride:c * rstride + rsize].copy_(nxt[c * stride + lsize + 1:c * stride + lsize + 1 + rsize])
+            held[r] = (nxt, stride)
+            held[partner] = (right, rstride)
     for r in range(world):
-        sub, size = held[r]
-        run(f"sub/r{r}", lambda: ops.build_sub(sub, size, n, k, t, r, out, perm))
+        sub, stride = held[r]
+        run(f"sub/r{r}", lambda: ops.build_sub(sub, stride, n, k, t, r, out, perm))
     return out, perm

@@ -50,24 +50,18 @@ def _stamp(level, j, c, i):
 
 
 class FakeOps:
-    """Stamps every packed value with (level, subtree, array, position) and
-    every node with its own id, and checks each stamp where it is consumed."""
+    """Stamps every point value with (level, subtree, array, position) and
+    every node with its own id, and checks each stamp where it is consumed
+    (the real layout: split writes the children in in-order layout, left
+    child first, one slot for the node, then the right child)."""
 
     def __init__(self, rank):
         self.rank = rank
 
-    def _pack_children(self, n, k, level, j, nxt, stride):
-        s = (1 << level) - 1 + j
-        lc = 2 * s + 1
-        off = 0
-        for child, cj in ((lc, 2 * j), (lc + 1, 2 * j + 1)):
-            if child >= n:
-                continue
-            size = treemath.subtree_size(child, n)
-            i = torch.arange(size)
-            for c in range(k + 1):
-                nxt[c * stride + off:c * stride + off + size] = _stamp(level + 1, cj, c, i)
-            off += size
+    def _fill(self, buf, stride, k, level, j, size, off=0):
+        i = torch.arange(size)
+        for c in range(k + 1):
+            buf[c * stride + off:c * stride + off + size] = _stamp(level, j, c, i)
 
     def _place(self, out, perm, node):
         perm[node] = node
@@ -80,17 +74,20 @@ class FakeOps:
             got = sub[c * stride:c * stride + size]
             assert torch.equal(got, _stamp(level, j, c, i).to(torch.int32)), (self.rank, level, j, c)
 
-    def build_top(self, points, top, out, perm, sub, stride):
-        n, k = points.shape
-        assert top == 1
-        self._place(out, perm, 0)
-        self._pack_children(n, k, 0, 0, sub, stride)
-
-    def build_split(self, sub, stride, n, k, level, j, levels, out, perm, nxt, next_stride):
-        assert levels == 1
-        self._check(sub, stride, n, k, level, j)
-        self._place(out, perm, (1 << level) - 1 + j)
-        self._pack_children(n, k, level, j, nxt, next_stride)
+    def build_split(self, points, sub, stride, n, k, level, j, out, perm, nxt):
+        assert stride % 4 == 0
+        if level == 0:
+            assert points is not None and stride == multigpu.ceil4(n)
+        else:
+            self._check(sub, stride, n, k, level, j)
+        s = (1 << level) - 1 + j
+        self._place(out, perm, s)
+        lc = 2 * s + 1
+        lsize = treemath.subtree_size(lc, n) if lc < n else 0
+        if lc < n:
+            self._fill(nxt, stride, k, level + 1, 2 * j, lsize)
+        if lc + 1 < n:
+            self._fill(nxt, stride, k, level + 1, 2 * j + 1, treemath.subtree_size(lc + 1, n), off=lsize + 1)
 
     def build_sub(self, sub, stride, n, k, top, j, out, perm):
         self._check(sub, stride, n, k, top, j)

@@ -70,6 +70,7 @@ step_degen() {  # ncu launch lists of adversarial 10M builds (where the time goe
 }
 step_knobs() {  # per-class times of 100M builds under tuning switches (KNOBS overrides the list)
   python tools/knobs.py 100000000 3 rr uniform -- ${KNOBS:-"" LBKD_SUBTREE_BITS=11 LBKD_SUBTREE=sel}
+  python tools/knobs.py 100000000 3 widest clustered -- ${KNOBS:-"" LBKD_SUBTREE_BITS=11 LBKD_SUBTREE=sel}
 }
 step_big() { timeout 900 python tools/big_build.py 1000000000 clustered 3 > gpurun_out/big_1b.log 2>&1; tail -1 gpurun_out/big_1b.log | cut -c1-600; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv,noheader

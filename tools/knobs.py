@@ -15,8 +15,8 @@ sys.path.insert(0, sys.argv[1] + "/tools")
 import paper_2211_00120_b200 as kd
 from paper_2211_00120_b200 import _native, datagen
 n, k, mode, kind = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
-from one_build import ADV
-pts = ADV[kind](n, k) if kind in ADV else datagen.make(kind, n, k, seed=0)
+from adv import make
+pts = make(kind, n, k)
 d = torch.from_numpy(pts).cuda(); out = torch.empty_like(d); perm = torch.empty(n, dtype=torch.int32, device="cuda")
 f = (lambda: kd.build_round_robin_cuda(d, out=out, perm=perm, check_finite=False)) if mode == "rr" else \
     (lambda: kd.build_widest_cuda(d, out=out, perm=perm, check_finite=False))
@@ -45,8 +45,13 @@ if __name__ == "__main__":
         for kv in filter(None, v.split(",")):
             a, b = kv.split("=", 1)
             env[a] = b
-        r = subprocess.run([sys.executable, "-c", CHILD, root, n, k, mode, kind], env=env, capture_output=True,
-                           text=True, timeout=600)
+        try:
+            r = subprocess.run([sys.executable, "-c", CHILD, root, n, k, mode, kind], env=env, capture_output=True,
+                               text=True, timeout=int(os.environ.get("KNOBS_TIMEOUT", "180")))
+        except subprocess.TimeoutExpired:
+            print(json.dumps({"variant": v or "default", "n": int(n), "mode": mode, "kind": kind, "error": "timeout"}),
+                  flush=True)
+            continue
         line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
         res = json.loads(line[0][7:]) if line else {"error": (r.stderr or r.stdout)[-400:]}
         print(json.dumps({"variant": v or "default", "n": int(n), "k": int(k), "mode": mode, "kind": kind, **res}),

@@ -3,6 +3,7 @@ import sys
 import numpy as np
 import torch
 sys.path.insert(0, __file__.rsplit('/tools/', 1)[0])
+sys.path.insert(0, __file__.rsplit('/', 1)[0])
 import paper_2211_00120_b200 as kd
 from paper_2211_00120_b200 import datagen
 
@@ -11,13 +12,9 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 mode = sys.argv[3] if len(sys.argv) > 3 else "rr"
 kind = sys.argv[4] if len(sys.argv) > 4 else "uniform"
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 2
-ADV = {  # adversarial inputs of tools/robust_time.py
-    "identical": lambda n, k: np.full((n, k), 0.25, np.float32),
-    "huge": lambda n, k: (10.0 ** np.random.default_rng(4).uniform(-30, 30, (n, k))).astype(np.float32),
-    "constaxis": lambda n, k: np.c_[datagen.uniform(n, k - 1, seed=3), np.zeros(n, np.float32)],
-    "sorted": lambda n, k: np.sort(datagen.uniform(n, k, seed=2), axis=0),
-}
-pts = ADV[kind](n, k) if kind in ADV else datagen.make(kind, n, k, seed=0)
+from adv import make  # noqa: E402
+
+pts = make(kind, n, k)
 d = torch.from_numpy(pts).cuda()
 out = torch.empty_like(d); perm = torch.empty(n, dtype=torch.int32, device="cuda")
 for _ in range(reps):
