@@ -100,7 +100,7 @@ def load():
         lib.lbkd_build_rr_top.restype = i32
         lib.lbkd_build_rr_sub.argtypes = [vp, vp, i64, i64, i32, i32, i64, vp, vp, vp]
         lib.lbkd_build_rr_sub.restype = i32
-        lib.lbkd_build_rr_split.argtypes = [vp, vp, i64, i64, i32, i32, i64, i32, vp, vp, vp, i64, vp]
+        lib.lbkd_build_rr_split.argtypes = [vp, vp, vp, i64, i64, i32, i32, i64, vp, vp, vp, vp]
         lib.lbkd_build_rr_split.restype = i32
         lib.lbkd_update_tags_rr.argtypes = [vp, i64, i32, i32, vp]
         lib.lbkd_update_tags_rr.restype = i32

@@ -1,13 +1,19 @@
 // capi.cu -- C ABI and host orchestration (see include/lbkd_b200.h).
 //
 // One build = the reference's loop (builder.py:224-232) re-cut for B200:
-//   global levels l = 0 .. lam0-1  (segments larger than a CTA can hold)
-//       rekey+histogram -> plan -> up to 4 onesweep digit passes, the last
-//       one fused with updateTags (pivot -> node, others -> child segment)
-//   in-CTA levels lam0 .. L-2      (one CTA per level-lam0 subtree)
-//       subtree_kernel: all remaining levels in shared memory
-// Everything is enqueued on the caller's stream with device-side plans, so
-// the only host synchronisation is the final non-finite check.
+//   prologue                     AoS -> SoA working set W[0], non-finite flag,
+//                                world box / root dim (init_stats + root)
+//   global levels 0 .. lam0-1    per level (select.cu): hist -> pick ->
+//                                filter -> select -> stable 3-way partition
+//                                (segments larger than one CTA can hold)
+//   in-CTA levels lam0 .. L-1    one CTA per level-lam0 subtree finishes it in
+//                                shared memory (subtree.cu / subtree_sel.cu)
+// LBKD_ALGO=sort swaps the global levels for the literal per-level segmented
+// radix sort (global_sort.cu).  Everything is enqueued on the caller's stream
+// with device-side plans and replayed as a CUDA graph when repeated; the
+// only host synchronisation is the final non-finite check.  Builds on one
+// context are ordered by an event (they share its scratch).  Float64 input
+// goes through rank64.cu first (lbkd_build_*_f64).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>

@@ -12,15 +12,21 @@
 // reference's arrangement is observable: the next level orders its nodes by
 // a total order of its own.  So one level is
 //   hist   : per-segment histogram of the key c[dim] in 2^D equal-width
-//            buckets over the segment's exact [min, max] (HBM read 4 B/pt)
+//            buckets over the node's box (levels < 6; from level 6 on it is
+//            fused into the previous level's partition)   (HBM read 4 B/pt)
 //   pick   : bucket holding rank pivot_off, rank inside it     (per segment)
-//   filter : the elements of that bucket -> candidate records  (4 B/pt)
-//   select : radix select over the candidates' composite key (k coords +
-//            index) -> the node's point, written to its level-order slot
+//   filter : the elements of that bucket -> candidate records, per-tile and
+//            per-subtile counts of the elements below it      (4 B/pt)
+//   select : radix select over the candidates' composite key (chain coords +
+//            index) -> the node's point, written to its level-order slot;
+//            the tile counts become per-segment exclusive prefixes.  The top
+//            levels run each segment on a thread-block CLUSTER (DSMEM
+//            merges), so millions of candidates (tie-heavy / wide-range
+//            data) do not serialise on one SM
 //   part   : stable 3-way partition of every segment around its pivot
-//            (read + write k coords + index = 8(k+1) B/pt, decoupled
-//            lookback for the per-segment prefix), fused with the exact
-//            [min, max] of the children's next key
+//            (read + write k coords + index = 8(k+1) B/pt through a TMA-fed
+//            shared-memory ring per warp; destinations from the select's
+//            prefixes, no lookback), fused with the next level's histogram
 // The partition is stable, so every segment keeps the INPUT order of its
 // points; the in-CTA phase (subtree.cu) derives its chain orders from that.
 //
@@ -522,7 +528,12 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
     __shared__ u32 red[2][32];
     __shared__ u32 s_misc[4];
     __shared__ u32 wtot[32];
-    __shared__ u32 c_mm[2][CS];  // rank 0: every CTA's candidate range
+    // rank 0: every CTA's candidate range, double-buffered by round: a round
+    // that ends right after reading it (constant field -> break) has no
+    // further cluster barrier, so a fast CTA's next write must not land in
+    // the buffer a slow CTA is still reading
+    __shared__ u32 c_mm[2][2][CS];
+    int mm_buf = 0;
     __shared__ Chain s_ch;
     // the hardware's rank inside the cluster and the cluster's index (a 1-D
     // grid of 1-D clusters: cluster c holds blocks c * CS .. c * CS + CS - 1)
@@ -593,8 +604,8 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
                 const u32 b0 = __reduce_max_sync(kFullMask, lane < NT / 32 ? red[1][lane] : 0u);
                 if (lane == 0) {
                     if constexpr (CS > 1) {
-                        r0(&c_mm[0][0])[crank] = a0;
-                        r0(&c_mm[1][0])[crank] = b0;
+                        r0(&c_mm[mm_buf][0][0])[crank] = a0;
+                        r0(&c_mm[mm_buf][1][0])[crank] = b0;
                     } else {
                         s_misc[0] = a0;
                         s_misc[1] = b0;
@@ -607,9 +618,10 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
                 mx = 0u;
 #pragma unroll
                 for (int q = 0; q < CS; ++q) {
-                    mn = min(mn, r0(&c_mm[0][0])[q]);
-                    mx = max(mx, r0(&c_mm[1][0])[q]);
+                    mn = min(mn, r0(&c_mm[mm_buf][0][0])[q]);
+                    mx = max(mx, r0(&c_mm[mm_buf][1][0])[q]);
                 }
+                mm_buf ^= 1;
             } else {
                 __syncthreads();
                 mn = s_misc[0];
@@ -1319,15 +1331,15 @@ void launch_sel_select(const SelArgs& a, int b, cudaStream_t st) {
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, kern, a, sel_tile(b));
     };
-    // LBKD_SELECT_CLUSTER bit 0: clusters of 8 x 256 threads at nseg <= 16
-    // (4: of 4 x 1024), bit 1: clusters of 4 x 256 at nseg <= 128
+    // LBKD_SELECT_CLUSTER (default 6): bit 2 -- clusters of 4 x 1024 threads
+    // at nseg <= 16, bit 1 -- clusters of 4 x 256 at nseg <= 128; 0 = one
+    // CTA per segment everywhere.  (Clusters of 8 measured unreliable here.)
     static const int csel = [] {
         const char* e = getenv("LBKD_SELECT_CLUSTER");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 6;
     }();
     if (a.g.nseg <= 16) {
-        if (csel & 1) cluster_go(sel_select_kernel<256, 8>, 256, 8);
-        else if (csel & 4) cluster_go(sel_select_kernel<1024, 4>, 1024, 4);
+        if (csel & 4) cluster_go(sel_select_kernel<1024, 4>, 1024, 4);
         else sel_select_kernel<1024, 1><<<g, 1024, 0, st>>>(a, sel_tile(b));
     } else if (a.g.nseg <= 128 && (csel & 2)) {
         cluster_go(sel_select_kernel<256, 4>, 256, 4);
@@ -1356,11 +1368,6 @@ void launch_sel_part(const SelArgs& a0, int b, cudaStream_t st) {
     if (grid > cap) grid = cap;
     // register-resident subtile: (KMAX + 1) x 8 words per lane
     const int d0 = a.mode == kRoundRobin ? a.g.l % a.k : -1;  // RR: every segment splits dim l mod k
-    // LBKD_PART_CFG: 0 = 3 stages x 2 CTAs per SM (default), 1 = 2 stages x 3 CTAs per SM
-    static const int pcfg = [] {
-        const char* e = getenv("LBKD_PART_CFG");
-        return e ? atoi(e) : 0;
-    }();
     auto bulk_go = [&](auto kern, int KM, int nst = kPStages, int minb = 2) {
         const size_t sm = kPRingOff + sizeof(u32) * (size_t)(kPThreads / 32) * nst * (KM + 1) * kSub;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1368,8 +1375,7 @@ void launch_sel_part(const SelArgs& a0, int b, cudaStream_t st) {
         if (g2 > 148ull * minb) g2 = 148ull * minb;  // persistent: minb CTAs per SM
         kern<<<(unsigned)g2, kPThreads, sm, st>>>(a, T);
     };
-#define LBKD_PART_D(KM, D) \
-    if (pcfg == 1) bulk_go(sel_part_bulk_kernel<KM, D, 2, 3>, KM, 2, 3); else bulk_go(sel_part_bulk_kernel<KM, D>, KM)
+#define LBKD_PART_D(KM, D) bulk_go(sel_part_bulk_kernel<KM, D>, KM)
 #define LBKD_PART(KM)                                                                          \
     switch (d0) {                                                                              \
         case 0: LBKD_PART_D(KM, 0); break;                                                     \

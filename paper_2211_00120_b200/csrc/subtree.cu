@@ -776,7 +776,22 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                     v += rs[i];
                 }
             }
-            const u32 ex = block_exclusive_scan<u32>(v, scratch, nullptr);
+            u32 ex;
+            if (nloc <= 32) {  // every segment is in warp 0: a warp scan, no block barriers
+                if (warp == 0) {
+                    u32 x = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const u32 y = __shfl_up_sync(kFullMask, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    ex = x - v;
+                } else {
+                    ex = 0u;  // (no segments on the other warps)
+                }
+            } else {
+                ex = block_exclusive_scan<u32>(v, scratch, nullptr);
+            }
             u32 run = ex;
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -955,7 +970,8 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                 // begins at sb in every list
                 const u32 key = (act && l2 <= L - 2) ? (u32)LB[rko[l2 % k] + lid] - sb : 0u;
                 // the keys (segment-local ranks < 31) present in my node as
-                // a bit set: one segmented OR over the node's lanes
+                // a bit set: one segmented OR over the node's lanes (measured
+                // faster than a bit-serial compare over warp-wide ballots)
                 u32 rank = 0;
                 if (act) {
                     const u32 keys = __reduce_or_sync(eq, 1u << key);

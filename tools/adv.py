@@ -8,6 +8,8 @@ ADV = {
     "huge": lambda n, k: (10.0 ** np.random.default_rng(4).uniform(-30, 30, (n, k))).astype(np.float32),
     "constaxis": lambda n, k: np.c_[datagen.uniform(n, k - 1, seed=3), np.zeros(n, np.float32)],
     "sorted": lambda n, k: np.sort(datagen.uniform(n, k, seed=2), axis=0),
+    # float64 input (the reference's own dtype): the lbkd_build_*_f64 path
+    "uniform64": lambda n, k: np.random.default_rng(0).random((n, k)),
 }
 
 

@@ -14,6 +14,7 @@
 #   full       ncu --set full captures of the partition / in-CTA / filter kernels
 #   robust     tools/robust_time.py + tools/quick_time.py
 #   degen      ncu launch lists of adversarial 10M builds (identical, huge range, constant axis, ties)
+#   evidence   the round's committed evidence (launch lists, ncu captures, robustness and config timings)
 #   knobs      tools/knobs.py: per-kernel-class times under env variants ($KNOBS)
 #   big        tools/big_build.py (1B clustered, sharded decomposition on one GPU)
 # Env: TEST_ARGS (extra pytest args), KSEL (ncu kernel regex for `full`, default all three)
@@ -71,6 +72,40 @@ step_degen() {  # ncu launch lists of adversarial 10M builds (where the time goe
 step_knobs() {  # per-class times of 100M builds under tuning switches (KNOBS overrides the list)
   python tools/knobs.py 100000000 3 rr uniform -- ${KNOBS:-"" LBKD_SUBTREE_BITS=11 LBKD_SUBTREE=sel}
   python tools/knobs.py 100000000 3 widest clustered -- ${KNOBS:-"" LBKD_SUBTREE_BITS=11 LBKD_SUBTREE=sel}
+}
+step_evidence() {  # the round's committed evidence -> gpurun_out/r02_* (copied to profiles/ by hand)
+  R=gpurun_out/r02
+  L=$(python tools/one_build.py 100000000 3 rr uniform 1 | awk '/launches per build/{print $4}')
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s $L -c $L --csv --log-file ${R}_launches_100m_float3.csv python tools/one_build.py 100000000 3 rr uniform 2 > /dev/null 2>&1
+  python tools/launches.py ${R}_launches_100m_float3.csv > ${R}_launches_100m_float3.txt
+  python tools/ncu_traffic.py ${R}_launches_100m_float3.csv ${R}_ncu_traffic.json > /dev/null
+  L=$(python tools/one_build.py 100000000 3 widest clustered 1 | awk '/launches per build/{print $4}')
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s $L -c $L --csv --log-file ${R}_launches_100m_clustered_widest.csv python tools/one_build.py 100000000 3 widest clustered 2 > /dev/null 2>&1
+  python tools/launches.py ${R}_launches_100m_clustered_widest.csv > ${R}_launches_100m_clustered_widest.txt
+  python tools/ncu_traffic.py ${R}_launches_100m_clustered_widest.csv ${R}_ncu_traffic_widest.json > /dev/null
+  for ks in sel_part subtree sel_filter; do
+    skip=0; [ "$ks" = sel_part ] && skip=4; [ "$ks" = sel_filter ] && skip=6
+    ncu --set full --clock-control none --import-source on -k regex:$ks -s $skip -c 1 -o ${R}_full_$ks python tools/one_build.py 100000000 3 rr uniform 1 > /dev/null 2>&1
+    python tools/ncu_summary.py ${R}_full_$ks.ncu-rep > ${R}_ncu_full_$ks.txt 2>&1
+    python tools/ncu_lines.py ${R}_full_$ks.ncu-rep 60 > ${R}_ncu_lines_$ks.txt 2>&1
+  done
+  python tools/ncu_issue.py ${R}_full_subtree.ncu-rep ${R}_ncu_issue_subtree.json > /dev/null 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:subtree -c 1 -o ${R}_full_subsel_widest python tools/one_build.py 100000000 3 widest clustered 1 > /dev/null 2>&1
+  python tools/ncu_summary.py ${R}_full_subsel_widest.ncu-rep > ${R}_ncu_full_subsel_widest.txt 2>&1
+  python tools/ncu_issue.py ${R}_full_subsel_widest.ncu-rep ${R}_ncu_issue_subtree_widest.json > /dev/null 2>&1
+  rm -f ${R}_full_*.ncu-rep
+  { for kind in uniform clustered identical huge constaxis ties sorted; do
+      KNOBS_TIMEOUT=120 python tools/knobs.py 10000000 3 rr $kind -- ""; KNOBS_TIMEOUT=120 python tools/knobs.py 10000000 3 widest $kind -- ""
+    done; KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 3 rr ties -- ""; } > ${R}_robust_knobs.txt 2>&1
+  { KNOBS_TIMEOUT=300 python tools/knobs.py 100000000 3 rr uniform -- "" LBKD_ALGO=sort LBKD_SELECT_CLUSTER=0
+    KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 2 rr uniform -- ""
+    KNOBS_TIMEOUT=120 python tools/knobs.py 10000000 4 rr uniform -- ""
+    KNOBS_TIMEOUT=120 python tools/knobs.py 1000000 3 rr uniform -- ""
+    KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 3 widest clustered -- ""
+    KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 3 rr clustered -- ""
+    KNOBS_TIMEOUT=300 python tools/knobs.py 100000000 3 rr uniform64 -- ""
+    KNOBS_TIMEOUT=300 python tools/knobs.py 10000000 4 rr uniform64 -- ""; } > ${R}_configs_knobs.txt 2>&1
+  cat ${R}_launches_100m_float3.txt | head -20
 }
 step_big() { timeout 900 python tools/big_build.py 1000000000 clustered 3 > gpurun_out/big_1b.log 2>&1; tail -1 gpurun_out/big_1b.log | cut -c1-600; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv,noheader
