@@ -363,16 +363,21 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # clocks sampled from before the warm-up (nvidia-smi needs ~1 s to start)
+    # through the timed region
+    sampler = ClockSampler()
+    sampler.start()
+    time.sleep(1.0)
+    # profiling on from the warm-up: every kernel launch is bracketed by CUDA
+    # events on the build stream, captured with the build into its CUDA graph
+    # (event-record nodes), so the per-kernel device times below are those of
+    # the LAST timed build, inside the timed region, without host launch gaps
+    _native.set_profile(True, local)
     for _ in range(args.warmup):
         build(d_pts, out, perm)
     launches = kd.builder.last_launch_count(local)
 
-    # ---- device-resident timed region (profiling events on the build stream:
-    # each kernel launch of the LAST timed build is bracketed, so the
-    # per-kernel device times below come from inside the timed region)
-    _native.set_profile(True, local)
-    sampler = ClockSampler()
-    sampler.start()
+    # ---- device-resident timed region
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)

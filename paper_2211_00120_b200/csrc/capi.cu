@@ -141,13 +141,16 @@ static int prof_begin(lbkd_ctx* c, cudaStream_t st) {
         if (cudaEventCreate(&e) != cudaSuccess) return 1;
         c->ev.push_back(e);
     }
-    cudaEventRecord(c->ev[c->n_ev_used], st);
+    // external record: inside a stream capture the event becomes a real
+    // event-record node of the graph, so a replayed graph times its kernels
+    // back to back (no host launch gaps inside the brackets)
+    cudaEventRecordWithFlags(c->ev[c->n_ev_used], st, cudaEventRecordExternal);
     return 0;
 }
 static void prof_end(lbkd_ctx* c, cudaStream_t st, int cls, double bytes) {
     c->launches += 1;
     if (!c->profile) return;
-    cudaEventRecord(c->ev[c->n_ev_used + 1], st);
+    cudaEventRecordWithFlags(c->ev[c->n_ev_used + 1], st, cudaEventRecordExternal);
     const int i = c->n_ev_used / 2;
     if ((int)c->ev_cls.size() <= i) {
         c->ev_cls.resize(i + 1);
@@ -563,11 +566,10 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     // the select path is a fixed, host-sync-free sequence for given buffers:
     // capture it once into a CUDA graph and replay it (the sort path carries
     // per-launch lookback epochs and is always launched directly)
-    // (profiled builds launch directly: event timing of graph-recorded events
-    // is not available)
     // (value-table builds carry their table in the kernel arguments: never graphed)
-    const bool graphable =
-        c->use_graph && c->algo == 0 && !c->profile && !d_trace && bp.pts == d_points && !bp.wt.v;
+    // (profiled builds are graphed too: their event brackets are event-record
+    // nodes, and a replay times the kernels of THAT replay)
+    const bool graphable = c->use_graph && c->algo == 0 && !d_trace && bp.pts == d_points && !bp.wt.v;
     lbkd_ctx::GraphKey key{d_points, d_out, d_perm, d_dims, c->bf.err, n_in, k, mode, c->algo, bp.subtree_sel, c->check,
                            c->profile};
     lbkd_ctx::GraphEntry* hit = nullptr;

@@ -370,4 +370,24 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T* total) {
     return r;
 }
 
+// Exclusive block scan with ONE barrier: warp scans, lane 31 publishes its
+// warp's total into buf[warp], one barrier, then every thread adds the totals
+// of the warps before its own (broadcast loads).  buf (32 entries) must not
+// be written again before the caller's next barrier.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan_1b(T v, T* buf) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) buf[warp] = x;
+    __syncthreads();
+    T pre = T(0);
+    for (int w = 0; w < warp; ++w) pre += buf[w];
+    return pre + x - v;
+}
+
 }  // namespace lbkd

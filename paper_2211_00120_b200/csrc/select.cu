@@ -388,27 +388,38 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
 // part index of both is relative to the TILE's first segment.
 // ---------------------------------------------------------------------------
 constexpr int kSub = 256;  // positions per warp subtile (32 lanes x 8 rows)
+constexpr int kFCap = 256;  // filter: candidate records staged per CTA
 
 template <int THREADS>
-__global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
+__global__ void __launch_bounds__(THREADS, 2048 / THREADS) sel_filter_kernel(SelArgs a) {
     // CTA = a contiguous run of tiles; per tile every warp owns one 256-
     // position subtile (8 items per thread, thread-contiguous).  Counts of
     // elements below b*: per (subtile, part) one plain store by the warp,
     // per (tile, part) one global atomic per warp (tile_lt is zeroed per
-    // level).  The rare hits (1 / 2^D of the points) append their candidate
-    // record through a warp-aggregated atomic.  No block barrier.
+    // level).  The rare hits (1 / 2^D of the points) are staged in the CTA's
+    // shared memory (shared-atomic slots) and appended to their segments'
+    // candidate ranges once, at the end, one global atomic per segment per
+    // 32 records (the per-warp global atomic on ONE fill counter per segment
+    // serialised at the top levels); a full staging area falls back to
+    // per-warp global reservations.  Two block barriers (start, end).
     constexpr int ITEMS = 8;
     constexpr int T = THREADS * ITEMS;
     constexpr int NSUB = T / kSub;
     const LevelGeom& g = a.g;
     const u32* W = a.bf.w[a.par];
     const int k = a.k, R = k + 2;
+    extern __shared__ u32 fsm[];  // [0] staged count, [kFCap] segment ids, [kFCap * R] records
+    u32* const s_seg = fsm + 1;
+    u32* const s_rec = s_seg + kFCap;
+    for (int e = threadIdx.x; e < kFCap; e += THREADS) s_seg[e] = ~0u;
+    if (threadIdx.x == 0) fsm[0] = 0u;
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u32 ltm = lanemask_lt();
     const u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
     u64 t1 = t0 + a.tiles_per_cta;
     if (t1 > a.ntiles) t1 = a.ntiles;
-    if (t0 >= t1) return;
+    if (t0 >= t1) return;  // (the whole CTA)
     SegCursor sc;
     sc.init(g, t0 * T);
     u64 cj = ~0ull;
@@ -475,18 +486,35 @@ __global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
                     const u32 y = __shfl_up_sync(kFullMask, x, o);
                     if (lane >= o) x += y;
                 }
-                u32 base = 0;
-                if (lane == 31) base = atomicAdd(&sel[kSelFill], wtot);
-                base = __shfl_sync(kFullMask, base, 31);
-                u32 slot = sel[kSelOff] + base + x - nh;
-                while (hits) {
-                    const int i = __ffs(hits) - 1;
-                    hits &= hits - 1;
-                    const u32 r = (u32)(threadIdx.x * ITEMS + i);
-                    u32* rec = a.cand + (u64)slot * R;
-                    for (int c = 0; c <= k; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
-                    rec[k + 1] = (u32)(ts + r);
-                    ++slot;
+                u32 pos = 0;
+                if (lane == 31) pos = atomicAdd(&fsm[0], wtot);
+                pos = __shfl_sync(kFullMask, pos, 31);
+                if (pos + wtot <= (u32)kFCap) {  // staged in shared memory
+                    u32 q = pos + x - nh;
+                    while (hits) {
+                        const int i = __ffs(hits) - 1;
+                        hits &= hits - 1;
+                        const u32 r = (u32)(threadIdx.x * ITEMS + i);
+                        u32* rec = s_rec + q * R;
+                        for (int c = 0; c <= k; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
+                        rec[k + 1] = (u32)(ts + r);
+                        s_seg[q] = (u32)j;
+                        ++q;
+                    }
+                } else {  // staging full (tie-heavy data): reserve in the segment directly
+                    u32 base = 0;
+                    if (lane == 31) base = atomicAdd(&sel[kSelFill], wtot);
+                    base = __shfl_sync(kFullMask, base, 31);
+                    u32 slot = sel[kSelOff] + base + x - nh;
+                    while (hits) {
+                        const int i = __ffs(hits) - 1;
+                        hits &= hits - 1;
+                        const u32 r = (u32)(threadIdx.x * ITEMS + i);
+                        u32* rec = a.cand + (u64)slot * R;
+                        for (int c = 0; c <= k; ++c) rec[c] = W[(u64)c * a.bf.stride + ts + r];
+                        rec[k + 1] = (u32)(ts + r);
+                        ++slot;
+                    }
                 }
             }
         }
@@ -495,6 +523,25 @@ __global__ void __launch_bounds__(THREADS) sel_filter_kernel(SelArgs a) {
             a.sub_lt[s * 2 + 1] = nlt_s[1];
         }
         (void)ltm;
+    }
+    // the staged candidates -> their segments' ranges: per 32 records one
+    // global reservation per distinct segment (peers by __match_any_sync)
+    __syncthreads();
+    const u32 nst = min(fsm[0], (u32)kFCap);
+    for (u32 e0 = (u32)warp * 32u; e0 < nst; e0 += (u32)THREADS) {
+        const u32 e = e0 + (u32)lane;
+        const u32 js = e < nst ? s_seg[e] : ~0u;  // ~0: a slot of an overflowed reservation, never written
+        const u32 peers = __match_any_sync(kFullMask, js);
+        const int leader = __ffs(peers) - 1;
+        u32 base = 0;
+        if (js != ~0u && lane == leader) base = atomicAdd(&a.sel[(u64)js * kSelW + kSelFill], (u32)__popc(peers));
+        base = __shfl_sync(kFullMask, base, leader);
+        if (js != ~0u) {
+            const u32 slot = a.sel[(u64)js * kSelW + kSelOff] + base + (u32)__popc(peers & ltm);
+            const u32* src = s_rec + e * R;
+            u32* rec = a.cand + (u64)slot * R;
+            for (int c = 0; c < R; ++c) rec[c] = src[c];
+        }
     }
 }
 
@@ -1302,11 +1349,16 @@ void launch_sel_filter(const SelArgs& a0, int b, cudaStream_t st) {
     a.tiles_per_cta = (int)tpc;
     const unsigned g2 = (unsigned)((a.ntiles + tpc - 1) / tpc);
     (void)grid;
+    const size_t sm = sizeof(u32) * (1 + (size_t)kFCap * (1 + a.k + 2));  // count, segment ids, records
+    auto go = [&](auto kern, int nt) {
+        if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kern<<<g2, nt, sm, st>>>(a);
+    };
     switch (T) {
-        case 2048: sel_filter_kernel<256><<<g2, 256, 0, st>>>(a); break;
-        case 1024: sel_filter_kernel<128><<<g2, 128, 0, st>>>(a); break;
-        case 512: sel_filter_kernel<64><<<g2, 64, 0, st>>>(a); break;
-        default: sel_filter_kernel<32><<<g2, 32, 0, st>>>(a); break;
+        case 2048: go(sel_filter_kernel<256>, 256); break;
+        case 1024: go(sel_filter_kernel<128>, 128); break;
+        case 512: go(sel_filter_kernel<64>, 64); break;
+        default: go(sel_filter_kernel<32>, 32); break;
     }
 }
 

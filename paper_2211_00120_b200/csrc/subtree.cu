@@ -234,7 +234,7 @@ __device__ __noinline__ bool bucket_list(unsigned short* __restrict__ out, int m
         acc(c.w);
     }
     big = __reduce_max_sync(kFullMask, big);
-    const u32 ex = block_exclusive_scan<u32>(s, scratch, nullptr);
+    const u32 ex = block_exclusive_scan_1b<u32>(s, scratch);
     scratch[32 + warp] = big;
     u32 run = ex;
     auto starts = [&](u32 c) -> u32 {
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                     ex = 0u;  // (no segments on the other warps)
                 }
             } else {
-                ex = block_exclusive_scan<u32>(v, scratch, nullptr);
+                ex = block_exclusive_scan_1b<u32>(v, scratch);
             }
             u32 run = ex;
 #pragma unroll
@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a
                     }
                 }
             }
-            const u64 ex64 = block_exclusive_scan<u64>((u64)va | ((u64)vb << 32), scratch64, nullptr);
+            const u64 ex64 = block_exclusive_scan_1b<u64>((u64)va | ((u64)vb << 32), scratch64);
             if (p0 < mc) {
                 u32 exa = (u32)ex64, exb = (u32)(ex64 >> 32);
 #pragma unroll
