@@ -43,6 +43,9 @@ __device__ inline void widest_chain(u64 s, int k, const uint8_t* split_dims, Cha
 
 // per-segment pick record of the select path
 enum { kSelLo = 0, kSelShift, kSelB, kSelR, kSelC, kSelOff, kSelFill, kSelW = 8 };
+// sel[kSelB] of a segment whose node box is a single point: the node is the
+// element at in-order position sel[kSelLo] (pick / filter, select.cu)
+constexpr u32 kSelPositional = 0xffffffffu;
 
 // Working set of the global levels.
 // Points travel with their sort: W[buf] holds k coordinate arrays and one

@@ -354,6 +354,27 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
 __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
     __shared__ u32 wtot[32];
     const u64 j = blockIdx.x;
+    // a node box that is a single point (every coordinate of every point of
+    // the segment equal): the within-node order is the input order, which is
+    // the segment's order in W (stable partitions) -- the node is the element
+    // at in-order offset pivot_off, no histogram and no candidates to sort
+    {
+        const float* box = a.boxes_in + j * 2ull * a.k;
+        bool point = true;
+        for (int d = 0; d < a.k; ++d) point &= box[d] == box[a.k + d];
+        if (point) {
+            if (threadIdx.x == 0) {
+                u32* sel = a.sel + j * kSelW;
+                sel[kSelLo] = (u32)(v_ibegin(a.g, j) + v_pivot(a.g, j));  // the node's position
+                sel[kSelB] = kSelPositional;
+                sel[kSelR] = 0u;
+                sel[kSelC] = 1u;
+                sel[kSelOff] = atomicAdd(a.cand_ctr, 1u);
+                sel[kSelFill] = 0u;
+            }
+            return;
+        }
+    }
     const int nb = 1 << a.D;
     const int per = nb / 256;
     const u32* h = a.hist + j * (u64)nb;
@@ -449,7 +470,18 @@ __global__ void __launch_bounds__(THREADS, 2048 / THREADS) sel_filter_kernel(Sel
             const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
             u32 hits = 0, nlt = 0;
             const u32 r0 = (u32)threadIdx.x * ITEMS;
-            if (r0 >= ra && r0 + ITEMS <= rb) {
+            if (bs == kSelPositional) {  // (pick: a point box) the node is at in-order position sel[kSelLo]
+                const u32 npos = sel[kSelLo];
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 r = r0 + (u32)i;
+                    if (r >= ra && r < rb) {
+                        const u32 p = (u32)(ts + r);
+                        if (p == npos) hits |= 1u << i;
+                        nlt += p < npos ? 1u : 0u;
+                    }
+                }
+            } else if (r0 >= ra && r0 + ITEMS <= rb) {
                 // the thread's 8 keys lie in this part: two 16-byte loads (the
                 // SoA columns are 16-byte aligned and tiles start at multiples
                 // of T words)
@@ -1383,16 +1415,19 @@ void launch_sel_select(const SelArgs& a, int b, cudaStream_t st) {
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, kern, a, sel_tile(b));
     };
-    // LBKD_SELECT_CLUSTER (default 6): bit 2 -- clusters of 4 x 1024 threads
-    // at nseg <= 16, bit 1 -- clusters of 4 x 256 at nseg <= 128; 0 = one
-    // CTA per segment everywhere.  (Clusters of 8 measured unreliable here.)
+    // LBKD_SELECT_CLUSTER (default 10): at nseg <= 16 clusters of 8 (bit 3)
+    // or 4 (bit 2) CTAs of 1024 threads; at nseg <= 128 clusters of 8 (bit 4)
+    // or 4 (bit 1) CTAs of 256; 0 = one CTA per segment everywhere
     static const int csel = [] {
         const char* e = getenv("LBKD_SELECT_CLUSTER");
-        return e ? atoi(e) : 6;
+        return e ? atoi(e) : 10;
     }();
     if (a.g.nseg <= 16) {
-        if (csel & 4) cluster_go(sel_select_kernel<1024, 4>, 1024, 4);
+        if (csel & 8) cluster_go(sel_select_kernel<1024, 8>, 1024, 8);
+        else if (csel & 4) cluster_go(sel_select_kernel<1024, 4>, 1024, 4);
         else sel_select_kernel<1024, 1><<<g, 1024, 0, st>>>(a, sel_tile(b));
+    } else if (a.g.nseg <= 128 && (csel & 16)) {
+        cluster_go(sel_select_kernel<256, 8>, 256, 8);
     } else if (a.g.nseg <= 128 && (csel & 2)) {
         cluster_go(sel_select_kernel<256, 4>, 256, 4);
     } else if (a.g.nseg >= 2048) {

@@ -168,6 +168,11 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
     if (src) asm volatile("cp.async.wait_all;" ::: "memory");
     // input row of a local id (the final tie-break of every chain)
     auto idx_of = [&](u32 lid) -> u32 { return vin ? vin[lid] : lid; };
+    // input-row order of two local ids: a subtree that arrives in input order
+    // (select path, single-CTA builds) has local ids in input-row order
+    // already -- no global load of the rows
+    const bool lid_is_row_order = !a.entry_sorted || !vin;
+    auto row_less = [&](u32 x, u32 y) -> bool { return lid_is_row_order ? x < y : idx_of(x) < idx_of(y); };
     // subtree root box (global phase: boxes of level lam0; single-CTA build:
     // reduced here) and, for widest, the dims of the ancestors above the root
     if (a.from_pts) {
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             const u32 kx = flip_key(P[d * Mp + x]), ky = flip_key(P[d * Mp + y]);
             if (kx != ky) return kx < ky;
         }
-        return idx_of(x) < idx_of(y);
+        return row_less(x, y);
     };
     // widest: chain of a node = its dim, then its ancestors' dims (repeats
     // dropped).  Ancestors inside the subtree come from ndim (heap order),
@@ -396,8 +401,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 bool have = false;
                 u32 rank = 0;
                 if (s[kSgDeg]) {  // identical points: the input order decides
-                    const u32 ii = idx_of(ci);
-                    for (u32 jj = 0; jj < C; ++jj) rank += idx_of(cand[off + jj]) < ii ? 1u : 0u;
+                    for (u32 jj = 0; jj < C; ++jj) rank += row_less(cand[off + jj], ci) ? 1u : 0u;
                     if (rank == s[kSgR]) s[kSgPiv] = ci;
                     continue;
                 }
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             if (kp != kv) {
                 lt = kp < kv;
             } else if (s[kSgDeg]) {
-                lt = idx_of((u32)p) < idx_of(piv);
+                lt = row_less((u32)p, piv);
             } else {
                 Chain wch;
                 if (a.mode == kWidest) widest_chain_of(hbase + t, dl, wch);
@@ -560,7 +564,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                         const u32 ol = __shfl_sync(kFullMask, lid, i);
                         if (act && tie && ((actm >> i) & 1u) && i != lane && ok == key) {
                             const bool lt = rr_exact ? less_tie(ol, lid, (int)ch.m, [&](int f) -> int { return ch.d[f]; })
-                                                     : idx_of(ol) < idx_of(lid);
+                                                     : row_less(ol, lid);
                             rank += lt ? 1u : 0u;
                         }
                     }
