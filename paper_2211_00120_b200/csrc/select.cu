@@ -40,8 +40,30 @@
 
 namespace lbkd {
 
+// Round-robin: the dimension a level-l node's points are bucketed by -- the
+// first dimension of its chain (l, l-1, ... mod k, truncated near the root)
+// in which its box is not a single value.  Every point of the node ties on
+// the chain dims before it (they lie in the box), so the node's order is the
+// same order without them; bucketing a pinned dim would put the whole node
+// into one bucket.  -1: every chain dim is pinned (the order is the input
+// order: pick makes the segment positional).
+__device__ __forceinline__ int rr_key_dim(const float* box, int k, int l) {
+    const int m = l + 1 < k ? l + 1 : k;
+    for (int i = 0; i < m; ++i) {
+        const int d = (l - i) % k;
+        if (box[d] < box[k + d]) return d;
+    }
+    return -1;
+}
+
+// the key dimension of segment t of the level (widest: the node's split dim,
+// pinned only when the whole box is a point)
 __device__ __forceinline__ int seg_key_dim(const SelArgs& a, u64 t) {
-    return a.mode == kRoundRobin ? (a.g.l % a.k) : (int)a.split_dims[a.g.Fl + a.g.sbase + t];
+    if (a.mode == kRoundRobin) {
+        const int d = rr_key_dim(a.boxes_in + t * 2ull * a.k, a.k, a.g.l);
+        return d >= 0 ? d : a.g.l % a.k;
+    }
+    return (int)a.split_dims[a.g.Fl + a.g.sbase + t];
 }
 
 __device__ __forceinline__ int bitlen32(u32 v) { return v ? 32 - __clz(v) : 0; }
@@ -361,7 +383,11 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
     {
         const float* box = a.boxes_in + j * 2ull * a.k;
         bool point = true;
-        for (int d = 0; d < a.k; ++d) point &= box[d] == box[a.k + d];
+        if (a.mode == kRoundRobin) {
+            point = rr_key_dim(box, a.k, a.g.l) < 0;  // every chain dim pinned
+        } else {
+            for (int d = 0; d < a.k; ++d) point &= box[d] == box[a.k + d];
+        }
         if (point) {
             if (threadIdx.x == 0) {
                 u32* sel = a.sel + j * kSelW;
@@ -446,6 +472,7 @@ __global__ void __launch_bounds__(THREADS, 2048 / THREADS) sel_filter_kernel(Sel
     u64 cj = ~0ull;
     Bucketer cbk{};
     u32 cbs = 0;
+    int cdk = 0;
     for (u64 t = t0; t < t1; ++t) {
         const u64 ts = t * T;
         const u64 cnt = g.nview - ts < (u64)T ? g.nview - ts : (u64)T;
@@ -460,14 +487,15 @@ __global__ void __launch_bounds__(THREADS, 2048 / THREADS) sel_filter_kernel(Sel
             const u32 ra = part ? r1a : r0a, rb = part ? r1b : r0b;
             if (!((part == 0 || has1) && ra < rb)) continue;
             u32* sel = a.sel + j * kSelW;
-            if (j != cj) {  // the segment's bucketer, kept while tiles stay in it
+            if (j != cj) {  // the segment's bucketer and key dim, kept while tiles stay in it
                 cj = j;
                 cbk = make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D);
                 cbs = sel[kSelB];
+                cdk = seg_key_dim(a, j);
             }
             const Bucketer bk = cbk;
             const u32 bs = cbs;
-            const u32* kp = W + (u64)seg_key_dim(a, j) * a.bf.stride + ts;
+            const u32* kp = W + (u64)cdk * a.bf.stride + ts;
             u32 hits = 0, nlt = 0;
             const u32 r0 = (u32)threadIdx.x * ITEMS;
             if (bs == kSelPositional) {  // (pick: a point box) the node is at in-order position sel[kSelLo]
@@ -1203,6 +1231,10 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
                     const u64 cn = 2 * (g.Fl + g.sbase + hseg) + 1;
                     hdn0 = cn < g.n ? (int)a.split_dims[cn] : 0;
                     hdn1 = cn + 1 < g.n ? (int)a.split_dims[cn + 1] : 0;
+                } else {  // round-robin: the children's key dims at level l + 1 (rr_key_dim)
+                    const int e0 = rr_key_dim(c0, k, g.l + 1), e1 = rr_key_dim(c1, k, g.l + 1);
+                    hdn0 = e0 >= 0 ? e0 : dn;
+                    hdn1 = e1 >= 0 ? e1 : dn;
                 }
                 hb0 = make_bucketer(c0[hdn0], c0[k + hdn0], kFuseD);
                 hb1 = make_bucketer(c1[hdn1], c1[k + hdn1], kFuseD);
@@ -1277,7 +1309,11 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
                 const u64 j = tp.j0 + (in1 ? 1 : 0);
                 const float* cb = a.boxes_out + (2 * j + side) * 2ull * k;
                 const u64 cn = 2 * (g.Fl + g.sbase + j) + 1 + side;
-                const int dnc = D0 >= 0 ? dn : (cn < g.n ? (int)a.split_dims[cn] : 0);
+                int dnc = D0 >= 0 ? dn : (cn < g.n ? (int)a.split_dims[cn] : 0);
+                if (D0 >= 0) {
+                    const int e = rr_key_dim(cb, k, g.l + 1);
+                    if (e >= 0) dnc = e;
+                }
                 const Bucketer hb = make_bucketer(cb[dnc], cb[k + dnc], kFuseD);
                 atomicAdd(&a.hist_next[(2 * j + side) * (u64)kFuseBins + bucket_of(hb, V(dnc, i))], 1u);
             }
