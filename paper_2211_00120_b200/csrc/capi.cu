@@ -252,6 +252,7 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0, bool need_w_bufs =
         if ((rc = grow(c->bf.seg_or, dummy, nseg))) return rc;
         for (int i = 0; i < 2; ++i) {
             if ((rc = grow(c->bf.boxes[i], dummy, nseg * 2 * (size_t)LBKD_MAX_K))) return rc;
+            if ((rc = grow(c->bf.bmode[i], dummy, nseg))) return rc;
             if ((rc = grow(c->bf.state[i], dummy, nseg))) return rc;
         }
         c->cap_seg = nseg;
@@ -392,6 +393,9 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.out_pts = bp.out_pts;
         a.boxes_in = bf.boxes[par];
         a.boxes_out = bf.boxes[par ^ 1];
+        a.bmode_in = bf.bmode[par];
+        a.bmode_out = bf.bmode[par ^ 1];
+        if (l == lfrom) CK(cudaMemsetAsync(bf.bmode[par], 0, nseg, st));  // the view root: value-linear
         a.tile_lt = bf.tile_lt;
         a.sub_lt = bf.sub_lt;
         a.ppos = bf.ppos;
@@ -1052,6 +1056,7 @@ void lbkd_destroy(lbkd_ctx* c) {
     for (int i = 0; i < 2; ++i) {
         cudaFree(c->bf.w[i]);
         cudaFree(c->bf.boxes[i]);
+        cudaFree(c->bf.bmode[i]);
         cudaFree(c->bf.state[i]);
     }
     cudaFree(c->bf.hist);

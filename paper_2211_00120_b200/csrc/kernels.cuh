@@ -42,7 +42,7 @@ __device__ inline void widest_chain(u64 s, int k, const uint8_t* split_dims, Cha
 }
 
 // per-segment pick record of the select path
-enum { kSelLo = 0, kSelShift, kSelB, kSelR, kSelC, kSelOff, kSelFill, kSelW = 8 };
+enum { kSelLo = 0, kSelShift, kSelB, kSelR, kSelC, kSelOff, kSelFill, kSelMode, kSelW = 8 };
 // sel[kSelB] of a segment whose node box is a single point: the node is the
 // element at in-order position sel[kSelLo] (pick / filter, select.cu)
 constexpr u32 kSelPositional = 0xffffffffu;
@@ -77,6 +77,7 @@ struct Buffers {
     u64* moved;       // per pass launch: points the launch reordered (profiling)
     u32* err;         // [0] non-finite flag
     float* boxes[2];  // widest: boxes of the level's nodes [nseg][2k]
+    uint8_t* bmode[2];  // bucket mode of the level's nodes (0 value-linear, 1 key-linear)
 };
 
 struct BuildParams {
@@ -119,6 +120,8 @@ struct SelArgs {
     float* out_pts;
     const float* boxes_in;  // widest: boxes of the level's segments
     float* boxes_out;       //         boxes of their children
+    const uint8_t* bmode_in;  // bucket mode of the level's segments
+    uint8_t* bmode_out;       //   and of their children (select.cu)
     u32* tile_lt;          // [tiles][2] below-pivot counts -> exclusive prefixes
     u32* sub_lt;           // [subtiles][2] below-pivot counts per 256-position warp subtile
     u32* ppos;             // [nseg] in-order position of each segment's pivot

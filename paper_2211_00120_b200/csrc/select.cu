@@ -82,24 +82,50 @@ __device__ __forceinline__ u32 bucket_shift(u32 lo, u32 hi, int D) {
 // is monotone (IEEE subtraction, multiplication by a positive scale and the
 // truncation are monotone) and identical in hist and filter, which is all
 // the selection needs.  -0.0 and +0.0 land in the same bucket.
+//
+// KEY-linear mode (mode 1): equal widths of the order-flipped key range --
+// right for data spread over many binades (log-like, e.g. 1e-30..1e30),
+// where value-linear buckets put almost the whole node into its lowest
+// bucket.  A node's mode is set by its parent's selection (select kernel):
+// once a pivot bucket held more than 1/32 of its node, the children use key
+// buckets (and pass that on).  Uniform data never triggers it.
 struct Bucketer {
-    float hlo, scale;  // halves: no overflow of hi - lo for any finite box
-    u32 top;
+    float hlo, scale;  // value mode: halves (no overflow of hi - lo); key mode: scale < 0,
+    u32 top;           //   hlo = the flipped key of lo, -scale - 1 = the shift
 };
 
-__device__ __forceinline__ Bucketer make_bucketer(float lo, float hi, int D) {
+__device__ __forceinline__ Bucketer make_bucketer(float lo, float hi, int D, int mode = 0) {
     Bucketer b;
+    b.top = (1u << D) - 1u;
+    if (mode) {
+        const u32 klo = flip_key(lo), khi = flip_key(hi);
+        u32 sh = 0;
+        while (((khi - klo) >> sh) > b.top) ++sh;
+        b.hlo = __uint_as_float(klo);
+        b.scale = -(float)(sh + 1u);
+        return b;
+    }
     b.hlo = 0.5f * lo;
     const float w = 0.5f * hi - b.hlo;
     b.scale = w > 0.0f ? __fdiv_rn((float)(1u << D), w) : 0.0f;
-    b.top = (1u << D) - 1u;
     return b;
 }
 
-__device__ __forceinline__ u32 bucket_of(const Bucketer& b, u32 bits) {
+__device__ __forceinline__ u32 bucket_key(const Bucketer& b, u32 bits) {  // key mode: a shift of the flipped key
+    const u32 r = (flip_key(__uint_as_float(bits)) - __float_as_uint(b.hlo)) >> ((u32)(-b.scale) - 1u);
+    return r < b.top ? r : b.top;
+}
+
+__device__ __forceinline__ u32 bucket_val(const Bucketer& b, u32 bits) {
     // fp32, round-to-nearest each step: monotone in the key
     const float x = __fmul_rn(__fsub_rn(0.5f * __uint_as_float(bits), b.hlo), b.scale);
     return x < (float)b.top ? (u32)x : b.top;  // NaN (non-finite input, reported later) -> top
+}
+
+__device__ __forceinline__ bool key_mode(const Bucketer& b) { return b.scale < 0.0f; }
+
+__device__ __forceinline__ u32 bucket_of(const Bucketer& b, u32 bits) {
+    return key_mode(b) ? bucket_key(b, bits) : bucket_val(b, bits);
 }
 
 // Incremental segment cursor over the view's in-order positions for a CTA
@@ -278,7 +304,7 @@ void launch_root(const BuildParams& bp, const Buffers& bf, const u32* minmax, cu
 
 __device__ __forceinline__ Bucketer seg_bucketer(const SelArgs& a, u64 t, int d) {
     const float* box = a.boxes_in + t * 2ull * a.k;
-    return make_bucketer(box[d], box[a.k + d], a.D);
+    return make_bucketer(box[d], box[a.k + d], a.D, a.bmode_in[t]);
 }
 
 // ---------------------------------------------------------------------------
@@ -312,7 +338,8 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
         __syncthreads();
     };
     const u32* W = a.bf.w[a.par];
-    int dk = -1;
+    int dk = -1, dk1 = -1;
+    u64 nseg_c = ~0ull;  // segment whose key dim dk1 holds
     Bucketer bk{};
     const u32* kp = nullptr;
     for (u64 t = t0; t < t1; ++t) {
@@ -340,30 +367,42 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
             const bool use = (r >= r0a && r < r0b) || (has1 && r >= r1a && r < r1b);
             key[i] = use ? kp[ts + r] : 0u;
         }
-        if (has1 && seg_key_dim(a, cur + 1) != dk) {  // widest: the next segment splits another dim
-            const u32* k1 = W + (u64)seg_key_dim(a, cur + 1) * a.bf.stride;
+        if (has1 && nseg_c != cur + 1) {  // the next segment's key dim, once per segment
+            nseg_c = cur + 1;
+            dk1 = seg_key_dim(a, cur + 1);
+        }
+        if (has1 && dk1 != dk) {  // the next segment is keyed by another dim
+            const u32* k1 = W + (u64)dk1 * a.bf.stride;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const u32 r = (u32)(i * kHThreads + threadIdx.x);
                 if (r >= r1a && r < r1b) key[i] = k1[ts + r];
             }
         }
+        // (the bucket mode hoisted out of the per-key loops)
+        auto bin = [&](u32 ra, u32 rb) {
+            if (key_mode(bk)) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const u32 r = (u32)(i * kHThreads + threadIdx.x);
-            if (r >= r0a && r < r0b) atomicAdd(&h[bucket_of(bk, key[i])], 1u);
-        }
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 r = (u32)(i * kHThreads + threadIdx.x);
+                    if (r >= ra && r < rb) atomicAdd(&h[bucket_key(bk, key[i])], 1u);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 r = (u32)(i * kHThreads + threadIdx.x);
+                    if (r >= ra && r < rb) atomicAdd(&h[bucket_val(bk, key[i])], 1u);
+                }
+            }
+        };
+        bin(r0a, r0b);
         if (has1) {
             flush(cur);
             cur = cur + 1;
-            dk = seg_key_dim(a, cur);
+            dk = dk1;
             bk = seg_bucketer(a, cur, dk);
             kp = W + (u64)dk * a.bf.stride;
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const u32 r = (u32)(i * kHThreads + threadIdx.x);
-                if (r >= r1a && r < r1b) atomicAdd(&h[bucket_of(bk, key[i])], 1u);
-            }
+            bin(r1a, r1b);
         }
     }
     flush(cur);
@@ -418,6 +457,7 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
         const float* box = a.boxes_in + j * 2ull * a.k;
         sel[kSelLo] = __float_as_uint(box[d]);  // the filter rebuilds the bucketer
         sel[kSelShift] = __float_as_uint(box[a.k + d]);
+        sel[kSelMode] = a.bmode_in[j];
         sel[kSelB] = (u32)b;
         sel[kSelR] = po - cum;
         sel[kSelC] = C;
@@ -489,7 +529,8 @@ __global__ void __launch_bounds__(THREADS, 2048 / THREADS) sel_filter_kernel(Sel
             u32* sel = a.sel + j * kSelW;
             if (j != cj) {  // the segment's bucketer and key dim, kept while tiles stay in it
                 cj = j;
-                cbk = make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D);
+                cbk = make_bucketer(__uint_as_float(sel[kSelLo]), __uint_as_float(sel[kSelShift]), a.D,
+                                    (int)sel[kSelMode]);
                 cbs = sel[kSelB];
                 cdk = seg_key_dim(a, j);
             }
@@ -516,11 +557,20 @@ __global__ void __launch_bounds__(THREADS, 2048 / THREADS) sel_filter_kernel(Sel
                 const uint4 q0 = *reinterpret_cast<const uint4*>(kp + r0);
                 const uint4 q1 = *reinterpret_cast<const uint4*>(kp + r0 + 4);
                 const u32 key[ITEMS] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+                if (key_mode(bk)) {
 #pragma unroll
-                for (int i = 0; i < ITEMS; ++i) {
-                    const u32 b = bucket_of(bk, key[i]);
-                    if (b == bs) hits |= 1u << i;
-                    nlt += b < bs ? 1u : 0u;
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const u32 b = bucket_key(bk, key[i]);
+                        if (b == bs) hits |= 1u << i;
+                        nlt += b < bs ? 1u : 0u;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const u32 b = bucket_val(bk, key[i]);
+                        if (b == bs) hits |= 1u << i;
+                        nlt += b < bs ? 1u : 0u;
+                    }
                 }
             } else {
 #pragma unroll
@@ -851,6 +901,10 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
         }
         const u64 cnode = 2 * node + 1 + tid;
         if (a.mode == kWidest && cnode < g.n) a.split_dims[cnode] = (uint8_t)best;
+        // the children's bucket mode: key-linear once a pivot bucket held more
+        // than 1/32 of its node (value-linear buckets failing: log-like data)
+        const bool crowded = (u64)sel[kSelC] * 32ull > v_size(g, j);
+        a.bmode_out[c] = (a.bmode_in[j] || crowded) ? 1u : 0u;
     }
     // per-tile counts below the pivot -> exclusive prefixes in tile order
     __syncthreads();
@@ -1236,8 +1290,8 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
                     hdn0 = e0 >= 0 ? e0 : dn;
                     hdn1 = e1 >= 0 ? e1 : dn;
                 }
-                hb0 = make_bucketer(c0[hdn0], c0[k + hdn0], kFuseD);
-                hb1 = make_bucketer(c1[hdn1], c1[k + hdn1], kFuseD);
+                hb0 = make_bucketer(c0[hdn0], c0[k + hdn0], kFuseD, a.bmode_out[2 * hseg]);
+                hb1 = make_bucketer(c1[hdn1], c1[k + hdn1], kFuseD, a.bmode_out[2 * hseg + 1]);
             }
             if (fuse) {
                 if (hcnt >= a.hflush_every) hflush();  // 16-bit bins: flush before they could overflow
@@ -1314,7 +1368,7 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
                     const int e = rr_key_dim(cb, k, g.l + 1);
                     if (e >= 0) dnc = e;
                 }
-                const Bucketer hb = make_bucketer(cb[dnc], cb[k + dnc], kFuseD);
+                const Bucketer hb = make_bucketer(cb[dnc], cb[k + dnc], kFuseD, a.bmode_out[2 * j + side]);
                 atomicAdd(&a.hist_next[(2 * j + side) * (u64)kFuseBins + bucket_of(hb, V(dnc, i))], 1u);
             }
             const u32 ml = __ballot_sync(kFullMask, side == 0);

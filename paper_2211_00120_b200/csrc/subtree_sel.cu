@@ -94,6 +94,8 @@ __device__ __forceinline__ u32 seg_bucket(const u32* s, float v, u32 top) {
 template <int KT>
 __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(SubtreeArgs a, int b) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint8_t s_outer[LBKD_MAX_K];  // widest: distinct dims of the subtree root's ancestors
+    __shared__ int s_nouter;
     typedef unsigned short u16;
     const int k = KT ? KT : a.k;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -166,6 +168,24 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
         seg[lid] = 0;
     }
     if (src) asm volatile("cp.async.wait_all;" ::: "memory");
+    if (tid == 0) {  // (the chains' tail above the subtree: widest_chain_of)
+        int no = 0;
+        if (a.mode == kWidest && lam0 > 0) {
+            u32 seen = 0;
+            u64 s = ((1ull << (lam0 - 1)) - 1ull) + (j >> 1);  // parent of the subtree root
+            while (true) {
+                const int d = a.split_dims[s];
+                if (!((seen >> d) & 1u)) {
+                    seen |= 1u << d;
+                    s_outer[no++] = (uint8_t)d;
+                    if (no == k) break;
+                }
+                if (s == 0) break;
+                s = (s - 1) >> 1;
+            }
+        }
+        s_nouter = no;
+    }
     // input row of a local id (the final tie-break of every chain)
     auto idx_of = [&](u32 lid) -> u32 { return vin ? vin[lid] : lid; };
     // input-row order of two local ids: a subtree that arrives in input order
@@ -240,17 +260,15 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             h = (h - 1) >> 1;
             --dd;
         }
-        if (lam0 == 0) return;
-        u64 s = ((1ull << (lam0 - 1)) - 1ull) + (j >> 1);  // parent of the subtree root
-        while (true) {
-            const int d = a.split_dims[s];
+        // above the subtree: its ancestors' distinct dims in walk order,
+        // gathered once per CTA (s_outer) instead of a global walk per call
+        for (int q = 0; q < s_nouter; ++q) {
+            const int d = s_outer[q];
             if (!((seen >> d) & 1u)) {
                 seen |= 1u << d;
                 ch.d[ch.m++] = (uint8_t)d;
                 if ((int)ch.m == k) return;
             }
-            if (s == 0) return;
-            s = (s - 1) >> 1;
         }
     };
     auto first_argmax = [&](const float* box) -> int {
