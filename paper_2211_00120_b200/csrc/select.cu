@@ -1297,27 +1297,49 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
                 if (hcnt >= a.hflush_every) hflush();  // 16-bit bins: flush before they could overflow
                 ++hcnt;
             }
+            // (1) every row's side by one float compare, 2 bits per row; (2)
+            // the rare ties (-> chain, index) in a separate pass, so the
+            // call does not split the rows' instruction streams; (3) ranks,
+            // fused histogram and stores, the bucket mode hoisted out
+            u32 sides = 0;
 #pragma unroll
             for (int i = 0; i < kPRows; ++i) {
                 const float xf = __uint_as_float(V(dl0, i));
-                int side = xf < yf ? 0 : (xf > yf ? 1 : 2);  // -0.0 == +0.0 like numpy
-                if (side == 2) side = part_tie_side(a, tp.j0, ss + (u64)(i * 32 + lane));
-                const u32 ml = __ballot_sync(kFullMask, side == 0);
-                const u32 mr = __ballot_sync(kFullMask, side == 1);
-                const u32 dst = side == 0 ? bl + __popc(ml & lt) : br + __popc(mr & lt);
-                bl += __popc(ml);
-                br += __popc(mr);
-                if (fuse && side < 2) {
-                    const u32 kn = V(side ? hdn1 : hdn0, i);
-                    const u32 hbk = bucket_of(side ? hb1 : hb0, kn);
-                    atomicAdd(&wh[side * 256 + (hbk >> 1)], (hbk & 1u) ? 0x10000u : 1u);
-                }
-                if (side < 2) {
-#pragma unroll
-                    for (int c = 0; c <= KMAX; ++c)
-                        if (c < A) dcol[c][dst] = V(c, i);
+                const u32 sd = xf < yf ? 0u : (xf > yf ? 1u : 2u);  // -0.0 == +0.0 like numpy
+                sides |= sd << (2 * i);
+            }
+            if (__any_sync(kFullMask, (sides & 0xAAAAu) != 0u)) {
+                for (int i = 0; i < kPRows; ++i) {
+                    if (((sides >> (2 * i)) & 3u) == 2u) {
+                        const u32 sd = (u32)part_tie_side(a, tp.j0, ss + (u64)(i * 32 + lane));
+                        sides = (sides & ~(3u << (2 * i))) | (sd << (2 * i));
+                    }
                 }
             }
+            auto rows = [&](auto bucket_fn) {
+#pragma unroll
+                for (int i = 0; i < kPRows; ++i) {
+                    const int side = (int)((sides >> (2 * i)) & 3u);
+                    const u32 ml = __ballot_sync(kFullMask, side == 0);
+                    const u32 mr = __ballot_sync(kFullMask, side == 1);
+                    const u32 dst = side == 0 ? bl + __popc(ml & lt) : br + __popc(mr & lt);
+                    bl += __popc(ml);
+                    br += __popc(mr);
+                    if (fuse && side < 2) {
+                        const u32 kn = V(side ? hdn1 : hdn0, i);
+                        const u32 hbk = bucket_fn(side ? hb1 : hb0, kn);
+                        atomicAdd(&wh[side * 256 + (hbk >> 1)], (hbk & 1u) ? 0x10000u : 1u);
+                    }
+                    if (side < 2) {
+#pragma unroll
+                        for (int c = 0; c <= KMAX; ++c)
+                            if (c < A) dcol[c][dst] = V(c, i);
+                    }
+                }
+            };
+            // (both children of a node share their bucket mode: select.cu)
+            if (fuse && key_mode(hb0)) rows([](const Bucketer& b, u32 x) { return bucket_key(b, x); });
+            else rows([](const Bucketer& b, u32 x) { return bucket_val(b, x); });
         } else {
 #pragma unroll
         for (int i = 0; i < kPRows; ++i) {
