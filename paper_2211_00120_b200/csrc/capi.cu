@@ -98,6 +98,8 @@ struct lbkd_ctx {
         int slot = 0, pending = 0;
     } hp;
     size_t cap_cand = 0, cap_ptiles = 0, cap_piv = 0;
+    int pair_levels = 1;  // round robin: global levels two per partition (LBKD_PAIR=0: one)
+    int w_par_end = 0;  // W buffer holding the data after the global levels (level pairs shift it)
     // grow-only device allocations
     size_t cap_n = 0, cap_seg = 0, cap_tiles = 0, cap_w = 0, cap_copy = 0;
     Buffers bf{};
@@ -133,6 +135,13 @@ struct lbkd_ctx {
 // kernel classes of the profile (lbkd_profile_kernel)
 enum { kPInit = 0, kPHist, kPPick, kPFilter, kPSelect, kPPart, kPSubtree, kPSortPass, kPOther, kPClasses };
 
+static void prof_record(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
+}
+
 // open / close a profiled launch: events on the build stream around it
 static int prof_begin(lbkd_ctx* c, cudaStream_t st) {
     if (!c->profile) return 0;
@@ -143,14 +152,15 @@ static int prof_begin(lbkd_ctx* c, cudaStream_t st) {
     }
     // external record: inside a stream capture the event becomes a real
     // event-record node of the graph, so a replayed graph times its kernels
-    // back to back (no host launch gaps inside the brackets)
-    cudaEventRecordWithFlags(c->ev[c->n_ev_used], st, cudaEventRecordExternal);
+    // back to back (no host launch gaps inside the brackets); the flag is
+    // only legal while capturing (ungraphed builds: sort path, value tables)
+    prof_record(c->ev[c->n_ev_used], st);
     return 0;
 }
 static void prof_end(lbkd_ctx* c, cudaStream_t st, int cls, double bytes) {
     c->launches += 1;
     if (!c->profile) return;
-    cudaEventRecordWithFlags(c->ev[c->n_ev_used + 1], st, cudaEventRecordExternal);
+    prof_record(c->ev[c->n_ev_used + 1], st);
     const int i = c->n_ev_used / 2;
     if ((int)c->ev_cls.size() <= i) {
         c->ev_cls.resize(i + 1);
@@ -270,12 +280,17 @@ static int ensure(lbkd_ctx* c, u64 n, int k, int b, int lam0, bool need_w_bufs =
             if ((rc = grow(c->bf.chains, dummy, nseg))) return rc;
             if ((rc = grow(c->bf.sel, dummy, nseg * kSelW))) return rc;
             if ((rc = grow(c->bf.ppos, dummy, nseg))) return rc;
+            if ((rc = grow(c->bf.piv2, dummy, pv))) return rc;
+            if ((rc = grow(c->bf.chains2, dummy, nseg))) return rc;
+            if ((rc = grow(c->bf.ppos2, dummy, nseg))) return rc;
             c->cap_piv = pv;
         }
         const size_t pt = 2 * (n / 256 + 16);  // per 256-position subtile (tiles are coarser)
         if (pt > c->cap_ptiles) {
             if ((rc = grow(c->bf.tile_lt, dummy, pt))) return rc;
             if ((rc = grow(c->bf.sub_lt, dummy, pt))) return rc;
+            if ((rc = grow(c->bf.tile_lt2, dummy, 2 * pt))) return rc;
+            if ((rc = grow(c->bf.sub_lt2, dummy, 2 * pt))) return rc;
             c->cap_ptiles = pt;
         }
     }
@@ -347,31 +362,25 @@ static int run_levels_sort(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lt
 }
 
 // select path: the global levels [lfrom, lto) of the view bp -- per level
-// hist -> pick -> filter -> select -> partition (select.cu)
+// hist -> pick -> filter -> select -> partition (select.cu).  Level pairs
+// (bp.pair: round robin, 2 <= k <= 4): after level l's select, its children
+// are selected in the level-l layout (child hist -> pick -> filter pair ->
+// select) and ONE partition pass moves every point to its grandchild's run.
 static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cudaStream_t st) {
     Buffers& bf = c->bf;
     const int k = bp.k;
     const double A = 4.0 * (k + 1);
-    // from level kFuseFrom on (k <= 4) each level's histogram (D = 9) is
-    // accumulated by the previous level's partition kernel (widest: binned
+    // from level kFuseFrom on (k <= 4) each level's histogram (D = 9; 8 after
+    // a pair) is accumulated by the previous partition kernel (widest: binned
     // in each child's own split dim, written by the select kernel)
     const int kFuseFrom = 6;
     const bool fusable = k <= 4 && (bp.mode == kRoundRobin || getenv("LBKD_FUSE_WIDEST") == nullptr ||
                                     getenv("LBKD_FUSE_WIDEST")[0] != '0');
-    for (int l = lfrom; l < lto; ++l) {
-        const LevelGeom g = view_of(bp, l);
-        const u64 nseg = g.nseg;
-        const bool fused_in = fusable && l > lfrom && l >= kFuseFrom;
-        const bool fuse_next = fusable && l + 1 < lto && l + 1 >= kFuseFrom;
-        const int D = fused_in ? 9 : sel_digit_bits(nseg);  // 9 = kFuseD (select.cu)
-        const u32 par = (u32)((l - bp.lroot) & 1);
-        const double pts = (double)level_points(bp, l);
-        if (!fused_in) CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
-        CK(cudaMemsetAsync(bf.cand_ctr, 0, sizeof(u32), st));
-        {  // per-tile below-pivot counts accumulate atomically in the filter
-            const u64 T = (u64)sel_tile(bp.b);
-            CK(cudaMemsetAsync(bf.tile_lt, 0, 2 * ((g.nview + T - 1) / T) * sizeof(u32), st));
-        }
+    const bool pairs = bp.pair && bp.mode == kRoundRobin && k >= 2 && k <= 4;
+    u32 wpar = 0;       // W[wpar] holds level l's data
+    int fused_D = 0;    // D of the histogram the previous partition fused (0: none)
+    const u64 T = (u64)sel_tile(bp.b);
+    auto base_args = [&](const LevelGeom& g, int D, u32 bpar) {
         SelArgs a;
         memset(&a, 0, sizeof(a));
         a.g = g;
@@ -380,7 +389,7 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.wt = bp.wt;
         a.D = D;
         a.bf = bf;
-        a.par = par;
+        a.par = wpar;
         a.hist = bf.hist;
         a.sel = bf.sel;
         a.cand = bf.cand;
@@ -391,15 +400,32 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         a.split_dims = bp.split_dims;
         a.perm = bp.perm;
         a.out_pts = bp.out_pts;
-        a.boxes_in = bf.boxes[par];
-        a.boxes_out = bf.boxes[par ^ 1];
-        a.bmode_in = bf.bmode[par];
-        a.bmode_out = bf.bmode[par ^ 1];
-        if (l == lfrom) CK(cudaMemsetAsync(bf.bmode[par], 0, nseg, st));  // the view root: value-linear
+        a.boxes_in = bf.boxes[bpar];
+        a.boxes_out = bf.boxes[bpar ^ 1];
+        a.bmode_in = bf.bmode[bpar];
+        a.bmode_out = bf.bmode[bpar ^ 1];
         a.tile_lt = bf.tile_lt;
         a.sub_lt = bf.sub_lt;
         a.ppos = bf.ppos;
-        if (!fused_in) {
+        return a;
+    };
+    for (int l = lfrom; l < lto;) {
+        const LevelGeom g = view_of(bp, l);
+        const u64 nseg = g.nseg;
+        const bool pair = pairs && l + 1 < lto;
+        const int lnext = l + (pair ? 2 : 1);
+        static const bool pair_nofuse = getenv("LBKD_PAIR_NOFUSE") && getenv("LBKD_PAIR_NOFUSE")[0] == '1';
+        const bool fuse_next = fusable && lnext < lto && lnext >= kFuseFrom && !(pair && pair_nofuse);
+        const int D = fused_D ? fused_D : sel_digit_bits(nseg);
+        const u32 bpar = (u32)((l - bp.lroot) & 1);  // boxes / bucket modes alternate per level
+        const double pts = (double)level_points(bp, l);
+        if (!fused_D) CK(cudaMemsetAsync(bf.hist, 0, (nseg << D) * sizeof(u32), st));
+        CK(cudaMemsetAsync(bf.cand_ctr, 0, sizeof(u32), st));
+        const u64 ntl = (g.nview + T - 1) / T;  // per-tile below-pivot counts accumulate atomically in the filter
+        CK(cudaMemsetAsync(bf.tile_lt, 0, 2 * ntl * sizeof(u32), st));
+        SelArgs a = base_args(g, D, bpar);
+        if (l == lfrom) CK(cudaMemsetAsync(bf.bmode[bpar], 0, nseg, st));  // the view root: value-linear
+        if (!fused_D) {
             if (prof_begin(c, st)) return LBKD_ECUDA;
             launch_sel_hist(a, bp.b, st);
             prof_end(c, st, kPHist, 4.0 * pts);
@@ -413,16 +439,73 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
         if (prof_begin(c, st)) return LBKD_ECUDA;
         launch_sel_select(a, bp.b, st);
         prof_end(c, st, kPSelect, 0.0);
-        a.hist_next = nullptr;
-        if (fuse_next) {  // this level's histogram has been read by pick
-            CK(cudaMemsetAsync(bf.hist, 0, (2 * nseg * 512) * sizeof(u32), st));  // 2 children x 2^kFuseD
-            a.hist_next = bf.hist;
+        if (!pair) {
+            a.hist_next = nullptr;
+            if (fuse_next) {  // this level's histogram has been read by pick
+                CK(cudaMemsetAsync(bf.hist, 0, (2 * nseg * 512) * sizeof(u32), st));  // 2 children x 2^kFuseD
+                a.hist_next = bf.hist;
+            }
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            launch_sel_part(a, bp.b, st);
+            // reads every point of the level, writes all but the nodes
+            prof_end(c, st, kPPart, A * (2.0 * pts - (double)nseg));
+            fused_D = fuse_next ? 9 : 0;  // 9 = kFuseD (select.cu)
+        } else {
+            // ---- level l + 1, its segments still in the level-l layout ----
+            const LevelGeom g1 = view_of(bp, l + 1);
+            const int D1 = sel_digit_bits(g1.nseg) > 9 ? sel_digit_bits(g1.nseg) : 9;
+            SelArgs b = base_args(g1, D1, bpar ^ 1);
+            b.pair = 1;
+            b.g0 = g;
+            b.piv = bf.piv2;
+            b.chains = bf.chains2;
+            b.ppos = bf.ppos2;
+            b.piv0 = bf.piv;
+            b.chains0 = bf.chains;
+            b.ppos0 = bf.ppos;
+            b.tile_lt = bf.tile_lt2;
+            b.sub_lt = bf.sub_lt2;
+            b.lt_tstride = 2 * ntl;
+            b.lt_sstride = 2 * ntl * (T / 256);  // 256-position warp subtiles (select.cu kSub)
+            b.tile_lt0 = bf.tile_lt;
+            b.sub_lt0 = bf.sub_lt;
+            CK(cudaMemsetAsync(bf.hist, 0, (g1.nseg << D1) * sizeof(u32), st));
+            CK(cudaMemsetAsync(bf.cand_ctr, 0, sizeof(u32), st));
+            CK(cudaMemsetAsync(bf.tile_lt2, 0, 2 * b.lt_tstride * sizeof(u32), st));
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            launch_sel_child_hist(b, bp.b, st);
+            prof_end(c, st, kPHist, 8.0 * pts);
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            launch_sel_pick(b, st);
+            prof_end(c, st, kPPick, 4.0 * (double)(g1.nseg << D1));
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            launch_sel_filter_pair(b, bp.b, st);
+            prof_end(c, st, kPFilter, 8.0 * pts);
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            launch_sel_select(b, bp.b, st);
+            prof_end(c, st, kPSelect, 0.0);
+            b.hist_next = nullptr;
+            // the fused level-(l+2) histogram: 2^fd bins per grandchild (9:
+            // the partition's ring has 2 stages so the bins fit; LBKD_PAIR_FD)
+            static const int pair_fd = [] {
+                const char* e = getenv("LBKD_PAIR_FD");
+                return e && atoi(e) == 8 ? 8 : 9;
+            }();
+            b.fuse_d = pair_fd;
+            if (fuse_next) {  // 4 grandchildren x 2^fd per parent
+                CK(cudaMemsetAsync(bf.hist, 0, (4 * nseg << pair_fd) * sizeof(u32), st));
+                b.hist_next = bf.hist;
+            }
+            if (prof_begin(c, st)) return LBKD_ECUDA;
+            launch_sel_part_pair(b, bp.b, st);
+            // reads every point of level l, writes all but its nodes and their children's
+            prof_end(c, st, kPPart, A * (2.0 * pts - 3.0 * (double)nseg));
+            fused_D = fuse_next ? pair_fd : 0;
         }
-        if (prof_begin(c, st)) return LBKD_ECUDA;
-        launch_sel_part(a, bp.b, st);
-        // reads every point of the level, writes all but the nodes
-        prof_end(c, st, kPPart, A * (2.0 * pts - (double)nseg));
+        wpar ^= 1u;
+        l = lnext;
     }
+    c->w_par_end = (int)wpar;
     return LBKD_OK;
 }
 
@@ -436,7 +519,7 @@ static int run_levels(lbkd_ctx* c, const BuildParams& bp, int lfrom, int lto, cu
 static int run_subtrees(lbkd_ctx* c, const BuildParams& bp, int lam0, cudaStream_t st) {
     if (prof_begin(c, st)) return LBKD_ECUDA;
     const int entry_sorted = c->algo != 0 || lam0 == 0;
-    const int src_par = c->algo == 0 ? ((lam0 - bp.lroot) & 1) : -1;
+    const int src_par = c->algo != 0 ? -1 : (bp.pair ? c->w_par_end : ((lam0 - bp.lroot) & 1));
     launch_subtree(bp, c->bf, lam0, entry_sorted, src_par, st);
     // each point of the subtrees is read once (k coords + index) and written
     // once to its level-order slot (k coords + perm)
@@ -567,6 +650,7 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.dbg = d_trace;
     bp.wt = c->cur_wt;
     bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : (mode == kWidest ? 1 : 0);
+    bp.pair = c->pair_levels && mode == kRoundRobin && c->algo == 0 && !d_trace;
     // the select path is a fixed, host-sync-free sequence for given buffers:
     // capture it once into a CUDA graph and replay it (the sort path carries
     // per-launch lookback epochs and is always launched directly)
@@ -1016,6 +1100,7 @@ int lbkd_create(lbkd_ctx** out, int device) {
     cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
     lbkd_ctx* c = new lbkd_ctx();
     c->device = device;
+    if (const char* e = getenv("LBKD_PAIR")) c->pair_levels = e[0] != '0';
     const char* algo = getenv("LBKD_ALGO");
     if (algo && strcmp(algo, "sort") == 0) c->algo = 1;
     const char* gr = getenv("LBKD_GRAPH");
@@ -1069,6 +1154,11 @@ void lbkd_destroy(lbkd_ctx* c) {
     cudaFree(c->bf.tile_lt);
     cudaFree(c->bf.sub_lt);
     cudaFree(c->bf.ppos);
+    cudaFree(c->bf.piv2);
+    cudaFree(c->bf.chains2);
+    cudaFree(c->bf.ppos2);
+    cudaFree(c->bf.tile_lt2);
+    cudaFree(c->bf.sub_lt2);
     cudaFree(c->bf.seg_and);
     cudaFree(c->bf.seg_or);
     cudaFree(c->bf.status);

@@ -78,6 +78,14 @@ struct Buffers {
     u32* err;         // [0] non-finite flag
     float* boxes[2];  // widest: boxes of the level's nodes [nseg][2k]
     uint8_t* bmode[2];  // bucket mode of the level's nodes (0 value-linear, 1 key-linear)
+    // level pairs (select.cu, "two levels per partition"): the second
+    // level's pivot records / chains / positions and its below-pivot counts
+    // per child side ([2][tiles][2], [2][subtiles][2]) beside the first's
+    u32* piv2;
+    Chain* chains2;
+    u32* ppos2;
+    u32* tile_lt2;
+    u32* sub_lt2;
 };
 
 struct BuildParams {
@@ -94,6 +102,7 @@ struct BuildParams {
     int lroot = 0;         // sub-build: root node (level, index) of the view;
     u64 jroot = 0;         // the whole tree is (0, 0)
     WidthTab wt{};         // float64 builds: rank-coded coordinates' value table (else wt.v == null)
+    int pair = 0;          // round robin: global levels two per partition pass (select.cu)
 };
 
 inline LevelGeom view_of(const BuildParams& bp, int l) { return make_view(bp.n, l, bp.lroot, bp.jroot); }
@@ -130,6 +139,19 @@ struct SelArgs {
     int tiles_per_cta;
     u64 ntiles;
     WidthTab wt;           // widths of rank-coded (float64) builds
+    // level pairs: the second level of a pair (a.g = the children, level
+    // l + 1) still in its parents' layout (g0 = level l): parents' pivot
+    // records, chains, positions and below counts; side strides of the
+    // children's count arrays (tile_lt / sub_lt = [2][...][2])
+    int pair;
+    LevelGeom g0;
+    const u32* piv0;
+    const Chain* chains0;
+    const u32* ppos0;
+    const u32* tile_lt0;
+    const u32* sub_lt0;
+    u64 lt_tstride, lt_sstride;
+    int fuse_d;            // pair partition: bins of its fused histogram (2^fuse_d per grandchild)
 };
 int sel_digit_bits(u64 nseg);
 void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cudaStream_t st);
@@ -143,6 +165,9 @@ void launch_sel_select(const SelArgs& a, int b, cudaStream_t st);
 int sel_items(int b);
 int sel_tile(int b);
 void launch_sel_part(const SelArgs& a, int b, cudaStream_t st);
+void launch_sel_child_hist(const SelArgs& a, int b, cudaStream_t st);
+void launch_sel_filter_pair(const SelArgs& a, int b, cudaStream_t st);
+void launch_sel_part_pair(const SelArgs& a, int b, cudaStream_t st);
 
 // global_sort.cu
 void launch_init(const BuildParams& bp, const Buffers& bf, cudaStream_t st);

@@ -37,6 +37,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace lbkd {
 
@@ -64,6 +65,50 @@ __device__ __forceinline__ int seg_key_dim(const SelArgs& a, u64 t) {
         return d >= 0 ? d : a.g.l % a.k;
     }
     return (int)a.split_dims[a.g.Fl + a.g.sbase + t];
+}
+
+// Level pairs: the key of a level-(l+1) child that still lies in its
+// parent's layout.  rr_key_dim as usual; a child whose chain dims are all
+// pinned (its order is the input order) is keyed by its INDEX column (k),
+// key-linear over [0, n) -- an index is a nonnegative u32, so its float
+// bits' flipped key is the index plus 2^31, monotone -- instead of being
+// made positional (its in-order slot is not known before the split).
+struct PairKey {
+    int d;
+    float lo, hi;
+    int mode;
+};
+
+__device__ __forceinline__ PairKey pair_child_key(const float* box, uint8_t bmode, int k, int l1, u64 n) {
+    PairKey p;
+    const int d = rr_key_dim(box, k, l1);
+    if (d >= 0) {
+        p.d = d;
+        p.lo = box[d];
+        p.hi = box[k + d];
+        p.mode = bmode;
+    } else {
+        p.d = k;
+        p.lo = __uint_as_float(0u);
+        p.hi = __uint_as_float((u32)n);
+        p.mode = 1;
+    }
+    return p;
+}
+
+// side of the point at layout position pos against a pivot whose leading
+// coordinate it ties: the rest of the node's chain, then the input row
+// (0 below, 1 above, 2 the pivot itself)
+__device__ __noinline__ int tie_side_of(const u32* W, u64 stride, int k, const Chain* ch, const u32* pv, u64 pos) {
+    const u32 mm = ch->m;
+    for (u32 f = 1; f < mm; ++f) {
+        const int d = ch->d[f];
+        const u32 xx = flip_key(__uint_as_float(W[(u64)d * stride + pos]));
+        const u32 yy = flip_key(__uint_as_float(pv[d]));
+        if (xx != yy) return xx < yy ? 0 : 1;
+    }
+    const u32 xx = W[(u64)k * stride + pos], yy = pv[k];
+    return xx < yy ? 0 : (xx > yy ? 1 : 2);
 }
 
 __device__ __forceinline__ int bitlen32(u32 v) { return v ? 32 - __clz(v) : 0; }
@@ -126,6 +171,16 @@ __device__ __forceinline__ bool key_mode(const Bucketer& b) { return b.scale < 0
 
 __device__ __forceinline__ u32 bucket_of(const Bucketer& b, u32 bits) {
     return key_mode(b) ? bucket_key(b, bits) : bucket_val(b, bits);
+}
+
+// field-wise select of two bucketers (a conditional on the structs would
+// take their addresses: local memory)
+__device__ __forceinline__ Bucketer bsel2(bool second, const Bucketer& b0, const Bucketer& b1) {
+    Bucketer b;
+    b.hlo = second ? b1.hlo : b0.hlo;
+    b.scale = second ? b1.scale : b0.scale;
+    b.top = second ? b1.top : b0.top;
+    return b;
 }
 
 // Incremental segment cursor over the view's in-order positions for a CTA
@@ -419,7 +474,7 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
     // the segment equal): the within-node order is the input order, which is
     // the segment's order in W (stable partitions) -- the node is the element
     // at in-order offset pivot_off, no histogram and no candidates to sort
-    {
+    if (!a.pair) {  // (level pairs: such a child is keyed by its index column, pair_child_key)
         const float* box = a.boxes_in + j * 2ull * a.k;
         bool point = true;
         if (a.mode == kRoundRobin) {
@@ -453,11 +508,18 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
         while (cum + h[b] <= po) { cum += h[b]; ++b; }
         u32* sel = a.sel + j * kSelW;
         const u32 C = h[b];
-        const int d = seg_key_dim(a, j);
         const float* box = a.boxes_in + j * 2ull * a.k;
-        sel[kSelLo] = __float_as_uint(box[d]);  // the filter rebuilds the bucketer
-        sel[kSelShift] = __float_as_uint(box[a.k + d]);
-        sel[kSelMode] = a.bmode_in[j];
+        if (a.pair) {
+            const PairKey pk = pair_child_key(box, a.bmode_in[j], a.k, a.g.l, a.g.n);
+            sel[kSelLo] = __float_as_uint(pk.lo);
+            sel[kSelShift] = __float_as_uint(pk.hi);
+            sel[kSelMode] = (u32)pk.mode;
+        } else {
+            const int d = seg_key_dim(a, j);
+            sel[kSelLo] = __float_as_uint(box[d]);  // the filter rebuilds the bucketer
+            sel[kSelShift] = __float_as_uint(box[a.k + d]);
+            sel[kSelMode] = a.bmode_in[j];
+        }
         sel[kSelB] = (u32)b;
         sel[kSelR] = po - cum;
         sel[kSelC] = C;
@@ -725,16 +787,22 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
     const Chain ch = s_ch;
     // the segment's tiles: the first one holds it as part 1 unless the
     // segment starts exactly at the tile start
-    const u64 ib = v_ibegin(g, j);
+    // (level pairs: the candidates' positions and the count slots are those
+    // of the PARENT's layout, one count array per child side)
+    const u64 jl = a.pair ? (j >> 1) : j;
+    const LevelGeom& gl = a.pair ? a.g0 : g;
+    u32* const tlt = a.tile_lt + (a.pair ? (j & 1) * a.lt_tstride : 0ull);
+    u32* const slt = a.sub_lt + (a.pair ? (j & 1) * a.lt_sstride : 0ull);
+    const u64 ib = v_ibegin(gl, jl);
     const u64 tfirst = ib / (u64)T;
-    const u64 tlast = (ib + v_size(g, j) - 1) / (u64)T;
+    const u64 tlast = (ib + v_size(gl, jl) - 1) / (u64)T;
     const u32 pfirst = (ib == tfirst * (u64)T) ? 0u : 1u;
     auto count_below = [&](const u32* rec) {
         const u64 pos = rec[k + 1];
         const u64 t = pos / (u64)T;
         const u32 pt = t == tfirst ? pfirst : 0u;
-        atomicAdd(&a.tile_lt[t * 2 + pt], 1u);
-        atomicAdd(&a.sub_lt[(pos / (u64)kSub) * 2 + pt], 1u);
+        atomicAdd(&tlt[t * 2 + pt], 1u);
+        atomicAdd(&slt[(pos / (u64)kSub) * 2 + pt], 1u);
     };
     u32 n = sel[kSelC];
     u32 r = sel[kSelR];
@@ -911,7 +979,7 @@ __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
     u32 carry = 0;
     for (u64 t0 = tfirst; t0 <= tlast; t0 += NT) {
         const u64 t = t0 + tid;
-        u32* slot = t <= tlast ? &a.tile_lt[t * 2 + (t == tfirst ? pfirst : 0u)] : nullptr;
+        u32* slot = t <= tlast ? &tlt[t * 2 + (t == tfirst ? pfirst : 0u)] : nullptr;
         const u32 v = slot ? *slot : 0u;
         const u32 ex = block_exclusive_scan<u32>(v, wtot, nullptr);
         if (slot) *slot = carry + ex;
@@ -940,20 +1008,8 @@ constexpr int kPRows = kSub / 32;
 
 // equal leading coordinates: compare the rest of the node's chain, then the
 // input row (rare; re-reads the point from the source arrays)
-__device__ __noinline__ int part_tie_side(const SelArgs& a, u64 j, u64 pos) {
-    const int k = a.k, A = k + 1;
-    const u32* W = a.bf.w[a.par];
-    const Chain* ch = a.chains + j;
-    const u32* pv = a.piv + j * A;
-    const u32 mm = ch->m;
-    for (u32 f = 1; f < mm; ++f) {
-        const int d = ch->d[f];
-        const u32 xx = flip_key(__uint_as_float(W[(u64)d * a.bf.stride + pos]));
-        const u32 yy = flip_key(__uint_as_float(pv[d]));
-        if (xx != yy) return xx < yy ? 0 : 1;
-    }
-    const u32 xx = W[(u64)k * a.bf.stride + pos], yy = pv[k];
-    return xx < yy ? 0 : (xx > yy ? 1 : 2);
+__device__ __forceinline__ int part_tie_side(const SelArgs& a, u64 j, u64 pos) {
+    return tie_side_of(a.bf.w[a.par], a.bf.stride, a.k, a.chains + j, a.piv + j * (a.k + 1), pos);
 }
 
 // D0 >= 0: every segment's leading key is coordinate D0 (round-robin): full
@@ -1316,15 +1372,27 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
                     }
                 }
             }
+            // in phases so the rows' dependency chains overlap: all ballots,
+            // then the destinations (two running sums), then histogram + stores
             auto rows = [&](auto bucket_fn) {
+                u32 ml[kPRows], mr[kPRows], dsts[kPRows];
+#pragma unroll
+                for (int i = 0; i < kPRows; ++i) {
+                    const u32 sd = (sides >> (2 * i)) & 3u;
+                    ml[i] = __ballot_sync(kFullMask, sd == 0u);
+                    mr[i] = __ballot_sync(kFullMask, sd == 1u);
+                }
+#pragma unroll
+                for (int i = 0; i < kPRows; ++i) {
+                    const u32 sd = (sides >> (2 * i)) & 3u;
+                    dsts[i] = sd == 0u ? bl + __popc(ml[i] & lt) : br + __popc(mr[i] & lt);
+                    bl += __popc(ml[i]);
+                    br += __popc(mr[i]);
+                }
 #pragma unroll
                 for (int i = 0; i < kPRows; ++i) {
                     const int side = (int)((sides >> (2 * i)) & 3u);
-                    const u32 ml = __ballot_sync(kFullMask, side == 0);
-                    const u32 mr = __ballot_sync(kFullMask, side == 1);
-                    const u32 dst = side == 0 ? bl + __popc(ml & lt) : br + __popc(mr & lt);
-                    bl += __popc(ml);
-                    br += __popc(mr);
+                    const u32 dst = dsts[i];
                     if (fuse && side < 2) {
                         const u32 kn = V(side ? hdn1 : hdn0, i);
                         const u32 hbk = bucket_fn(side ? hb1 : hb0, kn);
@@ -1421,6 +1489,793 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
     if (fuse) hflush();
 }
 
+
+// ===========================================================================
+// Level pairs (round robin, k <= 4): two global levels per partition pass.
+// Level l runs hist -> pick -> filter -> select as above; its children (level
+// l + 1) are then selected while still in the level-l layout:
+//   child hist  : every point's side against its parent's pivot (chain on
+//                 ties), its child's key binned                 (8 B/pt)
+//   pick        : as above, keys by pair_child_key
+//   filter pair : the same sides, per (subtile, parent part, child side)
+//                 counts below b* and the candidates              (8 B/pt)
+//   select      : as above, count slots of the parent's layout per side
+//   part pair   : ONE stable 4-way partition of every parent into its four
+//                 grandchild runs (the three pivots are already written),
+//                 fused with the level-(l+2) histogram of the grandchildren
+// -- 16 B/pt of key reads replace one whole 8(k+1) B/pt partition pass and a
+// filter pass per pair of levels.
+// ===========================================================================
+
+// level-(l+1) histogram of the children of every level-l segment (2^D bins
+// per child, D = a.D); one CTA walks a contiguous run of tiles and flushes
+// its shared bins when the parent changes
+template <int ITEMS>
+__global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
+    extern __shared__ u32 h[];  // [2][2^D]
+    constexpr int T = kHThreads * ITEMS;
+    const int nb = 1 << a.D;
+    const LevelGeom& g0 = a.g0;
+    const int k = a.k, A = k + 1;
+    const u64 stride = a.bf.stride;
+    const u32* W = a.bf.w[a.par];
+    for (int i = threadIdx.x; i < 2 * nb; i += kHThreads) h[i] = 0u;
+    const u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
+    u64 t1 = t0 + a.tiles_per_cta;
+    if (t1 > a.ntiles) t1 = a.ntiles;
+    SegCursor sc;
+    sc.init(g0, t0 * T);
+    u64 cur = ~0ull;  // the parent whose children's bins are in h
+    __syncthreads();
+    auto flush = [&]() {
+        __syncthreads();
+        if (cur != ~0ull) {
+            u32* gh = a.hist + 2 * cur * (u64)nb;
+            for (int i = threadIdx.x; i < 2 * nb; i += kHThreads) {
+                const u32 v = h[i];
+                if (v) {
+                    atomicAdd(&gh[i], v);
+                    h[i] = 0u;
+                }
+            }
+        }
+        __syncthreads();
+    };
+    int dl = 0, dk0 = 0, dk1 = 0;
+    float y = 0.f;
+    Bucketer b0{}, b1{};
+    for (u64 t = t0; t < t1; ++t) {
+        const u64 ts = t * T;
+        const u64 cnt = g0.nview - ts < (u64)T ? g0.nview - ts : (u64)T;
+        u32 r0a, r0b, r1a, r1b;
+        bool has1;
+        sc.parts(g0, ts, cnt, r0a, r0b, r1a, r1b, has1);
+#pragma unroll 1
+        for (int p = 0; p < 2; ++p) {
+            if (p == 1 && !has1) break;
+            const u64 j = sc.cur + p;
+            const u32 ra = p ? r1a : r0a, rb = p ? r1b : r0b;
+            if (ra >= rb) continue;
+            if (j != cur) {
+                flush();
+                cur = j;
+                dl = a.chains0[j].d[0];
+                y = __uint_as_float(a.piv0[j * A + dl]);
+                const PairKey p0 = pair_child_key(a.boxes_in + (2 * j) * 2ull * k, a.bmode_in[2 * j], k, a.g.l, a.g.n);
+                const PairKey p1 =
+                    pair_child_key(a.boxes_in + (2 * j + 1) * 2ull * k, a.bmode_in[2 * j + 1], k, a.g.l, a.g.n);
+                dk0 = p0.d;
+                dk1 = p1.d;
+                b0 = make_bucketer(p0.lo, p0.hi, a.D, p0.mode);
+                b1 = make_bucketer(p1.lo, p1.hi, a.D, p1.mode);
+            }
+            // ITEMS consecutive positions per thread: both key columns
+            // loaded up front (16-byte loads) when the children share their
+            // key dim, so the loads do not wait on the side compares
+            const u32 r0 = (u32)threadIdx.x * ITEMS;
+            const bool same = dk0 == dk1;
+            u32 xk[ITEMS], kv[ITEMS];
+            const u32* kl = W + (u64)dl * stride + ts + r0;
+            const u32* kc = W + (u64)dk0 * stride + ts + r0;
+            if (ITEMS % 4 == 0 && r0 >= ra && r0 + ITEMS <= rb) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; i += 4) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(kl + i);
+                    xk[i] = q.x; xk[i + 1] = q.y; xk[i + 2] = q.z; xk[i + 3] = q.w;
+                }
+                if (same) {
+#pragma unroll
+                    for (int i = 0; i < ITEMS; i += 4) {
+                        const uint4 q = *reinterpret_cast<const uint4*>(kc + i);
+                        kv[i] = q.x; kv[i + 1] = q.y; kv[i + 2] = q.z; kv[i + 3] = q.w;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 r = r0 + (u32)i;
+                    const bool in = r >= ra && r < rb;
+                    xk[i] = in ? kl[i] : 0u;
+                    kv[i] = (in && same) ? kc[i] : 0u;
+                }
+            }
+            const bool ub = same && b0.hlo == b1.hlo && b0.scale == b1.scale && b0.top == b1.top;
+            if (ub && r0 >= ra && r0 + ITEMS <= rb) {
+                // common case: one key column and one bucketer for both
+                // children; sides by float compares, the rare ties apart
+                u32 sides = 0;
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const float x = __uint_as_float(xk[i]);
+                    sides |= (x < y ? 0u : (x > y ? 1u : 2u)) << (2 * i);
+                }
+                if (sides & 0xAAAAu) {
+                    for (int i = 0; i < ITEMS; ++i)
+                        if (((sides >> (2 * i)) & 3u) == 2u) {
+                            const u32 sd = (u32)tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A,
+                                                            ts + r0 + (u32)i);
+                            sides = (sides & ~(3u << (2 * i))) | (sd << (2 * i));
+                        }
+                }
+                auto items = [&](auto bucket_fn) {
+#pragma unroll
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const u32 sd = (sides >> (2 * i)) & 3u;
+                        if (sd < 2u) atomicAdd(&h[(int)sd * nb + (int)bucket_fn(b0, kv[i])], 1u);
+                    }
+                };
+                if (key_mode(b0)) items([](const Bucketer& bb, u32 x) { return bucket_key(bb, x); });
+                else items([](const Bucketer& bb, u32 x) { return bucket_val(bb, x); });
+                continue;
+            }
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const u32 r = r0 + (u32)i;
+                if (r >= ra && r < rb) {
+                    const float x = __uint_as_float(xk[i]);
+                    int side = x < y ? 0 : (x > y ? 1 : 2);  // -0.0 == +0.0 like numpy
+                    if (side == 2) side = tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A, ts + r);
+                    if (side < 2) {
+                        const u32 key = same ? kv[i] : W[(u64)(side ? dk1 : dk0) * stride + ts + r];
+                        const u32 b = bucket_of(bsel2(side != 0, b0, b1), key);
+                        atomicAdd(&h[side * nb + (int)b], 1u);
+                    }
+                }
+            }
+        }
+    }
+    flush();
+}
+
+// filter of the second level of a pair: per tile (parent parts as in the
+// filter above) every point's child side, then its child's bucket against
+// that child's b*: counts below b* per (subtile, part, side) and (tile,
+// part, side), and the hits as candidate records (position = the parent
+// layout's) staged per CTA like the filter above
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
+    constexpr int ITEMS = 8;
+    constexpr int T = THREADS * ITEMS;
+    constexpr int NSUB = T / kSub;
+    const LevelGeom& g0 = a.g0;
+    const u32* W = a.bf.w[a.par];
+    const u64 stride = a.bf.stride;
+    const int k = a.k, A = k + 1, R = k + 2;
+    extern __shared__ u32 fsm[];  // [0] staged count, [kFCap] segment ids, [kFCap * R] records
+    u32* const s_seg = fsm + 1;
+    u32* const s_rec = s_seg + kFCap;
+    for (int e = threadIdx.x; e < kFCap; e += THREADS) s_seg[e] = ~0u;
+    if (threadIdx.x == 0) fsm[0] = 0u;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u64 t0 = (u64)blockIdx.x * a.tiles_per_cta;
+    u64 t1 = t0 + a.tiles_per_cta;
+    if (t1 > a.ntiles) t1 = a.ntiles;
+    if (t0 < t1) {
+        SegCursor sc;
+        sc.init(g0, t0 * T);
+        u64 cj = ~0ull;
+        int dl = 0, dk0 = 0, dk1 = 0;
+        float y = 0.f;
+        Bucketer bk0{}, bk1{};
+        u32 bs0 = 0u, bs1 = 0u;
+        bool ub = false;  // the two children's bucketers are equal
+        for (u64 t = t0; t < t1; ++t) {
+            const u64 ts = t * T;
+            const u64 cnt = g0.nview - ts < (u64)T ? g0.nview - ts : (u64)T;
+            u32 r0a, r0b, r1a, r1b;
+            bool has1;
+            sc.parts(g0, ts, cnt, r0a, r0b, r1a, r1b, has1);
+            const u64 s = t * NSUB + warp;
+            u32 n00 = 0u, n01 = 0u, n10 = 0u, n11 = 0u;  // below counts [part][side]
+#pragma unroll 1
+            for (int part = 0; part < 2; ++part) {
+                const u64 j = sc.cur + part;
+                const u32 ra = part ? r1a : r0a, rb = part ? r1b : r0b;
+                if (!((part == 0 || has1) && ra < rb)) continue;
+                if (j != cj) {  // the parent's pivot and its children's picks, kept while tiles stay in it
+                    cj = j;
+                    dl = a.chains0[j].d[0];
+                    y = __uint_as_float(a.piv0[j * A + dl]);
+                    const u32* sl0 = a.sel + (2 * j) * kSelW;
+                    const u32* sl1 = sl0 + kSelW;
+                    bk0 = make_bucketer(__uint_as_float(sl0[kSelLo]), __uint_as_float(sl0[kSelShift]), a.D,
+                                        (int)sl0[kSelMode]);
+                    bk1 = make_bucketer(__uint_as_float(sl1[kSelLo]), __uint_as_float(sl1[kSelShift]), a.D,
+                                        (int)sl1[kSelMode]);
+                    bs0 = sl0[kSelB];
+                    bs1 = sl1[kSelB];
+                    dk0 = pair_child_key(a.boxes_in + (2 * j) * 2ull * k, a.bmode_in[2 * j], k, a.g.l, a.g.n).d;
+                    dk1 = pair_child_key(a.boxes_in + (2 * j + 1) * 2ull * k, a.bmode_in[2 * j + 1], k, a.g.l, a.g.n).d;
+                    ub = bk0.hlo == bk1.hlo && bk0.scale == bk1.scale && bk0.top == bk1.top;
+                }
+                const u32 r0 = (u32)threadIdx.x * ITEMS;
+                u32 key[ITEMS];
+                if (r0 >= ra && r0 + ITEMS <= rb) {
+                    const u32* kp = W + (u64)dl * stride + ts + r0;
+                    const uint4 q0 = *reinterpret_cast<const uint4*>(kp);
+                    const uint4 q1 = *reinterpret_cast<const uint4*>(kp + 4);
+                    key[0] = q0.x; key[1] = q0.y; key[2] = q0.z; key[3] = q0.w;
+                    key[4] = q1.x; key[5] = q1.y; key[6] = q1.z; key[7] = q1.w;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const u32 r = r0 + (u32)i;
+                        key[i] = (r >= ra && r < rb) ? W[(u64)dl * stride + ts + r] : 0u;
+                    }
+                }
+                // the children's key column up front when they share it
+                const bool same = dk0 == dk1;
+                u32 ck[ITEMS];
+                {
+                    const u32* kc = W + (u64)dk0 * stride + ts + r0;
+                    if (same && r0 >= ra && r0 + ITEMS <= rb) {
+                        const uint4 q0 = *reinterpret_cast<const uint4*>(kc);
+                        const uint4 q1 = *reinterpret_cast<const uint4*>(kc + 4);
+                        ck[0] = q0.x; ck[1] = q0.y; ck[2] = q0.z; ck[3] = q0.w;
+                        ck[4] = q1.x; ck[5] = q1.y; ck[6] = q1.z; ck[7] = q1.w;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < ITEMS; ++i) {
+                            const u32 r = r0 + (u32)i;
+                            ck[i] = (same && r >= ra && r < rb) ? kc[i] : 0u;
+                        }
+                    }
+                }
+                u32 hits = 0, hside = 0, nlt0 = 0, nlt1 = 0;
+                const bool inside = r0 >= ra && r0 + ITEMS <= rb;
+                if (inside && same && ub) {
+                    // common case: all 8 items in the part, both children keyed
+                    // by one column and one bucketer (their box ranges in the
+                    // key dim are the parent's): sides by float compares, the
+                    // rare ties apart, then one bucket per item
+                    u32 sides = 0;
+#pragma unroll
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const float x = __uint_as_float(key[i]);
+                        sides |= (x < y ? 0u : (x > y ? 1u : 2u)) << (2 * i);
+                    }
+                    if (sides & 0xAAAAu) {
+                        for (int i = 0; i < ITEMS; ++i)
+                            if (((sides >> (2 * i)) & 3u) == 2u) {
+                                const u32 sd = (u32)tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A,
+                                                                ts + r0 + (u32)i);
+                                sides = (sides & ~(3u << (2 * i))) | (sd << (2 * i));
+                            }
+                    }
+                    u32 cnt = 0;  // below b*: side 0 low half, side 1 high half
+                    auto items = [&](auto bucket_fn) {
+#pragma unroll
+                        for (int i = 0; i < ITEMS; ++i) {
+                            const u32 sd = (sides >> (2 * i)) & 3u;
+                            const u32 b = bucket_fn(bk0, ck[i]);
+                            const u32 bsel = sd ? bs1 : bs0;
+                            const bool in = sd < 2u;
+                            hits |= (in && b == bsel ? 1u : 0u) << i;
+                            hside |= (sd & 1u) << i;
+                            cnt += (in && b < bsel) ? (sd ? 0x10000u : 1u) : 0u;
+                        }
+                    };
+                    if (key_mode(bk0)) items([](const Bucketer& bb, u32 x) { return bucket_key(bb, x); });
+                    else items([](const Bucketer& bb, u32 x) { return bucket_val(bb, x); });
+                    nlt0 = cnt & 0xffffu;
+                    nlt1 = cnt >> 16;
+                } else {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const u32 r = r0 + (u32)i;
+                    if (r >= ra && r < rb) {
+                        const float x = __uint_as_float(key[i]);
+                        int side = x < y ? 0 : (x > y ? 1 : 2);
+                        if (side == 2) side = tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A, ts + r);
+                        if (side < 2) {
+                            const u32 kv = same ? ck[i] : W[(u64)(side ? dk1 : dk0) * stride + ts + r];
+                            const u32 b = bucket_of(bsel2(side != 0, bk0, bk1), kv);
+                            const u32 bsel = side ? bs1 : bs0;
+                            if (b == bsel) {
+                                hits |= 1u << i;
+                                hside |= (u32)side << i;
+                            }
+                            if (b < bsel) {
+                                if (side) ++nlt1;
+                                else ++nlt0;
+                            }
+                        }
+                    }
+                }
+                }
+                nlt0 = __reduce_add_sync(kFullMask, nlt0);
+                nlt1 = __reduce_add_sync(kFullMask, nlt1);
+                if (part) { n10 = nlt0; n11 = nlt1; }
+                else { n00 = nlt0; n01 = nlt1; }
+                if (lane == 0) {
+                    if (nlt0) atomicAdd(&a.tile_lt[t * 2 + part], nlt0);
+                    if (nlt1) atomicAdd(&a.tile_lt[a.lt_tstride + t * 2 + part], nlt1);
+                }
+                const u32 nh = (u32)__popc(hits);
+                const u32 wtot = __reduce_add_sync(kFullMask, nh);
+                if (wtot) {
+                    u32 x = nh;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const u32 yv = __shfl_up_sync(kFullMask, x, o);
+                        if (lane >= o) x += yv;
+                    }
+                    u32 pos = 0;
+                    if (lane == 31) pos = atomicAdd(&fsm[0], wtot);
+                    pos = __shfl_sync(kFullMask, pos, 31);
+                    const bool staged = pos + wtot <= (u32)kFCap;
+                    u32 q = pos + x - nh;
+                    while (hits) {
+                        const int i = __ffs(hits) - 1;
+                        hits &= hits - 1;
+                        const u32 r = r0 + (u32)i;
+                        const u32 c = (u32)(2 * j) + ((hside >> i) & 1u);
+                        u32* rec;
+                        if (staged) {  // staged in shared memory
+                            rec = s_rec + q * R;
+                            s_seg[q] = c;
+                            ++q;
+                        } else {  // staging full (tie-heavy data): a slot of the child's range directly
+                            u32* sel = a.sel + (u64)c * kSelW;
+                            rec = a.cand + (u64)(sel[kSelOff] + atomicAdd(&sel[kSelFill], 1u)) * R;
+                        }
+                        for (int cc = 0; cc < A; ++cc) rec[cc] = W[(u64)cc * stride + ts + r];
+                        rec[k + 1] = (u32)(ts + r);
+                    }
+                }
+            }
+            if (lane == 0) {
+                a.sub_lt[s * 2] = n00;
+                a.sub_lt[s * 2 + 1] = n10;
+                a.sub_lt[a.lt_sstride + s * 2] = n01;
+                a.sub_lt[a.lt_sstride + s * 2 + 1] = n11;
+            }
+        }
+    }
+    // the staged candidates -> their children's ranges (as in the filter above)
+    __syncthreads();
+    const u32 ltm = lanemask_lt();
+    const u32 nst = min(fsm[0], (u32)kFCap);
+    for (u32 e0 = (u32)warp * 32u; e0 < nst; e0 += (u32)THREADS) {
+        const u32 e = e0 + (u32)lane;
+        const u32 js = e < nst ? s_seg[e] : ~0u;
+        const u32 peers = __match_any_sync(kFullMask, js);
+        const int leader = __ffs(peers) - 1;
+        u32 base = 0;
+        if (js != ~0u && lane == leader) base = atomicAdd(&a.sel[(u64)js * kSelW + kSelFill], (u32)__popc(peers));
+        base = __shfl_sync(kFullMask, base, leader);
+        if (js != ~0u) {
+            const u32 slot = a.sel[(u64)js * kSelW + kSelOff] + base + (u32)__popc(peers & ltm);
+            const u32* src = s_rec + e * R;
+            u32* rec = a.cand + (u64)slot * R;
+            for (int c = 0; c < R; ++c) rec[c] = src[c];
+        }
+    }
+}
+
+// the pair partition: every parent segment -> its four grandchild runs
+//   LL [ib, ib + poL)          LR [ib + poL + 1, ib + po)
+//   RL [ib + po + 1, + poR)    RR [ib + po + 1 + poR + 1, ib + size)
+// (po, poL, poR: the parent's and the children's pivot offsets; their slots
+// stay holes).  A point's destination is its run's begin plus the number of
+// its run's points before it: per subtile from the two levels' below-pivot
+// prefixes (L before = level-l count; LL / RL before = level-(l+1) counts;
+// LR / RR by difference), inside the subtile by warp ballots.  Same TMA ring
+// and warp-owned subtile runs as sel_part_bulk_kernel; the fused histogram
+// bins the four grandchildren (2^FD bins each, 16-bit warp bins).
+struct PHdr2 {
+    u32 sl[3], tl[3], pp[3];  // part 0: lane's sub count words (l, L side, R side), tile prefixes, pivot positions
+    u32 y[3];                 // the three pivots' leading coordinates (parent, left child, right child)
+};
+
+template <int KMAX, int NST, int FD>
+__global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, int T) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int kGB = 1 << FD;  // bins per grandchild
+    constexpr int kWW = 2 * kGB;  // words of a warp's bins (4 grandchildren, two 16-bit bins per word)
+    const int lane = threadIdx.x & 31;
+    const int k = a.k, A = k + 1;
+    const LevelGeom& g0 = a.g0;  // parents: the layout
+    const LevelGeom& g1 = a.g;   // children
+    const u32* Wsrc = a.bf.w[a.par];
+    u32* Wdst = a.bf.w[a.par ^ 1u];
+    const u64 stride = a.bf.stride;
+    const u64 nsub = (g0.nview + kSub - 1) / kSub;
+    const int nsub_tile = T / kSub;
+    const u32 lt = lanemask_lt();
+    const int warp = threadIdx.x >> 5;
+    u64* bars = reinterpret_cast<u64*>(smem_raw) + warp * NST;
+    u32* ring = reinterpret_cast<u32*>(smem_raw + kPHistOff + sizeof(u32) * (kPThreads / 32) * kWW) +
+                (size_t)warp * NST * (KMAX + 1) * kSub;
+    if (lane == 0) {
+        for (int st = 0; st < NST; ++st) mbar_init(&bars[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](u64 s2, int st) {  // lane 0
+        const u64 ss2 = s2 * kSub;
+        const u64 cnt2 = g0.nview - ss2 < (u64)kSub ? g0.nview - ss2 : (u64)kSub;
+        const u32 bytes = (u32)(((cnt2 + 3) & ~3ull) * 4);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[st], bytes * (u32)A);
+        for (int c = 0; c < A; ++c)
+            bulk_g2s(ring + ((size_t)st * (KMAX + 1) + c) * kSub, Wsrc + (u64)c * stride + ss2, bytes, &bars[st]);
+    };
+    const u64 nw = (u64)gridDim.x * (kPThreads / 32);
+    const u64 chunk = (nsub + nw - 1) / nw;
+    u64 s = ((u64)blockIdx.x * (kPThreads / 32) + warp) * chunk;
+    const u64 s_end = s + chunk < nsub ? s + chunk : nsub;
+    if (lane == 0) {
+        for (int q = 0; q < NST - 1; ++q)
+            if (s + q < s_end) issue(s + q, q);
+    }
+    // fused level-(l+2) histogram: the four grandchildren of one parent
+    u32* wh = reinterpret_cast<u32*>(smem_raw + kPHistOff) + warp * kWW;
+    const bool fuse = a.hist_next != nullptr;
+    u64 hseg = ~0ull;
+    Bucketer hb0{}, hb1{}, hb2{}, hb3{};
+    int hd0 = 0, hd1 = 0, hd2 = 0, hd3 = 0;
+    bool hsides = false, hall = false;
+    int hmode = 4;  // 0: both sides value-linear, 3: both key-linear, else mixed / per grandchild
+    const int dn2 = (g1.l + 1) % k;
+    int hcnt = 0;
+    auto hflush = [&]() {
+        if (hseg != ~0ull) {
+            for (int i = lane; i < kWW; i += 32) {
+                const u32 v = wh[i];
+                if (v) {
+                    u32* gh = a.hist_next + (4 * hseg + i / (kGB / 2)) * (u64)kGB + 2 * (i % (kGB / 2));
+                    if (v & 0xffffu) atomicAdd(gh, v & 0xffffu);
+                    if (v >> 16) atomicAdd(gh + 1, v >> 16);
+                    wh[i] = 0u;
+                }
+            }
+        }
+        hcnt = 0;
+        __syncwarp();
+    };
+    if (fuse) {
+        for (int i = lane; i < kWW; i += 32) wh[i] = 0u;
+        __syncwarp();
+    }
+    const int tsh = 31 - __clz(T);
+    const int dl = g0.l % k, dl1 = g1.l % k;  // round robin: the parents' and children's leading dims
+    auto hdr_load = [&](u64 s2, PHdr2& h2) {
+        const u64 ss2 = s2 * kSub;
+        const u64 t2 = ss2 >> tsh;
+        const u64 j = v_seg_of(g0, ss2);
+        const u64 j0t = v_seg_of(g0, t2 << tsh);
+        const u32 pt = j == j0t ? 0u : 1u;
+        const int sin = (int)(s2 - t2 * (u64)nsub_tile);
+        const u64 w = (t2 * (u64)nsub_tile + lane) * 2 + pt;
+        h2.sl[0] = lane < sin ? a.sub_lt0[w] : 0u;
+        h2.sl[1] = lane < sin ? a.sub_lt[w] : 0u;
+        h2.sl[2] = lane < sin ? a.sub_lt[a.lt_sstride + w] : 0u;
+        h2.tl[0] = a.tile_lt0[t2 * 2 + pt];
+        h2.tl[1] = a.tile_lt[t2 * 2 + pt];
+        h2.tl[2] = a.tile_lt[a.lt_tstride + t2 * 2 + pt];
+        h2.pp[0] = a.ppos0[j];
+        h2.pp[1] = a.ppos[2 * j];
+        h2.pp[2] = a.ppos[2 * j + 1];
+        h2.y[0] = a.piv0[j * A + dl];
+        h2.y[1] = a.piv[(2 * j) * A + dl1];
+        h2.y[2] = a.piv[(2 * j + 1) * A + dl1];
+    };
+    // the four run bases of parent j at subtile start ss from its header
+    auto bases = [&](const PHdr2& h, u64 j, u64 ib, u64 ss, u32* b) {
+        const u32 nL = __reduce_add_sync(kFullMask, h.sl[0]) + h.tl[0];
+        const u32 nLL = __reduce_add_sync(kFullMask, h.sl[1]) + h.tl[1];
+        const u32 nRL = __reduce_add_sync(kFullMask, h.sl[2]) + h.tl[2];
+        const u64 before = ss > ib ? ss - ib : 0ull;
+        const u32 pb = (before > 0 && h.pp[0] < ss) ? 1u : 0u;
+        const u32 pLb = h.pp[1] < ss ? 1u : 0u;
+        const u32 pRb = h.pp[2] < ss ? 1u : 0u;
+        const u32 nR = (u32)before - nL - pb;
+        const u32 po = (u32)v_pivot(g0, j), poL = (u32)v_pivot(g1, 2 * j), poR = (u32)v_pivot(g1, 2 * j + 1);
+        const u32 ib32 = (u32)ib;
+        b[0] = ib32 + nLL;
+        b[1] = ib32 + poL + 1u + (nL - nLL - pLb);
+        b[2] = ib32 + po + 1u + nRL;
+        b[3] = ib32 + po + 1u + poR + 1u + (nR - nRL - pRb);
+    };
+    PHdr2 hn;
+    if (s < s_end) hdr_load(s, hn);
+    u32* dcol[KMAX + 1];
+#pragma unroll
+    for (int c = 0; c <= KMAX; ++c) dcol[c] = Wdst + (u64)(c < A ? c : 0) * stride;
+    u32 phases = 0u;
+    int stage = 0;
+    for (; s < s_end; ++s) {
+        const u64 ss = s * kSub;
+        const u64 cnt = g0.nview - ss < (u64)kSub ? g0.nview - ss : (u64)kSub;
+        const bool full = cnt == (u64)kSub;
+        if (lane == 0 && s + (NST - 1) < s_end) issue(s + (NST - 1), (stage + NST - 1) % NST);
+        mbar_wait(&bars[stage], (phases >> stage) & 1u);
+        phases ^= 1u << stage;
+        const u32* sv = ring + (size_t)stage * (KMAX + 1) * kSub + lane;
+#define V(c, i) (sv[(c) * kSub + (i) * 32])
+        const TileParts tp = tile_parts(g0, ss, cnt);
+        const PHdr2 h = hn;
+        if (s + 1 < s_end) hdr_load(s + 1, hn);
+        const u64 j0 = tp.j0;
+        if (full && !tp.has1 && tp.r0a == 0 && tp.r0b == (u32)kSub) {
+            // lean path: one parent covers the whole subtile
+            u32 b[4];
+            bases(h, j0, tp.ib0, ss, b);
+            const float y = __uint_as_float(h.y[0]);
+            const float yL = __uint_as_float(h.y[1]);
+            const float yR = __uint_as_float(h.y[2]);
+            if (fuse && j0 != hseg) {
+                hflush();
+                hseg = j0;
+                auto gset = [&](int q, int& hd, Bucketer& hbq) {
+                    const u64 c = 4 * hseg + q;
+                    const float* cb = a.boxes_out + c * 2ull * k;
+                    const int e = rr_key_dim(cb, k, g1.l + 1);
+                    hd = e >= 0 ? e : dn2;
+                    hbq = make_bucketer(cb[hd], cb[k + hd], FD, a.bmode_out[c]);
+                };
+                gset(0, hd0, hb0);
+                gset(1, hd1, hb1);
+                gset(2, hd2, hb2);
+                gset(3, hd3, hb3);
+                // the two grandchildren of a child share their key range and
+                // mode unless the child's own plane cut that key dim (k == 1
+                // or a pinned chain): then one bucketer per child side
+                auto same = [](const Bucketer& x, int dx, const Bucketer& z, int dz) {
+                    return dx == dz && x.hlo == z.hlo && x.scale == z.scale && x.top == z.top;
+                };
+                hsides = same(hb0, hd0, hb1, hd1) && same(hb2, hd2, hb3, hd3);
+                hall = hsides && same(hb0, hd0, hb2, hd2);  // k >= 3: one range for all four
+                hmode = hsides ? ((key_mode(hb0) ? 1 : 0) | (key_mode(hb2) ? 2 : 0)) : 4;
+            }
+            if (fuse) {
+                if (hcnt >= a.hflush_every) hflush();
+                ++hcnt;
+            }
+            // sides against the parent (2 bits per row), ties separately
+            u32 s1 = 0;
+#pragma unroll
+            for (int i = 0; i < kPRows; ++i) {
+                const float x = __uint_as_float(V(dl, i));
+                s1 |= (x < y ? 0u : (x > y ? 1u : 2u)) << (2 * i);
+            }
+            if (__any_sync(kFullMask, (s1 & 0xAAAAu) != 0u)) {
+                for (int i = 0; i < kPRows; ++i) {
+                    if (((s1 >> (2 * i)) & 3u) == 2u) {
+                        const u32 sd = (u32)tie_side_of(Wsrc, stride, k, a.chains0 + j0, a.piv0 + j0 * A,
+                                                        ss + (u64)(i * 32 + lane));
+                        s1 = (s1 & ~(3u << (2 * i))) | (sd << (2 * i));
+                    }
+                }
+            }
+            // sides against the child's pivot (3: the parent's pivot row)
+            u32 s2 = 0;
+#pragma unroll
+            for (int i = 0; i < kPRows; ++i) {
+                const u32 a1 = (s1 >> (2 * i)) & 3u;
+                u32 sd = 3u;
+                if (a1 < 2u) {
+                    const float x = __uint_as_float(V(dl1, i));
+                    const float yy = a1 ? yR : yL;
+                    sd = x < yy ? 0u : (x > yy ? 1u : 2u);
+                }
+                s2 |= sd << (2 * i);
+            }
+            if (__any_sync(kFullMask, (s2 & 0xAAAAu & ~(s2 << 1)) != 0u)) {  // some row == 2 (not 3)
+                for (int i = 0; i < kPRows; ++i) {
+                    if (((s2 >> (2 * i)) & 3u) == 2u) {
+                        const u64 c = 2 * j0 + ((s1 >> (2 * i)) & 1u);
+                        const u32 sd = (u32)tie_side_of(Wsrc, stride, k, a.chains + c, a.piv + c * A,
+                                                        ss + (u64)(i * 32 + lane));
+                        s2 = (s2 & ~(3u << (2 * i))) | (sd << (2 * i));
+                    }
+                }
+            }
+            // rows without any of the three pivots (all but <= 3 rows of a
+            // parent): two ballots, counts by difference
+            const bool allv = !__any_sync(kFullMask, ((s1 | s2) & 0xAAAAu) != 0u);
+            auto rows = [&](auto bucket_fn, auto av_tag) {
+                constexpr bool AV = decltype(av_tag)::value;
+#pragma unroll
+            for (int i = 0; i < kPRows; ++i) {
+                const u32 a1 = (s1 >> (2 * i)) & 3u, a2 = (s2 >> (2 * i)) & 3u;
+                const bool valid = AV || (a1 < 2u && a2 < 2u);
+                const u32 q = 2u * a1 + a2;  // grandchild (when valid)
+                const u32 mv = AV ? kFullMask : __ballot_sync(kFullMask, valid);
+                const u32 m1 = __ballot_sync(kFullMask, valid && a1 == 1u);
+                const u32 m2 = __ballot_sync(kFullMask, valid && a2 == 1u);
+                const u32 mine = mv & (a1 ? m1 : ~m1) & (a2 ? m2 : ~m2);
+                const u32 base = q == 0u ? b[0] : (q == 1u ? b[1] : (q == 2u ? b[2] : b[3]));
+                const u32 dst = base + (u32)__popc(mine & lt);
+                if (AV) {
+                    const u32 n11 = (u32)__popc(m1 & m2), c1 = (u32)__popc(m1), c2 = (u32)__popc(m2);
+                    b[0] += 32u - c1 - c2 + n11;
+                    b[1] += c2 - n11;
+                    b[2] += c1 - n11;
+                    b[3] += n11;
+                } else {
+                    b[0] += (u32)__popc(mv & ~m1 & ~m2);
+                    b[1] += (u32)__popc(mv & ~m1 & m2);
+                    b[2] += (u32)__popc(mv & m1 & ~m2);
+                    b[3] += (u32)__popc(mv & m1 & m2);
+                }
+                if (valid) {
+                    if (fuse) {
+                        u32 hbk;
+                        if (hall) {
+                            hbk = bucket_fn(hb0, V(hd0, i));
+                        } else if (hsides) {  // one bucketer per child side
+                            hbk = bucket_fn(bsel2(a1 != 0u, hb0, hb2), V(a1 ? hd2 : hd0, i));
+                        } else {
+                            const int hd = q == 0u ? hd0 : (q == 1u ? hd1 : (q == 2u ? hd2 : hd3));
+                            const Bucketer hbq = bsel2(q >= 2u, bsel2(q == 1u, hb0, hb1), bsel2(q == 3u, hb2, hb3));
+                            hbk = bucket_of(hbq, V(hd, i));
+                        }
+                        atomicAdd(&wh[q * (kGB / 2) + (hbk >> 1)], (hbk & 1u) ? 0x10000u : 1u);
+                    }
+#pragma unroll
+                    for (int c = 0; c <= KMAX; ++c)
+                        if (c < A) dcol[c][dst] = V(c, i);
+                }
+            }
+            };
+            auto bv = [](const Bucketer& bb, u32 x) { return bucket_val(bb, x); };
+            auto bkk = [](const Bucketer& bb, u32 x) { return bucket_key(bb, x); };
+            auto bo = [](const Bucketer& bb, u32 x) { return bucket_of(bb, x); };
+            // rows without pivots, in phases so the rows' dependency chains
+            // overlap: all ballots, then the destinations (a 4-wide running
+            // sum), then the histogram and the stores
+            auto rows_av = [&](auto bucket_fn) {
+                u32 m1[kPRows], m2[kPRows], dsts[kPRows];
+#pragma unroll
+                for (int i = 0; i < kPRows; ++i) {
+                    m1[i] = __ballot_sync(kFullMask, (s1 >> (2 * i)) & 1u);
+                    m2[i] = __ballot_sync(kFullMask, (s2 >> (2 * i)) & 1u);
+                }
+#pragma unroll
+                for (int i = 0; i < kPRows; ++i) {
+                    const u32 a1 = (s1 >> (2 * i)) & 1u, a2 = (s2 >> (2 * i)) & 1u;
+                    const u32 q = 2u * a1 + a2;
+                    const u32 mine = (a1 ? m1[i] : ~m1[i]) & (a2 ? m2[i] : ~m2[i]);
+                    const u32 base = q == 0u ? b[0] : (q == 1u ? b[1] : (q == 2u ? b[2] : b[3]));
+                    dsts[i] = base + (u32)__popc(mine & lt);
+                    const u32 n11 = (u32)__popc(m1[i] & m2[i]), c1 = (u32)__popc(m1[i]), c2 = (u32)__popc(m2[i]);
+                    b[0] += 32u - c1 - c2 + n11;
+                    b[1] += c2 - n11;
+                    b[2] += c1 - n11;
+                    b[3] += n11;
+                }
+#pragma unroll
+                for (int i = 0; i < kPRows; ++i) {
+                    const u32 a1 = (s1 >> (2 * i)) & 1u, a2 = (s2 >> (2 * i)) & 1u;
+                    const u32 q = 2u * a1 + a2;
+                    if (fuse) {
+                        u32 hbk;
+                        if (hall) {
+                            hbk = bucket_fn(hb0, V(hd0, i));
+                        } else if (hsides) {
+                            hbk = bucket_fn(bsel2(a1 != 0u, hb0, hb2), V(a1 ? hd2 : hd0, i));
+                        } else {
+                            const int hd = q == 0u ? hd0 : (q == 1u ? hd1 : (q == 2u ? hd2 : hd3));
+                            const Bucketer hbq = bsel2(q >= 2u, bsel2(q == 1u, hb0, hb1), bsel2(q == 3u, hb2, hb3));
+                            hbk = bucket_of(hbq, V(hd, i));
+                        }
+                        atomicAdd(&wh[q * (kGB / 2) + (hbk >> 1)], (hbk & 1u) ? 0x10000u : 1u);
+                    }
+#pragma unroll
+                    for (int c = 0; c <= KMAX; ++c)
+                        if (c < A) dcol[c][dsts[i]] = V(c, i);
+                }
+            };
+            if (allv) {
+                if (hmode == 0) rows_av(bv);
+                else if (hmode == 3) rows_av(bkk);
+                else rows_av(bo);
+            } else {
+                rows(bo, std::false_type{});
+            }
+        } else {
+            // general path (a parent boundary inside the subtile, or the
+            // view's last partial subtile): runs (part, grandchild), ranks by
+            // match_any, the fused histogram by global atomics
+            u32 b[2][4];
+            bases(h, j0, tp.ib0, ss, b[0]);
+            if (tp.has1) {
+                PHdr2 h1;  // the second parent's header (its tile part index)
+                const u64 j1 = j0 + 1;
+                const u64 t2 = ss >> tsh;
+                const u64 j0t = v_seg_of(g0, t2 << tsh);
+                const u32 pt = j1 == j0t ? 0u : 1u;
+                const int sin = (int)(s - t2 * (u64)nsub_tile);
+                const u64 w = (t2 * (u64)nsub_tile + lane) * 2 + pt;
+                h1.sl[0] = lane < sin ? a.sub_lt0[w] : 0u;
+                h1.sl[1] = lane < sin ? a.sub_lt[w] : 0u;
+                h1.sl[2] = lane < sin ? a.sub_lt[a.lt_sstride + w] : 0u;
+                h1.tl[0] = a.tile_lt0[t2 * 2 + pt];
+                h1.tl[1] = a.tile_lt[t2 * 2 + pt];
+                h1.tl[2] = a.tile_lt[a.lt_tstride + t2 * 2 + pt];
+                h1.pp[0] = a.ppos0[j1];
+                h1.pp[1] = a.ppos[2 * j1];
+                h1.pp[2] = a.ppos[2 * j1 + 1];
+                bases(h1, j1, tp.ib1, ss, b[1]);
+            } else {
+                b[1][0] = b[1][1] = b[1][2] = b[1][3] = 0u;
+            }
+#pragma unroll 1
+            for (int i = 0; i < kPRows; ++i) {
+                const u32 r = (u32)(i * 32 + lane);
+                const bool in0 = r >= tp.r0a && r < tp.r0b, in1 = r >= tp.r1a && r < tp.r1b;
+                u32 run = 8u;  // 8: no run (outside the parts, or one of the three pivots)
+                if (in0 || in1) {
+                    const u64 j = j0 + (in1 ? 1 : 0);
+                    const u64 pos = ss + r;
+                    const float x = __uint_as_float(V(dl, i));
+                    const float yv = __uint_as_float(a.piv0[j * A + dl]);
+                    int a1 = x < yv ? 0 : (x > yv ? 1 : 2);
+                    if (a1 == 2) a1 = tie_side_of(Wsrc, stride, k, a.chains0 + j, a.piv0 + j * A, pos);
+                    if (a1 < 2) {
+                        const u64 c = 2 * j + a1;
+                        const float x2 = __uint_as_float(V(dl1, i));
+                        const float y2 = __uint_as_float(a.piv[c * A + dl1]);
+                        int a2 = x2 < y2 ? 0 : (x2 > y2 ? 1 : 2);
+                        if (a2 == 2) a2 = tie_side_of(Wsrc, stride, k, a.chains + c, a.piv + c * A, pos);
+                        if (a2 < 2) {
+                            const u32 q = 2u * (u32)a1 + (u32)a2;
+                            run = (in1 ? 4u : 0u) + q;
+                            if (fuse) {
+                                const u64 gc = 4 * j + q;
+                                const float* cb = a.boxes_out + gc * 2ull * k;
+                                const int e = rr_key_dim(cb, k, g1.l + 1);
+                                const int dnc = e >= 0 ? e : dn2;
+                                const Bucketer hbq = make_bucketer(cb[dnc], cb[k + dnc], FD, a.bmode_out[gc]);
+                                atomicAdd(&a.hist_next[gc * (u64)kGB + bucket_of(hbq, V(dnc, i))], 1u);
+                            }
+                        }
+                    }
+                }
+                const u32 peers = __match_any_sync(kFullMask, run);
+                u32 dst = 0;
+#pragma unroll
+                for (int rr = 0; rr < 8; ++rr)
+                    if (run == (u32)rr) dst = b[rr >> 2][rr & 3];
+                dst += (u32)__popc(peers & lt);
+#pragma unroll
+                for (int rr = 0; rr < 8; ++rr) b[rr >> 2][rr & 3] += (u32)__popc(__ballot_sync(kFullMask, run == (u32)rr));
+                if (run < 8u) {
+#pragma unroll
+                    for (int c = 0; c <= KMAX; ++c)
+                        if (c < A) dcol[c][dst] = V(c, i);
+                }
+            }
+        }
+#undef V
+        __syncwarp();
+        stage = stage + 1 == NST ? 0 : stage + 1;
+    }
+    if (fuse) hflush();
+}
 
 // ---------------------------------------------------------------------------
 // host side
@@ -1595,6 +2450,83 @@ void launch_sel_part(const SelArgs& a0, int b, cudaStream_t st) {
     }
 #undef LBKD_PART
 #undef LBKD_PART_D
+}
+
+void launch_sel_child_hist(const SelArgs& a0, int b, cudaStream_t st) {
+    SelArgs a = a0;
+    int items = (1 << (b - 1)) / kHThreads;
+    if (items > 8) items = 8;
+    const u64 T = (u64)kHThreads * items;
+    a.ntiles = (a.g0.nview + T - 1) / T;
+    const u64 target = 148 * 16;
+    u64 tpc = (a.ntiles + target - 1) / target;
+    if (tpc < 1) tpc = 1;
+    a.tiles_per_cta = (int)tpc;
+    const unsigned grid = (unsigned)((a.ntiles + tpc - 1) / tpc);
+    const size_t sm = sizeof(u32) * 2 << a.D;
+    auto go = [&](auto kern) {
+        if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kern<<<grid, kHThreads, sm, st>>>(a);
+    };
+    switch (items) {
+        case 8: go(sel_child_hist_kernel<8>); break;
+        case 4: go(sel_child_hist_kernel<4>); break;
+        case 2: go(sel_child_hist_kernel<2>); break;
+        default: go(sel_child_hist_kernel<1>); break;
+    }
+}
+
+void launch_sel_filter_pair(const SelArgs& a0, int b, cudaStream_t st) {
+    SelArgs a = a0;
+    const int T = sel_tile(b);
+    a.ntiles = (a.g0.nview + T - 1) / T;
+    const u64 per_sm = T >= 2048 ? 32 : 64;
+    const u64 target = 148 * per_sm;
+    u64 tpc = (a.ntiles + target - 1) / target;
+    if (tpc < 1) tpc = 1;
+    a.tiles_per_cta = (int)tpc;
+    const unsigned g2 = (unsigned)((a.ntiles + tpc - 1) / tpc);
+    const size_t sm = sizeof(u32) * (1 + (size_t)kFCap * (1 + a.k + 2));
+    auto go = [&](auto kern, int nt) {
+        if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kern<<<g2, nt, sm, st>>>(a);
+    };
+    switch (T) {
+        case 2048: go(sel_filter_pair_kernel<256>, 256); break;
+        case 1024: go(sel_filter_pair_kernel<128>, 128); break;
+        case 512: go(sel_filter_pair_kernel<64>, 64); break;
+        default: go(sel_filter_pair_kernel<32>, 32); break;
+    }
+}
+
+void launch_sel_part_pair(const SelArgs& a0, int b, cudaStream_t st) {
+    SelArgs a = a0;
+    a.hflush_every = 255;
+    if (const char* e = getenv("LBKD_HFLUSH_EVERY")) {
+        const int v = atoi(e);
+        if (v >= 1 && v < 255) a.hflush_every = v;
+    }
+    const int T = sel_tile(b);
+    const u64 nsub = (a.g0.nview + kSub - 1) / kSub;
+    const u64 per_cta = kPThreads / 32;
+    auto go = [&](auto kern, int KM, int nst, int fd) {
+        const size_t sm = kPHistOff + sizeof(u32) * (size_t)(kPThreads / 32) * (2u << fd) +
+                          sizeof(u32) * (size_t)(kPThreads / 32) * nst * (KM + 1) * kSub;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        u64 g2 = (nsub + per_cta - 1) / per_cta;
+        if (g2 > 148ull * 2) g2 = 148ull * 2;
+        kern<<<(unsigned)g2, kPThreads, sm, st>>>(a, T);
+    };
+    // a.fuse_d: 8 (3-stage ring) or 9 (2-stage ring: the 4 KB warp bins fit)
+#define LBKD_PP(KM)                                                              \
+    if (a.fuse_d >= 9) go(sel_part_pair_kernel<KM, 2, 9>, KM, 2, 9);             \
+    else go(sel_part_pair_kernel<KM, kPStages, 8>, KM, kPStages, 8);
+    switch (a.k) {
+        case 2: LBKD_PP(2); break;
+        case 3: LBKD_PP(3); break;
+        default: LBKD_PP(4); break;
+    }
+#undef LBKD_PP
 }
 
 }  // namespace lbkd

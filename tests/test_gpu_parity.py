@@ -290,6 +290,29 @@ def test_profile_classes_cover_the_build():
     assert part[1] > 0 and part[2] > 0
 
 
+@pytest.mark.parametrize("algo", ["sort", "select"])
+def test_profiled_ungraphed_builds(algo):
+    """Profiling an ungraphed build (the sort path; float64 widest, whose
+    value table is a kernel argument) records plain events and stays exact."""
+    from paper_2211_00120_b200 import _native
+
+    pts = datagen.uniform(300001, 3, seed=7)
+    ref = oracle.build_rr(pts)
+    _native.set_algorithm(algo)
+    _native.set_profile(True)
+    try:
+        _, perm = gpu_rr(pts)
+        assert np.array_equal(perm, ref)
+        assert sum(v[0] for v in _native.profile_kernels().values()) == kd.builder.last_launch_count(0)
+        p64 = np.random.default_rng(3).random((50001, 3))
+        t = build_widest(p64)
+        wp, wd = oracle.rec_build(p64, widest=True)
+        assert np.array_equal(t.payload, wp.astype(np.int64)) and np.array_equal(t.split_dims, wd)
+    finally:
+        _native.set_profile(False)
+        _native.set_algorithm("select")
+
+
 def test_pipelined_host_builds():
     """lbkd_build_rr_host: consecutive host-buffer builds overlap and each
     returns its own exact result; a non-finite input is reported at join."""
