@@ -176,6 +176,11 @@ int lbkd_profile_kernel(lbkd_ctx *ctx, int cls, int *n_launches, double *ms, dou
  * digit pass (1) kernel. */
 int lbkd_set_algorithm(lbkd_ctx *ctx, int algo);
 int lbkd_get_algorithm(const lbkd_ctx *ctx);
+/* Round-robin select path: 1 = the global levels two per partition pass
+ * (the second level selected in the first's layout, one 4-way partition;
+ * default), 0 = one level per pass.  Env LBKD_PAIR=0 at context creation.
+ * Both are bit-exact. */
+int lbkd_set_level_pairs(lbkd_ctx *ctx, int on);
 /* In-CTA phase (the last levels, one CTA per subtree): -1 = default per
  * split rule (round-robin: presorted chain lists; widest: per-level
  * selection), 0 = presorted lists, 1 = selection.  Env LBKD_SUBTREE=lists|sel

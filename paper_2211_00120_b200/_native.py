@@ -33,7 +33,7 @@ EXPORTED = (
     "lbkd_last_launch_count", "lbkd_strerror", "lbkd_last_cuda_error",
     "lbkd_set_profile", "lbkd_profile_read",
     "lbkd_build_rr_top", "lbkd_build_rr_sub", "lbkd_build_rr_split",
-    "lbkd_profile_kernel", "lbkd_set_algorithm", "lbkd_get_algorithm",
+    "lbkd_profile_kernel", "lbkd_set_algorithm", "lbkd_get_algorithm", "lbkd_set_level_pairs",
     "lbkd_build_rr_host", "lbkd_build_widest_host", "lbkd_host_join",
     "lbkd_set_subtree_kernel",
     "lbkd_knn", "lbkd_radius_count", "lbkd_radius_scratch_len", "lbkd_radius_fill",
@@ -125,6 +125,8 @@ def load():
         lib.lbkd_set_algorithm.restype = i32
         lib.lbkd_get_algorithm.argtypes = [vp]
         lib.lbkd_get_algorithm.restype = i32
+        lib.lbkd_set_level_pairs.argtypes = [vp, i32]
+        lib.lbkd_set_level_pairs.restype = i32
         lib.lbkd_build_rr_host.argtypes = [vp, vp, vp, i64, i32, vp, vp]
         lib.lbkd_build_rr_host.restype = i32
         lib.lbkd_build_widest_host.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp]
@@ -216,6 +218,11 @@ def set_algorithm(algo: str, device: int = 0) -> None:
     """Global-level algorithm of this thread's context: "select" (pivot
     selection + stable partition, default) or "sort" (per-level radix sort)."""
     check(load().lbkd_set_algorithm(context(device), ALGORITHMS.index(algo)), "lbkd_set_algorithm")
+
+
+def set_level_pairs(on: bool, device: int = 0) -> None:
+    """Round robin: two global levels per partition pass (default) or one."""
+    check(load().lbkd_set_level_pairs(context(device), 1 if on else 0), "lbkd_set_level_pairs")
 
 
 def set_subtree_kernel(which: str, device: int = 0) -> None:

@@ -1343,6 +1343,13 @@ int lbkd_set_algorithm(lbkd_ctx* c, int algo) {
 
 int lbkd_get_algorithm(const lbkd_ctx* c) { return c ? c->algo : -1; }
 
+int lbkd_set_level_pairs(lbkd_ctx* c, int on) {
+    if (!c || on < 0 || on > 1) return LBKD_EINVAL_SHAPE;
+    if (c->pair_levels != on) drop_graph(c);  // (the cached graphs hold the other schedule)
+    c->pair_levels = on;
+    return LBKD_OK;
+}
+
 int lbkd_set_subtree_kernel(lbkd_ctx* c, int which) {
     if (!c || which < -1 || which > 1) return LBKD_EINVAL_SHAPE;
     c->subtree_sel = which;

@@ -92,6 +92,23 @@ def test_adversarial_10m(name):
     assert np.array_equal(dims.cpu().numpy(), wd), name
 
 
+@pytest.mark.parametrize("pairs", [True, False])
+@pytest.mark.parametrize("name", ["identical", "huge_range", "constant_axis", "two_values", "one_hot_line", "sorted"])
+def test_level_pairs_both_schedules(name, pairs):
+    """Round robin with the global levels two per partition pass (default:
+    the second level selected in the first's layout -- identical children
+    keyed by their index column) and one per pass: both exact, for odd and
+    even numbers of global levels and k = 2, 3, 4."""
+    _native.set_level_pairs(pairs)
+    try:
+        for n, k in ((1_500_001, 3), (2_500_001, 2), (600_001, 4)):
+            pts = _adversarial(name, n, k, seed=n % 91)
+            _, perm = kd.build_round_robin_cuda(_dev(pts))
+            assert np.array_equal(perm.cpu().numpy().view(np.uint32), oracle.rec_build(pts)), (name, n, k)
+    finally:
+        _native.set_level_pairs(True)
+
+
 def test_ties_100m_rr():
     """64 values per axis at the headline size (ties at every level)."""
     pts = datagen.ties(100_000_000, 3, seed=1)
