@@ -1885,8 +1885,13 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
 // and warp-owned subtile runs as sel_part_bulk_kernel; the fused histogram
 // bins the four grandchildren (2^FD bins each, 16-bit warp bins).
 struct PHdr2 {
-    u32 sl[3], tl[3], pp[3];  // part 0: lane's sub count words (l, L side, R side), tile prefixes, pivot positions
-    u32 y[3];                 // the three pivots' leading coordinates (parent, left child, right child)
+    u32 sl[3], tl[3];  // a part's lane sub count words (level l, L side, R side) and tile prefixes
+};
+// a parent's geometry and its three pivots (positions, leading coordinates)
+struct PPar {
+    u64 j;
+    u32 ib, ie, po, poL, poR, pp0, ppL, ppR;
+    float y, yL, yR;
 };
 
 template <int KMAX, int NST, int FD>
@@ -1961,12 +1966,41 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
     }
     const int tsh = 31 - __clz(T);
     const int dl = g0.l % k, dl1 = g1.l % k;  // round robin: the parents' and children's leading dims
-    auto hdr_load = [&](u64 s2, PHdr2& h2) {
+    auto load_par = [&](u64 j) {
+        PPar p;
+        p.j = j;
+        const u64 ib = v_ibegin(g0, j);
+        p.ib = (u32)ib;
+        p.ie = (u32)(ib + v_size(g0, j));
+        p.po = (u32)v_pivot(g0, j);
+        p.poL = (u32)v_pivot(g1, 2 * j);
+        p.poR = (u32)v_pivot(g1, 2 * j + 1);
+        p.pp0 = a.ppos0[j];
+        p.ppL = a.ppos[2 * j];
+        p.ppR = a.ppos[2 * j + 1];
+        p.y = __uint_as_float(a.piv0[j * A + dl]);
+        p.yL = __uint_as_float(a.piv[(2 * j) * A + dl1]);
+        p.yR = __uint_as_float(a.piv[(2 * j + 1) * A + dl1]);
+        return p;
+    };
+    // the parent of the last lean subtile: subtiles inside it skip the
+    // 64-bit geometry (tile_parts, v_seg_of, v_pivot) and the pivot loads
+    PPar cp;
+    cp.j = ~0ull;
+    cp.ib = cp.ie = 0u;
+    // part p's count words of subtile s2 whose part p is segment j (j == ~0:
+    // the subtile's first segment)
+    auto hdr_load = [&](u64 s2, u64 j, PHdr2& h2) {
         const u64 ss2 = s2 * kSub;
         const u64 t2 = ss2 >> tsh;
-        const u64 j = v_seg_of(g0, ss2);
-        const u64 j0t = v_seg_of(g0, t2 << tsh);
-        const u32 pt = j == j0t ? 0u : 1u;
+        const u64 tstart = t2 << tsh;
+        u32 pt;
+        if (j == ~0ull && ss2 >= cp.ib && ss2 < cp.ie) {
+            pt = tstart >= cp.ib ? 0u : 1u;  // (the tile starts inside the cached parent, or before it)
+        } else {
+            if (j == ~0ull) j = v_seg_of(g0, ss2);
+            pt = j == v_seg_of(g0, tstart) ? 0u : 1u;
+        }
         const int sin = (int)(s2 - t2 * (u64)nsub_tile);
         const u64 w = (t2 * (u64)nsub_tile + lane) * 2 + pt;
         h2.sl[0] = lane < sin ? a.sub_lt0[w] : 0u;
@@ -1975,32 +2009,25 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
         h2.tl[0] = a.tile_lt0[t2 * 2 + pt];
         h2.tl[1] = a.tile_lt[t2 * 2 + pt];
         h2.tl[2] = a.tile_lt[a.lt_tstride + t2 * 2 + pt];
-        h2.pp[0] = a.ppos0[j];
-        h2.pp[1] = a.ppos[2 * j];
-        h2.pp[2] = a.ppos[2 * j + 1];
-        h2.y[0] = a.piv0[j * A + dl];
-        h2.y[1] = a.piv[(2 * j) * A + dl1];
-        h2.y[2] = a.piv[(2 * j + 1) * A + dl1];
     };
-    // the four run bases of parent j at subtile start ss from its header
-    auto bases = [&](const PHdr2& h, u64 j, u64 ib, u64 ss, u32* b) {
+    // the four run bases of a parent at subtile start ss
+    auto bases = [&](const PHdr2& h, const PPar& p, u64 ss, u32* b) {
         const u32 nL = __reduce_add_sync(kFullMask, h.sl[0]) + h.tl[0];
         const u32 nLL = __reduce_add_sync(kFullMask, h.sl[1]) + h.tl[1];
         const u32 nRL = __reduce_add_sync(kFullMask, h.sl[2]) + h.tl[2];
-        const u64 before = ss > ib ? ss - ib : 0ull;
-        const u32 pb = (before > 0 && h.pp[0] < ss) ? 1u : 0u;
-        const u32 pLb = h.pp[1] < ss ? 1u : 0u;
-        const u32 pRb = h.pp[2] < ss ? 1u : 0u;
-        const u32 nR = (u32)before - nL - pb;
-        const u32 po = (u32)v_pivot(g0, j), poL = (u32)v_pivot(g1, 2 * j), poR = (u32)v_pivot(g1, 2 * j + 1);
-        const u32 ib32 = (u32)ib;
-        b[0] = ib32 + nLL;
-        b[1] = ib32 + poL + 1u + (nL - nLL - pLb);
-        b[2] = ib32 + po + 1u + nRL;
-        b[3] = ib32 + po + 1u + poR + 1u + (nR - nRL - pRb);
+        const u32 s32 = (u32)ss;
+        const u32 before = s32 > p.ib ? s32 - p.ib : 0u;
+        const u32 pb = (before > 0 && p.pp0 < s32) ? 1u : 0u;
+        const u32 pLb = p.ppL < s32 ? 1u : 0u;
+        const u32 pRb = p.ppR < s32 ? 1u : 0u;
+        const u32 nR = before - nL - pb;
+        b[0] = p.ib + nLL;
+        b[1] = p.ib + p.poL + 1u + (nL - nLL - pLb);
+        b[2] = p.ib + p.po + 1u + nRL;
+        b[3] = p.ib + p.po + 1u + p.poR + 1u + (nR - nRL - pRb);
     };
     PHdr2 hn;
-    if (s < s_end) hdr_load(s, hn);
+    if (s < s_end) hdr_load(s, ~0ull, hn);
     u32* dcol[KMAX + 1];
 #pragma unroll
     for (int c = 0; c <= KMAX; ++c) dcol[c] = Wdst + (u64)(c < A ? c : 0) * stride;
@@ -2015,17 +2042,23 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
         phases ^= 1u << stage;
         const u32* sv = ring + (size_t)stage * (KMAX + 1) * kSub + lane;
 #define V(c, i) (sv[(c) * kSub + (i) * 32])
-        const TileParts tp = tile_parts(g0, ss, cnt);
+        bool lean = full && ss >= cp.ib && ss + kSub <= cp.ie;
+        TileParts tp;
+        if (!lean) {
+            tp = tile_parts(g0, ss, cnt);
+            if (full && !tp.has1 && tp.r0a == 0 && tp.r0b == (u32)kSub) {
+                cp = load_par(tp.j0);
+                lean = true;
+            }
+        }
         const PHdr2 h = hn;
-        if (s + 1 < s_end) hdr_load(s + 1, hn);
-        const u64 j0 = tp.j0;
-        if (full && !tp.has1 && tp.r0a == 0 && tp.r0b == (u32)kSub) {
+        if (s + 1 < s_end) hdr_load(s + 1, ~0ull, hn);
+        if (lean) {
             // lean path: one parent covers the whole subtile
+            const u64 j0 = cp.j;
             u32 b[4];
-            bases(h, j0, tp.ib0, ss, b);
-            const float y = __uint_as_float(h.y[0]);
-            const float yL = __uint_as_float(h.y[1]);
-            const float yR = __uint_as_float(h.y[2]);
+            bases(h, cp, ss, b);
+            const float y = cp.y, yL = cp.yL, yR = cp.yR;
             if (fuse && j0 != hseg) {
                 hflush();
                 hseg = j0;
@@ -2171,17 +2204,8 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                 for (int i = 0; i < kPRows; ++i) {
                     const u32 a1 = (s1 >> (2 * i)) & 1u, a2 = (s2 >> (2 * i)) & 1u;
                     const u32 q = 2u * a1 + a2;
-                    if (fuse) {
-                        u32 hbk;
-                        if (hall) {
-                            hbk = bucket_fn(hb0, V(hd0, i));
-                        } else if (hsides) {
-                            hbk = bucket_fn(bsel2(a1 != 0u, hb0, hb2), V(a1 ? hd2 : hd0, i));
-                        } else {
-                            const int hd = q == 0u ? hd0 : (q == 1u ? hd1 : (q == 2u ? hd2 : hd3));
-                            const Bucketer hbq = bsel2(q >= 2u, bsel2(q == 1u, hb0, hb1), bsel2(q == 3u, hb2, hb3));
-                            hbk = bucket_of(hbq, V(hd, i));
-                        }
+                    if (fuse) {  // (hall: one bucketer for the four grandchildren)
+                        const u32 hbk = bucket_fn(hb0, V(hd0, i));
                         atomicAdd(&wh[q * (kGB / 2) + (hbk >> 1)], (hbk & 1u) ? 0x10000u : 1u);
                     }
 #pragma unroll
@@ -2189,10 +2213,12 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                         if (c < A) dcol[c][dsts[i]] = V(c, i);
                 }
             };
-            if (allv) {
-                if (hmode == 0) rows_av(bv);
-                else if (hmode == 3) rows_av(bkk);
-                else rows_av(bo);
+            // (two compact variants of the hot loop: instruction-cache misses
+            // measured expensive; everything else takes the generic rows)
+            if (allv && (!fuse || (hall && hmode == 0))) {
+                rows_av(bv);
+            } else if (allv && hall && hmode == 3) {
+                rows_av(bkk);
             } else {
                 rows(bo, std::false_type{});
             }
@@ -2200,26 +2226,17 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
             // general path (a parent boundary inside the subtile, or the
             // view's last partial subtile): runs (part, grandchild), ranks by
             // match_any, the fused histogram by global atomics
+            const u64 j0 = tp.j0;
             u32 b[2][4];
-            bases(h, j0, tp.ib0, ss, b[0]);
+            {
+                PHdr2 h0;  // (the prefetched header may have used the cache)
+                hdr_load(s, j0, h0);
+                bases(h0, load_par(j0), ss, b[0]);
+            }
             if (tp.has1) {
                 PHdr2 h1;  // the second parent's header (its tile part index)
-                const u64 j1 = j0 + 1;
-                const u64 t2 = ss >> tsh;
-                const u64 j0t = v_seg_of(g0, t2 << tsh);
-                const u32 pt = j1 == j0t ? 0u : 1u;
-                const int sin = (int)(s - t2 * (u64)nsub_tile);
-                const u64 w = (t2 * (u64)nsub_tile + lane) * 2 + pt;
-                h1.sl[0] = lane < sin ? a.sub_lt0[w] : 0u;
-                h1.sl[1] = lane < sin ? a.sub_lt[w] : 0u;
-                h1.sl[2] = lane < sin ? a.sub_lt[a.lt_sstride + w] : 0u;
-                h1.tl[0] = a.tile_lt0[t2 * 2 + pt];
-                h1.tl[1] = a.tile_lt[t2 * 2 + pt];
-                h1.tl[2] = a.tile_lt[a.lt_tstride + t2 * 2 + pt];
-                h1.pp[0] = a.ppos0[j1];
-                h1.pp[1] = a.ppos[2 * j1];
-                h1.pp[2] = a.ppos[2 * j1 + 1];
-                bases(h1, j1, tp.ib1, ss, b[1]);
+                hdr_load(s, j0 + 1, h1);
+                bases(h1, load_par(j0 + 1), ss, b[1]);
             } else {
                 b[1][0] = b[1][1] = b[1][2] = b[1][3] = 0u;
             }
