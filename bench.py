@@ -97,10 +97,10 @@ def ncu_issue(name, mode: str = "rr"):
 
 
 KERNEL_NAMES = {
-    "partition": "sel_part_kernel (stable 3-way partition, global levels)",
+    "partition": "sel_part_pair_kernel / sel_part_bulk_kernel (stable 4-way partition per level pair, 3-way per single level)",
     "subtree": "subtree_rr_kernel / subtree_kernel (in-CTA levels)",
-    "hist": "sel_hist_kernel (per-segment bucket histogram)",
-    "filter": "sel_filter_kernel (candidate filter)",
+    "hist": "sel_hist_kernel / sel_child_hist_kernel (per-segment bucket histograms)",
+    "filter": "sel_filter_kernel / sel_filter_pair_kernel (candidate filters)",
     "select": "sel_select_kernel (pivot radix select)",
     "pick": "sel_pick_kernel",
     "init": "init_stats_kernel (AoS -> SoA, world box)",

@@ -83,12 +83,17 @@ step_evidence() {  # the round's committed evidence -> gpurun_out/r02_* (copied 
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s $L -c $L --csv --log-file ${R}_launches_100m_clustered_widest.csv python tools/one_build.py 100000000 3 widest clustered 2 > /dev/null 2>&1
   python tools/launches.py ${R}_launches_100m_clustered_widest.csv > ${R}_launches_100m_clustered_widest.txt
   python tools/ncu_traffic.py ${R}_launches_100m_clustered_widest.csv ${R}_ncu_traffic_widest.json > /dev/null
-  for ks in sel_part subtree sel_filter; do
-    skip=0; [ "$ks" = sel_part ] && skip=4; [ "$ks" = sel_filter ] && skip=6
+  # round robin: the pair kernels (4th launch = levels 6/7), the single-level
+  # partition / filter (last global level), the in-CTA kernel
+  for spec in sel_part_pair:3 sel_filter_pair:3 sel_child_hist:3 sel_part_bulk:0 sel_filter_kernel:4 subtree:0; do
+    ks=${spec%%:*}; skip=${spec##*:}
     ncu --set full --clock-control none --import-source on -k regex:$ks -s $skip -c 1 -o ${R}_full_$ks python tools/one_build.py 100000000 3 rr uniform 1 > /dev/null 2>&1
     python tools/ncu_summary.py ${R}_full_$ks.ncu-rep > ${R}_ncu_full_$ks.txt 2>&1
     python tools/ncu_lines.py ${R}_full_$ks.ncu-rep 60 > ${R}_ncu_lines_$ks.txt 2>&1
   done
+  # widest: its single-level partition (5th launch)
+  ncu --set full --clock-control none --import-source on -k regex:sel_part_bulk -s 4 -c 1 -o ${R}_full_part_widest python tools/one_build.py 100000000 3 widest clustered 1 > /dev/null 2>&1
+  python tools/ncu_summary.py ${R}_full_part_widest.ncu-rep > ${R}_ncu_full_part_widest.txt 2>&1
   python tools/ncu_issue.py ${R}_full_subtree.ncu-rep ${R}_ncu_issue_subtree.json > /dev/null 2>&1
   ncu --set full --clock-control none --import-source on -k regex:subtree -c 1 -o ${R}_full_subsel_widest python tools/one_build.py 100000000 3 widest clustered 1 > /dev/null 2>&1
   python tools/ncu_summary.py ${R}_full_subsel_widest.ncu-rep > ${R}_ncu_full_subsel_widest.txt 2>&1
@@ -97,12 +102,12 @@ step_evidence() {  # the round's committed evidence -> gpurun_out/r02_* (copied 
   { for kind in uniform clustered identical huge constaxis ties sorted; do
       KNOBS_TIMEOUT=120 python tools/knobs.py 10000000 3 rr $kind -- ""; KNOBS_TIMEOUT=120 python tools/knobs.py 10000000 3 widest $kind -- ""
     done; KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 3 rr ties -- ""; } > ${R}_robust_knobs.txt 2>&1
-  { KNOBS_TIMEOUT=300 python tools/knobs.py 100000000 3 rr uniform -- "" LBKD_ALGO=sort LBKD_SELECT_CLUSTER=0
+  { KNOBS_TIMEOUT=300 python tools/knobs.py 100000000 3 rr uniform -- "" LBKD_PAIR=0 LBKD_ALGO=sort LBKD_SELECT_CLUSTER=0
     KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 2 rr uniform -- ""
     KNOBS_TIMEOUT=120 python tools/knobs.py 10000000 4 rr uniform -- ""
     KNOBS_TIMEOUT=120 python tools/knobs.py 1000000 3 rr uniform -- ""
     KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 3 widest clustered -- ""
-    KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 3 rr clustered -- ""
+    KNOBS_TIMEOUT=120 python tools/knobs.py 100000000 3 rr clustered -- "" LBKD_PAIR=0
     KNOBS_TIMEOUT=300 python tools/knobs.py 100000000 3 rr uniform64 -- ""
     KNOBS_TIMEOUT=300 python tools/knobs.py 10000000 4 rr uniform64 -- ""; } > ${R}_configs_knobs.txt 2>&1
   cat ${R}_launches_100m_float3.txt | head -20

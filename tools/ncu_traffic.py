@@ -8,7 +8,8 @@ import sys
 sys.path.insert(0, __file__.rsplit("/", 1)[0])
 from launches import load  # noqa: E402
 
-CLASSES = [("sel_part", "partition"), ("subtree", "subtree"), ("sel_hist", "hist"), ("sel_filter", "filter"),
+CLASSES = [("sel_part", "partition"), ("subtree", "subtree"), ("sel_hist", "hist"), ("sel_child_hist", "hist"),
+           ("sel_filter", "filter"),
            ("sel_select", "select"), ("sel_pick", "pick"), ("init_stats", "init"), ("pass_kernel", "sort_pass")]
 
 
