@@ -111,6 +111,47 @@ __device__ __noinline__ int tie_side_of(const u32* W, u64 stride, int k, const C
     return xx < yy ? 0 : (xx > yy ? 1 : 2);
 }
 
+// the same, skipping the chain fields whose dim the node's box pins (every
+// point of the node ties there: identical / tie-heavy data)
+__device__ __noinline__ int tie_side_pinned(const u32* W, u64 stride, int k, const Chain* ch, const u32* pv, u64 pos,
+                                            u32 pinned) {
+    const u32 mm = ch->m;
+    for (u32 f = 1; f < mm; ++f) {
+        if ((pinned >> f) & 1u) continue;
+        const int d = ch->d[f];
+        const u32 xx = flip_key(__uint_as_float(W[(u64)d * stride + pos]));
+        const u32 yy = flip_key(__uint_as_float(pv[d]));
+        if (xx != yy) return xx < yy ? 0 : 1;
+    }
+    const u32 xx = W[(u64)k * stride + pos], yy = pv[k];
+    return xx < yy ? 0 : (xx > yy ? 1 : 2);
+}
+
+// chain fields (bit f) whose dim a box pins
+__device__ __forceinline__ u32 pinned_fields(const Chain* ch, const float* box, int k) {
+    u32 m = 0;
+    for (u32 f = 1; f < ch->m; ++f) {
+        const int d = ch->d[f];
+        if (!(box[d] < box[k + d])) m |= 1u << f;
+    }
+    return m;
+}
+
+// the same, for a row of a partition subtile staged in shared memory (the
+// warp's TMA ring: column c of row i at sv[c * 256 + i * 32], sv = the
+// lane's base) -- no global re-reads on tie-heavy data
+__device__ __forceinline__ u32 tie_side_ring(const u32* sv, int i, int k, const Chain* ch, const u32* pv) {
+    const u32 mm = ch->m;
+    for (u32 f = 1; f < mm; ++f) {
+        const int d = ch->d[f];
+        const u32 xx = flip_key(__uint_as_float(sv[d * 256 + i * 32]));
+        const u32 yy = flip_key(__uint_as_float(pv[d]));
+        if (xx != yy) return xx < yy ? 0u : 1u;
+    }
+    const u32 xx = sv[k * 256 + i * 32], yy = pv[k];
+    return xx < yy ? 0u : (xx > yy ? 1u : 2u);
+}
+
 __device__ __forceinline__ int bitlen32(u32 v) { return v ? 32 - __clz(v) : 0; }
 
 // equal-width buckets of [lo, hi]: shift such that (hi - lo) >> shift < 2^D
@@ -1365,9 +1406,12 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
                 sides |= sd << (2 * i);
             }
             if (__any_sync(kFullMask, (sides & 0xAAAAu) != 0u)) {
+                const Chain* tch = a.chains + tp.j0;
+                const u32* tpv = a.piv + tp.j0 * A;
+#pragma unroll 1
                 for (int i = 0; i < kPRows; ++i) {
                     if (((sides >> (2 * i)) & 3u) == 2u) {
-                        const u32 sd = (u32)part_tie_side(a, tp.j0, ss + (u64)(i * 32 + lane));
+                        const u32 sd = tie_side_ring(sv, i, k, tch, tpv);
                         sides = (sides & ~(3u << (2 * i))) | (sd << (2 * i));
                     }
                 }
@@ -1542,6 +1586,7 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
         __syncthreads();
     };
     int dl = 0, dk0 = 0, dk1 = 0;
+    u32 pinm = 0;
     float y = 0.f;
     Bucketer b0{}, b1{};
     for (u64 t = t0; t < t1; ++t) {
@@ -1561,6 +1606,9 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
                 cur = j;
                 dl = a.chains0[j].d[0];
                 y = __uint_as_float(a.piv0[j * A + dl]);
+                // (the children's boxes pin what the parent's does in every
+                // chain dim but its split dim)
+                pinm = pinned_fields(a.chains0 + j, a.boxes_in + (2 * j) * 2ull * k, k);
                 const PairKey p0 = pair_child_key(a.boxes_in + (2 * j) * 2ull * k, a.bmode_in[2 * j], k, a.g.l, a.g.n);
                 const PairKey p1 =
                     pair_child_key(a.boxes_in + (2 * j + 1) * 2ull * k, a.bmode_in[2 * j + 1], k, a.g.l, a.g.n);
@@ -1612,8 +1660,8 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
                 if (sides & 0xAAAAu) {
                     for (int i = 0; i < ITEMS; ++i)
                         if (((sides >> (2 * i)) & 3u) == 2u) {
-                            const u32 sd = (u32)tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A,
-                                                            ts + r0 + (u32)i);
+                            const u32 sd = (u32)tie_side_pinned(W, stride, k, a.chains0 + j, a.piv0 + j * A,
+                                                            ts + r0 + (u32)i, pinm);
                             sides = (sides & ~(3u << (2 * i))) | (sd << (2 * i));
                         }
                 }
@@ -1634,7 +1682,7 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
                 if (r >= ra && r < rb) {
                     const float x = __uint_as_float(xk[i]);
                     int side = x < y ? 0 : (x > y ? 1 : 2);  // -0.0 == +0.0 like numpy
-                    if (side == 2) side = tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A, ts + r);
+                    if (side == 2) side = tie_side_pinned(W, stride, k, a.chains0 + j, a.piv0 + j * A, ts + r, pinm);
                     if (side < 2) {
                         const u32 key = same ? kv[i] : W[(u64)(side ? dk1 : dk0) * stride + ts + r];
                         const u32 b = bucket_of(bsel2(side != 0, b0, b1), key);
@@ -1676,6 +1724,7 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
         sc.init(g0, t0 * T);
         u64 cj = ~0ull;
         int dl = 0, dk0 = 0, dk1 = 0;
+        u32 pinm = 0;
         float y = 0.f;
         Bucketer bk0{}, bk1{};
         u32 bs0 = 0u, bs1 = 0u;
@@ -1697,6 +1746,7 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
                     cj = j;
                     dl = a.chains0[j].d[0];
                     y = __uint_as_float(a.piv0[j * A + dl]);
+                    pinm = pinned_fields(a.chains0 + j, a.boxes_in + (2 * j) * 2ull * k, k);
                     const u32* sl0 = a.sel + (2 * j) * kSelW;
                     const u32* sl1 = sl0 + kSelW;
                     bk0 = make_bucketer(__uint_as_float(sl0[kSelLo]), __uint_as_float(sl0[kSelShift]), a.D,
@@ -1758,8 +1808,8 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
                     if (sides & 0xAAAAu) {
                         for (int i = 0; i < ITEMS; ++i)
                             if (((sides >> (2 * i)) & 3u) == 2u) {
-                                const u32 sd = (u32)tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A,
-                                                                ts + r0 + (u32)i);
+                                const u32 sd = (u32)tie_side_pinned(W, stride, k, a.chains0 + j, a.piv0 + j * A,
+                                                                ts + r0 + (u32)i, pinm);
                                 sides = (sides & ~(3u << (2 * i))) | (sd << (2 * i));
                             }
                     }
@@ -1787,7 +1837,7 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
                     if (r >= ra && r < rb) {
                         const float x = __uint_as_float(key[i]);
                         int side = x < y ? 0 : (x > y ? 1 : 2);
-                        if (side == 2) side = tie_side_of(W, stride, k, a.chains0 + j, a.piv0 + j * A, ts + r);
+                        if (side == 2) side = tie_side_pinned(W, stride, k, a.chains0 + j, a.piv0 + j * A, ts + r, pinm);
                         if (side < 2) {
                             const u32 kv = same ? ck[i] : W[(u64)(side ? dk1 : dk0) * stride + ts + r];
                             const u32 b = bucket_of(bsel2(side != 0, bk0, bk1), kv);
@@ -1824,24 +1874,49 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
                     u32 pos = 0;
                     if (lane == 31) pos = atomicAdd(&fsm[0], wtot);
                     pos = __shfl_sync(kFullMask, pos, 31);
-                    const bool staged = pos + wtot <= (u32)kFCap;
-                    u32 q = pos + x - nh;
-                    while (hits) {
-                        const int i = __ffs(hits) - 1;
-                        hits &= hits - 1;
-                        const u32 r = r0 + (u32)i;
-                        const u32 c = (u32)(2 * j) + ((hside >> i) & 1u);
-                        u32* rec;
-                        if (staged) {  // staged in shared memory
-                            rec = s_rec + q * R;
-                            s_seg[q] = c;
+                    const bool staged = pos + wtot <= (u32)kFCap;  // (warp-uniform)
+                    if (staged) {  // staged in shared memory
+                        u32 q = pos + x - nh;
+                        while (hits) {
+                            const int i = __ffs(hits) - 1;
+                            hits &= hits - 1;
+                            const u32 r = r0 + (u32)i;
+                            u32* rec = s_rec + q * R;
+                            s_seg[q] = (u32)(2 * j) + ((hside >> i) & 1u);
                             ++q;
-                        } else {  // staging full (tie-heavy data): a slot of the child's range directly
-                            u32* sel = a.sel + (u64)c * kSelW;
-                            rec = a.cand + (u64)(sel[kSelOff] + atomicAdd(&sel[kSelFill], 1u)) * R;
+                            for (int cc = 0; cc < A; ++cc) rec[cc] = W[(u64)cc * stride + ts + r];
+                            rec[k + 1] = (u32)(ts + r);
                         }
-                        for (int cc = 0; cc < A; ++cc) rec[cc] = W[(u64)cc * stride + ts + r];
-                        rec[k + 1] = (u32)(ts + r);
+                    } else {
+                        // staging full (tie-heavy data): slots of the children's
+                        // ranges directly, one reservation per child side per warp
+                        const u32 hL = hits & ~hside, hR = hits & hside;
+                        const u32 nL = (u32)__popc(hL), nR = (u32)__popc(hR);
+                        u32 xl = nL, xr = nR;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const u32 yl = __shfl_up_sync(kFullMask, xl, o);
+                            const u32 yr = __shfl_up_sync(kFullMask, xr, o);
+                            if (lane >= o) { xl += yl; xr += yr; }
+                        }
+                        u32* const selL = a.sel + (2 * j) * kSelW;
+                        u32* const selR = selL + kSelW;
+                        u32 bL = 0, bR = 0;
+                        if (lane == 31) {
+                            if (xl) bL = selL[kSelOff] + atomicAdd(&selL[kSelFill], xl);
+                            if (xr) bR = selR[kSelOff] + atomicAdd(&selR[kSelFill], xr);
+                        }
+                        bL = __shfl_sync(kFullMask, bL, 31) + xl - nL;
+                        bR = __shfl_sync(kFullMask, bR, 31) + xr - nR;
+                        while (hits) {
+                            const int i = __ffs(hits) - 1;
+                            hits &= hits - 1;
+                            const u32 r = r0 + (u32)i;
+                            const u32 slot = ((hside >> i) & 1u) ? bR++ : bL++;
+                            u32* rec = a.cand + (u64)slot * R;
+                            for (int cc = 0; cc < A; ++cc) rec[cc] = W[(u64)cc * stride + ts + r];
+                            rec[k + 1] = (u32)(ts + r);
+                        }
                     }
                 }
             }
@@ -2095,10 +2170,10 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                 s1 |= (x < y ? 0u : (x > y ? 1u : 2u)) << (2 * i);
             }
             if (__any_sync(kFullMask, (s1 & 0xAAAAu) != 0u)) {
+#pragma unroll 1
                 for (int i = 0; i < kPRows; ++i) {
                     if (((s1 >> (2 * i)) & 3u) == 2u) {
-                        const u32 sd = (u32)tie_side_of(Wsrc, stride, k, a.chains0 + j0, a.piv0 + j0 * A,
-                                                        ss + (u64)(i * 32 + lane));
+                        const u32 sd = tie_side_ring(sv, i, k, a.chains0 + j0, a.piv0 + j0 * A);
                         s1 = (s1 & ~(3u << (2 * i))) | (sd << (2 * i));
                     }
                 }
@@ -2117,11 +2192,11 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                 s2 |= sd << (2 * i);
             }
             if (__any_sync(kFullMask, (s2 & 0xAAAAu & ~(s2 << 1)) != 0u)) {  // some row == 2 (not 3)
+#pragma unroll 1
                 for (int i = 0; i < kPRows; ++i) {
                     if (((s2 >> (2 * i)) & 3u) == 2u) {
                         const u64 c = 2 * j0 + ((s1 >> (2 * i)) & 1u);
-                        const u32 sd = (u32)tie_side_of(Wsrc, stride, k, a.chains + c, a.piv + c * A,
-                                                        ss + (u64)(i * 32 + lane));
+                        const u32 sd = tie_side_ring(sv, i, k, a.chains + c, a.piv + c * A);
                         s2 = (s2 & ~(3u << (2 * i))) | (sd << (2 * i));
                     }
                 }

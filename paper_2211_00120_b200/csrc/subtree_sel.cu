@@ -83,12 +83,95 @@ size_t subtree_sel_smem_bytes(int b, int k) { return sel_layout(b, k).total; }
 // kSgLo / kSgHi: bucketer (half lo, scale); kSgDeg: the node box is a point
 // (every coordinate of every point in it is equal: the order is the input order)
 enum { kSgSize = 0, kSgPo, kSgDim, kSgB, kSgR, kSgOff, kSgCnt, kSgFill, kSgPiv, kSgLo, kSgHi, kSgDeg };
+// candidate sets above this size are resolved by a CTA-wide radix select
+// instead of all-pairs comparison (O(C^2): the tie-heavy widest cliff)
+constexpr u32 kBigCand = 128;
 
 // block-phase bucket of coordinate v in a segment (fp32, round-to-nearest
 // each step: monotone in v; NaN -> the top bucket)
 __device__ __forceinline__ u32 seg_bucket(const u32* s, float v, u32 top) {
     const float x = __fmul_rn(__fsub_rn(0.5f * v, __uint_as_float(s[kSgLo])), __uint_as_float(s[kSgHi]));
     return x < (float)top ? (u32)x : top;
+}
+
+// CTA-wide radix select of rank r among C candidates (local ids in cs) under
+// the composite key (chain coordinates flipped, then the row: rowv[x], or x
+// when local ids are in row order); losers are overwritten with 0xffff.  Out
+// of line: only tie-heavy candidate sets take it (kBigCand).
+__device__ __noinline__ void big_select(unsigned short* cs, u32 C, u32 r, const float* P, int Mp, const Chain& wch,
+                                        const u32* rowv, u32* hist, u32* piv) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    u32* rh = hist;        // 256 bins
+    u32* rr = hist + 256;  // [2][warps] reductions, [3] pick
+    u32 n = C;
+    auto field = [&](int f, u32 x) -> u32 {
+        return f < (int)wch.m ? flip_key(P[(int)wch.d[f] * Mp + x]) : (rowv ? rowv[x] : x);
+    };
+    for (int f = 0; f <= (int)wch.m && n > 1; ++f) {
+        while (n > 1) {
+            u32 mn = 0xffffffffu, mx = 0u;
+            for (u32 q = tid; q < C; q += kSelThreads) {
+                const u32 x = cs[q];
+                if (x == 0xffffu) continue;
+                const u32 v = field(f, x);
+                mn = min(mn, v);
+                mx = max(mx, v);
+            }
+            mn = __reduce_min_sync(kFullMask, mn);
+            mx = __reduce_max_sync(kFullMask, mx);
+            if (lane == 0) { rr[warp] = mn; rr[kSelWarps + warp] = mx; }
+            for (int i = tid; i < 256; i += kSelThreads) rh[i] = 0u;
+            __syncthreads();
+            mn = 0xffffffffu;
+            mx = 0u;
+            for (int w = 0; w < kSelWarps; ++w) { mn = min(mn, rr[w]); mx = max(mx, rr[kSelWarps + w]); }
+            if (mn == mx) {  // field constant over the live set
+                __syncthreads();
+                break;
+            }
+            u32 sh = 0;
+            while (((mx - mn) >> sh) > 255u) ++sh;
+            for (u32 q = tid; q < C; q += kSelThreads) {
+                const u32 x = cs[q];
+                if (x != 0xffffu) atomicAdd(&rh[(field(f, x) - mn) >> sh], 1u);
+            }
+            __syncthreads();
+            if (warp == 0) {  // bucket holding rank r: 8 bins per lane
+                u32 c8[8], sum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) { c8[q] = rh[lane * 8 + q]; sum += c8[q]; }
+                u32 xs = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 y = __shfl_up_sync(kFullMask, xs, o);
+                    if (lane >= o) xs += y;
+                }
+                u32 cum = xs - sum;
+                if (r >= cum && r < xs) {
+                    int bsel = 0;
+                    for (int q = 0; q < 8; ++q) {
+                        if (cum + c8[q] > r) { bsel = lane * 8 + q; break; }
+                        cum += c8[q];
+                    }
+                    rr[2 * kSelWarps] = (u32)bsel;
+                    rr[2 * kSelWarps + 1] = cum;
+                    rr[2 * kSelWarps + 2] = rh[bsel];
+                }
+            }
+            __syncthreads();
+            const u32 bsel = rr[2 * kSelWarps];
+            r -= rr[2 * kSelWarps + 1];
+            n = rr[2 * kSelWarps + 2];
+            for (u32 q = tid; q < C; q += kSelThreads) {
+                const u32 x = cs[q];
+                if (x != 0xffffu && ((field(f, x) - mn) >> sh) != bsel) cs[q] = 0xffffu;
+            }
+            __syncthreads();
+        }
+    }
+    for (u32 q = tid; q < C; q += kSelThreads)
+        if (cs[q] != 0xffffu) *piv = cs[q];  // the one live candidate
+    __syncthreads();
 }
 
 template <int KT>
@@ -393,6 +476,21 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
             if (bk == s[kSgB]) cand[s[kSgOff] + atomicAdd(&s[kSgFill], 1u)] = (u16)p;
         }
         __syncthreads();
+        // ---- big candidate sets (tie-heavy / identical / sorted data: the
+        // pivot's bucket can hold most of a node): radix select over the
+        // composite key (chain coordinates, then the row), the whole CTA on
+        // one segment at a time -- per round the live range, 256 buckets,
+        // the bucket holding rank r; losers are marked dead in place
+        for (int t = 0; t < nloc; ++t) {
+            u32* s = sv + t * kSegWords;
+            const u32 C = s[kSgCnt];
+            if (C <= kBigCand) continue;  // (CTA-uniform)
+            u16* cs = cand + s[kSgOff];
+            Chain wch;
+            if (a.mode == kWidest) widest_chain_of(hbase + t, dl, wch);
+            else rr_chain(lam, k, wch);
+            big_select(cs, C, s[kSgR], P, Mp, wch, lid_is_row_order ? nullptr : vin, hist, &s[kSgPiv]);
+        }
         // ---- resolve: rank of each candidate inside its segment by
         // comparison, one thread per candidate over the whole CTA (a warp per
         // segment left most warps idle at the top levels, where one or two
@@ -412,6 +510,7 @@ __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(Sub
                 const int t = lo;
                 u32* s = sv + t * kSegWords;
                 const u32 C = s[kSgCnt], off = s[kSgOff];
+                if (C > kBigCand) continue;  // (selected above)
                 const int d = (int)s[kSgDim];
                 const u32 ci = cand[q];
                 const float ki = P[d * Mp + ci];  // finite: float order == flipped-key order
