@@ -132,7 +132,7 @@ __device__ __forceinline__ u32 pinned_fields(const Chain* ch, const float* box, 
     u32 m = 0;
     for (u32 f = 1; f < ch->m; ++f) {
         const int d = ch->d[f];
-        if (!(box[d] < box[k + d])) m |= 1u << f;
+        if (box[d] == box[k + d]) m |= 1u << f;  // (== : a NaN bound from non-finite input pins nothing)
     }
     return m;
 }
