@@ -538,6 +538,7 @@ static int begin_build(lbkd_ctx* c, int k, cudaStream_t st) {
     c->k_last = k;
     c->ctr = 0;
     if (!c->err_sticky) CK(cudaMemsetAsync(bf.err, 0, sizeof(u32) * 4, st));
+    else CK(cudaMemsetAsync(bf.err + 1, 0, sizeof(u32), st));  // (the abort word is per build)
     return LBKD_OK;
 }
 

@@ -75,7 +75,7 @@ struct Buffers {
     u64* status;      // [tiles][256] decoupled-lookback words
     u32* tile_ctr;    // one counter per pass launch
     u64* moved;       // per pass launch: points the launch reordered (profiling)
-    u32* err;         // [0] non-finite flag
+    u32* err;         // [0] non-finite flag (sticky over pipelined host builds), [1] this build's abort word
     float* boxes[2];  // widest: boxes of the level's nodes [nseg][2k]
     uint8_t* bmode[2];  // bucket mode of the level's nodes (0 value-linear, 1 key-linear)
     // level pairs (select.cu, "two levels per partition"): the second
@@ -200,6 +200,7 @@ struct SubtreeArgs {
                        // order T(parent); select path: in input order
     int src_par;       // select path: W[src_par] holds the subtree (else prev_state)
     int bucket_lists;  // RR list kernel: chain orders by one bucket pass each (env LBKD_BUCKET=0: radix passes)
+    const u32* abort_word;  // non-null and set: non-finite input, return at once
     WidthTab wt;       // widths of rank-coded (float64) builds
 };
 

@@ -152,6 +152,12 @@ __device__ __forceinline__ u32 tie_side_ring(const u32* sv, int i, int k, const 
     return xx < yy ? 0u : (xx > yy ? 1u : 2u);
 }
 
+// the build's abort word (Buffers::err[1], set with the non-finite flag by
+// the init / check kernels): every later kernel of the build returns at
+// once, so NaN / inf input never drives the selection's invariants (the
+// counts of one kernel against the compares of the next) out of range
+__device__ __forceinline__ bool aborted(const SelArgs& a) { return a.bf.err && a.bf.err[1] != 0u; }
+
 __device__ __forceinline__ int bitlen32(u32 v) { return v ? 32 - __clz(v) : 0; }
 
 // equal-width buckets of [lo, hi]: shift such that (hi - lo) >> shift < 2^D
@@ -317,7 +323,10 @@ __global__ void __launch_bounds__(256) init_stats_kernel(const float* __restrict
         }
         w0[(u64)k * stride + i] = (u32)i;
     }
-    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) {
+        atomicOr(err, 1u);
+        atomicOr(err + 1, 1u);  // this build's abort word (kernels after init return at once)
+    }
 #pragma unroll
     for (int c = 0; c < LBKD_MAX_K; ++c) {
         if (c < k) {
@@ -345,7 +354,10 @@ __global__ void check_finite_kernel(const float* __restrict__ pts, u64 total, u3
     bool bad = false;
     for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < total; e += (u64)gridDim.x * blockDim.x)
         bad |= !isfinite(__ldg(pts + e));
-    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) {
+        atomicOr(err, 1u);
+        atomicOr(err + 1, 1u);
+    }
 }
 
 void launch_check_finite(const float* pts, u64 total, u32* err, cudaStream_t st) {
@@ -412,6 +424,7 @@ constexpr int kHThreads = 256;
 
 template <int ITEMS>
 __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     extern __shared__ u32 h[];
     constexpr int T = kHThreads * ITEMS;
     const int nb = 1 << a.D;
@@ -509,6 +522,7 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
 // rank r inside it; reserves the segment's candidate range.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     __shared__ u32 wtot[32];
     const u64 j = blockIdx.x;
     // a node box that is a single point (every coordinate of every point of
@@ -582,6 +596,7 @@ constexpr int kFCap = 256;  // filter: candidate records staged per CTA
 
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 2048 / THREADS) sel_filter_kernel(SelArgs a) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     // CTA = a contiguous run of tiles; per tile every warp owns one 256-
     // position subtile (8 items per thread, thread-contiguous).  Counts of
     // elements below b*: per (subtile, part) one plain store by the warp,
@@ -783,6 +798,7 @@ __device__ __forceinline__ u32 rec_field(const u32* rec, const Chain& ch, int f,
 // per phase, and rank 0 alone writes the segment's results.
 template <int NT, int CS>
 __global__ void __launch_bounds__(NT) sel_select_kernel(SelArgs a, int T) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     namespace cg = cooperative_groups;
     __shared__ u32 hist[256];
     __shared__ u32 red[2][32];
@@ -1057,6 +1073,7 @@ __device__ __forceinline__ int part_tie_side(const SelArgs& a, u64 j, u64 pos) {
 // single-part subtiles take a lean path (float compares, no part masks)
 template <int KMAX, int D0>
 __global__ void __launch_bounds__(kPThreads, KMAX <= 4 ? 2 : 1) sel_part_kernel(SelArgs a, int T) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     const int lane = threadIdx.x & 31;
     const int k = a.k, A = k + 1;
     const LevelGeom& g = a.g;
@@ -1233,6 +1250,7 @@ struct PHdr {
 // NST ring stages, MINB CTAs per SM (occupancy variants, LBKD_PART_CFG)
 template <int KMAX, int D0, int NST = kPStages, int MINB = 2>
 __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs a, int T) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int kPStages = NST;
     const int lane = threadIdx.x & 31;
@@ -1556,6 +1574,7 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
 // its shared bins when the parent changes
 template <int ITEMS>
 __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     extern __shared__ u32 h[];  // [2][2^D]
     constexpr int T = kHThreads * ITEMS;
     const int nb = 1 << a.D;
@@ -1702,6 +1721,7 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
 // layout's) staged per CTA like the filter above
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     constexpr int ITEMS = 8;
     constexpr int T = THREADS * ITEMS;
     constexpr int NSUB = T / kSub;
@@ -1971,6 +1991,7 @@ struct PPar {
 
 template <int KMAX, int NST, int FD>
 __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, int T) {
+    if (aborted(a)) return;  // non-finite input: the build is reported, not run
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int kGB = 1 << FD;  // bins per grandchild
     constexpr int kWW = 2 * kGB;  // words of a warp's bins (4 grandchildren, two 16-bit bins per word)

@@ -366,6 +366,7 @@ __device__ __forceinline__ int entry_order(ET* buf0, ET* buf1, int m, const floa
 }
 
 __global__ void __launch_bounds__(kSubThreads, 1) subtree_kernel(SubtreeArgs a) {
+    if (a.abort_word && *a.abort_word) return;  // non-finite input (select.cu aborted)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M = a.M, k = a.k, tid = threadIdx.x;
     unsigned char* sp = smem_raw;
@@ -602,6 +603,7 @@ size_t subtree_rr_smem_bytes(int b, int k) {
 // shared-memory offsets become immediates); 0 = taken from the arguments
 template <int KT, int MPT>
 __global__ void __launch_bounds__(kRRThreads, 2) subtree_rr_kernel(SubtreeArgs a) {
+    if (a.abort_word && *a.abort_word) return;  // non-finite input (select.cu aborted)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef unsigned short u16;
     const int M = MPT ? MPT - 1 : a.M, k = KT ? KT : a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1048,6 +1050,7 @@ void launch_subtree(const BuildParams& bp, const Buffers& bf, int lam0, int entr
     a.split_dims = bp.split_dims;
     a.boxes0 = bf.boxes[lam0 & 1];
     a.dbg = bp.dbg;
+    a.abort_word = bf.err ? bf.err + 1 : nullptr;
     a.jbase = bp.jroot << (lam0 - bp.lroot);
     a.pbase = seg_ibegin(make_geom(bp.n, bp.lroot), bp.jroot);
     a.lfirst = bp.lroot;

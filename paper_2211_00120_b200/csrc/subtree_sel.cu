@@ -176,6 +176,7 @@ __device__ __noinline__ void big_select(unsigned short* cs, u32 C, u32 r, const 
 
 template <int KT>
 __global__ void __launch_bounds__(kSelThreads, kSelPerSM) subtree_sel_kernel(SubtreeArgs a, int b) {
+    if (a.abort_word && *a.abort_word) return;  // non-finite input (select.cu aborted)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint8_t s_outer[LBKD_MAX_K];  // widest: distinct dims of the subtree root's ancestors
     __shared__ int s_nouter;

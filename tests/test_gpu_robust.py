@@ -109,6 +109,23 @@ def test_level_pairs_both_schedules(name, pairs):
         _native.set_level_pairs(True)
 
 
+@pytest.mark.parametrize("dim", [0, 1, 2])
+def test_nonfinite_input_is_reported_not_crashing(dim):
+    """NaN / inf rows in a multi-level build (the level-pair kernels, the
+    partitions, the in-CTA kernels) end in the ValueError of
+    builder.py:134-135 -- never a device fault -- and the context keeps
+    working."""
+    pts = datagen.uniform(700_001, 3, seed=dim)
+    bad = pts.copy()
+    bad[::9973, dim] = np.nan
+    bad[5, (dim + 1) % 3] = np.inf
+    for fn in (kd.build_round_robin_cuda, kd.build_widest_cuda):
+        with pytest.raises(ValueError, match="finite"):
+            fn(_dev(bad))
+    _, perm = kd.build_round_robin_cuda(_dev(pts))
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), oracle.rec_build(pts))
+
+
 def test_ties_100m_rr():
     """64 values per axis at the headline size (ties at every level)."""
     pts = datagen.ties(100_000_000, 3, seed=1)
