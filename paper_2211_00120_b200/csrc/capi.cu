@@ -867,6 +867,7 @@ static int build_sub(lbkd_ctx* c, u32* d_sub, int64_t sub_stride, int64_t n_tota
     bp.lroot = root_level;
     bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : 0;
     bp.jroot = (u64)root_index;
+    bp.pair = c->pair_levels && c->algo == 0;  // (the sub-build's own global levels, two per pass)
     if ((rc = begin_order(c, st))) return rc;
     if ((rc = begin_build(c, k, st))) return rc;
     u32* const own_w0 = c->bf.w[0];
