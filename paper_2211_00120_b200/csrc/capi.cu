@@ -376,7 +376,10 @@ static int run_levels_select(lbkd_ctx* c, const BuildParams& bp, int lfrom, int 
     const int kFuseFrom = 6;
     const bool fusable = k <= 4 && (bp.mode == kRoundRobin || getenv("LBKD_FUSE_WIDEST") == nullptr ||
                                     getenv("LBKD_FUSE_WIDEST")[0] != '0');
-    const bool pairs = bp.pair && bp.mode == kRoundRobin && k >= 2 && k <= 4;
+    // (widest pairs are exact too -- the kernels take each node's split dim --
+    // but measured slower on config 5: 34.7 vs 33.3 ms, LBKD_PAIR_WIDEST=1)
+    static const bool pair_widest = getenv("LBKD_PAIR_WIDEST") && getenv("LBKD_PAIR_WIDEST")[0] == '1';
+    const bool pairs = bp.pair && k >= 2 && k <= 4 && (bp.mode == kRoundRobin || (pair_widest && fusable));
     u32 wpar = 0;       // W[wpar] holds level l's data
     int fused_D = 0;    // D of the histogram the previous partition fused (0: none)
     const u64 T = (u64)sel_tile(bp.b);
@@ -651,7 +654,7 @@ static int build(lbkd_ctx* c, const float* d_points, float* d_out, int64_t n_in,
     bp.dbg = d_trace;
     bp.wt = c->cur_wt;
     bp.subtree_sel = c->subtree_sel >= 0 ? c->subtree_sel : (mode == kWidest ? 1 : 0);
-    bp.pair = c->pair_levels && mode == kRoundRobin && c->algo == 0 && !d_trace;
+    bp.pair = c->pair_levels && c->algo == 0 && !d_trace;
     // the select path is a fixed, host-sync-free sequence for given buffers:
     // capture it once into a CUDA graph and replay it (the sort path carries
     // per-launch lookback epochs and is always launched directly)

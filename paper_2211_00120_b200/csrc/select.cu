@@ -79,9 +79,19 @@ struct PairKey {
     int mode;
 };
 
-__device__ __forceinline__ PairKey pair_child_key(const float* box, uint8_t bmode, int k, int l1, u64 n) {
+__device__ __forceinline__ PairKey pair_child_key(const float* box, uint8_t bmode, int k, int l1, u64 n,
+                                                  int wd = -1) {
     PairKey p;
-    const int d = rr_key_dim(box, k, l1);
+    // round robin: rr_key_dim; widest (wd = the child's split dim): that dim
+    // unless the box is a single point
+    int d;
+    if (wd < 0) {
+        d = rr_key_dim(box, k, l1);
+    } else {
+        bool point = true;
+        for (int c = 0; c < k; ++c) point &= box[c] == box[k + c];
+        d = point ? -1 : wd;
+    }
     if (d >= 0) {
         p.d = d;
         p.lo = box[d];
@@ -94,6 +104,13 @@ __device__ __forceinline__ PairKey pair_child_key(const float* box, uint8_t bmod
         p.mode = 1;
     }
     return p;
+}
+
+// the key of view segment c of level a.g.l (a pair's second level); widest:
+// the split dim the first level's select wrote for that node
+__device__ __forceinline__ PairKey pair_key_of(const SelArgs& a, u64 c) {
+    const int wd = a.mode == kWidest ? (int)a.split_dims[a.g.Fl + a.g.sbase + c] : -1;
+    return pair_child_key(a.boxes_in + c * 2ull * a.k, a.bmode_in[c], a.k, a.g.l, a.g.n, wd);
 }
 
 // side of the point at layout position pos against a pivot whose leading
@@ -565,7 +582,7 @@ __global__ void __launch_bounds__(256) sel_pick_kernel(SelArgs a) {
         const u32 C = h[b];
         const float* box = a.boxes_in + j * 2ull * a.k;
         if (a.pair) {
-            const PairKey pk = pair_child_key(box, a.bmode_in[j], a.k, a.g.l, a.g.n);
+            const PairKey pk = pair_key_of(a, j);
             sel[kSelLo] = __float_as_uint(pk.lo);
             sel[kSelShift] = __float_as_uint(pk.hi);
             sel[kSelMode] = (u32)pk.mode;
@@ -1628,9 +1645,8 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
                 // (the children's boxes pin what the parent's does in every
                 // chain dim but its split dim)
                 pinm = pinned_fields(a.chains0 + j, a.boxes_in + (2 * j) * 2ull * k, k);
-                const PairKey p0 = pair_child_key(a.boxes_in + (2 * j) * 2ull * k, a.bmode_in[2 * j], k, a.g.l, a.g.n);
-                const PairKey p1 =
-                    pair_child_key(a.boxes_in + (2 * j + 1) * 2ull * k, a.bmode_in[2 * j + 1], k, a.g.l, a.g.n);
+                const PairKey p0 = pair_key_of(a, 2 * j);
+                const PairKey p1 = pair_key_of(a, 2 * j + 1);
                 dk0 = p0.d;
                 dk1 = p1.d;
                 b0 = make_bucketer(p0.lo, p0.hi, a.D, p0.mode);
@@ -1666,8 +1682,9 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
                     kv[i] = (in && same) ? kc[i] : 0u;
                 }
             }
+            // (widest: a child split again in its parent's dim has its own range)
             const bool ub = same && b0.hlo == b1.hlo && b0.scale == b1.scale && b0.top == b1.top;
-            if (ub && r0 >= ra && r0 + ITEMS <= rb) {
+            if (same && key_mode(b0) == key_mode(b1) && r0 >= ra && r0 + ITEMS <= rb) {
                 // common case: one key column and one bucketer for both
                 // children; sides by float compares, the rare ties apart
                 u32 sides = 0;
@@ -1688,7 +1705,8 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
 #pragma unroll
                     for (int i = 0; i < ITEMS; ++i) {
                         const u32 sd = (sides >> (2 * i)) & 3u;
-                        if (sd < 2u) atomicAdd(&h[(int)sd * nb + (int)bucket_fn(b0, kv[i])], 1u);
+                        if (sd < 2u)
+                            atomicAdd(&h[(int)sd * nb + (int)bucket_fn(ub ? b0 : bsel2(sd != 0u, b0, b1), kv[i])], 1u);
                     }
                 };
                 if (key_mode(b0)) items([](const Bucketer& bb, u32 x) { return bucket_key(bb, x); });
@@ -1775,8 +1793,8 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
                                         (int)sl1[kSelMode]);
                     bs0 = sl0[kSelB];
                     bs1 = sl1[kSelB];
-                    dk0 = pair_child_key(a.boxes_in + (2 * j) * 2ull * k, a.bmode_in[2 * j], k, a.g.l, a.g.n).d;
-                    dk1 = pair_child_key(a.boxes_in + (2 * j + 1) * 2ull * k, a.bmode_in[2 * j + 1], k, a.g.l, a.g.n).d;
+                    dk0 = pair_key_of(a, 2 * j).d;
+                    dk1 = pair_key_of(a, 2 * j + 1).d;
                     ub = bk0.hlo == bk1.hlo && bk0.scale == bk1.scale && bk0.top == bk1.top;
                 }
                 const u32 r0 = (u32)threadIdx.x * ITEMS;
@@ -1814,7 +1832,7 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
                 }
                 u32 hits = 0, hside = 0, nlt0 = 0, nlt1 = 0;
                 const bool inside = r0 >= ra && r0 + ITEMS <= rb;
-                if (inside && same && ub) {
+                if (inside && same && key_mode(bk0) == key_mode(bk1)) {
                     // common case: all 8 items in the part, both children keyed
                     // by one column and one bucketer (their box ranges in the
                     // key dim are the parent's): sides by float compares, the
@@ -1838,7 +1856,7 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
 #pragma unroll
                         for (int i = 0; i < ITEMS; ++i) {
                             const u32 sd = (sides >> (2 * i)) & 3u;
-                            const u32 b = bucket_fn(bk0, ck[i]);
+                            const u32 b = bucket_fn(ub ? bk0 : bsel2(sd == 1u, bk0, bk1), ck[i]);
                             const u32 bsel = sd ? bs1 : bs0;
                             const bool in = sd < 2u;
                             hits |= (in && b == bsel ? 1u : 0u) << i;
@@ -1986,6 +2004,7 @@ struct PHdr2 {
 struct PPar {
     u64 j;
     u32 ib, ie, po, poL, poR, pp0, ppL, ppR;
+    int dl, dlL, dlR;  // the split dims of the parent and its children
     float y, yL, yR;
 };
 
@@ -1999,6 +2018,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
     const int k = a.k, A = k + 1;
     const LevelGeom& g0 = a.g0;  // parents: the layout
     const LevelGeom& g1 = a.g;   // children
+    const bool wide = a.mode == kWidest;
     const u32* Wsrc = a.bf.w[a.par];
     u32* Wdst = a.bf.w[a.par ^ 1u];
     const u64 stride = a.bf.stride;
@@ -2040,6 +2060,13 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
     bool hsides = false, hall = false;
     int hmode = 4;  // 0: both sides value-linear, 3: both key-linear, else mixed / per grandchild
     const int dn2 = (g1.l + 1) % k;
+    // a grandchild's key dim for the fused histogram: round robin
+    // rr_key_dim (-1: pinned, the level's dim); widest its split dim
+    auto gdim = [&](u64 c, const float* cb) -> int {
+        if (!wide) return rr_key_dim(cb, k, g1.l + 1);
+        const u64 node = ((2ull << g1.l) - 1ull) + (g1.sbase << 1) + c;
+        return node < g1.n ? (int)a.split_dims[node] : 0;
+    };
     int hcnt = 0;
     auto hflush = [&]() {
         if (hseg != ~0ull) {
@@ -2061,7 +2088,10 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
         __syncwarp();
     }
     const int tsh = 31 - __clz(T);
-    const int dl = g0.l % k, dl1 = g1.l % k;  // round robin: the parents' and children's leading dims
+    // split dims: round robin by level; widest per node (written by the selects)
+    auto sdim = [&](const LevelGeom& gg, u64 t, int rr_dim) -> int {
+        return wide ? (int)a.split_dims[gg.Fl + gg.sbase + t] : rr_dim;
+    };
     auto load_par = [&](u64 j) {
         PPar p;
         p.j = j;
@@ -2074,9 +2104,12 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
         p.pp0 = a.ppos0[j];
         p.ppL = a.ppos[2 * j];
         p.ppR = a.ppos[2 * j + 1];
-        p.y = __uint_as_float(a.piv0[j * A + dl]);
-        p.yL = __uint_as_float(a.piv[(2 * j) * A + dl1]);
-        p.yR = __uint_as_float(a.piv[(2 * j + 1) * A + dl1]);
+        p.dl = sdim(g0, j, g0.l % k);
+        p.dlL = sdim(g1, 2 * j, g1.l % k);
+        p.dlR = sdim(g1, 2 * j + 1, g1.l % k);
+        p.y = __uint_as_float(a.piv0[j * A + p.dl]);
+        p.yL = __uint_as_float(a.piv[(2 * j) * A + p.dlL]);
+        p.yR = __uint_as_float(a.piv[(2 * j + 1) * A + p.dlR]);
         return p;
     };
     // the parent of the last lean subtile: subtiles inside it skip the
@@ -2161,7 +2194,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                 auto gset = [&](int q, int& hd, Bucketer& hbq) {
                     const u64 c = 4 * hseg + q;
                     const float* cb = a.boxes_out + c * 2ull * k;
-                    const int e = rr_key_dim(cb, k, g1.l + 1);
+                    const int e = gdim(c, cb);
                     hd = e >= 0 ? e : dn2;
                     hbq = make_bucketer(cb[hd], cb[k + hd], FD, a.bmode_out[c]);
                 };
@@ -2187,7 +2220,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
             u32 s1 = 0;
 #pragma unroll
             for (int i = 0; i < kPRows; ++i) {
-                const float x = __uint_as_float(V(dl, i));
+                const float x = __uint_as_float(V(cp.dl, i));
                 s1 |= (x < y ? 0u : (x > y ? 1u : 2u)) << (2 * i);
             }
             if (__any_sync(kFullMask, (s1 & 0xAAAAu) != 0u)) {
@@ -2206,7 +2239,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                 const u32 a1 = (s1 >> (2 * i)) & 3u;
                 u32 sd = 3u;
                 if (a1 < 2u) {
-                    const float x = __uint_as_float(V(dl1, i));
+                    const float x = __uint_as_float(V(a1 ? cp.dlR : cp.dlL, i));
                     const float yy = a1 ? yR : yL;
                     sd = x < yy ? 0u : (x > yy ? 1u : 2u);
                 }
@@ -2324,15 +2357,18 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
             // match_any, the fused histogram by global atomics
             const u64 j0 = tp.j0;
             u32 b[2][4];
+            const PPar P0 = load_par(j0);
             {
                 PHdr2 h0;  // (the prefetched header may have used the cache)
                 hdr_load(s, j0, h0);
-                bases(h0, load_par(j0), ss, b[0]);
+                bases(h0, P0, ss, b[0]);
             }
+            PPar P1 = P0;
             if (tp.has1) {
                 PHdr2 h1;  // the second parent's header (its tile part index)
                 hdr_load(s, j0 + 1, h1);
-                bases(h1, load_par(j0 + 1), ss, b[1]);
+                P1 = load_par(j0 + 1);
+                bases(h1, P1, ss, b[1]);
             } else {
                 b[1][0] = b[1][1] = b[1][2] = b[1][3] = 0u;
             }
@@ -2343,15 +2379,16 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                 u32 run = 8u;  // 8: no run (outside the parts, or one of the three pivots)
                 if (in0 || in1) {
                     const u64 j = j0 + (in1 ? 1 : 0);
+                    const PPar& P = in1 ? P1 : P0;
                     const u64 pos = ss + r;
-                    const float x = __uint_as_float(V(dl, i));
-                    const float yv = __uint_as_float(a.piv0[j * A + dl]);
+                    const float x = __uint_as_float(V(P.dl, i));
+                    const float yv = P.y;
                     int a1 = x < yv ? 0 : (x > yv ? 1 : 2);
                     if (a1 == 2) a1 = tie_side_of(Wsrc, stride, k, a.chains0 + j, a.piv0 + j * A, pos);
                     if (a1 < 2) {
                         const u64 c = 2 * j + a1;
-                        const float x2 = __uint_as_float(V(dl1, i));
-                        const float y2 = __uint_as_float(a.piv[c * A + dl1]);
+                        const float x2 = __uint_as_float(V(a1 ? P.dlR : P.dlL, i));
+                        const float y2 = a1 ? P.yR : P.yL;
                         int a2 = x2 < y2 ? 0 : (x2 > y2 ? 1 : 2);
                         if (a2 == 2) a2 = tie_side_of(Wsrc, stride, k, a.chains + c, a.piv + c * A, pos);
                         if (a2 < 2) {
@@ -2360,7 +2397,7 @@ __global__ void __launch_bounds__(kPThreads, 2) sel_part_pair_kernel(SelArgs a, 
                             if (fuse) {
                                 const u64 gc = 4 * j + q;
                                 const float* cb = a.boxes_out + gc * 2ull * k;
-                                const int e = rr_key_dim(cb, k, g1.l + 1);
+                                const int e = gdim(gc, cb);
                                 const int dnc = e >= 0 ? e : dn2;
                                 const Bucketer hbq = make_bucketer(cb[dnc], cb[k + dnc], FD, a.bmode_out[gc]);
                                 atomicAdd(&a.hist_next[gc * (u64)kGB + bucket_of(hbq, V(dnc, i))], 1u);

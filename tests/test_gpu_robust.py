@@ -126,6 +126,40 @@ def test_nonfinite_input_is_reported_not_crashing(dim):
     assert np.array_equal(perm.cpu().numpy().view(np.uint32), oracle.rec_build(pts))
 
 
+_WIDEST_PAIRS = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2211_00120_b200 as kd
+from oracle import oracle
+from tests.test_gpu_robust import _adversarial
+from paper_2211_00120_b200 import datagen
+cases = [("uniform", datagen.uniform(1_500_001, 3, 1)), ("clustered", datagen.make("clustered", 600_001, 2, 2)),
+         ("ties", datagen.ties(1_000_003, 4, 3))]
+cases += [(nm, _adversarial(nm, 700_001, 3, 5)) for nm in ("identical", "huge_range", "constant_axis", "sorted")]
+for name, p in cases:
+    _, perm, dims = kd.build_widest_cuda(torch.from_numpy(np.ascontiguousarray(p)).cuda())
+    wp, wd = oracle.rec_build(p, widest=True)
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), wp), name
+    assert np.array_equal(dims.cpu().numpy(), wd), name
+print("WIDEST_PAIRS_OK")
+'''
+
+
+def test_widest_level_pairs_opt_in():
+    """Widest with its global levels two per partition pass (off by default:
+    measured slower on config 5; LBKD_PAIR_WIDEST=1): exact on normal and
+    adversarial inputs, odd and even level counts, k = 2, 3, 4."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LBKD_PAIR_WIDEST="1")
+    r = subprocess.run([sys.executable, "-c", _WIDEST_PAIRS, root], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=900)
+    assert "WIDEST_PAIRS_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
 def test_ties_100m_rr():
     """64 values per axis at the headline size (ties at every level)."""
     pts = datagen.ties(100_000_000, 3, seed=1)
