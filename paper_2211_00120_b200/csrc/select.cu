@@ -1590,7 +1590,7 @@ __global__ void __launch_bounds__(kPThreads, MINB) sel_part_bulk_kernel(SelArgs 
 // per child, D = a.D); one CTA walks a contiguous run of tiles and flushes
 // its shared bins when the parent changes
 template <int ITEMS>
-__global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
+__global__ void __launch_bounds__(kHThreads, 4) sel_child_hist_kernel(SelArgs a) {
     if (aborted(a)) return;  // non-finite input: the build is reported, not run
     extern __shared__ u32 h[];  // [2][2^D]
     constexpr int T = kHThreads * ITEMS;
@@ -1682,9 +1682,8 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
                     kv[i] = (in && same) ? kc[i] : 0u;
                 }
             }
-            // (widest: a child split again in its parent's dim has its own range)
             const bool ub = same && b0.hlo == b1.hlo && b0.scale == b1.scale && b0.top == b1.top;
-            if (same && key_mode(b0) == key_mode(b1) && r0 >= ra && r0 + ITEMS <= rb) {
+            if (ub && r0 >= ra && r0 + ITEMS <= rb) {
                 // common case: one key column and one bucketer for both
                 // children; sides by float compares, the rare ties apart
                 u32 sides = 0;
@@ -1706,7 +1705,7 @@ __global__ void __launch_bounds__(kHThreads) sel_child_hist_kernel(SelArgs a) {
                     for (int i = 0; i < ITEMS; ++i) {
                         const u32 sd = (sides >> (2 * i)) & 3u;
                         if (sd < 2u)
-                            atomicAdd(&h[(int)sd * nb + (int)bucket_fn(ub ? b0 : bsel2(sd != 0u, b0, b1), kv[i])], 1u);
+                            atomicAdd(&h[(int)sd * nb + (int)bucket_fn(b0, kv[i])], 1u);
                     }
                 };
                 if (key_mode(b0)) items([](const Bucketer& bb, u32 x) { return bucket_key(bb, x); });
@@ -1832,7 +1831,7 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
                 }
                 u32 hits = 0, hside = 0, nlt0 = 0, nlt1 = 0;
                 const bool inside = r0 >= ra && r0 + ITEMS <= rb;
-                if (inside && same && key_mode(bk0) == key_mode(bk1)) {
+                if (inside && same && ub) {
                     // common case: all 8 items in the part, both children keyed
                     // by one column and one bucketer (their box ranges in the
                     // key dim are the parent's): sides by float compares, the
@@ -1856,7 +1855,7 @@ __global__ void __launch_bounds__(THREADS) sel_filter_pair_kernel(SelArgs a) {
 #pragma unroll
                         for (int i = 0; i < ITEMS; ++i) {
                             const u32 sd = (sides >> (2 * i)) & 3u;
-                            const u32 b = bucket_fn(ub ? bk0 : bsel2(sd == 1u, bk0, bk1), ck[i]);
+                            const u32 b = bucket_fn(bk0, ck[i]);
                             const u32 bsel = sd ? bs1 : bs0;
                             const bool in = sd < 2u;
                             hits |= (in && b == bsel ? 1u : 0u) << i;
