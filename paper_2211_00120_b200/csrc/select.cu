@@ -29,6 +29,10 @@
 //            prefixes, no lookback), fused with the next level's histogram
 // The partition is stable, so every segment keeps the INPUT order of its
 // points; the in-CTA phase (subtree.cu) derives its chain orders from that.
+// Round robin (k = 2..4) runs the levels in PAIRS: after level l's select,
+// level l+1 is selected in level l's layout (child hist, pick, filter pair,
+// select with per-side counts) and one stable 4-way partition moves every
+// point to its grandchild's run -- see "Level pairs" below and DESIGN.md §2.
 //
 // Layout: in-order SoA as in global_sort.cu -- segment j of level l occupies
 // [ib(j), ib(j) + ss(j)) of W[(l - lfirst) & 1]; finished nodes leave a hole.
