@@ -363,7 +363,70 @@ __global__ void __launch_bounds__(256) init_stats_kernel(const float* __restrict
     }
 }
 
+// k = 3, 16-byte aligned input: four points per thread step -- three
+// 16-byte loads of 12 floats, one 16-byte store per SoA column
+__global__ void __launch_bounds__(256) init_stats3_kernel(const float4* __restrict__ pts4, u64 n, u32* w0, u64 stride,
+                                                          u32* err, u32* minmax) {
+    __shared__ u32 smn[3], smx[3];
+    if (threadIdx.x < 3) { smn[threadIdx.x] = 0xffffffffu; smx[threadIdx.x] = 0u; }
+    __syncthreads();
+    u32 mn[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, mx[3] = {0u, 0u, 0u};
+    bool bad = false;
+    auto one = [&](int c, float f) {
+        bad |= !isfinite(f);
+        const u32 key = flip_key(f);
+        mn[c] = min(mn[c], key);
+        mx[c] = max(mx[c], key);
+    };
+    const u64 ng = n / 4;
+    for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < ng; g += (u64)gridDim.x * blockDim.x) {
+        const float4 a = __ldg(pts4 + 3 * g), b = __ldg(pts4 + 3 * g + 1), c = __ldg(pts4 + 3 * g + 2);
+        const float x[4] = {a.x, a.w, b.z, c.y}, y[4] = {a.y, b.x, b.w, c.z}, z[4] = {a.z, b.y, c.x, c.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { one(0, x[i]); one(1, y[i]); one(2, z[i]); }
+        const u64 p = 4 * g;
+        *reinterpret_cast<uint4*>(w0 + p) = make_uint4(__float_as_uint(x[0]), __float_as_uint(x[1]), __float_as_uint(x[2]), __float_as_uint(x[3]));
+        *reinterpret_cast<uint4*>(w0 + stride + p) = make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]), __float_as_uint(y[3]));
+        *reinterpret_cast<uint4*>(w0 + 2 * stride + p) = make_uint4(__float_as_uint(z[0]), __float_as_uint(z[1]), __float_as_uint(z[2]), __float_as_uint(z[3]));
+        *reinterpret_cast<uint4*>(w0 + 3 * stride + p) = make_uint4((u32)p, (u32)p + 1u, (u32)p + 2u, (u32)p + 3u);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < n - 4 * ng) {  // the last n mod 4 points
+        const u64 i = 4 * ng + threadIdx.x;
+        const float* q = reinterpret_cast<const float*>(pts4) + 3 * i;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float f = __ldg(q + c);
+            one(c, f);
+            w0[c * stride + i] = __float_as_uint(f);
+        }
+        w0[3 * stride + i] = (u32)i;
+    }
+    if (__any_sync(kFullMask, bad) && (threadIdx.x & 31) == 0) {
+        atomicOr(err, 1u);
+        atomicOr(err + 1, 1u);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const u32 a = __reduce_min_sync(kFullMask, mn[c]);
+        const u32 b = __reduce_max_sync(kFullMask, mx[c]);
+        if ((threadIdx.x & 31) == 0) { atomicMin(&smn[c], a); atomicMax(&smx[c], b); }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        atomicMin(&minmax[threadIdx.x], smn[threadIdx.x]);
+        atomicMax(&minmax[3 + threadIdx.x], smx[threadIdx.x]);
+    }
+}
+
 void launch_init_stats(const BuildParams& bp, const Buffers& bf, u32* minmax, cudaStream_t st) {
+    if (bp.k == 3 && ((uintptr_t)bp.pts & 15u) == 0 && (bf.stride & 3u) == 0 && !getenv("LBKD_INIT_SCALAR")) {
+        u64 blocks = (bp.n / 4 + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        if (blocks < 1) blocks = 1;
+        init_stats3_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(bp.pts), bp.n, bf.w[0],
+                                                             bf.stride, bf.err, minmax);
+        return;
+    }
     u64 blocks = (bp.n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     init_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(bp.pts, bp.n, bp.k, bf.w[0], bf.stride, bf.err, minmax);
