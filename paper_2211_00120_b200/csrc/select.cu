@@ -551,14 +551,24 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
             bk = seg_bucketer(a, cur, dk);
             kp = W + (u64)dk * a.bf.stride;
         }
+        // ITEMS consecutive positions per thread
+        const u32 rb0 = (u32)threadIdx.x * ITEMS;
         u32 key[ITEMS];
+        // (vector loads only inside one part: the finished nodes' slots
+        // between segments are never written in this buffer)
+        if (ITEMS % 4 == 0 && ((rb0 >= r0a && rb0 + ITEMS <= r0b) || (has1 && rb0 >= r1a && rb0 + ITEMS <= r1b))) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            // only the tile's segment parts (the finished nodes between
-            // segments hold no data in this buffer)
-            const u32 r = (u32)(i * kHThreads + threadIdx.x);
-            const bool use = (r >= r0a && r < r0b) || (has1 && r >= r1a && r < r1b);
-            key[i] = use ? kp[ts + r] : 0u;
+            for (int i = 0; i < ITEMS; i += 4) {
+                const uint4 q = *reinterpret_cast<const uint4*>(kp + ts + rb0 + i);
+                key[i] = q.x; key[i + 1] = q.y; key[i + 2] = q.z; key[i + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const u32 r = rb0 + (u32)i;
+                const bool use = (r >= r0a && r < r0b) || (has1 && r >= r1a && r < r1b);
+                key[i] = use ? kp[ts + r] : 0u;
+            }
         }
         if (has1 && nseg_c != cur + 1) {  // the next segment's key dim, once per segment
             nseg_c = cur + 1;
@@ -568,7 +578,7 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
             const u32* k1 = W + (u64)dk1 * a.bf.stride;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const u32 r = (u32)(i * kHThreads + threadIdx.x);
+                const u32 r = rb0 + (u32)i;
                 if (r >= r1a && r < r1b) key[i] = k1[ts + r];
             }
         }
@@ -577,13 +587,13 @@ __global__ void __launch_bounds__(kHThreads) sel_hist_kernel(SelArgs a) {
             if (key_mode(bk)) {
 #pragma unroll
                 for (int i = 0; i < ITEMS; ++i) {
-                    const u32 r = (u32)(i * kHThreads + threadIdx.x);
+                    const u32 r = rb0 + (u32)i;
                     if (r >= ra && r < rb) atomicAdd(&h[bucket_key(bk, key[i])], 1u);
                 }
             } else {
 #pragma unroll
                 for (int i = 0; i < ITEMS; ++i) {
-                    const u32 r = (u32)(i * kHThreads + threadIdx.x);
+                    const u32 r = rb0 + (u32)i;
                     if (r >= ra && r < rb) atomicAdd(&h[bucket_val(bk, key[i])], 1u);
                 }
             }
