@@ -30,7 +30,10 @@
  * Threading: a context is used by one host thread at a time; work is
  * enqueued on `stream`.  The build calls end with one stream
  * synchronisation to read back the non-finite flag (disable with
- * lbkd_set_check(ctx, 0) to keep a build fully asynchronous).
+ * lbkd_set_check(ctx, 0) to keep a build fully asynchronous).  A build
+ * whose input holds a NaN or +-inf stops on the device right after its
+ * input pass (every later kernel returns at once) and reports
+ * LBKD_ENONFINITE; its outputs are then undefined.
  */
 #ifndef LBKD_B200_H
 #define LBKD_B200_H
